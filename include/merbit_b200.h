@@ -1,0 +1,276 @@
+/*
+ * merbit_b200.h -- C ABI of the B200-native MERBIT library (libmerbit_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/merbit): one-time TILE preprocessing
+ * (generate_tile), repeated descriptor-driven SpMV (spmv_merbit) and the
+ * PageRank driver (pagerank), all executed on an sm_100a GPU.  Plain pointers
+ * and sizes only; no C++ or torch types cross it.  The C++ mirror of the
+ * reference API (SimtConfig, TileMetadata, DualBuffer, SpmvBackend,
+ * make_backend, pagerank) is include/merbit_b200/merbit.hpp, header-only over
+ * these entry points; INTEGRATION.md shows the reference-side binding.
+ *
+ * Conventions
+ *  - Every function returns an mbx_status; on failure mbx_last_error() holds
+ *    a thread-local message.  Status codes mirror the reference's exception
+ *    taxonomy (include/merbit/types.hpp:23-65) so the C++ wrapper can rethrow
+ *    the same types, plus CUDA/NCCL/unsupported codes.
+ *  - "_host" pointers are host memory; "_dev" pointers are device memory of
+ *    the context's device.  Host-buffer calls synchronize the context stream
+ *    before returning; device-buffer calls are stream-ordered and
+ *    asynchronous.
+ *  - A context is one device + one stream; it is not thread-safe (the
+ *    reference's backends are single-caller too, backend.hpp:17-21).
+ *  - There is no CPU fallback: with no usable sm_100 device every compute
+ *    entry point fails with MBX_CUDA_ERROR.
+ */
+#ifndef MERBIT_B200_H
+#define MERBIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MBX_API __attribute__((visibility("default")))
+
+typedef enum {
+  MBX_OK = 0,
+  MBX_ERROR = 1,            /* merbit::error               */
+  MBX_IO_ERROR = 2,         /* merbit::io_error            */
+  MBX_PARSE_ERROR = 3,      /* merbit::parse_error         */
+  MBX_CONFIG_ERROR = 4,     /* merbit::config_error        */
+  MBX_DIMENSION_ERROR = 5,  /* merbit::dimension_error     */
+  MBX_CAPACITY_ERROR = 6,   /* merbit::capacity_error      */
+  MBX_CORRUPTION_ERROR = 7, /* merbit::corruption_error    */
+  MBX_CUDA_ERROR = 8,
+  MBX_NCCL_ERROR = 9,
+  MBX_UNSUPPORTED = 10
+} mbx_status;
+
+typedef enum { MBX_F32 = 0, MBX_F64 = 1 } mbx_precision;
+
+/* SimtConfig (include/merbit/config.hpp:18-38). */
+typedef struct {
+  int32_t omega;
+  int32_t sigma;
+  int32_t block_size;
+  int32_t offset_bits;
+} mbx_simt_config;
+
+/* TileMetadata header (include/merbit/tile.hpp:27-44). */
+typedef struct {
+  int32_t omega;
+  int32_t sigma;
+  int64_t n_rows;
+  int64_t nnz;
+  int64_t tile_num;
+  int64_t lane_num;
+  double preprocess_seconds; /* device time of the K1 kernels (T_p) */
+} mbx_tile_info;
+
+/* SpmvTrace routing counters (include/merbit/merbit_spmv.hpp:21-28). */
+typedef struct {
+  int64_t fast_tiles;
+  int64_t normal_tiles;
+  int64_t skipped_tiles;
+} mbx_spmv_trace;
+
+/* PageRankConfig (include/merbit/solvers.hpp:76-82). */
+typedef struct {
+  double damping;          /* 0.85 */
+  double err_tol;          /* 1e-10 */
+  int64_t max_iters;       /* 210 */
+  int64_t reference_iters; /* 210; the yardstick power run (178-191) */
+} mbx_pagerank_config;
+
+/* PageRankResult (solvers.hpp:84-93) plus the device-side reductions. */
+typedef struct {
+  int64_t iterations;
+  double final_err;          /* ERR vs the yardstick, inf-norm relative */
+  int32_t status;            /* 0 converged, 1 max_iterations */
+  double preprocess_seconds; /* T_p of the TILE used */
+  double iterate_seconds;    /* T_r: device time of the power loop */
+  double l1_residual;        /* ||pi_k - pi_{k-1}||_1 of the last iteration */
+  double mass;               /* ||pi_k||_1 */
+  double dangling_mass;      /* sum of pi_k over dangling vertices */
+} mbx_pagerank_result;
+
+typedef struct mbx_context_s mbx_context;
+typedef struct mbx_matrix_s mbx_matrix;
+typedef struct mbx_tile_s mbx_tile;
+typedef struct mbx_pagerank_plan_s mbx_pagerank_plan;
+
+/* ---- errors / build info ------------------------------------------------ */
+MBX_API const char* mbx_last_error(void);
+MBX_API const char* mbx_build_info(void);
+
+/* ---- configuration (host-only; no device needed) ------------------------ */
+/* SimtConfig::make (src/config.cpp:12-38): validates 2*ceil_log2(w*s)+s<=32
+ * and block_size % omega == 0; derives offset_bits. */
+MBX_API int mbx_config_make(int omega, int sigma, int block_size,
+                            mbx_simt_config* out);
+/* select_sigma (src/config.cpp:40-43): 14 for f32, 7 for f64; override>0
+ * wins.  Returns sigma (never fails). */
+MBX_API int mbx_select_sigma(int precision, int override_sigma);
+/* TILE counts (src/tile.cpp:33-35). */
+MBX_API int mbx_tile_counts(int64_t nnz, int64_t n_rows,
+                            const mbx_simt_config* c, int64_t* tile_num,
+                            int64_t* lane_num);
+/* metadata_footprint (src/tile.cpp:146-154). */
+MBX_API double mbx_metadata_footprint(int64_t nnz, int64_t n_rows,
+                                      const mbx_simt_config* c, double r_f);
+/* merge_search (src/merge_path.cpp:8-36) on host arrays. */
+MBX_API int mbx_merge_search(const int64_t* row_offsets_host, int64_t n_rows,
+                             int64_t nnz, int64_t diag, int64_t* x,
+                             int64_t* y);
+/* Multi-GPU row partition: cut the merge path at diagonals
+ * floor(g*(m+n)/parts) with merge_search and snap each cut to its row start.
+ * row_bounds_host has parts+1 entries, [0] = 0, [parts] = n_rows. */
+MBX_API int mbx_plan_row_shards(const int64_t* row_offsets_host,
+                                int64_t n_rows, int64_t nnz, int parts,
+                                int64_t* row_bounds_host);
+
+/* ---- context -------------------------------------------------------------- */
+MBX_API int mbx_device_count(int* count);
+MBX_API int mbx_context_create(int device, mbx_context** out);
+MBX_API int mbx_context_destroy(mbx_context* ctx);
+/* Adopt a caller stream (cudaStream_t as void*); NULL restores the
+ * context's own stream. */
+MBX_API int mbx_context_set_stream(mbx_context* ctx, void* stream);
+MBX_API void* mbx_context_stream(mbx_context* ctx);
+MBX_API int mbx_context_synchronize(mbx_context* ctx);
+/* Kernel launch shape of K2 (omega == 32): warps per CTA, resident CTAs per
+ * SM (persistent grid), hub-cache cap (-1 auto, 0 off).  Defaults 16/2/-1. */
+MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta,
+                                   int ctas_per_sm, int max_hubs);
+/* Number of merbit kernels this context launched so far. */
+MBX_API int64_t mbx_context_launch_count(const mbx_context* ctx);
+
+/* ---- matrices (device-resident CSR: T values, int32 columns, u32 rows) --- */
+/* Copies a host CsrMatrix<T> (include/merbit/csr.hpp:29-38) to the device
+ * once: int64 col_indices narrow to int32 (n_cols < 2^31), row_offsets to
+ * u32 (nnz < 2^32, the TILE capacity rule of tile.cpp:23-26). */
+MBX_API int mbx_matrix_upload(mbx_context* ctx, int precision, int64_t n_rows,
+                              int64_t n_cols, const int64_t* row_offsets_host,
+                              const int64_t* col_indices_host,
+                              const void* values_host, mbx_matrix** out);
+/* Same, with int32 column indices on the host. */
+MBX_API int mbx_matrix_upload_i32(mbx_context* ctx, int precision,
+                                  int64_t n_rows, int64_t n_cols,
+                                  const int64_t* row_offsets_host,
+                                  const int32_t* col_indices_host,
+                                  const void* values_host, mbx_matrix** out);
+/* Synthetic R-MAT input generated on the device (counter-based; identical to
+ * oracle/mo_rmat_csr).  kind 0: adjacency A (rows = source) with values
+ * lo + (hi-lo)*U(value_seed, k); kind 1: PageRank transition P = A^T D^-1
+ * (rows = destination, values 1/outdeg, solvers.hpp:36-74). */
+MBX_API int mbx_matrix_generate_rmat(mbx_context* ctx, int precision,
+                                     int scale, int edge_factor,
+                                     uint64_t seed, int kind,
+                                     uint64_t value_seed, double lo,
+                                     double hi, mbx_matrix** out);
+MBX_API int mbx_matrix_info(const mbx_matrix* m, int* precision,
+                            int64_t* n_rows, int64_t* n_cols, int64_t* nnz);
+/* Any output pointer may be NULL.  row_offsets as int64. */
+MBX_API int mbx_matrix_download(const mbx_matrix* m,
+                                int64_t* row_offsets_host,
+                                int32_t* col_indices_host, void* values_host);
+/* Device pointers of the matrix arrays (for fused/device-side callers). */
+MBX_API int mbx_matrix_device_ptrs(const mbx_matrix* m, const void** values,
+                                   const int32_t** col_indices,
+                                   const uint32_t** row_offsets);
+MBX_API int mbx_matrix_destroy(mbx_matrix* m);
+/* x hub cache (no reference counterpart; an sm_100a-specific preprocessing
+ * step next to generate_tile): ranks columns by reference count and stages
+ * the most referenced x entries in shared memory during SpMV.  Results are
+ * bitwise identical with and without it.  max_hubs < 0: as many as the
+ * shared-memory budget of the context tuning allows; 0: remove the cache. */
+MBX_API int mbx_matrix_build_xcache(mbx_context* ctx, mbx_matrix* m,
+                                    int max_hubs, double* seconds);
+MBX_API int mbx_matrix_xcache_info(const mbx_matrix* m, int* hubs,
+                                   double* coverage);
+
+/* ---- TILE preprocessing (K1) --------------------------------------------- */
+/* generate_tile(span row_offsets, n_rows, nnz, c) (src/tile.cpp:17-85) on
+ * the GPU; the arrays are byte-identical to the reference's. */
+MBX_API int mbx_generate_tile(mbx_context* ctx,
+                              const int64_t* row_offsets_host, int64_t n_rows,
+                              int64_t nnz, const mbx_simt_config* c,
+                              mbx_tile** out);
+/* generate_tile(const CsrMatrix&, c) (tile.hpp:54-58) from the resident
+ * matrix. */
+MBX_API int mbx_matrix_generate_tile(mbx_context* ctx, const mbx_matrix* m,
+                                     const mbx_simt_config* c,
+                                     mbx_tile** out);
+MBX_API int mbx_tile_get_info(const mbx_tile* t, mbx_tile_info* info);
+MBX_API int mbx_tile_download(const mbx_tile* t, uint32_t* tile_x_host,
+                              uint32_t* tile_y_host,
+                              uint32_t* lane_desc_host);
+/* Adopt host TILE arrays (e.g. an MBTL cache, tile.cpp:161-234). */
+MBX_API int mbx_tile_upload(mbx_context* ctx, const mbx_tile_info* info,
+                            const uint32_t* tile_x_host,
+                            const uint32_t* tile_y_host,
+                            const uint32_t* lane_desc_host, mbx_tile** out);
+MBX_API int mbx_tile_destroy(mbx_tile* t);
+
+/* ---- SpMV (K2 + K3) ------------------------------------------------------- */
+/* spmv_merbit (include/merbit/merbit_spmv.hpp:136-352): y = A x.  Every row
+ * of y is assigned (no zero-on-entry requirement).  Errors as the reference:
+ * config_error on omega/sigma or shape mismatch with the TILE (140-151),
+ * dimension_error is the caller's (sizes are implied by the matrix).
+ * trace may be NULL. */
+MBX_API int mbx_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                     const mbx_simt_config* c, const void* x_host,
+                     void* y_host, mbx_spmv_trace* trace);
+MBX_API int mbx_spmv_device(mbx_context* ctx, const mbx_matrix* m,
+                            const mbx_tile* t, const mbx_simt_config* c,
+                            const void* x_dev, void* y_dev);
+/* Routing counters only (device classification of every tile with the
+ * kernel's own predicate). */
+MBX_API int mbx_spmv_trace_counts(mbx_context* ctx, const mbx_tile* t,
+                                  mbx_spmv_trace* trace);
+/* Plain row-parallel CSR SpMV on the device (the yardstick kernel of
+ * pagerank, solvers.hpp:178-191, and a non-MERBIT comparator). */
+MBX_API int mbx_spmv_csr_device(mbx_context* ctx, const mbx_matrix* m,
+                                const void* x_dev, void* y_dev);
+
+/* ---- PageRank (K2/K3 in fused mode) --------------------------------------- */
+/* One-shot pagerank<T>(p, cfg, backend) (solvers.hpp:154-218): yardstick,
+ * power loop with the damping/teleport update, dangling redistribution, L1
+ * residual, mass check and ERR fused into the SpMV commit; early exit when
+ * ERR < err_tol.  pi0_host may be NULL (uniform 1/n, as the reference).
+ * reference_pi_host / residual_history_host (max_iters doubles) may be NULL. */
+MBX_API int mbx_pagerank(mbx_context* ctx, const mbx_matrix* p,
+                         const mbx_tile* t, const mbx_simt_config* c,
+                         const mbx_pagerank_config* cfg, const void* pi0_host,
+                         void* pi_host, void* reference_pi_host,
+                         double* residual_history_host,
+                         mbx_pagerank_result* result);
+/* Reusable plan: device buffers, dangling mask and the CUDA graph of the
+ * power loop are built once. */
+MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p,
+                                     const mbx_tile* t,
+                                     const mbx_simt_config* c,
+                                     const mbx_pagerank_config* cfg,
+                                     mbx_pagerank_plan** out);
+/* Runs the yardstick (if reference_iters > 0) and the power loop.  pi0_dev
+ * may be NULL (uniform).  The final iterate is left on the device
+ * (mbx_pagerank_plan_pi). Asynchronous; call mbx_pagerank_plan_result after
+ * a stream sync. */
+MBX_API int mbx_pagerank_plan_run(mbx_pagerank_plan* plan,
+                                  const void* pi0_dev);
+MBX_API int mbx_pagerank_plan_result(mbx_pagerank_plan* plan,
+                                     mbx_pagerank_result* result,
+                                     double* residual_history_host);
+MBX_API const void* mbx_pagerank_plan_pi(const mbx_pagerank_plan* plan);
+MBX_API const void* mbx_pagerank_plan_reference_pi(
+    const mbx_pagerank_plan* plan);
+MBX_API int mbx_pagerank_plan_destroy(mbx_pagerank_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MERBIT_B200_H */

@@ -1,0 +1,120 @@
+"""ctypes loader for libmerbit_b200.so (the C ABI in include/merbit_b200.h).
+
+There is no fallback: if the in-tree shared library is missing or fails to
+load, importing the package's compute API raises.  Build it with
+``python -c "import __graft_entry__; __graft_entry__.build()"`` or
+``make -C paper_2605_07391_b200/csrc``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmerbit_b200.so")
+
+
+class mbx_simt_config(C.Structure):
+    _fields_ = [("omega", C.c_int32), ("sigma", C.c_int32), ("block_size", C.c_int32),
+                ("offset_bits", C.c_int32)]
+
+
+class mbx_tile_info(C.Structure):
+    _fields_ = [("omega", C.c_int32), ("sigma", C.c_int32), ("n_rows", C.c_int64),
+                ("nnz", C.c_int64), ("tile_num", C.c_int64), ("lane_num", C.c_int64),
+                ("preprocess_seconds", C.c_double)]
+
+
+class mbx_spmv_trace(C.Structure):
+    _fields_ = [("fast_tiles", C.c_int64), ("normal_tiles", C.c_int64),
+                ("skipped_tiles", C.c_int64)]
+
+
+class mbx_pagerank_config(C.Structure):
+    _fields_ = [("damping", C.c_double), ("err_tol", C.c_double), ("max_iters", C.c_int64),
+                ("reference_iters", C.c_int64)]
+
+
+class mbx_pagerank_result(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("final_err", C.c_double), ("status", C.c_int32),
+                ("preprocess_seconds", C.c_double), ("iterate_seconds", C.c_double),
+                ("l1_residual", C.c_double), ("mass", C.c_double),
+                ("dangling_mass", C.c_double)]
+
+
+VP = C.c_void_p
+I64P = C.POINTER(C.c_int64)
+SIGNATURES = {
+    "mbx_last_error": ([], C.c_char_p),
+    "mbx_build_info": ([], C.c_char_p),
+    "mbx_config_make": ([C.c_int, C.c_int, C.c_int, C.POINTER(mbx_simt_config)], C.c_int),
+    "mbx_select_sigma": ([C.c_int, C.c_int], C.c_int),
+    "mbx_tile_counts": ([C.c_int64, C.c_int64, C.POINTER(mbx_simt_config), I64P, I64P], C.c_int),
+    "mbx_metadata_footprint": ([C.c_int64, C.c_int64, C.POINTER(mbx_simt_config), C.c_double],
+                               C.c_double),
+    "mbx_merge_search": ([VP, C.c_int64, C.c_int64, C.c_int64, I64P, I64P], C.c_int),
+    "mbx_plan_row_shards": ([VP, C.c_int64, C.c_int64, C.c_int, VP], C.c_int),
+    "mbx_device_count": ([C.POINTER(C.c_int)], C.c_int),
+    "mbx_context_create": ([C.c_int, C.POINTER(VP)], C.c_int),
+    "mbx_context_destroy": ([VP], C.c_int),
+    "mbx_context_set_stream": ([VP, VP], C.c_int),
+    "mbx_context_stream": ([VP], VP),
+    "mbx_context_synchronize": ([VP], C.c_int),
+    "mbx_context_launch_count": ([VP], C.c_int64),
+    "mbx_context_set_tuning": ([VP, C.c_int, C.c_int, C.c_int], C.c_int),
+    "mbx_matrix_build_xcache": ([VP, VP, C.c_int, C.POINTER(C.c_double)], C.c_int),
+    "mbx_matrix_xcache_info": ([VP, C.POINTER(C.c_int), C.POINTER(C.c_double)], C.c_int),
+    "mbx_matrix_upload": ([VP, C.c_int, C.c_int64, C.c_int64, VP, VP, VP, C.POINTER(VP)], C.c_int),
+    "mbx_matrix_upload_i32": ([VP, C.c_int, C.c_int64, C.c_int64, VP, VP, VP, C.POINTER(VP)],
+                              C.c_int),
+    "mbx_matrix_generate_rmat": ([VP, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_uint64,
+                                  C.c_double, C.c_double, C.POINTER(VP)], C.c_int),
+    "mbx_matrix_info": ([VP, C.POINTER(C.c_int), I64P, I64P, I64P], C.c_int),
+    "mbx_matrix_download": ([VP, VP, VP, VP], C.c_int),
+    "mbx_matrix_device_ptrs": ([VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)], C.c_int),
+    "mbx_matrix_destroy": ([VP], C.c_int),
+    "mbx_generate_tile": ([VP, VP, C.c_int64, C.c_int64, C.POINTER(mbx_simt_config),
+                           C.POINTER(VP)], C.c_int),
+    "mbx_matrix_generate_tile": ([VP, VP, C.POINTER(mbx_simt_config), C.POINTER(VP)], C.c_int),
+    "mbx_tile_get_info": ([VP, C.POINTER(mbx_tile_info)], C.c_int),
+    "mbx_tile_download": ([VP, VP, VP, VP], C.c_int),
+    "mbx_tile_upload": ([VP, C.POINTER(mbx_tile_info), VP, VP, VP, C.POINTER(VP)], C.c_int),
+    "mbx_tile_destroy": ([VP], C.c_int),
+    "mbx_spmv": ([VP, VP, VP, C.POINTER(mbx_simt_config), VP, VP, C.POINTER(mbx_spmv_trace)],
+                 C.c_int),
+    "mbx_spmv_device": ([VP, VP, VP, C.POINTER(mbx_simt_config), VP, VP], C.c_int),
+    "mbx_spmv_trace_counts": ([VP, VP, C.POINTER(mbx_spmv_trace)], C.c_int),
+    "mbx_spmv_csr_device": ([VP, VP, VP, VP], C.c_int),
+    "mbx_pagerank": ([VP, VP, VP, C.POINTER(mbx_simt_config), C.POINTER(mbx_pagerank_config), VP,
+                      VP, VP, VP, C.POINTER(mbx_pagerank_result)], C.c_int),
+    "mbx_pagerank_plan_create": ([VP, VP, VP, C.POINTER(mbx_simt_config),
+                                  C.POINTER(mbx_pagerank_config), C.POINTER(VP)], C.c_int),
+    "mbx_pagerank_plan_run": ([VP, VP], C.c_int),
+    "mbx_pagerank_plan_result": ([VP, C.POINTER(mbx_pagerank_result), VP], C.c_int),
+    "mbx_pagerank_plan_pi": ([VP], VP),
+    "mbx_pagerank_plan_reference_pi": ([VP], VP),
+    "mbx_pagerank_plan_destroy": ([VP], C.c_int),
+}
+
+_lib = None
+
+
+def lib():
+    """The loaded library.  Raises (never falls back) when it is absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} not built: run __graft_entry__.build() "
+                "(make -C paper_2605_07391_b200/csrc); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return sorted(SIGNATURES)

@@ -1,0 +1,986 @@
+// capi.cu -- the extern "C" boundary (include/merbit_b200.h): handles,
+// device memory, host<->device staging, error translation, the PageRank
+// plan with its CUDA graph.  No CPU compute path exists: every SpMV /
+// TILE / PageRank result comes from the kernels in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mbx_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+namespace mbx {
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "CUDA error %s (%s) at %s:%d in %s", cudaGetErrorName(e),
+                  cudaGetErrorString(e), file, line, what);
+    throw Error{MBX_CUDA_ERROR, buf};
+  }
+}
+
+size_t value_size(int precision) { return precision == MBX_F64 ? 8 : 4; }
+
+void* scratch(mbx_context* ctx, size_t bytes) {
+  if (bytes > ctx->scratch_bytes) {
+    if (ctx->scratch) MBX_CUDA(cudaFreeAsync(ctx->scratch, ctx->stream));
+    const size_t b = std::max<size_t>(bytes, 1 << 20);
+    MBX_CUDA(cudaMallocAsync(&ctx->scratch, b, ctx->stream));
+    ctx->scratch_bytes = b;
+  }
+  return ctx->scratch;
+}
+
+Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                       int block_size) {
+  Geometry g;
+  g.n_rows = t->info.n_rows;
+  g.nnz = t->info.nnz;
+  g.lane_num = t->info.lane_num;
+  g.tile_num = t->info.tile_num;
+  g.omega = t->info.omega;
+  g.sigma = t->info.sigma;
+  g.ob = t->offset_bits;
+  g.num_chunks = (g.lane_num + 31) / 32;
+  g.chunks_per_range = std::max(1, std::min(31, block_size / 32));
+  g.num_ranges = (g.num_chunks + g.chunks_per_range - 1) / g.chunks_per_range;
+  g.warps_per_cta = ctx->tuning.warps_per_cta;
+  g.grid = ctx->sm_count * ctx->tuning.ctas_per_sm;
+  g.hub_count = 0;
+  if (m->cols_hub && m->hub_avail > 0 && g.omega == 32 && ctx->tuning.max_hubs != 0 &&
+      (ctx->tuning.max_hubs < 0 || ctx->tuning.max_hubs >= m->hub_avail)) {
+    const int slots = max_hub_slots(ctx, g.warps_per_cta, ctx->tuning.ctas_per_sm, g.sigma,
+                                    m->precision);
+    if (slots >= m->hub_avail) g.hub_count = m->hub_avail;
+  }
+  return g;
+}
+
+}  // namespace mbx
+
+using mbx::fail;
+
+namespace {
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MBX_OK;
+  } catch (const mbx::Error& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return MBX_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MBX_ERROR;
+  }
+}
+
+void require(bool ok, int code, const std::string& msg) {
+  if (!ok) fail(code, msg);
+}
+
+void check_precision(int p) {
+  require(p == MBX_F32 || p == MBX_F64, MBX_CONFIG_ERROR, "precision must be MBX_F32 or MBX_F64");
+}
+
+struct Device {
+  explicit Device(int dev) {
+    MBX_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) MBX_CUDA(cudaSetDevice(dev));
+  }
+  ~Device() {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  int prev = 0;
+};
+
+void* dmalloc(mbx_context* ctx, size_t bytes) {
+  void* p = nullptr;
+  MBX_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 256), ctx->stream));
+  return p;
+}
+void dfree(mbx_context* ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+int config_offset_bits(int omega, int sigma, int block) {
+  if (omega < 1) fail(MBX_CONFIG_ERROR, "omega must be >= 1");
+  if (sigma < 1) fail(MBX_CONFIG_ERROR, "sigma must be >= 1");
+  if (block < omega)
+    fail(MBX_CONFIG_ERROR, "block_size " + std::to_string(block) + " smaller than omega " +
+                               std::to_string(omega));
+  if (block % omega != 0)
+    fail(MBX_CONFIG_ERROR, "block_size " + std::to_string(block) + " not a multiple of omega " +
+                               std::to_string(omega));
+  int ob = 0;
+  while ((int64_t(1) << ob) < int64_t(omega) * sigma) ++ob;
+  const int bits = 2 * ob + sigma;
+  if (bits > 32)
+    fail(MBX_CONFIG_ERROR, "infeasible descriptor layout: 2*ceil_log2(omega*sigma) + sigma = 2*" +
+                               std::to_string(ob) + " + " + std::to_string(sigma) + " = " +
+                               std::to_string(bits) + " exceeds 32");
+  return ob;
+}
+
+void check_config(const mbx_simt_config* c) {
+  require(c != nullptr, MBX_CONFIG_ERROR, "null config");
+  const int ob = config_offset_bits(c->omega, c->sigma, c->block_size);
+  require(ob == c->offset_bits, MBX_CONFIG_ERROR, "offset_bits inconsistent with omega*sigma");
+}
+
+void check_tile_matches(const mbx_matrix* m, const mbx_tile* t, const mbx_simt_config* c) {
+  if (t->info.omega != c->omega || t->info.sigma != c->sigma)
+    fail(MBX_CONFIG_ERROR, "tile metadata built for omega=" + std::to_string(t->info.omega) +
+                               " sigma=" + std::to_string(t->info.sigma) +
+                               ", run requested omega=" + std::to_string(c->omega) +
+                               " sigma=" + std::to_string(c->sigma));
+  if (t->info.n_rows != m->n_rows || t->info.nnz != m->nnz)
+    fail(MBX_CONFIG_ERROR, "tile metadata shape (" + std::to_string(t->info.n_rows) + " rows, " +
+                               std::to_string(t->info.nnz) +
+                               " nnz) does not match the matrix");
+}
+
+void tile_counts(int64_t nnz, int64_t n, int omega, int sigma, int64_t* tn, int64_t* ln) {
+  const int64_t total = nnz + n;
+  const int64_t span = int64_t(omega) * sigma;
+  *ln = total == 0 ? 0 : (total + sigma - 1) / sigma;
+  *tn = total == 0 ? 0 : (total + span - 1) / span;
+}
+
+mbx_tile* new_tile(mbx_context* ctx, const mbx_simt_config& c, int64_t n_rows, int64_t nnz) {
+  auto t = std::make_unique<mbx_tile>();
+  t->ctx = ctx;
+  t->info.omega = c.omega;
+  t->info.sigma = c.sigma;
+  t->info.n_rows = n_rows;
+  t->info.nnz = nnz;
+  tile_counts(nnz, n_rows, c.omega, c.sigma, &t->info.tile_num, &t->info.lane_num);
+  t->offset_bits = c.offset_bits;
+  t->tile_x = static_cast<uint32_t*>(dmalloc(ctx, (t->info.tile_num + 1) * 4 + 64));
+  t->tile_y = static_cast<uint32_t*>(dmalloc(ctx, (t->info.tile_num + 1) * 4 + 64));
+  t->lane_desc = static_cast<uint32_t*>(dmalloc(ctx, t->info.lane_num * 4 + 256));
+  return t.release();
+}
+
+void tile_capacity(int64_t n_rows, int64_t nnz) {
+  if (n_rows >= (int64_t(1) << 31))
+    fail(MBX_CAPACITY_ERROR, "row count " + std::to_string(n_rows) +
+                                 " collides with the long-row mark bit (limit 2^31)");
+  if (nnz > int64_t(0xFFFFFFFF))
+    fail(MBX_CAPACITY_ERROR,
+         "nonzero count " + std::to_string(nnz) + " exceeds the 32-bit tile cursor");
+}
+
+void generate_tile_timed(mbx_context* ctx, const uint32_t* ro_dev, int64_t n_rows, int64_t nnz,
+                         const mbx_simt_config& c, mbx_tile* t) {
+  cudaEvent_t e0, e1;
+  MBX_CUDA(cudaEventCreate(&e0));
+  MBX_CUDA(cudaEventCreate(&e1));
+  MBX_CUDA(cudaEventRecord(e0, ctx->stream));
+  mbx::launch_generate_tile(ctx, ro_dev, n_rows, nnz, c, t);
+  MBX_CUDA(cudaEventRecord(e1, ctx->stream));
+  MBX_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  MBX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  t->info.preprocess_seconds = ms * 1e-3;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+// ---- matrix upload ---------------------------------------------------------
+mbx_matrix* upload_common(mbx_context* ctx, int precision, int64_t n_rows, int64_t n_cols,
+                          const int64_t* ro, const void* cols, bool cols64,
+                          const void* vals) {
+  check_precision(precision);
+  require(n_rows >= 0 && n_cols >= 0, MBX_DIMENSION_ERROR, "negative matrix dimensions");
+  require(n_cols < (int64_t(1) << 31), MBX_CAPACITY_ERROR,
+          "n_cols must be < 2^31 (int32 device column indices)");
+  require(ro != nullptr, MBX_DIMENSION_ERROR, "null row_offsets");
+  const int64_t nnz = ro[n_rows];
+  require(ro[0] == 0 && nnz >= 0, MBX_DIMENSION_ERROR, "row_offsets must start at 0");
+  require(nnz <= int64_t(0xFFFFFFFF), MBX_CAPACITY_ERROR,
+          "nonzero count " + std::to_string(nnz) + " exceeds the 32-bit tile cursor");
+  require(nnz == 0 || (cols && vals), MBX_DIMENSION_ERROR, "null column or value array");
+  Device dg(ctx->device);
+  auto m = std::make_unique<mbx_matrix>();
+  m->ctx = ctx;
+  m->precision = precision;
+  m->n_rows = n_rows;
+  m->n_cols = n_cols;
+  m->nnz = nnz;
+  const size_t vs = mbx::value_size(precision);
+  m->vals = dmalloc(ctx, nnz * vs + 256);
+  m->cols = static_cast<int32_t*>(dmalloc(ctx, nnz * 4 + 256));
+  m->ro = static_cast<uint32_t*>(dmalloc(ctx, (n_rows + 1) * 4 + 64));
+  MBX_CUDA(cudaMemsetAsync(m->vals, 0, nnz * vs + 256, ctx->stream));
+  MBX_CUDA(cudaMemsetAsync(m->cols, 0, nnz * 4 + 256, ctx->stream));
+  if (nnz) MBX_CUDA(cudaMemcpyAsync(m->vals, vals, nnz * vs, cudaMemcpyHostToDevice, ctx->stream));
+  int* bad = static_cast<int*>(dmalloc(ctx, 64));
+  MBX_CUDA(cudaMemsetAsync(bad, 0, 8, ctx->stream));
+  {
+    int64_t* tmp = static_cast<int64_t*>(dmalloc(ctx, (n_rows + 1) * 8));
+    MBX_CUDA(cudaMemcpyAsync(tmp, ro, (n_rows + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    mbx::launch_narrow_rows(ctx, tmp, m->ro, n_rows + 1, bad);
+    dfree(ctx, tmp);
+  }
+  if (nnz) {
+    if (cols64) {
+      int64_t* tmp = static_cast<int64_t*>(dmalloc(ctx, nnz * 8));
+      MBX_CUDA(cudaMemcpyAsync(tmp, cols, nnz * 8, cudaMemcpyHostToDevice, ctx->stream));
+      mbx::launch_narrow_cols(ctx, tmp, m->cols, nnz, n_cols, bad + 1);
+      dfree(ctx, tmp);
+    } else {
+      MBX_CUDA(cudaMemcpyAsync(m->cols, cols, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
+    }
+  }
+  int hb[2] = {0, 0};
+  MBX_CUDA(cudaMemcpyAsync(hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+  dfree(ctx, bad);
+  if (hb[0] || hb[1]) {
+    mbx_matrix* raw = m.release();
+    mbx_matrix_destroy(raw);
+    fail(MBX_DIMENSION_ERROR, hb[0] ? "row_offsets not nondecreasing / out of u32 range"
+                                    : "column index outside [0, n_cols)");
+  }
+  return m.release();
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+MBX_API const char* mbx_last_error(void) { return g_last_error.c_str(); }
+
+MBX_API const char* mbx_build_info(void) {
+  return "libmerbit_b200 (sm_100a; MERBIT TILE preprocessing, descriptor SpMV, fused PageRank)";
+}
+
+MBX_API int mbx_config_make(int omega, int sigma, int block_size, mbx_simt_config* out) {
+  return guarded([&] {
+    const int ob = config_offset_bits(omega, sigma, block_size);
+    require(out != nullptr, MBX_ERROR, "null output");
+    *out = mbx_simt_config{omega, sigma, block_size, ob};
+  });
+}
+
+MBX_API int mbx_select_sigma(int precision, int override_sigma) {
+  if (override_sigma > 0) return override_sigma;
+  return precision == MBX_F64 ? 7 : 14;
+}
+
+MBX_API int mbx_tile_counts(int64_t nnz, int64_t n_rows, const mbx_simt_config* c,
+                            int64_t* tile_num, int64_t* lane_num) {
+  return guarded([&] {
+    require(c && c->omega >= 1 && c->sigma >= 1, MBX_CONFIG_ERROR, "bad config");
+    tile_counts(nnz, n_rows, c->omega, c->sigma, tile_num, lane_num);
+  });
+}
+
+MBX_API double mbx_metadata_footprint(int64_t nnz, int64_t n_rows, const mbx_simt_config* c,
+                                      double r_f) {
+  int64_t tn = 0, ln = 0;
+  tile_counts(nnz, n_rows, c->omega, c->sigma, &tn, &ln);
+  return 8.0 * double(tn + 1) + 4.0 * double(ln) * (1.0 - r_f);
+}
+
+MBX_API int mbx_merge_search(const int64_t* ro, int64_t n_rows, int64_t nnz, int64_t diag,
+                             int64_t* x, int64_t* y) {
+  return guarded([&] {
+    if (diag < 0 || diag > nnz + n_rows)
+      fail(MBX_DIMENSION_ERROR, "merge_search: diagonal " + std::to_string(diag) +
+                                    " outside [0, " + std::to_string(nnz + n_rows) + "]");
+    int64_t lo = std::max<int64_t>(diag - nnz, 0), hi = std::min<int64_t>(diag, n_rows);
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ro[mid + 1] <= diag - mid - 1)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    *x = diag - lo;
+    *y = std::min(lo, n_rows);
+  });
+}
+
+MBX_API int mbx_plan_row_shards(const int64_t* ro, int64_t n_rows, int64_t nnz, int parts,
+                                int64_t* bounds) {
+  return guarded([&] {
+    require(parts >= 1, MBX_CONFIG_ERROR, "parts must be >= 1");
+    bounds[0] = 0;
+    for (int g = 1; g < parts; ++g) {
+      const int64_t diag = (nnz + n_rows) * g / parts;
+      int64_t x = 0, y = 0;
+      int rc = mbx_merge_search(ro, n_rows, nnz, diag, &x, &y);
+      if (rc) fail(rc, g_last_error);
+      // snap to the start of the row the cut falls in: shard g owns rows
+      // [y(d_g), y(d_{g+1})); a row is never split across GPUs.
+      bounds[g] = std::max(bounds[g - 1], y);
+    }
+    bounds[parts] = n_rows;
+  });
+}
+
+MBX_API int mbx_device_count(int* count) {
+  return guarded([&] {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+
+MBX_API int mbx_context_create(int device, mbx_context** out) {
+  return guarded([&] {
+    int n = 0;
+    MBX_CUDA(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, MBX_CUDA_ERROR,
+            "no CUDA device " + std::to_string(device) + " (have " + std::to_string(n) + ")");
+    cudaDeviceProp prop;
+    MBX_CUDA(cudaGetDeviceProperties(&prop, device));
+    require(prop.major == 10, MBX_UNSUPPORTED,
+            std::string("libmerbit_b200 is built for sm_100a; device is ") + prop.name);
+    auto ctx = std::make_unique<mbx_context>();
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    Device dg(device);
+    MBX_CUDA(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+    ctx->stream = ctx->own;
+    *out = ctx.release();
+  });
+}
+
+MBX_API int mbx_context_destroy(mbx_context* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    Device dg(ctx->device);
+    if (ctx->scratch) cudaFreeAsync(ctx->scratch, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+  });
+}
+
+MBX_API int mbx_context_set_stream(mbx_context* ctx, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    if (s != ctx->stream) {
+      // order the new stream after everything queued so far
+      cudaEvent_t ev;
+      MBX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      MBX_CUDA(cudaEventRecord(ev, ctx->stream));
+      MBX_CUDA(cudaStreamWaitEvent(s, ev, 0));
+      cudaEventDestroy(ev);
+      ctx->stream = s;
+    }
+  });
+}
+
+MBX_API void* mbx_context_stream(mbx_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+MBX_API int mbx_context_synchronize(mbx_context* ctx) {
+  return guarded([&] { MBX_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+MBX_API int64_t mbx_context_launch_count(const mbx_context* ctx) {
+  return ctx ? ctx->launches : 0;
+}
+
+MBX_API int mbx_matrix_upload(mbx_context* ctx, int precision, int64_t n_rows, int64_t n_cols,
+                              const int64_t* ro, const int64_t* cols, const void* vals,
+                              mbx_matrix** out) {
+  return guarded(
+      [&] { *out = upload_common(ctx, precision, n_rows, n_cols, ro, cols, true, vals); });
+}
+
+MBX_API int mbx_matrix_upload_i32(mbx_context* ctx, int precision, int64_t n_rows,
+                                  int64_t n_cols, const int64_t* ro, const int32_t* cols,
+                                  const void* vals, mbx_matrix** out) {
+  return guarded(
+      [&] { *out = upload_common(ctx, precision, n_rows, n_cols, ro, cols, false, vals); });
+}
+
+MBX_API int mbx_matrix_generate_rmat(mbx_context* ctx, int precision, int scale,
+                                     int edge_factor, uint64_t seed, int kind,
+                                     uint64_t value_seed, double lo, double hi,
+                                     mbx_matrix** out) {
+  return guarded([&] {
+    check_precision(precision);
+    require(scale >= 1 && scale <= 30 && edge_factor >= 1, MBX_CONFIG_ERROR,
+            "rmat: scale in [1,30], edge_factor >= 1");
+    require(kind == 0 || kind == 1, MBX_CONFIG_ERROR, "rmat kind must be 0 or 1");
+    Device dg(ctx->device);
+    auto m = std::make_unique<mbx_matrix>();
+    m->ctx = ctx;
+    mbx::generate_rmat(ctx, precision, scale, edge_factor, seed, kind, value_seed, lo, hi,
+                       m.get());
+    *out = m.release();
+  });
+}
+
+MBX_API int mbx_matrix_info(const mbx_matrix* m, int* precision, int64_t* n_rows,
+                            int64_t* n_cols, int64_t* nnz) {
+  return guarded([&] {
+    require(m != nullptr, MBX_ERROR, "null matrix");
+    if (precision) *precision = m->precision;
+    if (n_rows) *n_rows = m->n_rows;
+    if (n_cols) *n_cols = m->n_cols;
+    if (nnz) *nnz = m->nnz;
+  });
+}
+
+MBX_API int mbx_matrix_download(const mbx_matrix* m, int64_t* ro, int32_t* cols, void* vals) {
+  return guarded([&] {
+    mbx_context* ctx = m->ctx;
+    Device dg(ctx->device);
+    if (ro) {
+      std::vector<uint32_t> r(m->n_rows + 1);
+      MBX_CUDA(cudaMemcpyAsync(r.data(), m->ro, (m->n_rows + 1) * 4, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int64_t i = 0; i <= m->n_rows; ++i) ro[i] = r[i];
+    }
+    if (cols && m->nnz)
+      MBX_CUDA(cudaMemcpyAsync(cols, m->cols, m->nnz * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (vals && m->nnz)
+      MBX_CUDA(cudaMemcpyAsync(vals, m->vals, m->nnz * mbx::value_size(m->precision),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+MBX_API int mbx_matrix_device_ptrs(const mbx_matrix* m, const void** values,
+                                   const int32_t** cols, const uint32_t** ro) {
+  return guarded([&] {
+    if (values) *values = m->vals;
+    if (cols) *cols = m->cols;
+    if (ro) *ro = m->ro;
+  });
+}
+
+MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta, int ctas_per_sm,
+                                   int max_hubs) {
+  return guarded([&] {
+    require(warps_per_cta >= 1 && warps_per_cta <= 32 && ctas_per_sm >= 1 && ctas_per_sm <= 32,
+            MBX_CONFIG_ERROR, "warps_per_cta in [1,32], ctas_per_sm in [1,32]");
+    ctx->tuning.warps_per_cta = warps_per_cta;
+    ctx->tuning.ctas_per_sm = ctas_per_sm;
+    ctx->tuning.max_hubs = max_hubs;
+  });
+}
+
+MBX_API int mbx_matrix_build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs,
+                                    double* seconds) {
+  return guarded([&] {
+    Device dg(ctx->device);
+    cudaEvent_t e0, e1;
+    MBX_CUDA(cudaEventCreate(&e0));
+    MBX_CUDA(cudaEventCreate(&e1));
+    MBX_CUDA(cudaEventRecord(e0, ctx->stream));
+    mbx::build_xcache(ctx, m, max_hubs);
+    MBX_CUDA(cudaEventRecord(e1, ctx->stream));
+    MBX_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    MBX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (seconds) *seconds = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
+MBX_API int mbx_matrix_xcache_info(const mbx_matrix* m, int* hubs, double* coverage) {
+  return guarded([&] {
+    if (hubs) *hubs = m->hub_avail;
+    if (coverage) *coverage = m->hub_coverage;
+  });
+}
+
+MBX_API int mbx_matrix_destroy(mbx_matrix* m) {
+  return guarded([&] {
+    if (!m) return;
+    mbx_context* ctx = m->ctx;
+    Device dg(ctx->device);
+    dfree(ctx, m->vals);
+    dfree(ctx, m->cols);
+    dfree(ctx, m->ro);
+    dfree(ctx, m->cols_hub);
+    dfree(ctx, m->hub_cols);
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    delete m;
+  });
+}
+
+MBX_API int mbx_generate_tile(mbx_context* ctx, const int64_t* ro, int64_t n_rows, int64_t nnz,
+                              const mbx_simt_config* c, mbx_tile** out) {
+  return guarded([&] {
+    check_config(c);
+    tile_capacity(n_rows, nnz);  // before touching the data (test_format.cpp:149-158)
+    require(n_rows >= 0 && nnz >= 0, MBX_DIMENSION_ERROR, "negative sizes");
+    require(ro != nullptr || n_rows + nnz == 0, MBX_DIMENSION_ERROR, "null row_offsets");
+    Device dg(ctx->device);
+    uint32_t* ro32 = static_cast<uint32_t*>(dmalloc(ctx, (n_rows + 1) * 4 + 64));
+    int* bad = static_cast<int*>(dmalloc(ctx, 64));
+    MBX_CUDA(cudaMemsetAsync(bad, 0, 8, ctx->stream));
+    if (ro) {
+      int64_t* tmp = static_cast<int64_t*>(dmalloc(ctx, (n_rows + 1) * 8));
+      MBX_CUDA(cudaMemcpyAsync(tmp, ro, (n_rows + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+      mbx::launch_narrow_rows(ctx, tmp, ro32, n_rows + 1, bad);
+      dfree(ctx, tmp);
+    } else {
+      MBX_CUDA(cudaMemsetAsync(ro32, 0, 4, ctx->stream));
+    }
+    mbx_tile* t = new_tile(ctx, *c, n_rows, nnz);
+    generate_tile_timed(ctx, ro32, n_rows, nnz, *c, t);
+    int hb = 0;
+    MBX_CUDA(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    dfree(ctx, ro32);
+    dfree(ctx, bad);
+    if (hb) {
+      mbx_tile_destroy(t);
+      fail(MBX_DIMENSION_ERROR, "row_offsets not nondecreasing / out of u32 range");
+    }
+    *out = t;
+  });
+}
+
+MBX_API int mbx_matrix_generate_tile(mbx_context* ctx, const mbx_matrix* m,
+                                     const mbx_simt_config* c, mbx_tile** out) {
+  return guarded([&] {
+    check_config(c);
+    tile_capacity(m->n_rows, m->nnz);
+    Device dg(ctx->device);
+    mbx_tile* t = new_tile(ctx, *c, m->n_rows, m->nnz);
+    generate_tile_timed(ctx, m->ro, m->n_rows, m->nnz, *c, t);
+    *out = t;
+  });
+}
+
+MBX_API int mbx_tile_get_info(const mbx_tile* t, mbx_tile_info* info) {
+  return guarded([&] {
+    require(t != nullptr, MBX_ERROR, "null tile");
+    *info = t->info;
+  });
+}
+
+MBX_API int mbx_tile_download(const mbx_tile* t, uint32_t* tx, uint32_t* ty, uint32_t* ld) {
+  return guarded([&] {
+    mbx_context* ctx = t->ctx;
+    Device dg(ctx->device);
+    if (tx)
+      MBX_CUDA(cudaMemcpyAsync(tx, t->tile_x, (t->info.tile_num + 1) * 4, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    if (ty)
+      MBX_CUDA(cudaMemcpyAsync(ty, t->tile_y, (t->info.tile_num + 1) * 4, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    if (ld && t->info.lane_num)
+      MBX_CUDA(cudaMemcpyAsync(ld, t->lane_desc, t->info.lane_num * 4, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+MBX_API int mbx_tile_upload(mbx_context* ctx, const mbx_tile_info* info, const uint32_t* tx,
+                            const uint32_t* ty, const uint32_t* ld, mbx_tile** out) {
+  return guarded([&] {
+    mbx_simt_config c;
+    int rc = mbx_config_make(info->omega, info->sigma, info->omega, &c);
+    if (rc) fail(rc, g_last_error);
+    tile_capacity(info->n_rows, info->nnz);
+    Device dg(ctx->device);
+    mbx_tile* t = new_tile(ctx, c, info->n_rows, info->nnz);
+    t->info.preprocess_seconds = info->preprocess_seconds;
+    MBX_CUDA(cudaMemcpyAsync(t->tile_x, tx, (t->info.tile_num + 1) * 4, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    MBX_CUDA(cudaMemcpyAsync(t->tile_y, ty, (t->info.tile_num + 1) * 4, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    if (t->info.lane_num)
+      MBX_CUDA(cudaMemcpyAsync(t->lane_desc, ld, t->info.lane_num * 4, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = t;
+  });
+}
+
+MBX_API int mbx_tile_destroy(mbx_tile* t) {
+  return guarded([&] {
+    if (!t) return;
+    mbx_context* ctx = t->ctx;
+    Device dg(ctx->device);
+    dfree(ctx, t->tile_x);
+    dfree(ctx, t->tile_y);
+    dfree(ctx, t->lane_desc);
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    delete t;
+  });
+}
+
+MBX_API int mbx_spmv_device(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                            const mbx_simt_config* c, const void* x, void* y) {
+  return guarded([&] {
+    check_config(c);
+    check_tile_matches(m, t, c);
+    Device dg(ctx->device);
+    const mbx::Geometry g = mbx::make_geometry(ctx, m, t, c->block_size);
+    void* ws = mbx::scratch(ctx, mbx::spmv_workspace_bytes(g, m->precision, false));
+    mbx::launch_spmv(ctx, m, t, g, x, y, ws, nullptr);
+  });
+}
+
+MBX_API int mbx_spmv_trace_counts(mbx_context* ctx, const mbx_tile* t, mbx_spmv_trace* trace) {
+  return guarded([&] {
+    Device dg(ctx->device);
+    unsigned long long* d = static_cast<unsigned long long*>(dmalloc(ctx, 64));
+    MBX_CUDA(cudaMemsetAsync(d, 0, 24, ctx->stream));
+    mbx::launch_trace_counts(ctx, t, d);
+    unsigned long long h[3];
+    MBX_CUDA(cudaMemcpyAsync(h, d, 24, cudaMemcpyDeviceToHost, ctx->stream));
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    dfree(ctx, d);
+    trace->fast_tiles = int64_t(h[0]);
+    trace->normal_tiles = int64_t(h[1]);
+    trace->skipped_tiles = int64_t(h[2]);
+  });
+}
+
+MBX_API int mbx_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                     const mbx_simt_config* c, const void* x_host, void* y_host,
+                     mbx_spmv_trace* trace) {
+  return guarded([&] {
+    check_config(c);
+    check_tile_matches(m, t, c);
+    Device dg(ctx->device);
+    const size_t vs = mbx::value_size(m->precision);
+    void* x = dmalloc(ctx, m->n_cols * vs + 256);
+    void* y = dmalloc(ctx, m->n_rows * vs + 256);
+    if (m->n_cols) MBX_CUDA(cudaMemcpyAsync(x, x_host, m->n_cols * vs, cudaMemcpyHostToDevice, ctx->stream));
+    const mbx::Geometry g = mbx::make_geometry(ctx, m, t, c->block_size);
+    void* ws = mbx::scratch(ctx, mbx::spmv_workspace_bytes(g, m->precision, false));
+    mbx::launch_spmv(ctx, m, t, g, x, y, ws, nullptr);
+    if (m->n_rows) MBX_CUDA(cudaMemcpyAsync(y_host, y, m->n_rows * vs, cudaMemcpyDeviceToHost, ctx->stream));
+    dfree(ctx, x);
+    dfree(ctx, y);
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (trace) {
+      int rc = mbx_spmv_trace_counts(ctx, t, trace);
+      if (rc) fail(rc, g_last_error);
+    }
+  });
+}
+
+MBX_API int mbx_spmv_csr_device(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y) {
+  return guarded([&] {
+    Device dg(ctx->device);
+    mbx::launch_csr(ctx, m, x, y, nullptr, nullptr, nullptr);
+  });
+}
+
+}  // extern "C"
+
+// ============================================================================
+// PageRank plan
+// ============================================================================
+struct mbx_pagerank_plan_s {
+  mbx_context* ctx = nullptr;
+  const mbx_matrix* p = nullptr;
+  const mbx_tile* t = nullptr;
+  mbx_simt_config c{};
+  mbx_pagerank_config cfg{};
+  mbx::Geometry g;
+  int64_t n = 0;
+  size_t vs = 4;
+  void* pi[2] = {nullptr, nullptr};
+  void* ref[2] = {nullptr, nullptr};
+  uint32_t* dangling = nullptr;
+  mbx::PrScalars* scal = nullptr;      // [max_iters + 1]
+  mbx::PrScalars* ref_scal = nullptr;  // [reference_iters + 1]
+  double* range_part = nullptr;
+  double* block_part = nullptr;
+  unsigned int* counter = nullptr;
+  int* flags = nullptr;  // [0] stop, [1] stop_iter
+  void* carry_ws = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int64_t graph_launches = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bool ran = false;
+};
+
+namespace {
+
+mbx::PrArgs pr_args(mbx_pagerank_plan* pl, int64_t r, const void* yard) {
+  mbx::PrArgs a;
+  a.pi_old = pl->pi[(r - 1) & 1];
+  a.dangling = pl->dangling;
+  a.yardstick = yard;
+  a.yard_const = pl->p->precision == MBX_F32 ? double(1.0f / float(pl->n)) : 1.0 / double(pl->n);
+  a.damping = pl->cfg.damping;
+  a.inv_n = 1.0 / double(pl->n);
+  a.prev = pl->scal + (r - 1);
+  a.next = pl->scal + r;
+  a.range_part = pl->range_part;
+  a.block_part = pl->block_part;
+  a.done_counter = pl->counter;
+  a.stop = pl->flags;
+  a.stop_iter = pl->flags + 1;
+  a.iter = int(r);
+  a.err_tol = pl->cfg.err_tol;
+  return a;
+}
+
+void launch_power_loop(mbx_pagerank_plan* pl) {
+  const void* yard = pl->cfg.reference_iters > 0 ? pl->ref[pl->cfg.reference_iters & 1] : nullptr;
+  for (int64_t r = 1; r <= pl->cfg.max_iters; ++r) {
+    const mbx::PrArgs a = pr_args(pl, r, yard);
+    mbx::launch_spmv(pl->ctx, pl->p, pl->t, pl->g, pl->pi[(r - 1) & 1], pl->pi[r & 1],
+                     pl->carry_ws, &a);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, const mbx_tile* t,
+                                     const mbx_simt_config* c, const mbx_pagerank_config* cfg,
+                                     mbx_pagerank_plan** out) {
+  return guarded([&] {
+    if (p->n_rows != p->n_cols) fail(MBX_DIMENSION_ERROR, "pagerank needs a square transition matrix");
+    if (p->n_rows < 1) fail(MBX_DIMENSION_ERROR, "pagerank needs at least one vertex");
+    if (!(cfg->damping >= 0.0 && cfg->damping <= 1.0)) fail(MBX_CONFIG_ERROR, "damping must lie in [0, 1]");
+    if (!(cfg->err_tol > 0.0)) fail(MBX_CONFIG_ERROR, "err_tol must be positive");
+    require(cfg->max_iters >= 0 && cfg->reference_iters >= 0, MBX_CONFIG_ERROR,
+            "iteration counts must be >= 0");
+    check_config(c);
+    check_tile_matches(p, t, c);
+    Device dg(ctx->device);
+    auto pl = std::make_unique<mbx_pagerank_plan>();
+    pl->ctx = ctx;
+    pl->p = p;
+    pl->t = t;
+    pl->c = *c;
+    pl->cfg = *cfg;
+    if (p->precision == MBX_F32) {
+      // PageRankConfig<float> stores damping / err_tol as float
+      pl->cfg.damping = double(float(cfg->damping));
+      pl->cfg.err_tol = double(float(cfg->err_tol));
+    }
+    pl->g = mbx::make_geometry(ctx, p, t, c->block_size);
+    pl->n = p->n_rows;
+    pl->vs = mbx::value_size(p->precision);
+    for (int i = 0; i < 2; ++i) pl->pi[i] = dmalloc(ctx, pl->n * pl->vs + 256);
+    if (cfg->reference_iters > 0)
+      for (int i = 0; i < 2; ++i) pl->ref[i] = dmalloc(ctx, pl->n * pl->vs + 256);
+    pl->dangling = static_cast<uint32_t*>(dmalloc(ctx, ((pl->n + 31) / 32) * 4 + 64));
+    mbx::launch_dangling_mask(ctx, p, pl->dangling);
+    pl->scal = static_cast<mbx::PrScalars*>(dmalloc(ctx, (cfg->max_iters + 1) * sizeof(mbx::PrScalars)));
+    pl->ref_scal = static_cast<mbx::PrScalars*>(
+        dmalloc(ctx, (cfg->reference_iters + 1) * sizeof(mbx::PrScalars)));
+    MBX_CUDA(cudaMemsetAsync(pl->scal, 0, (cfg->max_iters + 1) * sizeof(mbx::PrScalars), ctx->stream));
+    pl->range_part = static_cast<double*>(dmalloc(ctx, (pl->g.num_ranges + 1) * 4 * sizeof(double)));
+    const int64_t k3_blocks = (pl->g.num_ranges + 255) / 256 + 1;
+    const int64_t nb = std::max<int64_t>({k3_blocks, int64_t(mbx::csr_pr_blocks(ctx, p)),
+                                          int64_t(ctx->sm_count) * 4 + 1});
+    pl->block_part = static_cast<double*>(dmalloc(ctx, nb * 4 * sizeof(double)));
+    pl->counter = static_cast<unsigned int*>(dmalloc(ctx, 64));
+    pl->flags = static_cast<int*>(dmalloc(ctx, 64));
+    MBX_CUDA(cudaMemsetAsync(pl->counter, 0, 64, ctx->stream));
+    pl->carry_ws = dmalloc(ctx, mbx::spmv_workspace_bytes(pl->g, p->precision, true));
+    MBX_CUDA(cudaEventCreate(&pl->e0));
+    MBX_CUDA(cudaEventCreate(&pl->e1));
+    // Capture the whole fixed-count power loop once as a CUDA graph.
+    if (cfg->max_iters > 0 && cfg->max_iters <= 4096) {
+      MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+      const int64_t before = ctx->launches;
+      cudaGraph_t graph;
+      MBX_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        launch_power_loop(pl.get());
+      } catch (...) {
+        cudaStreamEndCapture(ctx->stream, &graph);
+        throw;
+      }
+      MBX_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+      MBX_CUDA(cudaGraphInstantiate(&pl->graph, graph, 0));
+      cudaGraphDestroy(graph);
+      pl->graph_launches = ctx->launches - before;
+      ctx->launches = before;
+    }
+    *out = pl.release();
+  });
+}
+
+MBX_API int mbx_pagerank_plan_run(mbx_pagerank_plan* pl, const void* pi0) {
+  return guarded([&] {
+    mbx_context* ctx = pl->ctx;
+    Device dg(ctx->device);
+    MBX_CUDA(cudaMemsetAsync(pl->flags, 0, 8, ctx->stream));
+    // Yardstick: fixed-count power run on the plain CSR kernel (178-191).
+    if (pl->cfg.reference_iters > 0) {
+      mbx::launch_pr_init(ctx, pl->p->precision, pl->n, nullptr, pl->ref[0], pl->dangling,
+                          pl->ref_scal, pl->block_part, pl->counter);
+      for (int64_t r = 1; r <= pl->cfg.reference_iters; ++r) {
+        mbx::PrArgs a;
+        a.pi_old = pl->ref[(r - 1) & 1];
+        a.dangling = pl->dangling;
+        a.yard_const = 1.0;
+        a.damping = pl->cfg.damping;
+        a.inv_n = 1.0 / double(pl->n);
+        a.prev = pl->ref_scal + (r - 1);
+        a.next = pl->ref_scal + r;
+        mbx::launch_csr(ctx, pl->p, pl->ref[(r - 1) & 1], pl->ref[r & 1], &a, pl->block_part,
+                        pl->counter);
+      }
+    }
+    mbx::launch_pr_init(ctx, pl->p->precision, pl->n, pi0, pl->pi[0], pl->dangling, pl->scal,
+                        pl->block_part, pl->counter);
+    MBX_CUDA(cudaEventRecord(pl->e0, ctx->stream));
+    if (pl->graph) {
+      MBX_CUDA(cudaGraphLaunch(pl->graph, ctx->stream));
+      ctx->launches += pl->graph_launches;
+    } else {
+      launch_power_loop(pl);
+    }
+    MBX_CUDA(cudaEventRecord(pl->e1, ctx->stream));
+    pl->ran = true;
+  });
+}
+
+MBX_API int mbx_pagerank_plan_result(mbx_pagerank_plan* pl, mbx_pagerank_result* res,
+                                     double* history) {
+  return guarded([&] {
+    require(pl->ran, MBX_ERROR, "plan has not run");
+    mbx_context* ctx = pl->ctx;
+    Device dg(ctx->device);
+    int flags[2];
+    MBX_CUDA(cudaMemcpyAsync(flags, pl->flags, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<mbx::PrScalars> sc(pl->cfg.max_iters + 1);
+    MBX_CUDA(cudaMemcpyAsync(sc.data(), pl->scal, sc.size() * sizeof(mbx::PrScalars),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int64_t iters = flags[0] ? flags[1] : pl->cfg.max_iters;
+    if (flags[0] == 2)
+      fail(MBX_ERROR, "pagerank: zero-norm iterate at iteration " + std::to_string(iters));
+    float ms = 0.f;
+    MBX_CUDA(cudaEventElapsedTime(&ms, pl->e0, pl->e1));
+    res->iterations = iters;
+    res->status = flags[0] == 1 ? 0 : 1;
+    res->final_err = iters > 0 ? sc[iters].err : std::numeric_limits<double>::infinity();
+    res->preprocess_seconds = pl->t->info.preprocess_seconds;
+    res->iterate_seconds = ms * 1e-3;
+    res->l1_residual = iters > 0 ? sc[iters].resid : 0.0;
+    res->mass = sc[iters].mass;
+    res->dangling_mass = sc[iters].dangling;
+    if (history)
+      for (int64_t r = 1; r <= pl->cfg.max_iters; ++r)
+        history[r - 1] = r <= iters ? sc[r].resid : 0.0;
+  });
+}
+
+MBX_API const void* mbx_pagerank_plan_pi(const mbx_pagerank_plan* pl) {
+  // The final iterate of the last run: pi[iterations & 1].  Synchronous read
+  // of the stop flag so early exits resolve to the right buffer.
+  if (!pl) return nullptr;
+  int flags[2] = {0, 0};
+  if (cudaMemcpyAsync(flags, pl->flags, 8, cudaMemcpyDeviceToHost, pl->ctx->stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(pl->ctx->stream) != cudaSuccess)
+    return nullptr;
+  const int64_t iters = flags[0] ? flags[1] : pl->cfg.max_iters;
+  return pl->pi[iters & 1];
+}
+
+MBX_API const void* mbx_pagerank_plan_reference_pi(const mbx_pagerank_plan* pl) {
+  if (!pl || pl->cfg.reference_iters == 0) return nullptr;
+  return pl->ref[pl->cfg.reference_iters & 1];
+}
+
+MBX_API int mbx_pagerank_plan_destroy(mbx_pagerank_plan* pl) {
+  return guarded([&] {
+    if (!pl) return;
+    mbx_context* ctx = pl->ctx;
+    Device dg(ctx->device);
+    if (pl->graph) cudaGraphExecDestroy(pl->graph);
+    for (void* b : {pl->pi[0], pl->pi[1], pl->ref[0], pl->ref[1]}) dfree(ctx, b);
+    dfree(ctx, pl->dangling);
+    dfree(ctx, pl->scal);
+    dfree(ctx, pl->ref_scal);
+    dfree(ctx, pl->range_part);
+    dfree(ctx, pl->block_part);
+    dfree(ctx, pl->counter);
+    dfree(ctx, pl->flags);
+    dfree(ctx, pl->carry_ws);
+    if (pl->e0) cudaEventDestroy(pl->e0);
+    if (pl->e1) cudaEventDestroy(pl->e1);
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    delete pl;
+  });
+}
+
+MBX_API int mbx_pagerank(mbx_context* ctx, const mbx_matrix* p, const mbx_tile* t,
+                         const mbx_simt_config* c, const mbx_pagerank_config* cfg,
+                         const void* pi0_host, void* pi_host, void* ref_host, double* history,
+                         mbx_pagerank_result* result) {
+  return guarded([&] {
+    mbx_pagerank_plan* pl = nullptr;
+    int rc = mbx_pagerank_plan_create(ctx, p, t, c, cfg, &pl);
+    if (rc) fail(rc, g_last_error);
+    std::unique_ptr<mbx_pagerank_plan, int (*)(mbx_pagerank_plan*)> guard(pl, mbx_pagerank_plan_destroy);
+    Device dg(ctx->device);
+    void* pi0 = nullptr;
+    if (pi0_host) {
+      pi0 = dmalloc(ctx, pl->n * pl->vs);
+      MBX_CUDA(cudaMemcpyAsync(pi0, pi0_host, pl->n * pl->vs, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    rc = mbx_pagerank_plan_run(pl, pi0);
+    if (rc) fail(rc, g_last_error);
+    rc = mbx_pagerank_plan_result(pl, result, history);
+    if (rc) fail(rc, g_last_error);
+    if (pi_host)
+      MBX_CUDA(cudaMemcpyAsync(pi_host, pl->pi[result->iterations & 1], pl->n * pl->vs,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    if (ref_host) {
+      if (cfg->reference_iters > 0) {
+        MBX_CUDA(cudaMemcpyAsync(ref_host, pl->ref[cfg->reference_iters & 1], pl->n * pl->vs,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+      } else {
+        // zero-iteration yardstick: the uniform start vector
+        if (p->precision == MBX_F32) {
+          float* r = static_cast<float*>(ref_host);
+          for (int64_t i = 0; i < pl->n; ++i) r[i] = 1.0f / float(pl->n);
+        } else {
+          double* r = static_cast<double*>(ref_host);
+          for (int64_t i = 0; i < pl->n; ++i) r[i] = 1.0 / double(pl->n);
+        }
+      }
+    }
+    dfree(ctx, pi0);
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,1017 @@
+// kernels.cu -- the sm_100a kernels of the MERBIT hot path.
+//
+//  K1 gen_tile_kernel      generate_tile (src/tile.cpp:17-85; paper Alg. 2)
+//  K2 spmv_w32_kernel      spmv_merbit tile loop (merbit_spmv.hpp:182-324;
+//     spmv_generic_kernel  paper Alg. 3-5), commit fused with the PageRank
+//                          update (solvers.hpp:99-115) in PR mode
+//  K3 fixup_kernel         ordered boundary-carry fold (merbit_spmv.hpp:
+//                          328-337) + PageRank scalar finalisation
+//  csr_kernel              spmv_csr_reference (reference.hpp:15-46): the
+//                          pagerank yardstick (solvers.hpp:178-191)
+//
+// Design: SpMV is HBM-bound integer/fp gather work, so no
+// tensor cores.  Values/columns stream once with 128-bit non-allocating
+// loads tagged L2 evict-first; x is gathered through the read-only path and
+// kept L2-resident (evict-normal); every row of y is ASSIGNED exactly once
+// (interior rows by the warp that closes them, boundary rows by K3), so no
+// zero-fill, no atomics, and bitwise run-to-run determinism.
+#include <cfloat>
+#include <cmath>
+
+#include "mbx_internal.h"
+
+namespace mbx {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kThreads = 256;  // K2 CTA: 8 warps
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// 16-byte streaming loads (values / columns are touched exactly once).
+__device__ __forceinline__ void ld_stream16(const float* p, float (&v)[4], uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+               : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld_stream16(const double* p, double (&v)[2], uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(v[0]), "=d"(v[1])
+               : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld_cols(const int32_t* p, int (&c)[4], uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3])
+               : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld_cols(const int32_t* p, int (&c)[2], uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+               : "=r"(c[0]), "=r"(c[1])
+               : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+template <typename T>
+struct VecOf {
+  static constexpr int N = 16 / sizeof(T);
+};
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Product staging: values[p] * x[col[p]] for p in [x0, x1).  ACCUM: return
+// this lane's running sum (fast path, merbit_spmv.hpp:58-77); else store
+// products to buf[p - x0] (merbit_spmv.hpp:244-249).  Lanes own aligned
+// 16-byte vectors, so the element->lane map is a pure function of x0.
+// ---------------------------------------------------------------------------
+template <typename T, bool ACCUM, int MAXV, bool HUB>
+__device__ __forceinline__ T stage_products(const T* __restrict__ vals,
+                                            const int32_t* __restrict__ cols,
+                                            const T* __restrict__ x, const T* hub,
+                                            int64_t x0, int64_t x1, T* buf, int lid,
+                                            uint64_t pol) {
+  constexpr int N = VecOf<T>::N;
+  const int64_t a0 = x0 & ~int64_t(N - 1);
+  const int nvec = static_cast<int>((x1 - a0 + N - 1) / N);
+  T acc = T(0);
+#pragma unroll
+  for (int it = 0; it < MAXV; ++it) {
+    const int v = lid + 32 * it;
+    if (v < nvec) {
+      const int64_t base = a0 + int64_t(v) * N;
+      T val[N];
+      int col[N];
+      ld_stream16(vals + base, val, pol);
+      ld_cols(cols + base, col, pol);
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        const int64_t idx = base + e;
+        if (idx >= x0 && idx < x1) {
+          // hub columns (sign bit set) are served from shared memory; the
+          // rest are gathered through the read-only path
+          T xv;
+          if (HUB)
+            xv = col[e] < 0 ? hub[col[e] & 0x7FFFFFFF] : __ldg(x + col[e]);
+          else
+            xv = __ldg(x + col[e]);
+          const T p = val[e] * xv;
+          if (ACCUM)
+            acc += p;
+          else
+            buf[idx - x0] = p;
+        }
+      }
+    }
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------------------
+// PageRank commit of one finished row w = (P pi_old)[row]:
+//   pi_new = damping * w + base  (rank_update, solvers.hpp:99-115)
+// plus the fused reductions (fp64): L1 residual, dangling mass of pi_new
+// (feeds the next iteration's base), mass (zero-norm check, 201-206) and
+// ERR vs the yardstick (rank_error, 118-131).
+// ---------------------------------------------------------------------------
+struct PrAcc {
+  double resid = 0.0, dang = 0.0, mass = 0.0, err = 0.0;
+};
+
+template <typename T>
+__device__ __forceinline__ void pr_commit(const PrArgs& pr, T base, int64_t row,
+                                          T w, T* __restrict__ out, PrAcc& a) {
+  const T pn = static_cast<T>(pr.damping) * w + base;
+  const T po = reinterpret_cast<const T*>(pr.pi_old)[row];
+  out[row] = pn;
+  a.resid += fabs(static_cast<double>(pn) - static_cast<double>(po));
+  if ((pr.dangling[row >> 5] >> (row & 31)) & 1u) a.dang += static_cast<double>(pn);
+  a.mass += fabs(static_cast<double>(pn));
+  const double s = pr.yardstick ? static_cast<double>(
+                                      reinterpret_cast<const T*>(pr.yardstick)[row])
+                                : pr.yard_const;
+  const double d = static_cast<double>(pn) - s;
+  if (s == 0.0) {
+    if (d != 0.0) a.err = INFINITY;
+  } else {
+    a.err = fmax(a.err, fabs(d / s));
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T pr_base(const PrArgs& pr) {
+  // base = (damping * dangling_mass + 1 - damping) / n, in fp64 then T
+  return static_cast<T>((pr.damping * pr.prev->dangling + (1.0 - pr.damping)) * pr.inv_n);
+}
+
+// Deterministic block reduction of PrAcc (fixed butterfly + fixed warp order)
+// followed by the last-block finalisation into *out.
+__device__ void pr_block_finish(PrAcc a, const PrArgs& pr, double* block_part,
+                                unsigned int* counter, PrScalars* out, bool check_stop) {
+  __shared__ double sm[4][32];
+  __shared__ bool is_last;
+  a.resid = warp_sum(a.resid);
+  a.dang = warp_sum(a.dang);
+  a.mass = warp_sum(a.mass);
+  a.err = warp_max(a.err);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  if (l == 0) {
+    sm[0][w] = a.resid;
+    sm[1][w] = a.dang;
+    sm[2][w] = a.mass;
+    sm[3][w] = a.err;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0, d = 0, m = 0, e = 0;
+    for (int i = 0; i < nw; ++i) {
+      r += sm[0][i];
+      d += sm[1][i];
+      m += sm[2][i];
+      e = fmax(e, sm[3][i]);
+    }
+    double* bp = block_part + 4 * blockIdx.x;
+    bp[0] = r;
+    bp[1] = d;
+    bp[2] = m;
+    bp[3] = e;
+    __threadfence();
+    const unsigned int prev = atomicAdd(counter, 1u);
+    is_last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  PrAcc t;
+  for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+    const volatile double* bp = block_part + 4 * b;
+    t.resid += bp[0];
+    t.dang += bp[1];
+    t.mass += bp[2];
+    t.err = fmax(t.err, bp[3]);
+  }
+  t.resid = warp_sum(t.resid);
+  t.dang = warp_sum(t.dang);
+  t.mass = warp_sum(t.mass);
+  t.err = warp_max(t.err);
+  __syncthreads();
+  if (l == 0) {
+    sm[0][w] = t.resid;
+    sm[1][w] = t.dang;
+    sm[2][w] = t.mass;
+    sm[3][w] = t.err;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0, d = 0, m = 0, e = 0;
+    for (int i = 0; i < nw; ++i) {
+      r += sm[0][i];
+      d += sm[1][i];
+      m += sm[2][i];
+      e = fmax(e, sm[3][i]);
+    }
+    out->resid = r;
+    out->dangling = d;
+    out->mass = m;
+    out->err = e;
+    if (check_stop && pr.stop) {
+      if (m == 0.0) {
+        *pr.stop = 2;  // zero-norm iterate (solvers.hpp:202-205)
+        *pr.stop_iter = pr.iter;
+      } else if (e < pr.err_tol) {
+        *pr.stop = 1;  // converged (solvers.hpp:210-213)
+        *pr.stop_iter = pr.iter;
+      }
+    }
+    *counter = 0;  // ready for the next launch
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2, omega == 32: one warp walks `chunks_per_range` consecutive tiles.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct SpmvParams {
+  const T* vals;
+  const int32_t* cols;
+  const T* x;
+  T* y;
+  const uint32_t* tile_x;
+  const uint32_t* tile_y;
+  const uint32_t* lane_desc;
+  const int32_t* hub_cols;
+  uint32_t* carry_row;
+  T* carry_val;
+  Geometry g;
+  PrArgs pr;
+};
+
+// Per-lane MERBIT walk of the lane's sigma steps (paper Alg. 4,
+// merbit_spmv.hpp:251-297) + warp segmented sum (Alg. 5, 85-117), with the
+// carry of the previous tile entering at lane 0.  Rows closed inside the
+// chunk land in buf[cnt + row - y0]; returns the new carry (open row y1).
+template <typename T, int SIGMA>
+__device__ __forceinline__ T lane_walk_and_scan(T* buf, int cnt, int sigma, uint32_t d,
+                                                int steps, int ob, int lid, T carry,
+                                                int xo, int r0) {
+  const uint32_t flags = d >> (2 * ob);
+  int r = r0;
+  T sum = T(0), head = T(0);
+  bool had_down = false;
+  const int S = SIGMA > 0 ? SIGMA : sigma;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    if (k < steps) {
+      if ((flags >> k) & 1u) {
+        if (!had_down) {
+          head = sum;  // first closure: the row may extend into earlier lanes
+          had_down = true;
+        } else {
+          buf[cnt + r] = sum;  // row opened and closed inside this lane
+        }
+        sum = T(0);
+        ++r;
+      } else {
+        sum += buf[xo++];
+      }
+    }
+  }
+  T tail = sum;
+  if (lid == 0) {
+    if (had_down)
+      head += carry;
+    else
+      tail += carry;
+  }
+  // inclusive segmented scan of the trailing sums (flag = lane closed a row)
+  T S_ = tail;
+  bool F = had_down;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const T su = __shfl_up_sync(kFull, S_, off);
+    const bool fu = __shfl_up_sync(kFull, F, off);
+    if (lid >= off && !F) {
+      S_ += su;
+      F = fu;
+    }
+  }
+  const T prevS = __shfl_up_sync(kFull, S_, 1);
+  if (had_down) buf[cnt + r0] = head + (lid > 0 ? prevS : T(0));
+  return __shfl_sync(kFull, S_, 31);
+}
+
+// One warp range: `chunks_per_range` consecutive tiles (chunk == tile here).
+template <typename T, int SIGMA, bool PR, bool HUB>
+__device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, T* buf,
+                                          int64_t range, int lid, uint64_t pol, T base) {
+  const Geometry& g = p.g;
+  const int sigma = SIGMA > 0 ? SIGMA : g.sigma;
+  const int64_t c0 = range * g.chunks_per_range;
+  const int nc = static_cast<int>(imin64(c0 + g.chunks_per_range, g.num_chunks) - c0);
+  const int64_t total = g.nnz + g.n_rows;
+  const int ob = g.ob;
+  const uint32_t omask = (1u << ob) - 1u;
+  constexpr int MAXV = SIGMA > 0 ? (32 * SIGMA + 2 * VecOf<T>::N + 31) / (32 * VecOf<T>::N) + 1 : 8;
+
+  // tile cursors of this range, one coalesced load
+  uint32_t mtx = 0, mty = 0;
+  if (lid <= nc) {
+    mtx = ld_stream_u32(p.tile_x + c0 + lid, pol);
+    mty = ld_stream_u32(p.tile_y + c0 + lid, pol);
+  }
+  const uint32_t head_row = __shfl_sync(kFull, mty, 0) & ~kLongRowMask;
+  const uint32_t tail_row = __shfl_sync(kFull, mty, nc) & ~kLongRowMask;
+  T carry = T(0), head_val = T(0);
+  bool head_open = true;
+  PrAcc acc;
+
+  for (int ci = 0; ci < nc; ++ci) {
+    const int64_t c = c0 + ci;
+    const uint32_t x0 = __shfl_sync(kFull, mtx, ci);
+    const uint32_t x1 = __shfl_sync(kFull, mtx, ci + 1);
+    const uint32_t ty0 = __shfl_sync(kFull, mty, ci);
+    const uint32_t y0 = ty0 & ~kLongRowMask;
+    const uint32_t y1 = __shfl_sync(kFull, mty, ci + 1) & ~kLongRowMask;
+    const int cnt = static_cast<int>(x1 - x0);
+    const int nrows = static_cast<int>(y1 - y0);
+    if (ty0 & kLongRowMask) {
+      // long-row tile: every step Right, one row (merbit_spmv.hpp:230-237)
+      T s = stage_products<T, true, MAXV, HUB>(p.vals, p.cols, p.x, hub, x0, x1, buf, lid, pol);
+      carry += warp_sum(s);
+      continue;
+    }
+    if (cnt == 0) {
+      // no nonzero: every step closes a row (merbit_spmv.hpp:217-224); the
+      // first closes the carried row, the rest are empty rows.
+      for (int k = lid; k < nrows; k += 32) buf[k] = k == 0 ? carry : T(0);
+      carry = T(0);
+    } else {
+      stage_products<T, false, MAXV, HUB>(p.vals, p.cols, p.x, hub, x0, x1, buf, lid, pol);
+      const int64_t j = c * 32 + lid;
+      const bool valid = j < g.lane_num;
+      const uint32_t d = valid ? ld_stream_u32(p.lane_desc + j, pol) : 0u;
+      const int steps = valid ? static_cast<int>(imin64(sigma, total - j * sigma)) : 0;
+      __syncwarp();
+      carry = lane_walk_and_scan<T, SIGMA>(buf, cnt, sigma, d, steps, ob, lid, carry,
+                                           static_cast<int>(d & omask),
+                                           static_cast<int>((d >> ob) & omask));
+    }
+    __syncwarp();
+    // coalesced commit of the rows closed in this tile (Alg. 6 load_mem)
+    for (int k = lid; k < nrows; k += 32) {
+      const T w = buf[cnt + k];
+      if (k == 0 && head_open) {
+        head_val = w;  // range head row: may continue from the previous range
+        continue;
+      }
+      const int64_t row = int64_t(y0) + k;
+      if (PR)
+        pr_commit<T>(p.pr, base, row, w, p.y, acc);
+      else
+        p.y[row] = w;
+    }
+    if (nrows > 0) head_open = false;
+    __syncwarp();
+  }
+  if (lid == 0) {
+    p.carry_row[2 * range] = head_row;
+    p.carry_val[2 * range] = head_open ? T(0) : head_val;
+    p.carry_row[2 * range + 1] = tail_row;
+    p.carry_val[2 * range + 1] = carry;
+  }
+  if (PR) {
+    acc.resid = warp_sum(acc.resid);
+    acc.dang = warp_sum(acc.dang);
+    acc.mass = warp_sum(acc.mass);
+    acc.err = warp_max(acc.err);
+    if (lid == 0) {
+      double* rp = p.pr.range_part + 4 * range;
+      rp[0] = acc.resid;
+      rp[1] = acc.dang;
+      rp[2] = acc.mass;
+      rp[3] = acc.err;
+    }
+  }
+}
+
+// K2, omega == 32: persistent CTAs; the x hub table is staged once per CTA,
+// then each warp strides over ranges (all ranges carry equal merge-path work).
+template <typename T, int SIGMA, bool PR, bool HUB>
+__global__ void __launch_bounds__(1024) spmv_w32_kernel(SpmvParams<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geometry& g = p.g;
+  const int sigma = SIGMA > 0 ? SIGMA : g.sigma;
+  if (PR && *p.pr.stop) return;
+  const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
+  T* hub = reinterpret_cast<T*>(smem_raw);
+  const int hub_pad = HUB ? ((g.hub_count + 3) & ~3) : 0;
+  T* buf = hub + hub_pad + size_t(warp) * (32 * sigma + 1);
+  if (HUB) {
+    for (int i = threadIdx.x; i < g.hub_count; i += blockDim.x) hub[i] = __ldg(p.x + p.hub_cols[i]);
+    __syncthreads();
+  }
+  const uint64_t pol = evict_first_policy();
+  T base = T(0);
+  if (PR) base = pr_base<T>(p.pr);
+  const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t range = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp; range < g.num_ranges;
+       range += wstride)
+    w32_range<T, SIGMA, PR, HUB>(p, hub, buf, range, lid, pol, base);
+}
+
+// ---------------------------------------------------------------------------
+// K2, any omega: lanes locate themselves through their own tile entry
+// (lane start = tile start + descriptor offsets).  No fast/skip routing;
+// used for the reference's small test configurations (omega = 4, ...).
+// ---------------------------------------------------------------------------
+template <typename T, bool PR>
+__global__ void __launch_bounds__(kThreads) spmv_generic_kernel(SpmvParams<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geometry& g = p.g;
+  const int sigma = g.sigma;
+  const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
+  const int64_t range = int64_t(blockIdx.x) * g.warps_per_cta + warp;
+  if (range >= g.num_ranges) return;
+  if (PR && *p.pr.stop) return;
+  T* buf = reinterpret_cast<T*>(smem_raw) + size_t(warp) * (32 * sigma + 1);
+  const uint64_t pol = evict_first_policy();
+  const int64_t c0 = range * g.chunks_per_range;
+  const int nc = static_cast<int>(imin64(c0 + g.chunks_per_range, g.num_chunks) - c0);
+  const int64_t total = g.nnz + g.n_rows;
+  const int ob = g.ob;
+  const uint32_t omask = (1u << ob) - 1u;
+
+  T carry = T(0), head_val = T(0);
+  bool head_open = true;
+  T base = T(0);
+  PrAcc acc;
+  if (PR) base = pr_base<T>(p.pr);
+  uint32_t head_row = 0, y1 = 0;
+
+  for (int ci = 0; ci < nc; ++ci) {
+    const int64_t j = (c0 + ci) * 32 + lid;
+    const bool valid = j < g.lane_num;
+    int64_t lx = g.nnz, ly = g.n_rows;
+    uint32_t d = 0;
+    int steps = 0;
+    if (valid) {
+      const int64_t tile = j / g.omega;
+      d = p.lane_desc[j];
+      lx = int64_t(p.tile_x[tile]) + (d & omask);
+      ly = int64_t(p.tile_y[tile] & ~kLongRowMask) + ((d >> ob) & omask);
+      steps = static_cast<int>(imin64(sigma, total - j * sigma));
+    }
+    const uint32_t flags = d >> (2 * ob);
+    const int live = steps >= 32 ? -1 : int((1u << steps) - 1u);
+    const int downs = __popc(flags & uint32_t(live));
+    const int rights = steps - downs;
+    const int64_t x0 = __shfl_sync(kFull, lx, 0);
+    const int64_t yy0 = __shfl_sync(kFull, ly, 0);
+    const int64_t x1 = __shfl_sync(kFull, lx + rights, 31);
+    const int64_t yy1 = __shfl_sync(kFull, ly + downs, 31);
+    if (ci == 0) head_row = static_cast<uint32_t>(yy0);
+    y1 = static_cast<uint32_t>(yy1);
+    const int cnt = static_cast<int>(x1 - x0);
+    const int nrows = static_cast<int>(yy1 - yy0);
+    stage_products<T, false, 12, false>(p.vals, p.cols, p.x, nullptr, x0, x1, buf, lid, pol);
+    __syncwarp();
+    carry = lane_walk_and_scan<T, 0>(buf, cnt, sigma, d, steps, ob, lid, carry,
+                                      static_cast<int>(lx - x0), static_cast<int>(ly - yy0));
+    __syncwarp();
+    for (int k = lid; k < nrows; k += 32) {
+      const T w = buf[cnt + k];
+      if (k == 0 && head_open) {
+        head_val = w;
+        continue;
+      }
+      const int64_t row = yy0 + k;
+      if (PR)
+        pr_commit<T>(p.pr, base, row, w, p.y, acc);
+      else
+        p.y[row] = w;
+    }
+    if (nrows > 0) head_open = false;
+    __syncwarp();
+  }
+  if (lid == 0) {
+    p.carry_row[2 * range] = head_row;
+    p.carry_val[2 * range] = head_open ? T(0) : head_val;
+    p.carry_row[2 * range + 1] = y1;
+    p.carry_val[2 * range + 1] = carry;
+  }
+  if (PR) {
+    acc.resid = warp_sum(acc.resid);
+    acc.dang = warp_sum(acc.dang);
+    acc.mass = warp_sum(acc.mass);
+    acc.err = warp_max(acc.err);
+    if (lid == 0) {
+      double* rp = p.pr.range_part + 4 * range;
+      rp[0] = acc.resid;
+      rp[1] = acc.dang;
+      rp[2] = acc.mass;
+      rp[3] = acc.err;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: boundary rows.  Carries are ordered by range, rows nondecreasing; each
+// run of equal rows is summed left to right (ascending block order, exactly
+// the reference's fold order) and ASSIGNED; the terminal row n is dropped.
+// ---------------------------------------------------------------------------
+template <typename T, bool PR>
+__global__ void __launch_bounds__(256) fixup_kernel(const uint32_t* __restrict__ crow,
+                                                    const T* __restrict__ cval,
+                                                    int64_t num_ranges, int64_t n_rows,
+                                                    T* __restrict__ y, PrArgs pr) {
+  if (PR && *pr.stop) return;
+  const int64_t rg = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t ne = 2 * num_ranges;
+  PrAcc acc;
+  T base = T(0);
+  if (PR) base = pr_base<T>(pr);
+  if (rg < num_ranges) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int64_t e = 2 * rg + s;
+      const uint32_t r = crow[e];
+      if (e > 0 && crow[e - 1] == r) continue;
+      T sum = T(0);
+      for (int64_t k = e; k < ne && crow[k] == r; ++k) sum += cval[k];
+      if (int64_t(r) < n_rows) {
+        if (PR)
+          pr_commit<T>(pr, base, r, sum, y, acc);
+        else
+          y[r] = sum;
+      }
+    }
+    if (PR) {
+      const double* rp = pr.range_part + 4 * rg;
+      acc.resid += rp[0];
+      acc.dang += rp[1];
+      acc.mass += rp[2];
+      acc.err = fmax(acc.err, rp[3]);
+    }
+  }
+  if (PR) pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, true);
+}
+
+// ---------------------------------------------------------------------------
+// K1: generate_tile.  One thread per lane: merge_search on its diagonal
+// (merge_path.cpp:8-36), the sigma-step walk (tile.cpp:59-69), the packed
+// descriptor (descriptor.hpp:31-43); the tile's lane group votes the
+// long-row mark (tile.cpp:75-77).  Arrays are byte-identical to the
+// reference.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void d_merge_search(const uint32_t* __restrict__ ro, int64_t n,
+                                               int64_t m, int64_t diag, int64_t& x,
+                                               int64_t& y) {
+  int64_t lo = diag - m > 0 ? diag - m : 0;
+  int64_t hi = diag < n ? diag : n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (int64_t(__ldg(ro + mid + 1)) <= diag - mid - 1)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  x = diag - lo;
+  y = lo < n ? lo : n;
+}
+
+__global__ void gen_tile_kernel(const uint32_t* __restrict__ ro, int64_t n, int64_t m,
+                                int omega, int sigma, int ob, int64_t lane_num,
+                                uint32_t* __restrict__ tile_x, uint32_t* __restrict__ tile_y,
+                                uint32_t* __restrict__ lane_desc, int small_omega) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lid = threadIdx.x & 31;
+  const bool valid = j < lane_num;
+  const int64_t total = m + n;
+  int64_t x = 0, y = 0;
+  const int64_t diag = j * sigma;
+  if (valid) d_merge_search(ro, n, m, diag, x, y);
+  int64_t tsx, tsy;
+  int leader = 0;
+  if (small_omega) {
+    leader = lid & ~(omega - 1);
+    tsx = __shfl_sync(kFull, x, leader);
+    tsy = __shfl_sync(kFull, y, leader);
+  } else {
+    tsx = tsy = 0;
+    if (valid) d_merge_search(ro, n, m, (j / omega) * int64_t(omega) * sigma, tsx, tsy);
+  }
+  uint32_t flags = 0;
+  if (valid) {
+    const int64_t steps = imin64(sigma, total - diag);
+    int64_t cx = x, cy = y;
+    int64_t end = cy < n ? int64_t(__ldg(ro + cy + 1)) : 0;
+    for (int64_t k = 0; k < steps; ++k) {
+      if (cy < n && cx < end) {
+        ++cx;
+      } else {
+        flags |= 1u << k;
+        ++cy;
+        end = cy < n ? int64_t(__ldg(ro + cy + 1)) : 0;
+      }
+    }
+    lane_desc[j] = (flags << (2 * ob)) | (uint32_t(y - tsy) << ob) | uint32_t(x - tsx);
+  }
+  if (small_omega) {
+    const unsigned ballot = __ballot_sync(kFull, valid && flags != 0u);
+    const unsigned gmask = omega >= 32 ? kFull : ((1u << omega) - 1u);
+    const bool any_down = ((ballot >> leader) & gmask) != 0u;
+    if (valid && lid == leader) {
+      tile_x[j / omega] = uint32_t(tsx);
+      tile_y[j / omega] = uint32_t(tsy) | (any_down ? 0u : kLongRowMask);
+    }
+  }
+}
+
+// omega not dividing 32: tile entries from the tile's first lane and an OR
+// over the tile's descriptor flags.
+__global__ void gen_tile_entries_kernel(const uint32_t* __restrict__ ro, int64_t n, int64_t m,
+                                        int omega, int sigma, int ob, int64_t lane_num,
+                                        int64_t tile_num, uint32_t* __restrict__ tile_x,
+                                        uint32_t* __restrict__ tile_y,
+                                        const uint32_t* __restrict__ lane_desc) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= tile_num) return;
+  int64_t x, y;
+  d_merge_search(ro, n, m, t * int64_t(omega) * sigma, x, y);
+  bool any_down = false;
+  for (int64_t j = t * omega; j < imin64((t + 1) * omega, lane_num); ++j)
+    any_down |= (lane_desc[j] >> (2 * ob)) != 0u;
+  tile_x[t] = uint32_t(x);
+  tile_y[t] = uint32_t(y) | (any_down ? 0u : kLongRowMask);
+}
+
+__global__ void tile_terminal_kernel(uint32_t* tile_x, uint32_t* tile_y, int64_t tile_num,
+                                     int64_t m, int64_t n) {
+  tile_x[tile_num] = uint32_t(m);
+  tile_y[tile_num] = uint32_t(n);  // never marked (tile.cpp:80-83)
+}
+
+// Routing counters with the kernel's predicate (merbit_spmv.hpp:217-237).
+__global__ void trace_kernel(const uint32_t* __restrict__ tile_x,
+                             const uint32_t* __restrict__ tile_y, int64_t tile_num,
+                             unsigned long long* counters) {
+  __shared__ unsigned long long s[3];
+  if (threadIdx.x < 3) s[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < tile_num) {
+    const uint32_t xs = tile_x[i + 1] - tile_x[i];
+    const int k = xs == 0 ? 2 : ((tile_y[i] & kLongRowMask) ? 0 : 1);
+    atomicAdd(&s[k], 1ull);
+  }
+  __syncthreads();
+  if (threadIdx.x < 3 && s[threadIdx.x]) atomicAdd(&counters[threadIdx.x], s[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// Plain CSR (warp per row, fp64 accumulation): the pagerank yardstick and a
+// non-MERBIT comparator.
+// ---------------------------------------------------------------------------
+template <typename T, bool PR>
+__global__ void __launch_bounds__(256) csr_kernel(const uint32_t* __restrict__ ro,
+                                                  const int32_t* __restrict__ cols,
+                                                  const T* __restrict__ vals,
+                                                  const T* __restrict__ x, T* __restrict__ y,
+                                                  int64_t n_rows, PrArgs pr) {
+  const int lid = threadIdx.x & 31;
+  const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  PrAcc acc;
+  T base = T(0);
+  if (PR) base = pr_base<T>(pr);
+  for (int64_t r = wid; r < n_rows; r += nwarps) {
+    double s = 0.0;
+    for (uint32_t k = ro[r] + lid; k < ro[r + 1]; k += 32)
+      s += double(vals[k]) * double(__ldg(x + cols[k]));
+    s = warp_sum(s);
+    if (lid == 0) {
+      if (PR)
+        pr_commit<T>(pr, base, r, T(s), y, acc);
+      else
+        y[r] = T(s);
+    }
+  }
+  if (PR) pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, false);
+}
+
+// pi_0 (copy or uniform) and its dangling mass.
+template <typename T>
+__global__ void pr_init_kernel(const T* __restrict__ pi0, T* __restrict__ pi, int64_t n,
+                               PrArgs pr) {
+  PrAcc acc;
+  const T u = T(1) / static_cast<T>(n);  // T(1)/static_cast<T>(n) (solvers.hpp:193)
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const T v = pi0 ? pi0[i] : u;
+    pi[i] = v;
+    if ((pr.dangling[i >> 5] >> (i & 31)) & 1u) acc.dang += double(v);
+    acc.mass += fabs(double(v));
+  }
+  pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, false);
+}
+
+__global__ void seen_columns_kernel(const int32_t* __restrict__ cols, int64_t nnz,
+                                    uint32_t* seen) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t c = uint32_t(cols[k]);
+    const uint32_t bit = 1u << (c & 31);
+    if (!(__ldg(seen + (c >> 5)) & bit)) atomicOr(seen + (c >> 5), bit);
+  }
+}
+
+__global__ void invert_mask_kernel(uint32_t* mask, int64_t n) {
+  const int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t words = (n + 31) / 32;
+  if (w >= words) return;
+  uint32_t v = ~mask[w];
+  const int64_t lim = n - w * 32;
+  if (lim < 32) v &= (1u << lim) - 1u;
+  mask[w] = v;
+}
+
+__global__ void narrow_cols_kernel(const int64_t* __restrict__ src, int32_t* __restrict__ dst,
+                                   int64_t n, int64_t limit, int* bad) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t v = src[i];
+    if (v < 0 || v >= limit) *bad = 1;
+    dst[i] = int32_t(v);
+  }
+}
+
+__global__ void narrow_rows_kernel(const int64_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                   int64_t n, int* bad) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t v = src[i];
+    if (v < 0 || v > int64_t(0xFFFFFFFF) || (i > 0 && src[i - 1] > v)) *bad = 1;
+    dst[i] = uint32_t(v);
+  }
+}
+
+inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148LL * 64) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return static_cast<unsigned>(b);
+}
+
+template <typename T, int SIGMA, bool PR, bool HUB>
+void launch_w32(mbx_context* ctx, const SpmvParams<T>& p, size_t smem) {
+  auto kern = spmv_w32_kernel<T, SIGMA, PR, HUB>;
+  static int configured = -1;
+  if (configured != ctx->device) {
+    int optin = 0;
+    MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    MBX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    configured = ctx->device;
+  }
+  const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
+  const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));
+  kern<<<grid, p.g.warps_per_cta * 32, smem, ctx->stream>>>(p);
+}
+
+template <typename T, bool PR>
+void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                   const Geometry& g, const void* x, void* y, void* ws, const PrArgs* pr) {
+  if (g.num_ranges == 0) return;
+  SpmvParams<T> p;
+  p.vals = static_cast<const T*>(m->vals);
+  p.cols = g.hub_count > 0 ? m->cols_hub : m->cols;
+  p.hub_cols = m->hub_cols;
+  p.x = static_cast<const T*>(x);
+  p.y = static_cast<T*>(y);
+  p.tile_x = t->tile_x;
+  p.tile_y = t->tile_y;
+  p.lane_desc = t->lane_desc;
+  p.g = g;
+  const int64_t ne = 2 * g.num_ranges;
+  p.carry_row = static_cast<uint32_t*>(ws);
+  const size_t row_bytes = ((ne * 4 + 255) / 256) * 256;
+  p.carry_val = reinterpret_cast<T*>(static_cast<char*>(ws) + row_bytes);
+  if (pr) p.pr = *pr;
+  if (g.omega == 32) {
+    const size_t smem = spmv_smem_bytes(g, m->precision);
+    constexpr int kDefSigma = sizeof(T) == 4 ? 14 : 7;
+    if (g.hub_count > 0) {
+      if (g.sigma == kDefSigma)
+        launch_w32<T, kDefSigma, PR, true>(ctx, p, smem);
+      else
+        launch_w32<T, 0, PR, true>(ctx, p, smem);
+    } else {
+      if (g.sigma == kDefSigma)
+        launch_w32<T, kDefSigma, PR, false>(ctx, p, smem);
+      else
+        launch_w32<T, 0, PR, false>(ctx, p, smem);
+    }
+  } else {
+    p.g.warps_per_cta = kThreads / 32;
+    const size_t smem = size_t(p.g.warps_per_cta) * (32 * g.sigma + 1) * sizeof(T);
+    const unsigned grid =
+        static_cast<unsigned>((g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta);
+    spmv_generic_kernel<T, PR><<<grid, kThreads, smem, ctx->stream>>>(p);
+  }
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+  const unsigned fgrid = static_cast<unsigned>((g.num_ranges + 255) / 256);
+  fixup_kernel<T, PR><<<fgrid, 256, 0, ctx->stream>>>(p.carry_row, p.carry_val,
+                                                     g.num_ranges, g.n_rows, p.y, p.pr);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+size_t spmv_smem_bytes(const Geometry& g, int precision) {
+  const size_t vs = value_size(precision);
+  const size_t hub = g.hub_count > 0 ? size_t((g.hub_count + 3) & ~3) : 0;
+  return (hub + size_t(g.warps_per_cta) * (32 * g.sigma + 1)) * vs;
+}
+
+int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, int sigma,
+                  int precision) {
+  int per_sm = 0, optin = 0;
+  MBX_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                                  ctx->device));
+  MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  const int64_t reserve = 1024;  // per-CTA system reservation
+  int64_t per_cta = per_sm / ctas_per_sm - reserve;
+  if (per_cta > optin) per_cta = optin;
+  const int64_t vs = int64_t(value_size(precision));
+  const int64_t bufs = int64_t(warps_per_cta) * (32 * sigma + 1) * vs;
+  const int64_t slots = (per_cta - bufs) / vs - 4;
+  return slots > 0 ? int(slots & ~int64_t(3)) : 0;
+}
+
+size_t spmv_workspace_bytes(const Geometry& g, int precision, bool pagerank) {
+  const int64_t ne = 2 * g.num_ranges;
+  size_t b = ((ne * 4 + 255) / 256) * 256 + ((ne * value_size(precision) + 255) / 256) * 256;
+  (void)pagerank;
+  return b + 256;
+}
+
+void launch_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, const Geometry& g,
+                 const void* x, void* y, void* ws, const PrArgs* pr) {
+  if (m->precision == MBX_F32) {
+    if (pr)
+      launch_spmv_t<float, true>(ctx, m, t, g, x, y, ws, pr);
+    else
+      launch_spmv_t<float, false>(ctx, m, t, g, x, y, ws, nullptr);
+  } else {
+    if (pr)
+      launch_spmv_t<double, true>(ctx, m, t, g, x, y, ws, pr);
+    else
+      launch_spmv_t<double, false>(ctx, m, t, g, x, y, ws, nullptr);
+  }
+}
+
+void launch_generate_tile(mbx_context* ctx, const uint32_t* ro, int64_t n_rows, int64_t nnz,
+                          const mbx_simt_config& c, mbx_tile* t) {
+  const int64_t lanes = t->info.lane_num, tiles = t->info.tile_num;
+  const bool small = c.omega <= 32 && (32 % c.omega) == 0;
+  if (lanes > 0) {
+    const int64_t blocks = (lanes + 255) / 256;
+    gen_tile_kernel<<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(
+        ro, n_rows, nnz, c.omega, c.sigma, c.offset_bits, lanes, t->tile_x, t->tile_y,
+        t->lane_desc, small ? 1 : 0);
+    ++ctx->launches;
+    MBX_CUDA(cudaGetLastError());
+    if (!small) {
+      gen_tile_entries_kernel<<<static_cast<unsigned>((tiles + 255) / 256), 256, 0,
+                                ctx->stream>>>(ro, n_rows, nnz, c.omega, c.sigma,
+                                               c.offset_bits, lanes, tiles, t->tile_x,
+                                               t->tile_y, t->lane_desc);
+      ++ctx->launches;
+      MBX_CUDA(cudaGetLastError());
+    }
+  }
+  tile_terminal_kernel<<<1, 1, 0, ctx->stream>>>(t->tile_x, t->tile_y, tiles, nnz, n_rows);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
+void launch_trace_counts(mbx_context* ctx, const mbx_tile* t, unsigned long long* counters) {
+  const int64_t tiles = t->info.tile_num;
+  if (tiles == 0) return;
+  trace_kernel<<<static_cast<unsigned>((tiles + 255) / 256), 256, 0, ctx->stream>>>(
+      t->tile_x, t->tile_y, tiles, counters);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
+int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m) {
+  return static_cast<int>(grid_for(m->n_rows * 32, 256, int64_t(ctx->sm_count) * 8));
+}
+
+void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
+                const PrArgs* pr, double* cta_part, unsigned int* counter) {
+  if (m->n_rows == 0) return;
+  const unsigned grid = static_cast<unsigned>(csr_pr_blocks(ctx, m));
+  PrArgs a;
+  if (pr) {
+    a = *pr;
+    a.block_part = cta_part;
+    a.done_counter = counter;
+  }
+  if (m->precision == MBX_F32) {
+    if (pr)
+      csr_kernel<float, true><<<grid, 256, 0, ctx->stream>>>(
+          m->ro, m->cols, static_cast<const float*>(m->vals), static_cast<const float*>(x),
+          static_cast<float*>(y), m->n_rows, a);
+    else
+      csr_kernel<float, false><<<grid, 256, 0, ctx->stream>>>(
+          m->ro, m->cols, static_cast<const float*>(m->vals), static_cast<const float*>(x),
+          static_cast<float*>(y), m->n_rows, a);
+  } else {
+    if (pr)
+      csr_kernel<double, true><<<grid, 256, 0, ctx->stream>>>(
+          m->ro, m->cols, static_cast<const double*>(m->vals), static_cast<const double*>(x),
+          static_cast<double*>(y), m->n_rows, a);
+    else
+      csr_kernel<double, false><<<grid, 256, 0, ctx->stream>>>(
+          m->ro, m->cols, static_cast<const double*>(m->vals), static_cast<const double*>(x),
+          static_cast<double*>(y), m->n_rows, a);
+  }
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
+void launch_pr_init(mbx_context* ctx, int precision, int64_t n, const void* pi0, void* pi,
+                    const uint32_t* dangling, PrScalars* out, double* block_part,
+                    unsigned int* counter) {
+  PrArgs a;
+  a.dangling = dangling;
+  a.next = out;
+  a.block_part = block_part;
+  a.done_counter = counter;
+  const unsigned grid = grid_for(n, 256, int64_t(ctx->sm_count) * 4);
+  if (precision == MBX_F32)
+    pr_init_kernel<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(pi0),
+                                                         static_cast<float*>(pi), n, a);
+  else
+    pr_init_kernel<double><<<grid, 256, 0, ctx->stream>>>(static_cast<const double*>(pi0),
+                                                          static_cast<double*>(pi), n, a);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
+void launch_dangling_mask(mbx_context* ctx, const mbx_matrix* m, uint32_t* mask) {
+  const int64_t words = (m->n_cols + 31) / 32;
+  MBX_CUDA(cudaMemsetAsync(mask, 0, size_t(words > 0 ? words : 1) * 4, ctx->stream));
+  if (m->nnz > 0) {
+    seen_columns_kernel<<<grid_for(m->nnz, 256), 256, 0, ctx->stream>>>(m->cols, m->nnz, mask);
+    ++ctx->launches;
+  }
+  if (words > 0) {
+    invert_mask_kernel<<<static_cast<unsigned>((words + 255) / 256), 256, 0, ctx->stream>>>(
+        mask, m->n_cols);
+    ++ctx->launches;
+  }
+  MBX_CUDA(cudaGetLastError());
+}
+
+void launch_narrow_cols(mbx_context* ctx, const int64_t* src, int32_t* dst, int64_t n,
+                        int64_t limit, int* bad) {
+  if (n == 0) return;
+  narrow_cols_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(src, dst, n, limit, bad);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
+void launch_narrow_rows(mbx_context* ctx, const int64_t* src, uint32_t* dst, int64_t n,
+                        int* bad) {
+  if (n == 0) return;
+  narrow_rows_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(src, dst, n, bad);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
+}  // namespace mbx

@@ -1,0 +1,158 @@
+// mbx_internal.h -- shared internals of libmerbit_b200.so (not installed).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "merbit_b200.h"
+
+namespace mbx {
+
+// Status carrier used inside the library; the C ABI converts it to an int
+// plus the thread-local message (capi.cu).
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+
+#define MBX_CUDA(call) ::mbx::cuda_check((call), #call, __FILE__, __LINE__)
+
+constexpr uint32_t kLongRowMask = 0x80000000u;  // tile.hpp:38
+
+// Kernel-side geometry of one SpMV launch.  A "chunk" is 32 consecutive
+// lanes (one warp's worth, = one tile when omega == 32); a "range" is
+// `chunks_per_range` consecutive chunks walked by one warp with its running
+// row partial kept in registers.  Ranges are the unit whose boundary rows go
+// through the carry table (the reference's per-block carries,
+// merbit_spmv.hpp:119-127).
+struct Geometry {
+  int64_t n_rows = 0, nnz = 0, lane_num = 0, tile_num = 0;
+  int64_t num_chunks = 0, num_ranges = 0;
+  int omega = 32, sigma = 14, ob = 9, chunks_per_range = 4;
+  int warps_per_cta = 8;
+  // persistent launch: grid = sm_count * ctas_per_sm, warps stride over ranges
+  int grid = 0;
+  // x hub cache: the first hub_count entries of the column-frequency order
+  // are staged in shared memory; encoded columns (sign bit) address them.
+  int hub_count = 0;
+};
+
+// Launch tuning knobs (context-wide; see mbx_context_set_tuning).
+struct Tuning {
+  int warps_per_cta = 16;
+  int ctas_per_sm = 2;
+  int max_hubs = -1;  // -1: fill the shared-memory budget; 0: disable
+};
+
+// Device-side reduction slots of one fused PageRank iteration.
+struct PrScalars {
+  double dangling;  // sum of pi over dangling vertices
+  double resid;     // sum |pi_new - pi_old|
+  double mass;      // sum |pi_new|
+  double err;       // max |pi_new - pi*| / pi*  (inf rules of rank_error)
+};
+
+struct PrArgs {
+  const void* pi_old = nullptr;        // x of this iteration
+  const uint32_t* dangling = nullptr;  // bit r set <=> vertex r dangling
+  const void* yardstick = nullptr;     // pi*; NULL => constant yard_const
+  double yard_const = 0.0;
+  double damping = 0.85;
+  double inv_n = 0.0;
+  const PrScalars* prev = nullptr;  // scalars of pi_old (dangling mass)
+  PrScalars* next = nullptr;        // scalars of pi_new (written by K3)
+  double* range_part = nullptr;     // 4 doubles per range (K2 -> K3)
+  double* block_part = nullptr;     // 4 doubles per K3 block
+  unsigned int* done_counter = nullptr;
+  int* stop = nullptr;         // set once converged / failed
+  int* stop_iter = nullptr;    // iteration that set stop
+  int iter = 0;                // 1-based
+  double err_tol = 0.0;
+};
+
+}  // namespace mbx
+
+struct mbx_context_s {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  // growable scratch (carry table etc.), stream-ordered reuse
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  void* host_scratch = nullptr;  // pinned staging
+  size_t host_scratch_bytes = 0;
+  mbx::Tuning tuning;
+};
+
+struct mbx_matrix_s {
+  mbx_context* ctx = nullptr;
+  int precision = MBX_F32;
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  void* vals = nullptr;        // T[nnz] (+ pad)
+  int32_t* cols = nullptr;     // int32[nnz] (+ pad)
+  uint32_t* ro = nullptr;      // u32[n_rows+1]
+  // x hub cache (mbx_matrix_build_xcache): hub_cols lists the most
+  // referenced columns in descending frequency; cols_hub is cols with every
+  // reference to hub slot s < hub_avail rewritten as (INT32_MIN | s).
+  int32_t* cols_hub = nullptr;
+  int32_t* hub_cols = nullptr;
+  int hub_avail = 0;
+  double hub_coverage = 0.0;  // fraction of nonzeros that reference a hub
+};
+
+struct mbx_tile_s {
+  mbx_context* ctx = nullptr;
+  mbx_tile_info info{};
+  int offset_bits = 0;
+  uint32_t* tile_x = nullptr;
+  uint32_t* tile_y = nullptr;
+  uint32_t* lane_desc = nullptr;
+};
+
+namespace mbx {
+
+size_t value_size(int precision);
+void* scratch(mbx_context* ctx, size_t bytes);
+void* host_scratch(mbx_context* ctx, size_t bytes);
+Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                       int block_size);
+size_t spmv_smem_bytes(const Geometry& g, int precision);
+int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, int sigma,
+                  int precision);
+void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs);
+
+// ---- kernels (kernels.cu) ----
+void launch_generate_tile(mbx_context* ctx, const uint32_t* ro, int64_t n_rows,
+                          int64_t nnz, const mbx_simt_config& c, mbx_tile* t);
+void launch_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                 const Geometry& g, const void* x, void* y, void* carry_ws,
+                 const PrArgs* pr);
+size_t spmv_workspace_bytes(const Geometry& g, int precision, bool pagerank);
+void launch_trace_counts(mbx_context* ctx, const mbx_tile* t,
+                         unsigned long long* counters_dev);
+void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
+                const PrArgs* pr, double* cta_part, unsigned int* counter);
+int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m);
+void launch_pr_init(mbx_context* ctx, int precision, int64_t n,
+                    const void* pi0, void* pi, const uint32_t* dangling,
+                    PrScalars* out, double* block_part, unsigned int* counter);
+void launch_dangling_mask(mbx_context* ctx, const mbx_matrix* m,
+                          uint32_t* mask_words);
+void launch_narrow_cols(mbx_context* ctx, const int64_t* src, int32_t* dst,
+                        int64_t n, int64_t limit, int* bad_flag);
+void launch_narrow_rows(mbx_context* ctx, const int64_t* src, uint32_t* dst,
+                        int64_t n, int* bad_flag);
+
+// ---- generators (generators.cu) ----
+void generate_rmat(mbx_context* ctx, int precision, int scale,
+                   int edge_factor, uint64_t seed, int kind,
+                   uint64_t value_seed, double lo, double hi, mbx_matrix* m);
+
+}  // namespace mbx

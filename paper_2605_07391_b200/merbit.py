@@ -1,0 +1,595 @@
+"""Host-side mirror of the reference API for the MERBIT path, over the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/merbit (the C++ mirror for C++ callers is
+include/merbit_b200/merbit.hpp).  Every compute call goes through
+libmerbit_b200.so on the GPU; nothing here computes on the CPU.
+
+    SimtConfig.make / select_sigma          config.hpp:18-42, src/config.cpp
+    generate_tile -> Tile (TileMetadata)    tile.hpp:27-58, src/tile.cpp:17-85
+    spmv_merbit(.., DualBuffer, trace)      merbit_spmv.hpp:136-352
+    SpmvBackend / MerbitB200Backend         backend.hpp:22-34, 112-136
+    make_backend / BackendKind              backend.hpp:138-169
+    pagerank -> PageRankResult              solvers.hpp:76-218
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import (mbx_pagerank_config, mbx_pagerank_result, mbx_simt_config,
+                   mbx_spmv_trace, mbx_tile_info)
+
+F32, F64 = 0, 1
+
+
+# ---------------------------------------------------------------------------
+# error taxonomy (include/merbit/types.hpp:23-65)
+# ---------------------------------------------------------------------------
+class MerbitError(RuntimeError):
+    code = 1
+
+
+class IoError(MerbitError):
+    code = 2
+
+
+class ParseError(MerbitError):
+    code = 3
+
+
+class ConfigError(MerbitError):
+    code = 4
+
+
+class DimensionError(MerbitError):
+    code = 5
+
+
+class CapacityError(MerbitError):
+    code = 6
+
+
+class CorruptionError(MerbitError):
+    code = 7
+
+
+class CudaError(MerbitError):
+    code = 8
+
+
+class NcclError(MerbitError):
+    code = 9
+
+
+class UnsupportedError(MerbitError):
+    code = 10
+
+
+_ERRORS = {c.code: c for c in (MerbitError, IoError, ParseError, ConfigError, DimensionError,
+                                CapacityError, CorruptionError, CudaError, NcclError,
+                                UnsupportedError)}
+
+
+def _check(rc):
+    if rc != 0:
+        msg = _lib.lib().mbx_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, MerbitError)(msg)
+
+
+def _precision_of(dtype) -> int:
+    dt = np.dtype(dtype)
+    if dt == np.float32:
+        return F32
+    if dt == np.float64:
+        return F64
+    raise ConfigError(f"unsupported value dtype {dt}")
+
+
+def _dtype_of(precision: int):
+    return np.float32 if precision == F32 else np.float64
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+# ---------------------------------------------------------------------------
+# SimtConfig (config.hpp:18-42)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class SimtConfig:
+    omega: int = 32
+    sigma: int = 14
+    block_size: int = 128
+    offset_bits: int = 9
+
+    @staticmethod
+    def make(omega: int, sigma: int, block_size: int) -> "SimtConfig":
+        c = mbx_simt_config()
+        _check(_lib.lib().mbx_config_make(omega, sigma, block_size, C.byref(c)))
+        return SimtConfig(c.omega, c.sigma, c.block_size, c.offset_bits)
+
+    def warps_per_block(self) -> int:
+        return self.block_size // self.omega
+
+    def steps_per_tile(self) -> int:
+        return self.omega * self.sigma
+
+    def steps_per_block(self) -> int:
+        return self.block_size * self.sigma
+
+    def _c(self) -> mbx_simt_config:
+        return mbx_simt_config(self.omega, self.sigma, self.block_size, self.offset_bits)
+
+
+def select_sigma(precision: str, override: int | None = None) -> int:
+    return _lib.lib().mbx_select_sigma(1 if precision == "f64" else 0, override or 0)
+
+
+def tile_counts(nnz: int, n_rows: int, c: SimtConfig):
+    t, l = C.c_int64(), C.c_int64()
+    cc = c._c()
+    _check(_lib.lib().mbx_tile_counts(nnz, n_rows, C.byref(cc), C.byref(t), C.byref(l)))
+    return t.value, l.value
+
+
+def metadata_footprint(nnz: int, n_rows: int, c: SimtConfig, r_f: float) -> float:
+    cc = c._c()
+    return _lib.lib().mbx_metadata_footprint(nnz, n_rows, C.byref(cc), r_f)
+
+
+def merge_search(row_offsets, n_rows: int, nnz: int, diag: int):
+    ro = np.ascontiguousarray(row_offsets, np.int64)
+    x, y = C.c_int64(), C.c_int64()
+    _check(_lib.lib().mbx_merge_search(_ptr(ro), n_rows, nnz, diag, C.byref(x), C.byref(y)))
+    return x.value, y.value
+
+
+def plan_row_shards(row_offsets, n_rows: int, nnz: int, parts: int) -> np.ndarray:
+    ro = np.ascontiguousarray(row_offsets, np.int64)
+    out = np.zeros(parts + 1, np.int64)
+    _check(_lib.lib().mbx_plan_row_shards(_ptr(ro), n_rows, nnz, parts, _ptr(out)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# context / matrices
+# ---------------------------------------------------------------------------
+def device_count() -> int:
+    n = C.c_int()
+    _check(_lib.lib().mbx_device_count(C.byref(n)))
+    return n.value
+
+
+class Context:
+    """One device + one stream (not thread-safe, like the reference backends)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        _check(_lib.lib().mbx_context_create(device, C.byref(h)))
+        self.h = h
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(_lib.lib().mbx_context_set_stream(self.h, stream_ptr))
+
+    @property
+    def stream(self) -> int:
+        return _lib.lib().mbx_context_stream(self.h) or 0
+
+    def synchronize(self):
+        _check(_lib.lib().mbx_context_synchronize(self.h))
+
+    def set_tuning(self, warps_per_cta: int = 16, ctas_per_sm: int = 2, max_hubs: int = -1):
+        """K2 launch shape (persistent grid) and x hub-cache cap (-1 auto, 0 off)."""
+        _check(_lib.lib().mbx_context_set_tuning(self.h, warps_per_cta, ctas_per_sm, max_hubs))
+
+    @property
+    def launch_count(self) -> int:
+        return _lib.lib().mbx_context_launch_count(self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lib().mbx_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class DeviceMatrix:
+    """A CsrMatrix<T> (csr.hpp:29-38) resident on the device."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self.h = handle
+        p, nr, nc, nnz = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
+        _check(_lib.lib().mbx_matrix_info(self.h, C.byref(p), C.byref(nr), C.byref(nc),
+                                          C.byref(nnz)))
+        self.precision, self.n_rows, self.n_cols, self.nnz = p.value, nr.value, nc.value, nnz.value
+
+    @property
+    def dtype(self):
+        return _dtype_of(self.precision)
+
+    @classmethod
+    def upload(cls, ctx: Context, n_rows, n_cols, row_offsets, col_indices, values):
+        ro = np.ascontiguousarray(row_offsets, np.int64)
+        vals = np.ascontiguousarray(values)
+        prec = _precision_of(vals.dtype)
+        h = C.c_void_p()
+        cols = np.asarray(col_indices)
+        if cols.dtype == np.int64:
+            cols = np.ascontiguousarray(cols)
+            _check(_lib.lib().mbx_matrix_upload(ctx.h, prec, n_rows, n_cols, _ptr(ro), _ptr(cols),
+                                                _ptr(vals), C.byref(h)))
+        else:
+            cols = np.ascontiguousarray(cols, np.int32)
+            _check(_lib.lib().mbx_matrix_upload_i32(ctx.h, prec, n_rows, n_cols, _ptr(ro),
+                                                    _ptr(cols), _ptr(vals), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_csr(cls, ctx: Context, a):
+        """`a` has n_rows, n_cols, row_offsets, col_indices, values (e.g. oracle.Csr)."""
+        return cls.upload(ctx, a.n_rows, a.n_cols, a.row_offsets, a.col_indices, a.values)
+
+    @classmethod
+    def rmat(cls, ctx: Context, scale: int, edge_factor: int = 16, seed: int = 1,
+             transition: bool = False, dtype=np.float32, value_seed: int = 2,
+             lo: float = 0.0, hi: float = 1.0):
+        h = C.c_void_p()
+        _check(_lib.lib().mbx_matrix_generate_rmat(ctx.h, _precision_of(dtype), scale,
+                                                   edge_factor, seed, 1 if transition else 0,
+                                                   value_seed, lo, hi, C.byref(h)))
+        return cls(ctx, h)
+
+    def download(self, want_values=True):
+        ro = np.zeros(self.n_rows + 1, np.int64)
+        cols = np.zeros(max(self.nnz, 1), np.int32)
+        vals = np.zeros(max(self.nnz, 1), self.dtype) if want_values else None
+        _check(_lib.lib().mbx_matrix_download(self.h, _ptr(ro), _ptr(cols), _ptr(vals)))
+        return ro, cols[:self.nnz], (vals[:self.nnz] if want_values else None)
+
+    def build_xcache(self, max_hubs: int = -1) -> float:
+        """Rank columns by reference count and stage the hottest x entries in
+        shared memory during SpMV (results bitwise unchanged).  Returns seconds."""
+        secs = C.c_double()
+        _check(_lib.lib().mbx_matrix_build_xcache(self.ctx.h, self.h, max_hubs, C.byref(secs)))
+        return secs.value
+
+    def xcache_info(self):
+        hubs, cov = C.c_int(), C.c_double()
+        _check(_lib.lib().mbx_matrix_xcache_info(self.h, C.byref(hubs), C.byref(cov)))
+        return hubs.value, cov.value
+
+    def device_ptrs(self):
+        v, c, r = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(_lib.lib().mbx_matrix_device_ptrs(self.h, C.byref(v), C.byref(c), C.byref(r)))
+        return v.value, c.value, r.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lib().mbx_matrix_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# TILE (tile.hpp:27-58)
+# ---------------------------------------------------------------------------
+class Tile:
+    """Device-resident TileMetadata."""
+
+    kLongRowMask = 0x80000000
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self.h = handle
+        info = mbx_tile_info()
+        _check(_lib.lib().mbx_tile_get_info(self.h, C.byref(info)))
+        self.omega, self.sigma = info.omega, info.sigma
+        self.n_rows, self.nnz = info.n_rows, info.nnz
+        self.tile_num, self.lane_num = info.tile_num, info.lane_num
+        self.preprocess_seconds = info.preprocess_seconds
+
+    def download(self):
+        tx = np.zeros(self.tile_num + 1, np.uint32)
+        ty = np.zeros(self.tile_num + 1, np.uint32)
+        ld = np.zeros(max(self.lane_num, 1), np.uint32)
+        _check(_lib.lib().mbx_tile_download(self.h, _ptr(tx), _ptr(ty), _ptr(ld)))
+        return tx, ty, ld[:self.lane_num]
+
+    @classmethod
+    def upload(cls, ctx: Context, omega, sigma, n_rows, nnz, tile_x, tile_y, lane_desc):
+        info = mbx_tile_info(omega, sigma, n_rows, nnz, 0, 0, 0.0)
+        h = C.c_void_p()
+        tx = np.ascontiguousarray(tile_x, np.uint32)
+        ty = np.ascontiguousarray(tile_y, np.uint32)
+        ld = np.ascontiguousarray(lane_desc, np.uint32)
+        if ld.size == 0:
+            ld = np.zeros(1, np.uint32)
+        _check(_lib.lib().mbx_tile_upload(ctx.h, C.byref(info), _ptr(tx), _ptr(ty), _ptr(ld),
+                                          C.byref(h)))
+        return cls(ctx, h)
+
+    def long_row_fraction(self) -> float:
+        """tile.cpp:135-144"""
+        if self.tile_num == 0:
+            return 0.0
+        _, ty, _ = self.download()
+        return float(np.count_nonzero(ty[:-1] & self.kLongRowMask)) / self.tile_num
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lib().mbx_tile_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def generate_tile(row_offsets, n_rows: int, nnz: int, c: SimtConfig,
+                  ctx: Context | None = None) -> Tile:
+    """generate_tile(span row_offsets, n_rows, nnz, c) on the GPU (tile.cpp:17-85)."""
+    ctx = ctx or default_context()
+    cc = c._c()
+    h = C.c_void_p()
+    ro = None if row_offsets is None else np.ascontiguousarray(row_offsets, np.int64)
+    _check(_lib.lib().mbx_generate_tile(ctx.h, _ptr(ro), n_rows, nnz, C.byref(cc), C.byref(h)))
+    return Tile(ctx, h)
+
+
+def generate_tile_for(m: DeviceMatrix, c: SimtConfig) -> Tile:
+    """generate_tile(const CsrMatrix&, c) from the resident matrix (tile.hpp:54-58)."""
+    cc = c._c()
+    h = C.c_void_p()
+    _check(_lib.lib().mbx_matrix_generate_tile(m.ctx.h, m.h, C.byref(cc), C.byref(h)))
+    return Tile(m.ctx, h)
+
+
+# ---------------------------------------------------------------------------
+# SpMV (merbit_spmv.hpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class SpmvTrace:
+    """merbit_spmv.hpp:21-28 (deposit logging is not supported on the device)."""
+    collect_deposits: bool = False
+    fast_tiles: int = 0
+    normal_tiles: int = 0
+    skipped_tiles: int = 0
+    deposits: list = field(default_factory=list)
+
+
+class DualBuffer:
+    """Host ping-pong output pair with the reference contract (dual_buffer.hpp:9-42):
+    after a multiply, last_output() holds the result and active() is all zeros."""
+
+    def __init__(self, n: int, dtype=np.float64):
+        self._bufs = [np.zeros(n, dtype), np.zeros(n, dtype)]
+        self._parity = 0
+
+    def size(self):
+        return self._bufs[0].size
+
+    def parity(self):
+        return self._parity
+
+    def active(self):
+        return self._bufs[self._parity]
+
+    def inactive(self):
+        return self._bufs[self._parity ^ 1]
+
+    def last_output(self):
+        return self._bufs[self._parity ^ 1]
+
+    def flip(self):
+        self._parity ^= 1
+
+
+def spmv_merbit(m: DeviceMatrix, t: Tile, c: SimtConfig, x, out: DualBuffer,
+                trace: SpmvTrace | None = None):
+    """y = A x into out.active(); companion zeroed; parity flipped."""
+    if trace is not None and trace.collect_deposits:
+        raise UnsupportedError("per-row deposit logging is not available on the device path")
+    xv = np.ascontiguousarray(x, m.dtype)
+    if xv.size != m.n_cols:
+        raise DimensionError(f"spmv: x has {xv.size} entries, matrix has {m.n_cols} columns")
+    if out.size() != m.n_rows:
+        raise DimensionError(f"spmv: output pair sized {out.size()} for {m.n_rows} rows")
+    y = out.active()
+    if y.dtype != m.dtype:
+        raise ConfigError("DualBuffer dtype does not match the matrix precision")
+    cc = c._c()
+    tr = mbx_spmv_trace() if trace is not None else None
+    _check(_lib.lib().mbx_spmv(m.ctx.h, m.h, t.h, C.byref(cc), _ptr(xv) if xv.size else None,
+                               _ptr(y) if y.size else None,
+                               C.byref(tr) if tr is not None else None))
+    out.inactive()[:] = 0
+    out.flip()
+    if trace is not None:
+        trace.fast_tiles += tr.fast_tiles
+        trace.normal_tiles += tr.normal_tiles
+        trace.skipped_tiles += tr.skipped_tiles
+    return out.last_output()
+
+
+def spmv_device(m: DeviceMatrix, t: Tile, c: SimtConfig, x_ptr: int, y_ptr: int):
+    cc = c._c()
+    _check(_lib.lib().mbx_spmv_device(m.ctx.h, m.h, t.h, C.byref(cc), x_ptr, y_ptr))
+
+
+def trace_counts(t: Tile) -> SpmvTrace:
+    tr = mbx_spmv_trace()
+    _check(_lib.lib().mbx_spmv_trace_counts(t.ctx.h, t.h, C.byref(tr)))
+    return SpmvTrace(False, tr.fast_tiles, tr.normal_tiles, tr.skipped_tiles)
+
+
+# ---------------------------------------------------------------------------
+# backends (backend.hpp)
+# ---------------------------------------------------------------------------
+class BackendKind(enum.Enum):
+    merbit_b200 = "merbit-b200"
+
+
+class SpmvBackend:
+    """backend.hpp:22-34"""
+
+    def apply(self, x):
+        raise NotImplementedError
+
+    def name(self) -> str:
+        raise NotImplementedError
+
+    def preprocess_seconds(self) -> float:
+        return self._preprocess_seconds
+
+
+class MerbitB200Backend(SpmvBackend):
+    """MerbitBackend (backend.hpp:112-136) on the GPU: the constructor uploads
+    the CSR once and builds the TILE (T_p = K1 device time); apply() returns an
+    internal buffer valid until the next apply()."""
+
+    def __init__(self, a, c: SimtConfig, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.c = c
+        self.matrix = DeviceMatrix.from_csr(self.ctx, a)
+        self.tile_ = generate_tile_for(self.matrix, c)
+        self._preprocess_seconds = self.tile_.preprocess_seconds
+        self.buffer = DualBuffer(self.matrix.n_rows, self.matrix.dtype)
+
+    def apply(self, x):
+        return spmv_merbit(self.matrix, self.tile_, self.c, x, self.buffer)
+
+    def name(self):
+        return "merbit-b200"
+
+    def tile(self):
+        return self.tile_
+
+
+def make_backend(kind: BackendKind, a, c: SimtConfig, ctx: Context | None = None):
+    """make_backend (backend.hpp:152-169) for the GPU kind."""
+    if kind is BackendKind.merbit_b200:
+        return MerbitB200Backend(a, c, ctx)
+    raise ConfigError("unknown backend kind")
+
+
+# ---------------------------------------------------------------------------
+# PageRank (solvers.hpp:76-218)
+# ---------------------------------------------------------------------------
+@dataclass
+class PageRankConfig:
+    damping: float = 0.85
+    err_tol: float = 1e-10
+    max_iters: int = 210
+    reference_iters: int = 210
+
+    def _c(self):
+        return mbx_pagerank_config(self.damping, self.err_tol, self.max_iters,
+                                   self.reference_iters)
+
+
+@dataclass
+class PageRankResult:
+    pi: np.ndarray
+    reference_pi: np.ndarray | None
+    iterations: int
+    final_err: float
+    status: str
+    preprocess_seconds: float
+    iterate_seconds: float
+    l1_residual: float = 0.0
+    mass: float = 0.0
+    dangling_mass: float = 0.0
+    residual_history: np.ndarray | None = None
+
+
+def pagerank(p, cfg: PageRankConfig, backend: MerbitB200Backend | None = None,
+             c: SimtConfig | None = None, pi0=None) -> PageRankResult:
+    """pagerank<T>(p, cfg, backend): the power loop runs fused on the device.
+
+    `p` is the transition matrix (host CSR) when `backend` is None; otherwise the
+    backend's resident matrix and TILE are used."""
+    if backend is None:
+        dt = np.asarray(p.values).dtype
+        c = c or SimtConfig.make(32, select_sigma("f64" if dt == np.float64 else "f32"), 128)
+        backend = MerbitB200Backend(p, c)
+    m, t, c = backend.matrix, backend.tile_, backend.c
+    pi = np.zeros(m.n_rows, m.dtype)
+    ref = np.zeros(m.n_rows, m.dtype)
+    hist = np.zeros(max(cfg.max_iters, 1), np.float64)
+    res = mbx_pagerank_result()
+    cc, pc = c._c(), cfg._c()
+    p0 = None if pi0 is None else np.ascontiguousarray(pi0, m.dtype)
+    _check(_lib.lib().mbx_pagerank(m.ctx.h, m.h, t.h, C.byref(cc), C.byref(pc), _ptr(p0),
+                                   _ptr(pi), _ptr(ref), _ptr(hist), C.byref(res)))
+    return PageRankResult(pi=pi, reference_pi=ref, iterations=res.iterations,
+                          final_err=res.final_err,
+                          status="converged" if res.status == 0 else "max_iterations",
+                          preprocess_seconds=res.preprocess_seconds,
+                          iterate_seconds=res.iterate_seconds, l1_residual=res.l1_residual,
+                          mass=res.mass, dangling_mass=res.dangling_mass,
+                          residual_history=hist[:res.iterations])
+
+
+class PageRankPlan:
+    """Device-resident reusable power loop (buffers + CUDA graph built once)."""
+
+    def __init__(self, m: DeviceMatrix, t: Tile, c: SimtConfig, cfg: PageRankConfig):
+        self.m, self.t, self.c, self.cfg = m, t, c, cfg
+        h = C.c_void_p()
+        cc, pc = c._c(), cfg._c()
+        _check(_lib.lib().mbx_pagerank_plan_create(m.ctx.h, m.h, t.h, C.byref(cc), C.byref(pc),
+                                                   C.byref(h)))
+        self.h = h
+
+    def run(self, pi0_ptr: int | None = None):
+        _check(_lib.lib().mbx_pagerank_plan_run(self.h, pi0_ptr))
+
+    def result(self, want_history=False):
+        res = mbx_pagerank_result()
+        hist = np.zeros(max(self.cfg.max_iters, 1), np.float64) if want_history else None
+        _check(_lib.lib().mbx_pagerank_plan_result(self.h, C.byref(res), _ptr(hist)))
+        return res, hist
+
+    def pi_ptr(self) -> int:
+        return _lib.lib().mbx_pagerank_plan_pi(self.h) or 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lib().mbx_pagerank_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

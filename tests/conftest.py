@@ -1,0 +1,27 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and libmerbit_b200.so")
+    config.addinivalue_line("markers", "slow: large-scale case (R-MAT scale >= 20)")
+
+
+@pytest.fixture(scope="session")
+def ctx():
+    import paper_2605_07391_b200 as mb
+    return mb.Context(0)
+
+
+@pytest.fixture(scope="session")
+def golden():
+    import json
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    return {name: json.load(open(os.path.join(here, f"{name}.json")))
+            for name in ("walkthrough", "fuzz_corpus", "pagerank")}

@@ -1,0 +1,191 @@
+"""GPU K2+K3 SpMV parity (merbit_spmv.hpp:136-352) against the oracle, with the
+reference's own test cases (test_kernel.cpp) and BASELINE-size R-MAT inputs.
+Tolerances: ToleranceBound 4 eps len max|A| max|x| on the fuzz corpus
+(checks.hpp:20-42); north-star 1e-5 (fp32) / 1e-12 (fp64) relative to the
+row-sum magnitude sum|a||x| at scale."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2605_07391_b200 as mb
+from helpers import CONFIGS, first_violation, h, tolerance_bound
+
+pytestmark = pytest.mark.gpu
+
+
+def run(ctx, a, c, x, trace=None):
+    m = mb.DeviceMatrix.from_csr(ctx, a)
+    t = mb.generate_tile_for(m, c)
+    buf = mb.DualBuffer(a.n_rows, a.values.dtype)
+    return mb.spmv_merbit(m, t, c, x, buf, trace).copy()
+
+
+def test_walkthrough_exact(ctx):
+    # test_kernel.cpp:30-46
+    a = O.walkthrough()
+    for (w, s, b) in [(4, 4, 4), (4, 4, 8), (32, 7, 64), (32, 14, 128)]:
+        for dt in (np.float64, np.float32):
+            y = run(ctx, a.astype(dt), mb.SimtConfig.make(w, s, b), np.ones(8, dt))
+            assert y.tolist() == [15, 0, 40, 36, 119, 141, 177, 67]
+
+
+def test_fuzz_corpus_within_bound(ctx, golden):
+    """test_kernel.cpp:48-77 / acceptance c1 over the whole 504-matrix corpus."""
+    for e in golden["fuzz_corpus"]:
+        m64 = O.random_matrix(e["shape"], e["seed"])
+        x64 = O.seed_test_vector(m64.n_cols, -1.0, 1.0, e["seed"])
+        for dt in (np.float64, np.float32):
+            a = m64.astype(dt)
+            x = x64.astype(dt)
+            want = O.spmv_csr_f64(a.astype(np.float64), x.astype(np.float64))
+            bound = tolerance_bound(a, x, dt)
+            for (w, s, b) in CONFIGS:
+                got = run(ctx, a, mb.SimtConfig.make(w, s, b), x)
+                assert first_violation(bound, want, got) == -1, (e["shape"], e["seed"], w, s, dt)
+
+
+def test_block_sizes_bound_and_bitwise_repeat(ctx):
+    # test_kernel.cpp:79-99
+    for shape in O.SHAPES:
+        a = O.random_matrix(shape, 202)
+        x = O.seed_test_vector(a.n_cols, -1, 1, 17)
+        want = O.spmv_csr_f64(a, x)
+        bound = tolerance_bound(a, x, np.float64)
+        for block in (32, 128, 256, 992):
+            c = mb.SimtConfig.make(32, 7, block)
+            got = run(ctx, a, c, x)
+            assert first_violation(bound, want, got) == -1
+            assert np.array_equal(got.view(np.uint64), run(ctx, a, c, x).view(np.uint64))
+
+
+def test_dual_buffer_alternating_matches_fresh(ctx):
+    # test_kernel.cpp:116-134
+    a = O.random_matrix("uniform", 404)
+    c = mb.SimtConfig.make(32, 7, 128)
+    m = mb.DeviceMatrix.from_csr(ctx, a)
+    t = mb.generate_tile_for(m, c)
+    alt = mb.DualBuffer(a.n_rows)
+    for it in range(10):
+        x = O.seed_test_vector(a.n_cols, -1, 1, 1000 + it)
+        mb.spmv_merbit(m, t, c, x, alt)
+        fresh = mb.DualBuffer(a.n_rows)
+        mb.spmv_merbit(m, t, c, x, fresh)
+        assert np.array_equal(alt.last_output(), fresh.last_output())
+        assert not alt.active().any()
+
+
+def test_long_row_fast_path(ctx):
+    # test_kernel.cpp:160-176 / acceptance c6
+    for s in (7, 14):
+        c = mb.SimtConfig.make(32, s, 128)
+        width = 10 * c.steps_per_tile()
+        a = O.single_dense_row(width, 11)
+        x = O.seed_test_vector(width, 0.25, 1.75, 13)
+        tr = mb.SpmvTrace()
+        y = run(ctx, a, c, x, tr)
+        assert tr.fast_tiles == 10
+        want = O.spmv_csr_f64(a, x)
+        assert abs(y[0] - want[0]) / abs(want[0]) <= 1e-12
+
+
+def test_trace_counts_match_reference(ctx, golden):
+    for e in golden["fuzz_corpus"][:120]:
+        m = O.random_matrix(e["shape"], e["seed"])
+        c = mb.SimtConfig.make(32, 14, 128)
+        t = mb.generate_tile_for(mb.DeviceMatrix.from_csr(ctx, m), c)
+        tr = mb.trace_counts(t)
+        assert [tr.fast_tiles, tr.normal_tiles, tr.skipped_tiles] == e["tiles"]["32,14"]["trace"]
+
+
+def test_edge_shapes(ctx):
+    # test_kernel.cpp:220-239
+    c = mb.SimtConfig.make(4, 4, 8)
+    empty = O.Csr(37, 5, np.zeros(38, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    y = run(ctx, empty, c, np.full(5, 3.0))
+    assert y.shape == (37,) and not y.any()
+    none = O.Csr(0, 0, np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    assert run(ctx, none, c, np.zeros(0)).size == 0
+
+
+def test_error_paths(ctx):
+    # test_kernel.cpp:241-267
+    a = O.walkthrough()
+    c = mb.SimtConfig.make(4, 4, 4)
+    m = mb.DeviceMatrix.from_csr(ctx, a)
+    t = mb.generate_tile_for(m, c)
+    x = np.ones(8)
+    with pytest.raises(mb.ConfigError):
+        mb.spmv_merbit(m, t, mb.SimtConfig.make(32, 7, 64), x, mb.DualBuffer(8))
+    stale = mb.generate_tile_for(mb.DeviceMatrix.from_csr(ctx, O.single_dense_row(16, 3)), c)
+    with pytest.raises(mb.ConfigError):
+        mb.spmv_merbit(m, stale, c, x, mb.DualBuffer(8))
+    with pytest.raises(mb.DimensionError):
+        mb.spmv_merbit(m, t, c, np.ones(7), mb.DualBuffer(8))
+    with pytest.raises(mb.DimensionError):
+        mb.spmv_merbit(m, t, c, x, mb.DualBuffer(7))
+    with pytest.raises(mb.ConfigError):
+        mb.SimtConfig.make(32, 20, 32)
+    bad = O.Csr(2, 2, np.array([0, 1, 2]), np.array([0, 5], np.int32), np.ones(2))
+    with pytest.raises(mb.DimensionError):
+        mb.DeviceMatrix.upload(ctx, 2, 2, bad.row_offsets, bad.col_indices.astype(np.int64),
+                               bad.values)
+
+
+def _rel_err(y, want, mag):
+    return np.abs(np.asarray(y, np.float64) - want) / np.where(mag > 0, mag, 1.0)
+
+
+@pytest.mark.parametrize("scale", [16, 20])
+def test_rmat_fp32_within_1e5(ctx, scale):
+    """C1 (scale 20): y within 1e-5 of the fp64-accumulated oracle relative to
+    sum|a||x| per row; also reports the reference fp32 sequential distance."""
+    m = mb.DeviceMatrix.rmat(ctx, scale, 16, seed=1, dtype=np.float32)
+    ro, cols, vals = m.download()
+    a = O.Csr(m.n_rows, m.n_cols, ro, cols, vals)
+    x = O.hash_uniform(1, m.n_cols, -1.0, 1.0, np.float32)
+    c = mb.SimtConfig.make(32, 14, 128)
+    t = mb.generate_tile_for(m, c)
+    buf = mb.DualBuffer(m.n_rows, np.float32)
+    y = mb.spmv_merbit(m, t, c, x, buf).copy()
+    want, mag = O.spmv_csr_f32_acc64(a, x, nthreads=8)
+    assert _rel_err(y, want, mag).max() <= 1e-5
+    empty = np.diff(ro) == 0
+    assert not y[empty].any()
+    y2 = mb.spmv_merbit(m, t, c, x, buf)
+    assert np.array_equal(y.view(np.uint32), y2.view(np.uint32))  # deterministic
+
+
+@pytest.mark.parametrize("scale", [16, 20])
+def test_rmat_fp64_within_1e12(ctx, scale):
+    m = mb.DeviceMatrix.rmat(ctx, scale, 16, seed=1, dtype=np.float64, lo=-1.0, hi=1.0)
+    ro, cols, vals = m.download()
+    a = O.Csr(m.n_rows, m.n_cols, ro, cols, vals)
+    x = O.hash_uniform(1, m.n_cols, -1.0, 1.0, np.float64)
+    c = mb.SimtConfig.make(32, 7, 128)
+    t = mb.generate_tile_for(m, c)
+    y = mb.spmv_merbit(m, t, c, x, mb.DualBuffer(m.n_rows, np.float64))
+    want, mag = O.spmv_csr_f64(a, x, nthreads=8, want_abs=True)
+    assert _rel_err(y, want, mag).max() <= 1e-12
+
+
+def test_power_law_long_and_empty_rows_fp64(ctx):
+    """C3-style: Zipf row lengths with rows of >= 100*omega*sigma nonzeros and
+    exactly 10% empty rows (small analogue of BASELINE config 3)."""
+    rng = np.random.default_rng(5)
+    n = 1 << 14
+    lens = np.minimum((40000 / (np.arange(n) + 1) ** 0.9).astype(np.int64) + 1, n)
+    lens[rng.permutation(n)[: n // 10]] = 0
+    ro = np.zeros(n + 1, np.int64)
+    ro[1:] = np.cumsum(lens)
+    cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) if l else
+                           np.zeros(0, np.int64) for l in lens]).astype(np.int32)
+    vals = rng.uniform(-1, 1, ro[-1])
+    a = O.Csr(n, n, ro, cols, vals)
+    x = rng.uniform(-1, 1, n)
+    c = mb.SimtConfig.make(32, 7, 128)
+    tr = mb.SpmvTrace()
+    y = run(ctx, a, c, x, tr)
+    want, mag = O.spmv_csr_f64(a, x, want_abs=True)
+    assert _rel_err(y, want, mag).max() <= 1e-12
+    assert tr.fast_tiles >= 100 and tr.skipped_tiles >= 0
+    assert not y[lens == 0].any()
