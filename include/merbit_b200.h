@@ -143,9 +143,13 @@ MBX_API int mbx_context_set_stream(mbx_context* ctx, void* stream);
 MBX_API void* mbx_context_stream(mbx_context* ctx);
 MBX_API int mbx_context_synchronize(mbx_context* ctx);
 /* Kernel launch shape of K2 (omega == 32): warps per CTA, resident CTAs per
- * SM (persistent grid), hub-cache cap (-1 auto, 0 off).  Defaults 16/2/-1. */
+ * SM (persistent grid), hub-cache cap (-1 auto, 0 off).  Defaults 32/1/-1. */
 MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta,
                                    int ctas_per_sm, int max_hubs);
+/* Shared-memory budget per SM for K2 (bytes; the rest is L1) and L2
+ * prefetch of the next tile's streams (0/1).  Defaults 147456 / 1. */
+MBX_API int mbx_context_set_tuning_ex(mbx_context* ctx, int smem_per_sm,
+                                      int prefetch);
 /* Number of merbit kernels this context launched so far. */
 MBX_API int64_t mbx_context_launch_count(const mbx_context* ctx);
 
@@ -192,6 +196,11 @@ MBX_API int mbx_matrix_build_xcache(mbx_context* ctx, mbx_matrix* m,
                                     int max_hubs, double* seconds);
 MBX_API int mbx_matrix_xcache_info(const mbx_matrix* m, int* hubs,
                                    double* coverage);
+/* Device pointers of the hub-encoded column array and the hub column list
+ * (NULL when no cache is built). */
+MBX_API int mbx_matrix_xcache_ptrs(const mbx_matrix* m,
+                                   const int32_t** cols_hub,
+                                   const int32_t** hub_cols);
 
 /* ---- TILE preprocessing (K1) --------------------------------------------- */
 /* generate_tile(span row_offsets, n_rows, nnz, c) (src/tile.cpp:17-85) on

@@ -59,6 +59,7 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   g.num_ranges = (g.num_chunks + g.chunks_per_range - 1) / g.chunks_per_range;
   g.warps_per_cta = ctx->tuning.warps_per_cta;
   g.grid = ctx->sm_count * ctx->tuning.ctas_per_sm;
+  g.prefetch = ctx->tuning.prefetch;
   g.hub_count = 0;
   if (m->cols_hub && m->hub_avail > 0 && g.omega == 32 && ctx->tuning.max_hubs != 0 &&
       (ctx->tuning.max_hubs < 0 || ctx->tuning.max_hubs >= m->hub_avail)) {
@@ -483,6 +484,13 @@ MBX_API int mbx_matrix_device_ptrs(const mbx_matrix* m, const void** values,
   });
 }
 
+MBX_API int mbx_context_set_tuning_ex(mbx_context* ctx, int smem_per_sm, int prefetch) {
+  return guarded([&] {
+    ctx->tuning.smem_per_sm = smem_per_sm;
+    ctx->tuning.prefetch = prefetch;
+  });
+}
+
 MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta, int ctas_per_sm,
                                    int max_hubs) {
   return guarded([&] {
@@ -517,6 +525,14 @@ MBX_API int mbx_matrix_xcache_info(const mbx_matrix* m, int* hubs, double* cover
   return guarded([&] {
     if (hubs) *hubs = m->hub_avail;
     if (coverage) *coverage = m->hub_coverage;
+  });
+}
+
+MBX_API int mbx_matrix_xcache_ptrs(const mbx_matrix* m, const int32_t** cols_hub,
+                                   const int32_t** hub_cols) {
+  return guarded([&] {
+    if (cols_hub) *cols_hub = m->cols_hub;
+    if (hub_cols) *hub_cols = m->hub_cols;
   });
 }
 

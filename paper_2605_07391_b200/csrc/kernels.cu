@@ -323,7 +323,7 @@ __device__ __forceinline__ T lane_walk_and_scan(T* buf, int cnt, int sigma, uint
 }
 
 // One warp range: `chunks_per_range` consecutive tiles (chunk == tile here).
-template <typename T, int SIGMA, bool PR, bool HUB>
+template <typename T, int SIGMA, bool PR, bool HUB, bool PF>
 __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, T* buf,
                                           int64_t range, int lid, uint64_t pol, T base) {
   const Geometry& g = p.g;
@@ -356,6 +356,23 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
     const uint32_t y1 = __shfl_sync(kFull, mty, ci + 1) & ~kLongRowMask;
     const int cnt = static_cast<int>(x1 - x0);
     const int nrows = static_cast<int>(y1 - y0);
+    if (PF && ci + 1 < nc) {
+      // warm L2 with the next tile's value/column/descriptor lines so its
+      // loads do not pay DRAM latency on the critical path
+      const uint32_t px1 = __shfl_sync(kFull, mtx, ci + 2);
+      const uintptr_t vb = reinterpret_cast<uintptr_t>(p.vals + x1) & ~uintptr_t(127);
+      const uintptr_t ve = reinterpret_cast<uintptr_t>(p.vals + px1);
+      const uintptr_t cb = reinterpret_cast<uintptr_t>(p.cols + x1) & ~uintptr_t(127);
+      const uintptr_t ce = reinterpret_cast<uintptr_t>(p.cols + px1);
+      const int nvl = static_cast<int>((ve - vb + 127) >> 7);
+      const int ncl = static_cast<int>((ce - cb + 127) >> 7);
+      for (int l = lid; l <= nvl + ncl; l += 32) {
+        const uintptr_t a = l < nvl ? vb + (uintptr_t(l) << 7)
+                            : l < nvl + ncl ? cb + (uintptr_t(l - nvl) << 7)
+                                            : reinterpret_cast<uintptr_t>(p.lane_desc + (c + 1) * 32);
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a));
+      }
+    }
     if (ty0 & kLongRowMask) {
       // long-row tile: every step Right, one row (merbit_spmv.hpp:230-237)
       T s = stage_products<T, true, MAXV, HUB>(p.vals, p.cols, p.x, hub, x0, x1, buf, lid, pol);
@@ -418,7 +435,7 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
 
 // K2, omega == 32: persistent CTAs; the x hub table is staged once per CTA,
 // then each warp strides over ranges (all ranges carry equal merge-path work).
-template <typename T, int SIGMA, bool PR, bool HUB>
+template <typename T, int SIGMA, bool PR, bool HUB, bool PF>
 __global__ void __launch_bounds__(1024) spmv_w32_kernel(SpmvParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geometry& g = p.g;
@@ -438,7 +455,7 @@ __global__ void __launch_bounds__(1024) spmv_w32_kernel(SpmvParams<T> p) {
   const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t range = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp; range < g.num_ranges;
        range += wstride)
-    w32_range<T, SIGMA, PR, HUB>(p, hub, buf, range, lid, pol, base);
+    w32_range<T, SIGMA, PR, HUB, PF>(p, hub, buf, range, lid, pol, base);
 }
 
 // ---------------------------------------------------------------------------
@@ -786,13 +803,14 @@ inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148LL * 64) {
 
 template <typename T, int SIGMA, bool PR, bool HUB>
 void launch_w32(mbx_context* ctx, const SpmvParams<T>& p, size_t smem) {
-  auto kern = spmv_w32_kernel<T, SIGMA, PR, HUB>;
-  static int configured = -1;
-  if (configured != ctx->device) {
+  auto kern = p.g.prefetch ? spmv_w32_kernel<T, SIGMA, PR, HUB, true>
+                           : spmv_w32_kernel<T, SIGMA, PR, HUB, false>;
+  static int configured[2] = {-1, -1};
+  if (configured[p.g.prefetch ? 1 : 0] != ctx->device) {
     int optin = 0;
     MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     MBX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    configured = ctx->device;
+    configured[p.g.prefetch ? 1 : 0] = ctx->device;
   }
   const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
   const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));
@@ -863,6 +881,8 @@ int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, in
                                   ctx->device));
   MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const int64_t reserve = 1024;  // per-CTA system reservation
+  if (ctx->tuning.smem_per_sm > 0 && ctx->tuning.smem_per_sm < per_sm)
+    per_sm = ctx->tuning.smem_per_sm;
   int64_t per_cta = per_sm / ctas_per_sm - reserve;
   if (per_cta > optin) per_cta = optin;
   const int64_t vs = int64_t(value_size(precision));

@@ -40,13 +40,19 @@ struct Geometry {
   // x hub cache: the first hub_count entries of the column-frequency order
   // are staged in shared memory; encoded columns (sign bit) address them.
   int hub_count = 0;
+  int prefetch = 0;
 };
 
 // Launch tuning knobs (context-wide; see mbx_context_set_tuning).
 struct Tuning {
-  int warps_per_cta = 16;
-  int ctas_per_sm = 2;
+  int warps_per_cta = 32;
+  int ctas_per_sm = 1;
   int max_hubs = -1;  // -1: fill the shared-memory budget; 0: disable
+  // Shared memory K2 may take per SM.  The rest stays L1, which also stages
+  // every in-flight miss: a hub table that squeezes L1 below ~80 KB starves
+  // memory-level parallelism (measured, profiles/).
+  int smem_per_sm = 144 * 1024;
+  int prefetch = 1;  // L2 prefetch of the next tile's value/column lines
 };
 
 // Device-side reduction slots of one fused PageRank iteration.

@@ -185,9 +185,15 @@ class Context:
     def synchronize(self):
         _check(_lib.lib().mbx_context_synchronize(self.h))
 
-    def set_tuning(self, warps_per_cta: int = 16, ctas_per_sm: int = 2, max_hubs: int = -1):
-        """K2 launch shape (persistent grid) and x hub-cache cap (-1 auto, 0 off)."""
+    def set_tuning(self, warps_per_cta: int = 32, ctas_per_sm: int = 1, max_hubs: int = -1,
+                   smem_per_sm: int | None = None, prefetch: int | None = None):
+        """K2 launch shape (persistent grid), x hub-cache cap (-1 auto, 0 off),
+        shared-memory budget per SM and L2 prefetch of the next tile."""
         _check(_lib.lib().mbx_context_set_tuning(self.h, warps_per_cta, ctas_per_sm, max_hubs))
+        if smem_per_sm is not None or prefetch is not None:
+            _check(_lib.lib().mbx_context_set_tuning_ex(
+                self.h, 147456 if smem_per_sm is None else smem_per_sm,
+                1 if prefetch is None else prefetch))
 
     @property
     def launch_count(self) -> int:

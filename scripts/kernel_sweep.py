@@ -41,11 +41,11 @@ yref = None
 tiles = {}
 combos = []
 for tu in args.tunings.split(","):
-    w_, c_, h_ = (int(v) for v in tu.split(":"))
+    f = [int(v) for v in tu.split(":")] + [144, 1]
     for b in [int(v) for v in args.blocks.split(",")]:
-        combos.append((w_, c_, h_, b))
-for (wpc, cps, hubs, b) in combos:
-    ctx.set_tuning(wpc, cps, hubs)
+        combos.append((f[0], f[1], f[2], f[3], f[4], b))
+for (wpc, cps, hubs, smem_kb, pf, b) in combos:
+    ctx.set_tuning(wpc, cps, hubs, smem_kb * 1024, pf)
     xc_s = P.build_xcache(hubs)
     nh, cov = P.xcache_info()
     c = mb.SimtConfig.make(32, sigma, b)
@@ -70,7 +70,7 @@ for (wpc, cps, hubs, b) in combos:
         else:
             same = bool(torch.equal(y.view(torch.int32 if vs == 4 else torch.int64),
                                     yref.view(torch.int32 if vs == 4 else torch.int64)))
-    row = {"warps": wpc, "ctas_per_sm": cps, "hubs": nh, "hub_cov": round(cov, 3),
+    row = {"warps": wpc, "ctas_per_sm": cps, "smem_kb": smem_kb, "pf": pf, "hubs": nh, "hub_cov": round(cov, 3),
            "xcache_ms": round(xc_s * 1e3, 3), "block": b, "spmv_us": round(ts * 1e6, 1),
            "spmv_gbs": round(bs / ts / 1e9, 1), "spmv_frac": round(bs / ts / 1e9 / peak, 4),
            "gflops": round(2 * m / ts / 1e9, 1), "tile_ms": round(t.preprocess_seconds * 1e3, 3),

@@ -1,0 +1,124 @@
+// ref_driver.cpp -- the drop-in proof: the reference's OWN drivers and test
+// helpers (pagerank, spmv_csr_reference, generate_tile, the fuzz generators
+// and ToleranceBound, all compiled from /root/reference/proj) running over
+// merbit::B200Backend (include/merbit_b200/reference_backend.hpp).
+//
+// Built by oracle/Makefile into oracle/_ref/b200_ref_driver (it compiles the
+// reference sources, so it lives with the other reference builds); run by
+// tests/test_gpu_cpp.py on the GPU box.  One [PASS]/[FAIL] line per check,
+// mirroring tests/acceptance.cpp; exit status = number of failures.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "merbit/backend.hpp"
+#include "merbit/fixtures.hpp"
+#include "merbit/random.hpp"
+#include "merbit/reference.hpp"
+#include "merbit/solvers.hpp"
+#include "merbit/tile.hpp"
+#include "merbit_b200/reference_backend.hpp"
+#include "support/checks.hpp"
+#include "support/generators.hpp"
+
+using namespace merbit;
+
+namespace {
+
+int failures = 0;
+
+void report(bool ok, const std::string& what) {
+  std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", what.c_str());
+  if (!ok) ++failures;
+}
+
+bool same_tile(const TileMetadata& a, const TileMetadata& b) {
+  return a.tile_num == b.tile_num && a.lane_num == b.lane_num && a.tile_x == b.tile_x &&
+         a.tile_y == b.tile_y && a.lane_desc == b.lane_desc;
+}
+
+template <typename T>
+bool corpus_agreement(const SimtConfig& c, int seeds, std::string& detail) {
+  for (std::uint64_t seed = 1; seed <= std::uint64_t(seeds); ++seed) {
+    for (auto shape : testing::kAllShapes) {
+      const CsrMatrix<T> a = coo_to_csr<T>(testing::random_matrix(shape, seed));
+      const auto x = seed_test_vector<T>(a.n_cols, -1.0, 1.0, seed);
+      B200Backend<T> gpu(a, c);
+      if (!same_tile(gpu.tile(), generate_tile(a, c))) {
+        detail = std::string("TILE ") + testing::shape_name(shape) + " seed " + std::to_string(seed);
+        return false;
+      }
+      const auto want = spmv_csr_reference(a, std::span<const T>(x));
+      const testing::ToleranceBound<T> bound(a, x);
+      const auto& got = gpu.apply(std::span<const T>(x));
+      if (testing::first_violation<T>(bound, want, got) != -1) {
+        detail = std::string("y ") + testing::shape_name(shape) + " seed " + std::to_string(seed);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
+}  // namespace
+
+int main() {
+  // 1. walkthrough fixture (test_kernel.cpp:30-46, test_format.cpp:59-110)
+  {
+    const auto a = walkthrough_fixture<double>();
+    for (const SimtConfig& c : {SimtConfig::make(4, 4, 4), SimtConfig::make(32, 14, 128)}) {
+      B200Backend<double> gpu(a, c);
+      const std::vector<double> x(8, 1.0);
+      const auto& y = gpu.apply(std::span<const double>(x));
+      report(y == std::vector<double>{15, 0, 40, 36, 119, 141, 177, 67} &&
+                 same_tile(gpu.tile(), generate_tile(a, c)),
+             "walkthrough exact y and byte-identical TILE omega=" + std::to_string(c.omega));
+    }
+  }
+  // 2. fuzz corpus agreement within the reference's ToleranceBound
+  for (const SimtConfig& c : {SimtConfig::make(32, 14, 128), SimtConfig::make(32, 7, 128),
+                              SimtConfig::make(4, 4, 16)}) {
+    std::string d64, d32;
+    const bool ok = corpus_agreement<double>(c, 12, d64) && corpus_agreement<float>(c, 12, d32);
+    report(ok, "fuzz corpus (12 seeds x 6 shapes, f64+f32) sigma=" + std::to_string(c.sigma) +
+                   " " + d64 + d32);
+  }
+  // 3. the reference's pagerank driver over the GPU backend (acceptance c9)
+  {
+    const auto p = build_transition(ring_with_chords<double>(100, 260, 42));
+    const SimtConfig c = SimtConfig::make(32, 7, 128);
+    B200Backend<double> gpu(p, c);
+    double worst_mass = 0.0;
+    const auto watch = [&](index_t, const std::vector<double>& pi, double) {
+      double mass = 0.0;
+      for (double v : pi) mass += std::abs(v);
+      worst_mass = std::max(worst_mass, std::abs(mass - 1.0));
+    };
+    const auto run = pagerank<double>(p, {}, gpu, watch);
+    CsrReferenceBackend<double> csr(p);
+    const auto want = pagerank<double>(p, {}, csr);
+    double dev = 0.0;
+    for (std::size_t i = 0; i < run.pi.size(); ++i) dev = std::max(dev, std::abs(run.pi[i] - want.pi[i]));
+    report(run.status == SolveStatus::converged && run.iterations <= 210 &&
+               run.final_err < 1e-10 && worst_mass <= 1e-12 && dev <= 1e-12,
+           "reference pagerank<double> over B200Backend: " + std::to_string(run.iterations) +
+               " iterations, max |pi - pi_csr| = " + std::to_string(dev));
+  }
+  // 4. error taxonomy survives the boundary (test_kernel.cpp:241-267)
+  {
+    const auto a = walkthrough_fixture<double>();
+    B200Backend<double> gpu(a, SimtConfig::make(4, 4, 4));
+    bool threw = false;
+    try {
+      const std::vector<double> x(7, 1.0);
+      gpu.apply(std::span<const double>(x));
+    } catch (const dimension_error&) {
+      threw = true;
+    }
+    report(threw, "short x raises merbit::dimension_error through the C ABI");
+  }
+  std::printf("%d failure(s)\n", failures);
+  return failures;
+}

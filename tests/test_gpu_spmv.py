@@ -189,3 +189,24 @@ def test_power_law_long_and_empty_rows_fp64(ctx):
     assert _rel_err(y, want, mag).max() <= 1e-12
     assert tr.fast_tiles >= 100 and tr.skipped_tiles >= 0
     assert not y[lens == 0].any()
+
+
+@pytest.mark.parametrize("tuning", [(32, 1, 0, 147456, 1), (16, 2, 0, 147456, 0),
+                                    (8, 4, 0, 147456, 1), (32, 1, -1, 131072, 1),
+                                    (16, 2, -1, 147456, 0)])
+def test_launch_shapes_and_hub_cache_are_bitwise_invariant(tuning):
+    """Every K2 launch shape, the L2 prefetch and the shared-memory x hub cache
+    change only speed: y is bitwise identical to the default launch."""
+    ctx = mb.Context(0)
+    m = mb.DeviceMatrix.rmat(ctx, 16, 16, seed=4, dtype=np.float32)
+    c = mb.SimtConfig.make(32, 14, 128)
+    t = mb.generate_tile_for(m, c)
+    x = O.hash_uniform(9, m.n_cols, -1.0, 1.0, np.float32)
+    y0 = mb.spmv_merbit(m, t, c, x, mb.DualBuffer(m.n_rows, np.float32)).copy()
+    w, cps, hubs, smem, pf = tuning
+    ctx.set_tuning(w, cps, hubs, smem, pf)
+    m.build_xcache(hubs)
+    if hubs != 0:
+        assert m.xcache_info()[0] > 0
+    y1 = mb.spmv_merbit(m, t, c, x, mb.DualBuffer(m.n_rows, np.float32))
+    assert np.array_equal(y0.view(np.uint32), y1.view(np.uint32))
