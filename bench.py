@@ -1,20 +1,26 @@
 #!/usr/bin/env python
-"""Benchmark of the MERBIT hot path on B200 (contract: see DESIGN.md).
+"""Benchmark of the MERBIT hot path on B200 (contract and derivations: DESIGN.md).
 
-Workload at N=1 (BASELINE.json configs[1]): PageRank, 100 fixed iterations
-(reference_iters=0, err_tol=1e-30 so every run does all 100), fp32, on the
-transition matrix of a synthetic R-MAT scale-24 graph (edge factor 16,
-Graph500 a,b,c,d, duplicates merged, natural vertex order), TILE built once
-(preprocessing amortised).  One "step" = one 100-iteration PageRank run.
+Workload (BASELINE.json configs[1]): PageRank, 100 fixed iterations
+(reference_iters=0, err_tol=1e-30, so every run does all 100), fp32, on the
+transition matrix of a synthetic R-MAT graph (default scale 24: edge factor
+16, Graph500 a,b,c,d, duplicates merged, natural vertex order), TILE built
+once (preprocessing amortised).  One "step" = one 100-iteration PageRank run.
+At N>1 GPUs (torchrun) the SAME matrix is row-sharded (merge-path balanced)
+with one NCCL all-gather of pi per iteration: strong scaling.  --scale 27
+gives BASELINE config C4.
 
-  value      iterations/s with the matrix resident in HBM (CUDA graph replay)
-  e2e        same metric through the one-shot C-ABI call mbx_pagerank with
-             pinned HOST buffers (pi0 in, pi out) inside the timed region
-  roofline   one fused PageRank iteration (K2 spmv_w32<float,14,PR> + K3
-             fixup) against measured HBM copy bandwidth: algorithmic bytes
-             8m + 16n + 4 per iteration
-  spmv       the plain SpMV (K2+K3) on the same matrix: GFLOP/s = 2m/t and
-             GB/s over 8m + 12n + 4
+  value      iterations/s, matrix resident in HBM (CUDA-graph replay), max
+             over ranks of the device time
+  e2e        same metric with pinned HOST buffers inside the timed region:
+             N=1 the one-shot C-ABI call mbx_pagerank (pi0 in, pi out);
+             N>1 each rank's pi0 slice H2D + run + its pi slice D2H
+  roofline   the fused PageRank iteration on one GPU (K2 spmv_w32 + K3
+             fixup) vs measured HBM copy bandwidth; algorithmic bytes per
+             iteration 8m + 16n + 4 (fp32)
+  spmv       plain SpMV (K2+K3) on the same matrix (fp32) and on an fp64
+             R-MAT of the same scale: GFLOP/s = 2m/t, GB/s over 8m+12n+4 /
+             12m+20n+4
   cpu_baseline  the reference's own MerbitBackend<float> PageRank
              (oracle/_ref, ThreadPool(nproc)) on this box's host cores
 
@@ -37,9 +43,8 @@ METRIC = "SpMV GFLOP/s & HBM GB/s vs roofline; PageRank iters/sec at 1/2/4/8 B20
 
 
 def measured_peak():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
@@ -101,7 +106,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_pagerank(ro, cols, n, iters_per_step, steps, warmup, nthreads, want_line=False):
+def cpu_reference_pagerank(ro, cols, n, iters_per_step, steps, warmup, nthreads):
     """The reference's pagerank<float> with MerbitBackend on ThreadPool(nthreads)
     (oracle/_ref = the unmodified reference compiled from its sources)."""
     import numpy as np
@@ -109,29 +114,23 @@ def cpu_reference_pagerank(ro, cols, n, iters_per_step, steps, warmup, nthreads,
     import oracle as O
     vals = O.transition_values(n, cols, np.float32)
     a = O.Csr(n, n, ro, cols, vals)
-    t0 = time.perf_counter()
     eng = O.RefEngine(a, 32, 14, 128, nthreads)
-    setup = time.perf_counter() - t0
     for _ in range(warmup):
         eng.pagerank(0.85, 1e-30, iters_per_step, 0)
-    secs = 0.0
-    done = 0
+    secs, done = 0.0, 0
     for _ in range(steps):
         r = eng.pagerank(0.85, 1e-30, iters_per_step, 0)
         secs += r["seconds"]
         done += r["iterations"]
+    pre = eng.preprocess_seconds
     eng.close()
-    return {"value": done / secs, "seconds": secs, "iterations": done,
-            "preprocess_seconds": eng.preprocess_seconds, "setup_seconds": setup}
+    return {"value": done / secs, "seconds": secs, "iterations": done, "preprocess_seconds": pre}
 
 
 def run_reference(args):
     """--impl reference: the reference CPU implementation on this box's cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
-    import numpy as np
-
     import oracle as O
     if O.ref() is None:
         print(json.dumps({"impl": "reference",
@@ -142,29 +141,62 @@ def run_reference(args):
     p = O.rmat(args.scale, 16, 1, transposed=True, nthreads=nthreads)
     gen = time.perf_counter() - t0
     iters = args.ref_iters_per_step
-    r = cpu_reference_pagerank(p.row_offsets, p.col_indices, p.n_rows, iters,
-                               args.steps, args.warmup, nthreads)
+    r = cpu_reference_pagerank(p.row_offsets, p.col_indices, p.n_rows, iters, args.steps,
+                               args.warmup, nthreads)
     v = r["value"]
-    line = {
+    print(json.dumps({
         "metric": METRIC, "impl": "reference", "value": v, "unit": "iters/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * r["seconds"] / max(args.steps, 1),
-        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"pagerank fp32 R-MAT scale {args.scale} (transition, "
-                               f"edge factor 16, natural order); {iters} iterations per step",
+        "ms_per_step": 1e3 * r["seconds"] / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"pagerank fp32, R-MAT scale {args.scale} transition (edge factor "
+                               f"16, natural vertex order); {iters} iterations per step",
                    "scale": args.scale, "nnz": p.nnz, "n": p.n_rows, "omega": 32, "sigma": 14,
                    "block_size": 128, "threads": nthreads},
         "cpu_baseline": {"value": v, "unit": "iters/s", "cores": nthreads, "kind": "reference",
-                         "sample": f"{args.steps} x {iters} PageRank iterations of the "
-                                   f"reference MerbitBackend<float> on ThreadPool({nthreads})"},
-        "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+                         "sample": f"{args.steps} x {iters} PageRank iterations of the reference "
+                                   f"MerbitBackend<float> on ThreadPool({nthreads})"},
+        "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_preprocess_seconds": r["preprocess_seconds"],
-        "input_generation_seconds": gen,
-    }
-    print(json.dumps(line))
+        "input_generation_seconds": gen}))
     return 0
+
+
+def time_device(stream, fn, reps):
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / reps
+
+
+def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak):
+    """Plain SpMV (K2+K3) on an R-MAT matrix of the given precision."""
+    import numpy as np
+    import torch
+    t_dt = torch.float32 if dtype == np.float32 else torch.float64
+    vs = 4 if dtype == np.float32 else 8
+    A = mb.DeviceMatrix.rmat(ctx, scale, 16, seed=1, transition=True, dtype=dtype)
+    c = mb.SimtConfig.make(32, 14 if vs == 4 else 7, 128)
+    t = mb.generate_tile_for(A, c)
+    x = torch.rand(A.n_cols, device="cuda", dtype=t_dt)
+    y = torch.empty(A.n_rows, device="cuda", dtype=t_dt)
+    for _ in range(3):
+        mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr())
+    ts = time_device(stream, lambda: mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr()), reps)
+    m, n = A.nnz, A.n_rows
+    b = m * (vs + 4) + 2 * n * vs + 4 * (n + 1)
+    out = {"dtype": "f32" if vs == 4 else "f64", "ms": ts * 1e3, "gflops": 2 * m / ts / 1e9,
+           "gbs": b / ts / 1e9, "frac": b / ts / 1e9 / peak, "bytes": b, "nnz": m,
+           "preprocess_ms": t.preprocess_seconds * 1e3,
+           "preprocess_over_spmv": t.preprocess_seconds / ts}
+    del A, t, x, y
+    return out
 
 
 def main():
@@ -178,28 +210,47 @@ def main():
     ap.add_argument("--block-size", type=int, default=128)
     ap.add_argument("--ref-iters-per-step", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--spmv-reps", type=int, default=50)
+    ap.add_argument("--no-extras", action="store_true", help="skip the spmv f32/f64 extras")
+    ap.add_argument("--spmv-reps", type=int, default=30)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
 
+    import ctypes as C
+
     import numpy as np
     import torch
+    import torch.distributed as dist
 
     import paper_2605_07391_b200 as mb
+    from paper_2605_07391_b200 import _lib
+    from paper_2605_07391_b200.merbit import ShardGroup, nccl_unique_id, row_slice
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        raise SystemExit("multi-GPU bench path: see bench_multi (not in this build)")
+        # gloo only bootstraps (NCCL id broadcast, barriers, max-over-ranks);
+        # the pi exchange is the library's own NCCL all-gather
+        dist.init_process_group("gloo")
     torch.cuda.set_device(local)
-    # A real (non-NULL) stream shared by torch events and the library: the
-    # library never runs on the legacy default stream.
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = mb.Context(local)
     ctx.set_stream(stream.cuda_stream)
+    peak, peak_kind = measured_peak()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
 
     scale = args.scale
     t0 = time.perf_counter()
@@ -207,120 +258,141 @@ def main():
     gen_s = time.perf_counter() - t0
     n, m = P.n_rows, P.nnz
     cfg = mb.SimtConfig.make(32, 14, args.block_size)
-    tile = mb.generate_tile_for(P, cfg)
     prc = mb.PageRankConfig(0.85, 1e-30, args.iters, 0)
-    plan = mb.PageRankPlan(P, tile, cfg, prc)
+    ro_host = None
+    if world == 1:
+        tile = mb.generate_tile_for(P, cfg)
+        runner = mb.PageRankPlan(P, tile, cfg, prc)
+        local_rows, local_nnz = n, m
+        run = runner.run
+        pre_ms = tile.preprocess_seconds * 1e3
+    else:
+        ro_host, _, _ = P.download(want_values=False)
+        bounds = mb.plan_row_shards(ro_host, n, m, world)
+        Lm = row_slice(P, int(bounds[rank]), int(bounds[rank + 1]))
+        del P
+        tile = mb.generate_tile_for(Lm, cfg)
+        ids = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        runner = ShardGroup(ctx, n, world, bounds, rank, [(Lm, tile)], cfg, prc, ids[0])
+        local_rows, local_nnz = int(bounds[rank + 1] - bounds[rank]), Lm.nnz
+        run = runner.run
+        pre_ms = tile.preprocess_seconds * 1e3
 
     for _ in range(args.warmup):
-        plan.run()
-    torch.cuda.synchronize()
+        run()
+    barrier()
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.2)
+    launches0 = ctx.launch_count
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    launches0 = ctx.launch_count
-    torch.cuda.synchronize()
+    barrier()
     ev0.record(stream)
     for _ in range(args.steps):
-        plan.run()
+        run()
     ev1.record(stream)
-    torch.cuda.synchronize()
-    launches = ctx.launch_count - launches0
+    barrier()
     clocks = sampler.stop()
-    ms_total = ev0.elapsed_time(ev1)
-    res, hist = plan.result(want_history=True)
-    assert res.iterations == args.iters
+    launches = ctx.launch_count - launches0
+    ms_local = ev0.elapsed_time(ev1)
+    ms_total = max_over_ranks(ms_local)
+    res, hist = runner.result(want_history=True)
+    assert res.iterations == args.iters, res.iterations
     iters_per_s = args.iters * args.steps / (ms_total * 1e-3)
-    t_iter = ms_total * 1e-3 / (args.iters * args.steps)
-    peak, peak_kind = measured_peak()
-    b_iter = 8 * m + 16 * n + 4
-    achieved = b_iter / t_iter / 1e9
+    t_iter_local = ms_local * 1e-3 / (args.iters * args.steps)
+    b_iter = 8 * local_nnz + 16 * local_rows + 4
+    achieved = b_iter / t_iter_local / 1e9
 
-    # plain SpMV on the same matrix (K2 + K3), device buffers
-    x = torch.rand(n, device="cuda", dtype=torch.float32)
-    y = torch.empty(n, device="cuda", dtype=torch.float32)
-    for _ in range(5):
-        mb.spmv_device(P, tile, cfg, x.data_ptr(), y.data_ptr())
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.spmv_reps):
-        mb.spmv_device(P, tile, cfg, x.data_ptr(), y.data_ptr())
-    e1.record(stream)
-    torch.cuda.synchronize()
-    t_spmv = e0.elapsed_time(e1) * 1e-3 / args.spmv_reps
-    b_spmv = 8 * m + 12 * n + 4
+    # e2e with pinned host buffers inside the timed region
+    if world == 1:
+        pi0 = torch.full((n,), 1.0 / n, dtype=torch.float32).pin_memory()
+        pi_out = torch.empty(n, dtype=torch.float32).pin_memory()
+        L = _lib.lib()
+        cc, pc = cfg._c(), prc._c()
+        rr = _lib.mbx_pagerank_result()
 
-    # e2e: one-shot C-ABI call with pinned host buffers (pi0 in, pi out)
-    pi0 = torch.full((n,), 1.0 / n, dtype=torch.float32).pin_memory()
-    pi_out = torch.empty(n, dtype=torch.float32).pin_memory()
-    import ctypes as C
+        def e2e_call():
+            rc = L.mbx_pagerank(ctx.h, P.h, tile.h, C.byref(cc), C.byref(pc), pi0.data_ptr(),
+                                pi_out.data_ptr(), None, None, C.byref(rr))
+            if rc:
+                raise RuntimeError(L.mbx_last_error().decode())
+        h2d = d2h = 4 * n
+    else:
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        pi0 = torch.full((r1 - r0,), 1.0 / n, dtype=torch.float32).pin_memory()
+        pi_out = torch.empty(r1 - r0, dtype=torch.float32).pin_memory()
+        pi0_dev = torch.empty(n, device="cuda", dtype=torch.float32)
 
-    from paper_2605_07391_b200 import _lib
-    L = _lib.lib()
-    cc, pc = cfg._c(), prc._c()
-    rr = _lib.mbx_pagerank_result()
-
-    def e2e_call():
-        rc = L.mbx_pagerank(ctx.h, P.h, tile.h, C.byref(cc), C.byref(pc), pi0.data_ptr(),
-                            pi_out.data_ptr(), None, None, C.byref(rr))
-        if rc:
-            raise RuntimeError(L.mbx_last_error().decode())
+        def e2e_call():
+            pi0_dev[r0:r1].copy_(pi0, non_blocking=True)  # this rank's rows of pi0
+            runner.run(pi0_dev.data_ptr())
+            runner.download_local(pi_out.data_ptr())  # this rank's rows of pi
+        h2d = d2h = 4 * (r1 - r0)
     e2e_call()
-    torch.cuda.synchronize()
+    barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         e2e_call()
-    torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t0) / args.steps
+    barrier()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
     e2e_val = args.iters / e2e_s
-    mass = float(pi_out.double().sum())
+    mass = float(pi_out.double().sum()) if world == 1 else res.mass
 
+    extras = {}
     cpu = None
-    if not args.no_cpu_baseline and rank == 0:
-        import oracle as O
-        if O.ref() is not None:
-            ro, cols, _ = P.download(want_values=False)
-            nthreads = os.cpu_count() or 1
-            r = cpu_reference_pagerank(ro, cols, n, 2, 3, 1, nthreads)
-            cpu = {"value": r["value"], "unit": "iters/s", "cores": nthreads,
-                   "kind": "reference",
-                   "sample": f"3 x 2 PageRank iterations (after 1 warm-up) of the reference "
-                             f"MerbitBackend<float> on ThreadPool({nthreads}), same scale-{scale}"
-                             f" transition matrix; reference generate_tile took "
-                             f"{r['preprocess_seconds']:.2f} s"}
+    if rank == 0 and world == 1:
+        if not args.no_extras:
+            extras["spmv_f32"] = spmv_numbers(mb, ctx, stream, scale, np.float32, args.spmv_reps,
+                                              peak)
+            extras["spmv_f64"] = spmv_numbers(mb, ctx, stream, scale, np.float64, args.spmv_reps,
+                                              peak)
+        if not args.no_cpu_baseline:
+            import oracle as O
+            if O.ref() is not None:
+                ro, cols, _ = P.download(want_values=False)
+                nthreads = os.cpu_count() or 1
+                r = cpu_reference_pagerank(ro, cols, n, 2, 3, 1, nthreads)
+                cpu = {"value": r["value"], "unit": "iters/s", "cores": nthreads,
+                       "kind": "reference",
+                       "sample": f"3 x 2 PageRank iterations (after 1 warm-up) of the reference "
+                                 f"MerbitBackend<float> on ThreadPool({nthreads}), same scale-"
+                                 f"{scale} transition matrix; its generate_tile took "
+                                 f"{r['preprocess_seconds']:.2f} s"}
     line = {
         "metric": METRIC, "value": iters_per_s, "unit": "iters/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
         "config": {"workload": f"pagerank {args.iters} iterations fp32, R-MAT scale {scale} "
                                f"transition (edge factor 16, natural vertex order), "
-                               f"preprocessing amortised",
+                               f"preprocessing amortised"
+                               + (f", {world} row shards + NCCL all-gather" if world > 1 else ""),
                    "scale": scale, "n": n, "nnz": m, "omega": 32, "sigma": 14,
                    "block_size": args.block_size,
-                   "l2": "inputs (values+cols ~%.1f GB) larger than L2; no flush" % (8 * m / 1e9)},
+                   "l2": "inputs (values+cols %.1f GB per GPU) larger than L2; no flush"
+                         % (8 * local_nnz / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "PageRank iteration: spmv_w32_kernel<float,14,PR> + fixup",
-                     "bytes_per_launch": b_iter},
-        "spmv": {"ms": t_spmv * 1e3, "gflops": 2 * m / t_spmv / 1e9,
-                 "gbs": b_spmv / t_spmv / 1e9, "frac": b_spmv / t_spmv / 1e9 / peak,
-                 "bytes": b_spmv},
-        "preprocess_ms": tile.preprocess_seconds * 1e3,
-        "preprocess_over_spmv": tile.preprocess_seconds / t_spmv,
-        "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": 4 * n,
-                "d2h_bytes_per_step": 4 * n, "mass": mass},
+                     "kernel": "fused PageRank iteration (spmv_w32_kernel<float,14,PR> + "
+                               "fixup_kernel) on rank 0",
+                     "bytes_per_launch": b_iter, "us_per_iteration": t_iter_local * 1e6},
+        "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "mass": mass},
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": cpu,
+        "preprocess_ms": pre_ms,
         "l1_residual_last": res.l1_residual,
         "input_generation_seconds": gen_s,
     }
+    line.update(extras)
     if rank == 0:
         print(json.dumps(line))
+    if world > 1:
+        runner.close()
+        dist.destroy_process_group()
     return 0
 
 

@@ -279,6 +279,45 @@ MBX_API const void* mbx_pagerank_plan_reference_pi(
     const mbx_pagerank_plan* plan);
 MBX_API int mbx_pagerank_plan_destroy(mbx_pagerank_plan* plan);
 
+/* ---- multi-GPU row-sharded PageRank (one process per GPU) ---------------- */
+/* GPU g owns rows [row_bounds[g], row_bounds[g+1]) of P (mbx_plan_row_shards)
+ * with its own TILE; pi travels between iterations through one in-place
+ * ncclAllGather per iteration over NVLink, the rank's reduction scalars
+ * riding in the tail of its chunk.  Replaces the reference's single-process
+ * pagerank loop (solvers.hpp:193-215) for the sharded case; reference_iters
+ * must be 0 (the yardstick run is single-GPU). */
+typedef struct mbx_shard_group_s mbx_shard_group;
+/* ncclGetUniqueId (128 bytes), to be broadcast by the caller's bootstrap. */
+MBX_API int mbx_nccl_unique_id(void* id128);
+/* Rows [r0, r1) of a resident matrix as a new matrix (columns unchanged). */
+MBX_API int mbx_matrix_row_slice(mbx_context* ctx, const mbx_matrix* m,
+                                 int64_t r0, int64_t r1, mbx_matrix** out);
+/* nlocal shards (ranks rank0 .. rank0+nlocal-1) of a world-rank group.
+ * nccl_id NULL: every shard is local (nlocal == world), all on this context's
+ * device sharing one buffer -- no exchange is needed (single-GPU check of the
+ * sharded path).  Otherwise nlocal == 1 and NCCL connects the world. */
+MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global,
+                                   int world, const int64_t* row_bounds_host,
+                                   int rank0, int nlocal,
+                                   mbx_matrix* const* local_matrices,
+                                   mbx_tile* const* local_tiles,
+                                   const mbx_simt_config* c,
+                                   const mbx_pagerank_config* cfg,
+                                   const void* nccl_id,
+                                   mbx_shard_group** out);
+/* pi0_dev: optional start vector (n_global entries on this device; each
+ * shard reads its own rows); NULL = uniform 1/n like the reference. */
+MBX_API int mbx_shard_group_run(mbx_shard_group* group, const void* pi0_dev);
+MBX_API int mbx_shard_group_result(mbx_shard_group* group,
+                                   mbx_pagerank_result* result,
+                                   double* residual_history_host);
+/* The full pi (n_global entries) -- every rank holds all of it. */
+MBX_API int mbx_shard_group_gather_pi(mbx_shard_group* group, void* pi_host);
+/* Only this process's rows (its shards in rank order). */
+MBX_API int mbx_shard_group_download_local(mbx_shard_group* group,
+                                           void* pi_local_host);
+MBX_API int mbx_shard_group_destroy(mbx_shard_group* group);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,16 @@ SIGNATURES = {
     "mbx_pagerank_plan_pi": ([VP], VP),
     "mbx_pagerank_plan_reference_pi": ([VP], VP),
     "mbx_pagerank_plan_destroy": ([VP], C.c_int),
+    "mbx_nccl_unique_id": ([VP], C.c_int),
+    "mbx_matrix_row_slice": ([VP, VP, C.c_int64, C.c_int64, C.POINTER(VP)], C.c_int),
+    "mbx_shard_group_create": ([VP, C.c_int64, C.c_int, VP, C.c_int, C.c_int, VP, VP,
+                                C.POINTER(mbx_simt_config), C.POINTER(mbx_pagerank_config), VP,
+                                C.POINTER(VP)], C.c_int),
+    "mbx_shard_group_run": ([VP, VP], C.c_int),
+    "mbx_shard_group_result": ([VP, C.POINTER(mbx_pagerank_result), VP], C.c_int),
+    "mbx_shard_group_gather_pi": ([VP, VP], C.c_int),
+    "mbx_shard_group_download_local": ([VP, VP], C.c_int),
+    "mbx_shard_group_destroy": ([VP], C.c_int),
 }
 
 _lib = None

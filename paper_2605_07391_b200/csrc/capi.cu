@@ -23,6 +23,8 @@ namespace mbx {
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
 
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
 void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e != cudaSuccess) {
     char buf[512];

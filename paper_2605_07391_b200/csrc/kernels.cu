@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(const uint32_t* __restrict__
       acc.err = fmax(acc.err, rp[3]);
     }
   }
-  if (PR) pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, true);
+  if (PR) pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, pr.check_stop != 0);
 }
 
 // ---------------------------------------------------------------------------

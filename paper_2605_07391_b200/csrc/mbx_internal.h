@@ -18,6 +18,7 @@ struct Error {
 };
 
 [[noreturn]] void fail(int code, const std::string& msg);
+void set_last_error(const std::string& msg);
 void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 
 #define MBX_CUDA(call) ::mbx::cuda_check((call), #call, __FILE__, __LINE__)
@@ -79,6 +80,9 @@ struct PrArgs {
   int* stop_iter = nullptr;    // iteration that set stop
   int iter = 0;                // 1-based
   double err_tol = 0.0;
+  // 1: K3's last block decides convergence.  0 (row shards): the scalars are
+  // partial; the combine kernel after the exchange decides.
+  int check_stop = 1;
 };
 
 }  // namespace mbx

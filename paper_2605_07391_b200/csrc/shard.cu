@@ -1,0 +1,557 @@
+// shard.cu -- row-sharded multi-GPU PageRank (BASELINE config C4).
+//
+// One process per GPU.  GPU g owns the merge-path-balanced row block
+// [b_g, b_{g+1}) of P (mbx_plan_row_shards: diagonal cuts snapped to row
+// starts) with its own TILE; its column indices are remapped once into the
+// padded exchange layout  pos(v) = owner(v) * chunk + (v - b_owner(v)),  so
+// one in-place ncclAllGather of equal-size chunks per iteration delivers the
+// whole pi vector to every GPU.  The tail of each chunk carries that rank's
+// fp64 reduction scalars (dangling mass, L1 residual, mass, ERR), so the
+// same collective doubles as the all-reduce; a one-warp combine kernel folds
+// the G tails in rank order (deterministic, identical on every rank) and
+// decides convergence.  Iteration = K2 + K3 (PR mode, local rows) ->
+// ncclAllGather -> combine, captured once as a CUDA graph.
+//
+// Virtual mode (nccl_id == NULL, nlocal == world): all shards live in one
+// process on one device and write into one shared buffer, so no exchange is
+// needed -- the sharded kernels, remap and combine are verified on a single
+// GPU (tests/test_gpu_shards.py).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mbx_internal.h"
+
+#define MBX_NCCL(call)                                                                   \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      ::mbx::fail(MBX_NCCL_ERROR, std::string("NCCL error ") + ncclGetErrorString(r_) + \
+                                      " in " #call);                                     \
+  } while (0)
+
+namespace mbx {
+namespace {
+
+__global__ void remap_cols_kernel(const int32_t* __restrict__ in, int64_t nnz,
+                                  const int64_t* __restrict__ bounds, int world,
+                                  int64_t chunk_elems, int32_t* __restrict__ out) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t v = in[k];
+    int g = 0;
+    while (g + 1 < world && bounds[g + 1] <= v) ++g;
+    out[k] = int32_t(int64_t(g) * chunk_elems + (v - bounds[g]));
+  }
+}
+
+__global__ void seen_flags_kernel(const int32_t* __restrict__ cols, int64_t nnz, uint8_t* seen) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
+       k += int64_t(gridDim.x) * blockDim.x)
+    seen[cols[k]] = 1;
+}
+
+__global__ void local_dangling_kernel(const uint8_t* __restrict__ seen, int64_t r0, int64_t rows,
+                                      uint32_t* __restrict__ bits) {
+  const int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= (rows + 31) / 32) return;
+  uint32_t v = 0;
+  for (int b = 0; b < 32; ++b) {
+    const int64_t i = w * 32 + b;
+    if (i < rows && !seen[r0 + i]) v |= 1u << b;
+  }
+  bits[w] = v;
+}
+
+// pi_0 = 1/n on the shard's rows; the rank's dangling count goes to the
+// tail as an exact integer, so its mass (count * 1/n in fp64) is exact and
+// independent of the reduction order.
+template <typename T>
+__global__ void shard_init_kernel(T* __restrict__ pi, int64_t rows, T val,
+                                  const uint32_t* __restrict__ dangling,
+                                  unsigned long long* count) {
+  unsigned long long c = 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    pi[i] = val;
+    if ((i & 31) == 0) c += __popc(dangling[i >> 5] & (rows - i >= 32 ? 0xFFFFFFFFu
+                                                                       : (1u << (rows - i)) - 1u));
+  }
+  for (int o = 16; o >= 1; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+__global__ void shard_init_tail_kernel(const unsigned long long* count, int64_t rows, double val,
+                                       PrScalars* tail) {
+  tail->dangling = double(*count) * val;
+  tail->mass = double(rows) * val;
+  tail->resid = 0.0;
+  tail->err = 0.0;
+}
+
+// Fold the world tails in rank order into the global scalars of iteration
+// `iter` and decide convergence (solvers.hpp:201-213).
+__global__ void combine_kernel(const unsigned char* __restrict__ pi_base, int64_t chunk_bytes,
+                               int64_t tail_off, int world, PrScalars* out, int* stop,
+                               int* stop_iter, int iter, double err_tol) {
+  if (threadIdx.x != 0) return;
+  if (stop && *stop) return;
+  double d = 0.0, r = 0.0, m = 0.0, e = 0.0;
+  for (int g = 0; g < world; ++g) {
+    const PrScalars* t =
+        reinterpret_cast<const PrScalars*>(pi_base + int64_t(g) * chunk_bytes + tail_off);
+    d += t->dangling;
+    r += t->resid;
+    m += t->mass;
+    e = fmax(e, t->err);
+  }
+  out->dangling = d;
+  out->resid = r;
+  out->mass = m;
+  out->err = e;
+  if (iter > 0 && stop) {
+    if (m == 0.0) {
+      *stop = 2;
+      *stop_iter = iter;
+    } else if (e < err_tol) {
+      *stop = 1;
+      *stop_iter = iter;
+    }
+  }
+}
+
+__global__ void slice_rows_kernel(const uint32_t* __restrict__ ro, int64_t r0, int64_t rows,
+                                  uint32_t* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= rows;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = ro[r0 + i] - ro[r0];
+}
+
+struct Shard {
+  int g = 0;
+  int64_t r0 = 0, r1 = 0;
+  mbx_matrix view{};  // the local matrix with remapped columns (non-owning)
+  const mbx_tile* tile = nullptr;
+  Geometry geo;
+  int32_t* cols_remap = nullptr;
+  uint32_t* dangling = nullptr;
+  double* range_part = nullptr;
+  double* block_part = nullptr;
+  unsigned int* counter = nullptr;
+  void* carry_ws = nullptr;
+};
+
+}  // namespace
+}  // namespace mbx
+
+struct mbx_shard_group_s {
+  mbx_context* ctx = nullptr;
+  int precision = MBX_F32;
+  size_t vs = 4;
+  int world = 1, rank0 = 0, nlocal = 1;
+  int64_t n = 0;
+  std::vector<int64_t> bounds;
+  int64_t chunk_bytes = 0, chunk_elems = 0, tail_off = 0;
+  void* pi[2] = {nullptr, nullptr};
+  std::vector<mbx::Shard> shards;
+  mbx::PrScalars* gscal = nullptr;
+  int* flags = nullptr;
+  ncclComm_t comm = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int64_t graph_launches = 0;
+  mbx_simt_config c{};
+  mbx_pagerank_config cfg{};
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bool ran = false;
+};
+
+namespace {
+
+template <typename F>
+int sguard(F&& f) {
+  try {
+    f();
+    return MBX_OK;
+  } catch (const mbx::Error& e) {
+    mbx::set_last_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    mbx::set_last_error(e.what());
+    return MBX_ERROR;
+  }
+}
+
+void* dm(mbx_context* ctx, size_t b) {
+  void* p = nullptr;
+  MBX_CUDA(cudaMallocAsync(&p, std::max<size_t>(b, 256), ctx->stream));
+  return p;
+}
+
+void exchange_and_combine(mbx_shard_group* G, int slot, int iter) {
+  mbx_context* ctx = G->ctx;
+  unsigned char* base = static_cast<unsigned char*>(G->pi[slot]);
+  if (G->comm) {
+    // in-place all-gather: each rank's chunk (pi rows + scalar tail)
+    MBX_NCCL(ncclAllGather(base + int64_t(G->rank0) * G->chunk_bytes, base, G->chunk_bytes,
+                           ncclUint8, G->comm, ctx->stream));
+  }
+  mbx::combine_kernel<<<1, 32, 0, ctx->stream>>>(base, G->chunk_bytes, G->tail_off, G->world,
+                                                 G->gscal + iter, G->flags, G->flags + 1, iter,
+                                                 G->cfg.err_tol);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
+void launch_iteration(mbx_shard_group* G, int64_t r) {
+  mbx_context* ctx = G->ctx;
+  const int src = int((r - 1) & 1), dst = int(r & 1);
+  for (mbx::Shard& s : G->shards) {
+    mbx::PrArgs a;
+    unsigned char* pold = static_cast<unsigned char*>(G->pi[src]) + int64_t(s.g) * G->chunk_bytes;
+    unsigned char* pnew = static_cast<unsigned char*>(G->pi[dst]) + int64_t(s.g) * G->chunk_bytes;
+    a.pi_old = pold;
+    a.dangling = s.dangling;
+    a.yardstick = nullptr;
+    a.yard_const = G->precision == MBX_F32 ? double(1.0f / float(G->n)) : 1.0 / double(G->n);
+    a.damping = G->cfg.damping;
+    a.inv_n = 1.0 / double(G->n);
+    a.prev = G->gscal + (r - 1);
+    a.next = reinterpret_cast<mbx::PrScalars*>(pnew + G->tail_off);
+    a.range_part = s.range_part;
+    a.block_part = s.block_part;
+    a.done_counter = s.counter;
+    a.stop = G->flags;
+    a.stop_iter = G->flags + 1;
+    a.iter = int(r);
+    a.err_tol = G->cfg.err_tol;
+    a.check_stop = 0;
+    mbx::launch_spmv(ctx, &s.view, s.tile, s.geo, G->pi[src], pnew, s.carry_ws, &a);
+  }
+  exchange_and_combine(G, dst, int(r));
+}
+
+}  // namespace
+
+extern "C" {
+
+MBX_API int mbx_nccl_unique_id(void* id128) {
+  return sguard([&] {
+    ncclUniqueId id;
+    MBX_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "NCCL unique id is 128 bytes");
+    std::memcpy(id128, &id, sizeof(id));
+  });
+}
+
+MBX_API int mbx_matrix_row_slice(mbx_context* ctx, const mbx_matrix* m, int64_t r0, int64_t r1,
+                                 mbx_matrix** out) {
+  return sguard([&] {
+    if (r0 < 0 || r1 < r0 || r1 > m->n_rows) mbx::fail(MBX_DIMENSION_ERROR, "row slice out of range");
+    uint32_t b[2];
+    MBX_CUDA(cudaMemcpyAsync(&b[0], m->ro + r0, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MBX_CUDA(cudaMemcpyAsync(&b[1], m->ro + r1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    auto s = std::make_unique<mbx_matrix>();
+    s->ctx = ctx;
+    s->precision = m->precision;
+    s->n_rows = r1 - r0;
+    s->n_cols = m->n_cols;
+    s->nnz = int64_t(b[1]) - int64_t(b[0]);
+    const size_t vs = mbx::value_size(m->precision);
+    s->vals = dm(ctx, s->nnz * vs + 256);
+    s->cols = static_cast<int32_t*>(dm(ctx, s->nnz * 4 + 256));
+    s->ro = static_cast<uint32_t*>(dm(ctx, (s->n_rows + 1) * 4 + 64));
+    MBX_CUDA(cudaMemsetAsync(s->vals, 0, s->nnz * vs + 256, ctx->stream));
+    MBX_CUDA(cudaMemsetAsync(s->cols, 0, s->nnz * 4 + 256, ctx->stream));
+    if (s->nnz) {
+      MBX_CUDA(cudaMemcpyAsync(s->vals, static_cast<char*>(m->vals) + int64_t(b[0]) * vs,
+                               s->nnz * vs, cudaMemcpyDeviceToDevice, ctx->stream));
+      MBX_CUDA(cudaMemcpyAsync(s->cols, m->cols + b[0], s->nnz * 4, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    }
+    mbx::slice_rows_kernel<<<unsigned(ctx->sm_count) * 4, 256, 0, ctx->stream>>>(m->ro, r0, s->n_rows,
+                                                                                 s->ro);
+    ++ctx->launches;
+    MBX_CUDA(cudaGetLastError());
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = s.release();
+  });
+}
+
+MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world,
+                                   const int64_t* bounds, int rank0, int nlocal,
+                                   mbx_matrix* const* mats, mbx_tile* const* tiles,
+                                   const mbx_simt_config* c, const mbx_pagerank_config* cfg,
+                                   const void* nccl_id, mbx_shard_group** out) {
+  return sguard([&] {
+    if (world < 1 || nlocal < 1 || rank0 < 0 || rank0 + nlocal > world)
+      mbx::fail(MBX_CONFIG_ERROR, "shard group: bad world/rank/nlocal");
+    if (!nccl_id && nlocal != world)
+      mbx::fail(MBX_CONFIG_ERROR, "shard group: without NCCL every shard must be local");
+    if (cfg->reference_iters != 0)
+      mbx::fail(MBX_UNSUPPORTED, "shard group: the yardstick run (reference_iters > 0) is "
+                                 "single-GPU only");
+    if (!(cfg->damping >= 0.0 && cfg->damping <= 1.0))
+      mbx::fail(MBX_CONFIG_ERROR, "damping must lie in [0, 1]");
+    if (!(cfg->err_tol > 0.0)) mbx::fail(MBX_CONFIG_ERROR, "err_tol must be positive");
+    if (bounds[0] != 0 || bounds[world] != n_global)
+      mbx::fail(MBX_DIMENSION_ERROR, "row bounds must cover [0, n)");
+    auto G = std::make_unique<mbx_shard_group_s>();
+    G->ctx = ctx;
+    G->precision = mats[0]->precision;
+    G->vs = mbx::value_size(G->precision);
+    G->world = world;
+    G->rank0 = rank0;
+    G->nlocal = nlocal;
+    G->n = n_global;
+    G->bounds.assign(bounds, bounds + world + 1);
+    G->c = *c;
+    G->cfg = *cfg;
+    if (G->precision == MBX_F32) {
+      G->cfg.damping = double(float(cfg->damping));
+      G->cfg.err_tol = double(float(cfg->err_tol));
+    }
+    int64_t rows_max = 0;
+    for (int g = 0; g < world; ++g) rows_max = std::max(rows_max, bounds[g + 1] - bounds[g]);
+    G->tail_off = ((rows_max * int64_t(G->vs) + 255) / 256) * 256;
+    G->chunk_bytes = G->tail_off + 256;
+    G->chunk_elems = G->chunk_bytes / int64_t(G->vs);
+    if (G->chunk_elems * world >= (int64_t(1) << 31))
+      mbx::fail(MBX_CAPACITY_ERROR, "padded exchange layout exceeds int32 column indices");
+    cudaStream_t st = ctx->stream;
+    for (int i = 0; i < 2; ++i) {
+      G->pi[i] = dm(ctx, G->chunk_bytes * world);
+      MBX_CUDA(cudaMemsetAsync(G->pi[i], 0, G->chunk_bytes * world, st));
+    }
+    G->gscal = static_cast<mbx::PrScalars*>(dm(ctx, (cfg->max_iters + 1) * sizeof(mbx::PrScalars)));
+    MBX_CUDA(cudaMemsetAsync(G->gscal, 0, (cfg->max_iters + 1) * sizeof(mbx::PrScalars), st));
+    G->flags = static_cast<int*>(dm(ctx, 64));
+    int64_t* dbounds = static_cast<int64_t*>(dm(ctx, (world + 1) * 8));
+    MBX_CUDA(cudaMemcpyAsync(dbounds, bounds, (world + 1) * 8, cudaMemcpyHostToDevice, st));
+    // dangling vertices = empty columns of the GLOBAL P
+    uint8_t* seen = static_cast<uint8_t*>(dm(ctx, n_global + 64));
+    MBX_CUDA(cudaMemsetAsync(seen, 0, n_global + 64, st));
+    for (int i = 0; i < nlocal; ++i) {
+      if (mats[i]->nnz)
+        mbx::seen_flags_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, st>>>(mats[i]->cols,
+                                                                            mats[i]->nnz, seen);
+    }
+    if (nccl_id) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      MBX_CUDA(cudaStreamSynchronize(st));
+      MBX_NCCL(ncclCommInitRank(&G->comm, world, id, rank0));
+      MBX_NCCL(ncclAllReduce(seen, seen, n_global, ncclUint8, ncclMax, G->comm, st));
+    }
+    for (int i = 0; i < nlocal; ++i) {
+      mbx_matrix* m = mats[i];
+      const int g = rank0 + i;
+      if (m->n_rows != bounds[g + 1] - bounds[g] || m->n_cols != n_global)
+        mbx::fail(MBX_DIMENSION_ERROR, "shard matrix shape does not match its row bounds");
+      if (tiles[i]->info.n_rows != m->n_rows || tiles[i]->info.nnz != m->nnz ||
+          tiles[i]->info.omega != c->omega || tiles[i]->info.sigma != c->sigma)
+        mbx::fail(MBX_CONFIG_ERROR, "shard TILE does not match its matrix / config");
+      mbx::Shard s;
+      s.g = g;
+      s.r0 = bounds[g];
+      s.r1 = bounds[g + 1];
+      s.tile = tiles[i];
+      s.cols_remap = static_cast<int32_t*>(dm(ctx, m->nnz * 4 + 256));
+      MBX_CUDA(cudaMemsetAsync(s.cols_remap, 0, m->nnz * 4 + 256, st));
+      if (m->nnz)
+        mbx::remap_cols_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, st>>>(
+            m->cols, m->nnz, dbounds, world, G->chunk_elems, s.cols_remap);
+      s.view = *m;
+      s.view.cols = s.cols_remap;
+      s.view.cols_hub = nullptr;
+      s.view.hub_cols = nullptr;
+      s.view.hub_avail = 0;
+      s.view.n_cols = G->chunk_elems * world;
+      const int64_t rows = s.r1 - s.r0;
+      s.dangling = static_cast<uint32_t*>(dm(ctx, ((rows + 31) / 32) * 4 + 64));
+      mbx::local_dangling_kernel<<<unsigned((rows + 31) / 32 / 256 + 1), 256, 0, st>>>(
+          seen, s.r0, rows, s.dangling);
+      s.geo = mbx::make_geometry(ctx, &s.view, s.tile, c->block_size);
+      s.range_part = static_cast<double*>(dm(ctx, (s.geo.num_ranges + 1) * 4 * sizeof(double)));
+      // K3 blocks, or the pr_init grid (sm_count * 4) when a start vector is given
+      const int64_t nblk = std::max<int64_t>((s.geo.num_ranges + 255) / 256 + 1, ctx->sm_count * 4 + 1);
+      s.block_part = static_cast<double*>(dm(ctx, nblk * 4 * sizeof(double)));
+      s.counter = static_cast<unsigned int*>(dm(ctx, 64));
+      MBX_CUDA(cudaMemsetAsync(s.counter, 0, 64, st));
+      s.carry_ws = dm(ctx, mbx::spmv_workspace_bytes(s.geo, G->precision, true));
+      ctx->launches += 2;
+      G->shards.push_back(s);
+    }
+    MBX_CUDA(cudaGetLastError());
+    MBX_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(seen, st);
+    cudaFreeAsync(dbounds, st);
+    MBX_CUDA(cudaEventCreate(&G->e0));
+    MBX_CUDA(cudaEventCreate(&G->e1));
+    if (cfg->max_iters > 0 && cfg->max_iters <= 4096) {
+      MBX_CUDA(cudaStreamSynchronize(st));
+      const int64_t before = ctx->launches;
+      cudaGraph_t graph;
+      MBX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        for (int64_t r = 1; r <= cfg->max_iters; ++r) launch_iteration(G.get(), r);
+      } catch (...) {
+        cudaStreamEndCapture(st, &graph);
+        throw;
+      }
+      MBX_CUDA(cudaStreamEndCapture(st, &graph));
+      MBX_CUDA(cudaGraphInstantiate(&G->graph, graph, 0));
+      cudaGraphDestroy(graph);
+      G->graph_launches = ctx->launches - before;
+      ctx->launches = before;
+    }
+    *out = G.release();
+  });
+}
+
+MBX_API int mbx_shard_group_run(mbx_shard_group* G, const void* pi0_dev) {
+  return sguard([&] {
+    mbx_context* ctx = G->ctx;
+    cudaStream_t st = ctx->stream;
+    MBX_CUDA(cudaMemsetAsync(G->flags, 0, 8, st));
+    for (mbx::Shard& s : G->shards) {
+      unsigned char* p0 = static_cast<unsigned char*>(G->pi[0]) + int64_t(s.g) * G->chunk_bytes;
+      const int64_t rows = s.r1 - s.r0;
+      auto* tail = reinterpret_cast<mbx::PrScalars*>(p0 + G->tail_off);
+      if (pi0_dev) {
+        // caller's start vector: copy this shard's rows, reduce its dangling
+        // mass and mass deterministically into the chunk tail
+        mbx::launch_pr_init(ctx, G->precision, rows,
+                            static_cast<const char*>(pi0_dev) + s.r0 * int64_t(G->vs), p0,
+                            s.dangling, tail, s.block_part, s.counter);
+        continue;
+      }
+      auto* cnt = reinterpret_cast<unsigned long long*>(s.counter + 8);
+      MBX_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
+      const unsigned grid = unsigned(ctx->sm_count) * 4;
+      double val;
+      if (G->precision == MBX_F32) {
+        const float v = 1.0f / float(G->n);  // T(1)/static_cast<T>(n) (solvers.hpp:193)
+        val = double(v);
+        mbx::shard_init_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<float*>(p0), rows, v,
+                                                            s.dangling, cnt);
+      } else {
+        val = 1.0 / double(G->n);
+        mbx::shard_init_kernel<double><<<grid, 256, 0, st>>>(reinterpret_cast<double*>(p0), rows,
+                                                             val, s.dangling, cnt);
+      }
+      mbx::shard_init_tail_kernel<<<1, 1, 0, st>>>(cnt, rows, val, tail);
+      ctx->launches += 2;
+    }
+    MBX_CUDA(cudaGetLastError());
+    exchange_and_combine(G, 0, 0);
+    MBX_CUDA(cudaEventRecord(G->e0, st));
+    if (G->graph) {
+      MBX_CUDA(cudaGraphLaunch(G->graph, st));
+      ctx->launches += G->graph_launches;
+    } else {
+      for (int64_t r = 1; r <= G->cfg.max_iters; ++r) launch_iteration(G, r);
+    }
+    MBX_CUDA(cudaEventRecord(G->e1, st));
+    G->ran = true;
+  });
+}
+
+MBX_API int mbx_shard_group_result(mbx_shard_group* G, mbx_pagerank_result* res,
+                                   double* history) {
+  return sguard([&] {
+    if (!G->ran) mbx::fail(MBX_ERROR, "shard group has not run");
+    cudaStream_t st = G->ctx->stream;
+    int flags[2];
+    MBX_CUDA(cudaMemcpyAsync(flags, G->flags, 8, cudaMemcpyDeviceToHost, st));
+    std::vector<mbx::PrScalars> sc(G->cfg.max_iters + 1);
+    MBX_CUDA(cudaMemcpyAsync(sc.data(), G->gscal, sc.size() * sizeof(mbx::PrScalars),
+                             cudaMemcpyDeviceToHost, st));
+    MBX_CUDA(cudaStreamSynchronize(st));
+    const int64_t iters = flags[0] ? flags[1] : G->cfg.max_iters;
+    if (flags[0] == 2)
+      mbx::fail(MBX_ERROR, "pagerank: zero-norm iterate at iteration " + std::to_string(iters));
+    float ms = 0.f;
+    MBX_CUDA(cudaEventElapsedTime(&ms, G->e0, G->e1));
+    res->iterations = iters;
+    res->status = flags[0] == 1 ? 0 : 1;
+    res->final_err = iters > 0 ? sc[iters].err : 0.0;
+    res->preprocess_seconds = 0.0;
+    for (auto& s : G->shards) res->preprocess_seconds += s.tile->info.preprocess_seconds;
+    res->iterate_seconds = ms * 1e-3;
+    res->l1_residual = iters > 0 ? sc[iters].resid : 0.0;
+    res->mass = sc[iters].mass;
+    res->dangling_mass = sc[iters].dangling;
+    if (history)
+      for (int64_t r = 1; r <= G->cfg.max_iters; ++r) history[r - 1] = r <= iters ? sc[r].resid : 0.0;
+  });
+}
+
+// The full pi (every rank holds all chunks after the final exchange).
+MBX_API int mbx_shard_group_gather_pi(mbx_shard_group* G, void* pi_host) {
+  return sguard([&] {
+    cudaStream_t st = G->ctx->stream;
+    int flags[2];
+    MBX_CUDA(cudaMemcpyAsync(flags, G->flags, 8, cudaMemcpyDeviceToHost, st));
+    MBX_CUDA(cudaStreamSynchronize(st));
+    const int64_t iters = flags[0] ? flags[1] : G->cfg.max_iters;
+    const unsigned char* base = static_cast<const unsigned char*>(G->pi[iters & 1]);
+    for (int g = 0; g < G->world; ++g) {
+      const int64_t rows = G->bounds[g + 1] - G->bounds[g];
+      if (rows)
+        MBX_CUDA(cudaMemcpyAsync(static_cast<char*>(pi_host) + G->bounds[g] * int64_t(G->vs),
+                                 base + int64_t(g) * G->chunk_bytes, rows * G->vs,
+                                 cudaMemcpyDeviceToHost, st));
+    }
+    MBX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+// This process's rows of the final pi (its shards in rank order) to host.
+MBX_API int mbx_shard_group_download_local(mbx_shard_group* G, void* pi_local_host) {
+  return sguard([&] {
+    cudaStream_t st = G->ctx->stream;
+    int flags[2];
+    MBX_CUDA(cudaMemcpyAsync(flags, G->flags, 8, cudaMemcpyDeviceToHost, st));
+    MBX_CUDA(cudaStreamSynchronize(st));
+    const int64_t iters = flags[0] ? flags[1] : G->cfg.max_iters;
+    const unsigned char* base = static_cast<const unsigned char*>(G->pi[iters & 1]);
+    int64_t off = 0;
+    for (const mbx::Shard& s : G->shards) {
+      const int64_t rows = s.r1 - s.r0;
+      if (rows)
+        MBX_CUDA(cudaMemcpyAsync(static_cast<char*>(pi_local_host) + off * int64_t(G->vs),
+                                 base + int64_t(s.g) * G->chunk_bytes, rows * G->vs,
+                                 cudaMemcpyDeviceToHost, st));
+      off += rows;
+    }
+    MBX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+MBX_API int mbx_shard_group_destroy(mbx_shard_group* G) {
+  return sguard([&] {
+    if (!G) return;
+    cudaStream_t st = G->ctx->stream;
+    if (G->graph) cudaGraphExecDestroy(G->graph);
+    for (mbx::Shard& s : G->shards) {
+      for (void* p : {static_cast<void*>(s.cols_remap), static_cast<void*>(s.dangling),
+                      static_cast<void*>(s.range_part), static_cast<void*>(s.block_part),
+                      static_cast<void*>(s.counter), s.carry_ws})
+        if (p) cudaFreeAsync(p, st);
+    }
+    for (void* p : {G->pi[0], G->pi[1], static_cast<void*>(G->gscal), static_cast<void*>(G->flags)})
+      if (p) cudaFreeAsync(p, st);
+    if (G->e0) cudaEventDestroy(G->e0);
+    if (G->e1) cudaEventDestroy(G->e1);
+    cudaStreamSynchronize(st);
+    if (G->comm) ncclCommDestroy(G->comm);
+    delete G;
+  });
+}
+
+}  // extern "C"

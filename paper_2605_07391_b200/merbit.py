@@ -599,3 +599,70 @@ class PageRankPlan:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU row shards (shard.cu)
+# ---------------------------------------------------------------------------
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.lib().mbx_nccl_unique_id(buf))
+    return buf.raw
+
+
+def row_slice(m: DeviceMatrix, r0: int, r1: int) -> DeviceMatrix:
+    h = C.c_void_p()
+    _check(_lib.lib().mbx_matrix_row_slice(m.ctx.h, m.h, r0, r1, C.byref(h)))
+    return DeviceMatrix(m.ctx, h)
+
+
+class ShardGroup:
+    """Row-sharded PageRank: `shards` = [(DeviceMatrix, Tile)] owned by this
+    process for ranks rank0 .. rank0+len(shards)-1 of `world`.  nccl_id None:
+    all shards local, sharing one buffer (single-GPU check of the sharded
+    path); otherwise one shard per process joined over NCCL."""
+
+    def __init__(self, ctx: Context, n_global: int, world: int, bounds, rank0: int, shards,
+                 c: SimtConfig, cfg: PageRankConfig, nccl_id: bytes | None = None):
+        self.ctx, self.n, self.world, self.cfg = ctx, n_global, world, cfg
+        self.keep = shards
+        self.bounds = np.ascontiguousarray(bounds, np.int64)
+        mats = (C.c_void_p * len(shards))(*[m.h.value for m, _ in shards])
+        tiles = (C.c_void_p * len(shards))(*[t.h.value for _, t in shards])
+        self.dtype = shards[0][0].dtype
+        cc, pc = c._c(), cfg._c()
+        idb = None if nccl_id is None else C.create_string_buffer(nccl_id, 128)
+        h = C.c_void_p()
+        _check(_lib.lib().mbx_shard_group_create(ctx.h, n_global, world, _ptr(self.bounds), rank0,
+                                                 len(shards), mats, tiles, C.byref(cc), C.byref(pc),
+                                                 idb, C.byref(h)))
+        self.h = h
+
+    def run(self, pi0_ptr: int | None = None):
+        _check(_lib.lib().mbx_shard_group_run(self.h, pi0_ptr))
+
+    def result(self, want_history=False):
+        res = mbx_pagerank_result()
+        hist = np.zeros(max(self.cfg.max_iters, 1), np.float64) if want_history else None
+        _check(_lib.lib().mbx_shard_group_result(self.h, C.byref(res), _ptr(hist)))
+        return res, hist
+
+    def gather_pi(self):
+        pi = np.zeros(self.n, self.dtype)
+        _check(_lib.lib().mbx_shard_group_gather_pi(self.h, _ptr(pi)))
+        return pi
+
+    def download_local(self, host_ptr: int):
+        """This process's rows of the final pi into host memory at host_ptr."""
+        _check(_lib.lib().mbx_shard_group_download_local(self.h, host_ptr))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lib().mbx_shard_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,92 @@
+"""CPU, world_size 2 over gloo: the multi-GPU exchange protocol of shard.cu
+(merge-path row bounds from the product's mbx_plan_row_shards, padded chunks
+with an fp64 scalar tail, one all-gather per iteration, rank-order combine)
+reproduces the single-process PageRank.  The per-shard multiply here is the
+CPU oracle (the checker) -- this test covers the host logic and layout; the
+device kernels of the same protocol are covered by tests/test_gpu_shards.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as tmp
+
+import oracle as O
+import paper_2605_07391_b200 as mb
+
+SCALE, ITERS, C_ = 10, 30, 0.85
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p = O.rmat(SCALE, 16, 11, transposed=True)
+    n = p.n_rows
+    vals = O.transition_values(n, p.col_indices, np.float64)
+    b = mb.plan_row_shards(p.row_offsets, n, p.nnz, world)  # product host logic
+    rows_max = int(np.diff(b).max())
+    chunk = rows_max + 4  # pi rows, then 4 fp64 scalars (dangling, resid, mass, err)
+    r0, r1 = int(b[rank]), int(b[rank + 1])
+    ro = p.row_offsets[r0:r1 + 1] - p.row_offsets[r0]
+    cols = p.col_indices[p.row_offsets[r0]:p.row_offsets[r1]]
+    v = vals[p.row_offsets[r0]:p.row_offsets[r1]]
+    local = O.Csr(r1 - r0, n, ro, cols, v)
+    seen = torch.zeros(n, dtype=torch.uint8)
+    seen[torch.from_numpy(cols.astype(np.int64))] = 1
+    dist.all_reduce(seen, op=dist.ReduceOp.MAX)  # global empty columns
+    dang = (seen.numpy() == 0)[r0:r1]
+    # padded exchange buffer [world][chunk]
+    buf = torch.zeros(world * chunk, dtype=torch.float64)
+    pi_local = np.full(r1 - r0, 1.0 / n)
+    mine = torch.zeros(chunk, dtype=torch.float64)
+    mine[:r1 - r0] = torch.from_numpy(pi_local)
+    mine[rows_max] = pi_local[dang].sum()
+    dist.all_gather_into_tensor(buf, mine)
+    for _ in range(ITERS):
+        full = np.concatenate([buf[g * chunk:g * chunk + (b[g + 1] - b[g])].numpy()
+                               for g in range(world)])
+        dm = sum(float(buf[g * chunk + rows_max]) for g in range(world))  # rank order
+        w = O.spmv_csr_f64(local, full)
+        new = C_ * w + (C_ * dm + 1 - C_) / n
+        mine = torch.zeros(chunk, dtype=torch.float64)
+        mine[:r1 - r0] = torch.from_numpy(new)
+        mine[rows_max] = new[dang].sum()
+        mine[rows_max + 1] = np.abs(new - pi_local).sum()
+        pi_local = new
+        dist.all_gather_into_tensor(buf, mine)
+    full = np.concatenate([buf[g * chunk:g * chunk + (b[g + 1] - b[g])].numpy()
+                           for g in range(world)])
+    q.put((rank, full, [int(x) for x in b]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_two_rank_exchange_protocol(world):
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    out.sort(key=lambda t: t[0])
+    assert out[0][2] == out[1][2]  # both ranks derived identical bounds
+    assert np.array_equal(out[0][1], out[1][1])  # every rank holds the same pi
+    p = O.rmat(SCALE, 16, 11, transposed=True)
+    p64 = O.Csr(p.n_rows, p.n_cols, p.row_offsets, p.col_indices,
+                O.transition_values(p.n_rows, p.col_indices, np.float64))
+    want = O.pagerank(p64, C_, 1e-300, ITERS, 0)["pi"]
+    assert np.abs(out[0][1] - want).sum() <= 1e-13
