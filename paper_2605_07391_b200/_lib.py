@@ -119,6 +119,12 @@ def lib():
             raise RuntimeError(
                 f"{LIB_PATH} not built: run __graft_entry__.build() "
                 "(make -C paper_2605_07391_b200/csrc); there is no CPU fallback")
+        try:
+            # let PyTorch load its CUDA runtime pieces (and its NCCL) first;
+            # the library resolves NCCL lazily and reuses an already-loaded one
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         L = C.CDLL(LIB_PATH)
         for name, (args, res) in SIGNATURES.items():
             fn = getattr(L, name)

@@ -371,6 +371,12 @@ MBX_API int mbx_context_create(int device, mbx_context** out) {
     ctx->device = device;
     ctx->sm_count = prop.multiProcessorCount;
     Device dg(device);
+    // keep freed stream-ordered allocations in the pool: per-call buffers
+    // (PageRank plans, staging) must not be re-mapped from the OS each call
+    cudaMemPool_t pool;
+    MBX_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    MBX_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     MBX_CUDA(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
     ctx->stream = ctx->own;
     *out = ctx.release();

@@ -16,26 +16,70 @@
 // process on one device and write into one shared buffer, so no exchange is
 // needed -- the sharded kernels, remap and combine are verified on a single
 // GPU (tests/test_gpu_shards.py).
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "mbx_internal.h"
 
-#define MBX_NCCL(call)                                                                   \
-  do {                                                                                   \
-    ncclResult_t r_ = (call);                                                            \
-    if (r_ != ncclSuccess)                                                               \
-      ::mbx::fail(MBX_NCCL_ERROR, std::string("NCCL error ") + ncclGetErrorString(r_) + \
-                                      " in " #call);                                     \
-  } while (0)
-
 namespace mbx {
 namespace {
+
+// NCCL is resolved at first use, not linked: a process that already loaded
+// an NCCL (e.g. PyTorch's) keeps using that one -- two libnccl.so.2 of
+// different versions in one process break each other's symbol resolution.
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+const Nccl& nccl() {
+  static Nccl api{};
+  static std::string err;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    api.GetErrorString =
+        reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllGather ||
+        !api.AllReduce || !api.GetErrorString) {
+      err = "libnccl.so.2 lacks a required symbol";
+      api.GetUniqueId = nullptr;
+    }
+  });
+  if (!api.GetUniqueId) fail(MBX_NCCL_ERROR, err);
+  return api;
+}
+
+#define MBX_NCCL(call)                                                                \
+  do {                                                                                \
+    ncclResult_t r_ = (call);                                                         \
+    if (r_ != ncclSuccess)                                                            \
+      ::mbx::fail(MBX_NCCL_ERROR, std::string("NCCL error ") +                        \
+                                      ::mbx::nccl().GetErrorString(r_) + " in " #call); \
+  } while (0)
 
 __global__ void remap_cols_kernel(const int32_t* __restrict__ in, int64_t nnz,
                                   const int64_t* __restrict__ bounds, int world,
@@ -196,7 +240,7 @@ void exchange_and_combine(mbx_shard_group* G, int slot, int iter) {
   unsigned char* base = static_cast<unsigned char*>(G->pi[slot]);
   if (G->comm) {
     // in-place all-gather: each rank's chunk (pi rows + scalar tail)
-    MBX_NCCL(ncclAllGather(base + int64_t(G->rank0) * G->chunk_bytes, base, G->chunk_bytes,
+    MBX_NCCL(mbx::nccl().AllGather(base + int64_t(G->rank0) * G->chunk_bytes, base, G->chunk_bytes,
                            ncclUint8, G->comm, ctx->stream));
   }
   mbx::combine_kernel<<<1, 32, 0, ctx->stream>>>(base, G->chunk_bytes, G->tail_off, G->world,
@@ -241,7 +285,7 @@ extern "C" {
 MBX_API int mbx_nccl_unique_id(void* id128) {
   return sguard([&] {
     ncclUniqueId id;
-    MBX_NCCL(ncclGetUniqueId(&id));
+    MBX_NCCL(mbx::nccl().GetUniqueId(&id));
     static_assert(sizeof(id) == 128, "NCCL unique id is 128 bytes");
     std::memcpy(id128, &id, sizeof(id));
   });
@@ -344,8 +388,8 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
       MBX_CUDA(cudaStreamSynchronize(st));
-      MBX_NCCL(ncclCommInitRank(&G->comm, world, id, rank0));
-      MBX_NCCL(ncclAllReduce(seen, seen, n_global, ncclUint8, ncclMax, G->comm, st));
+      MBX_NCCL(mbx::nccl().CommInitRank(&G->comm, world, id, rank0));
+      MBX_NCCL(mbx::nccl().AllReduce(seen, seen, n_global, ncclUint8, ncclMax, G->comm, st));
     }
     for (int i = 0; i < nlocal; ++i) {
       mbx_matrix* m = mats[i];
@@ -549,7 +593,7 @@ MBX_API int mbx_shard_group_destroy(mbx_shard_group* G) {
     if (G->e0) cudaEventDestroy(G->e0);
     if (G->e1) cudaEventDestroy(G->e1);
     cudaStreamSynchronize(st);
-    if (G->comm) ncclCommDestroy(G->comm);
+    if (G->comm) mbx::nccl().CommDestroy(G->comm);
     delete G;
   });
 }
