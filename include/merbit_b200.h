@@ -147,7 +147,7 @@ MBX_API int mbx_context_synchronize(mbx_context* ctx);
 MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta,
                                    int ctas_per_sm, int max_hubs);
 /* Shared-memory budget per SM for K2 (bytes; the rest is L1) and L2
- * prefetch of the next tile's streams (0/1).  Defaults 147456 / 1. */
+ * prefetch of the next tile's streams (0/1).  Defaults 131072 / 0. */
 MBX_API int mbx_context_set_tuning_ex(mbx_context* ctx, int smem_per_sm,
                                       int prefetch);
 /* Number of merbit kernels this context launched so far. */

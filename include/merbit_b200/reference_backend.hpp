@@ -35,7 +35,8 @@ class B200Backend final : public SpmvBackend<T> {
         tile_(merbit_b200::generate_tile(matrix_, config_)),
         out_{std::vector<T>(static_cast<std::size_t>(a.n_rows)),
              std::vector<T>(static_cast<std::size_t>(a.n_rows))} {
-    this->preprocess_seconds_ = tile_.preprocess_seconds();
+    // T_p (backend.hpp:117-119): TILE (K1) + the x hub cache, device time
+    this->preprocess_seconds_ = tile_.preprocess_seconds() + matrix_.build_xcache();
   }
 
   const std::vector<T>& apply(std::span<const T> x) override {

@@ -34,28 +34,28 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 
 // 16-byte streaming loads (values / columns are touched exactly once).
 __device__ __forceinline__ void ld_stream16(const float* p, float (&v)[4], uint64_t pol) {
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
                : "l"(p), "l"(pol));
 }
 __device__ __forceinline__ void ld_stream16(const double* p, double (&v)[2], uint64_t pol) {
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
                : "=d"(v[0]), "=d"(v[1])
                : "l"(p), "l"(pol));
 }
 __device__ __forceinline__ void ld_cols(const int32_t* p, int (&c)[4], uint64_t pol) {
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3])
                : "l"(p), "l"(pol));
 }
 __device__ __forceinline__ void ld_cols(const int32_t* p, int (&c)[2], uint64_t pol) {
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
                : "=r"(c[0]), "=r"(c[1])
                : "l"(p), "l"(pol));
 }
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
                : "=r"(v)
                : "l"(p), "l"(pol));
   return v;
@@ -95,33 +95,62 @@ __device__ __forceinline__ T stage_products(const T* __restrict__ vals,
   constexpr int N = VecOf<T>::N;
   const int64_t a0 = x0 & ~int64_t(N - 1);
   const int nvec = static_cast<int>((x1 - a0 + N - 1) / N);
-  T acc = T(0);
+  // Three explicit phases so each tile pays one DRAM latency (all column and
+  // value vectors in flight together) and one L2 latency (all gathers in
+  // flight together) instead of one of each per 16-byte vector.
+  int col[MAXV][N];
+  T val[MAXV][N];
 #pragma unroll
   for (int it = 0; it < MAXV; ++it) {
     const int v = lid + 32 * it;
     if (v < nvec) {
-      const int64_t base = a0 + int64_t(v) * N;
-      T val[N];
-      int col[N];
-      ld_stream16(vals + base, val, pol);
-      ld_cols(cols + base, col, pol);
+      ld_cols(cols + a0 + int64_t(v) * N, col[it], pol);
+    } else {
 #pragma unroll
-      for (int e = 0; e < N; ++e) {
-        const int64_t idx = base + e;
-        if (idx >= x0 && idx < x1) {
-          // hub columns (sign bit set) are served from shared memory; the
-          // rest are gathered through the read-only path
-          T xv;
-          if (HUB)
-            xv = col[e] < 0 ? hub[col[e] & 0x7FFFFFFF] : __ldg(x + col[e]);
-          else
-            xv = __ldg(x + col[e]);
-          const T p = val[e] * xv;
-          if (ACCUM)
-            acc += p;
-          else
-            buf[idx - x0] = p;
-        }
+      for (int e = 0; e < N; ++e) col[it][e] = 0;
+    }
+  }
+  T xv[MAXV][N];
+#pragma unroll
+  for (int it = 0; it < MAXV; ++it) {
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      const int64_t idx = a0 + int64_t(lid + 32 * it) * N + e;
+      const bool ok = idx >= x0 && idx < x1;
+      // hub columns (sign bit set) are served from shared memory; the rest
+      // are gathered through the read-only path
+      if (!ok)
+        xv[it][e] = T(0);
+      else if (HUB && col[it][e] < 0)
+        xv[it][e] = hub[col[it][e] & 0x7FFFFFFF];
+      else
+        xv[it][e] = __ldg(x + col[it][e]);
+    }
+  }
+  // values last: their DRAM latency overlaps the gathers' L2 latency, and
+  // the column registers are already free (64-register budget at 1024 thr)
+#pragma unroll
+  for (int it = 0; it < MAXV; ++it) {
+    const int v = lid + 32 * it;
+    if (v < nvec) {
+      ld_stream16(vals + a0 + int64_t(v) * N, val[it], pol);
+    } else {
+#pragma unroll
+      for (int e = 0; e < N; ++e) val[it][e] = T(0);
+    }
+  }
+  T acc = T(0);
+#pragma unroll
+  for (int it = 0; it < MAXV; ++it) {
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      const int64_t idx = a0 + int64_t(lid + 32 * it) * N + e;
+      if (idx >= x0 && idx < x1) {
+        const T p = val[it][e] * xv[it][e];
+        if (ACCUM)
+          acc += p;
+        else
+          buf[idx - x0] = p;
       }
     }
   }
@@ -385,11 +414,12 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
       for (int k = lid; k < nrows; k += 32) buf[k] = k == 0 ? carry : T(0);
       carry = T(0);
     } else {
-      stage_products<T, false, MAXV, HUB>(p.vals, p.cols, p.x, hub, x0, x1, buf, lid, pol);
+      // descriptor first: its load overlaps the staging loads/gathers
       const int64_t j = c * 32 + lid;
       const bool valid = j < g.lane_num;
       const uint32_t d = valid ? ld_stream_u32(p.lane_desc + j, pol) : 0u;
       const int steps = valid ? static_cast<int>(imin64(sigma, total - j * sigma)) : 0;
+      stage_products<T, false, MAXV, HUB>(p.vals, p.cols, p.x, hub, x0, x1, buf, lid, pol);
       __syncwarp();
       carry = lane_walk_and_scan<T, SIGMA>(buf, cnt, sigma, d, steps, ob, lid, carry,
                                            static_cast<int>(d & omask),

@@ -52,8 +52,9 @@ struct Tuning {
   // Shared memory K2 may take per SM.  The rest stays L1, which also stages
   // every in-flight miss: a hub table that squeezes L1 below ~80 KB starves
   // memory-level parallelism (measured, profiles/).
-  int smem_per_sm = 144 * 1024;
-  int prefetch = 1;  // L2 prefetch of the next tile's value/column lines
+  int smem_per_sm = 128 * 1024;
+  int prefetch = 0;  // L2 prefetch of the next tile's value/column lines
+                     // (measured: costs request-port slots, off by default)
 };
 
 // Device-side reduction slots of one fused PageRank iteration.

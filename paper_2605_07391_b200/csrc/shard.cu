@@ -415,6 +415,8 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
       s.view.hub_cols = nullptr;
       s.view.hub_avail = 0;
       s.view.n_cols = G->chunk_elems * world;
+      // x hub cache over the remapped columns (owned by the group)
+      mbx::build_xcache(ctx, &s.view, ctx->tuning.max_hubs);
       const int64_t rows = s.r1 - s.r0;
       s.dangling = static_cast<uint32_t*>(dm(ctx, ((rows + 31) / 32) * 4 + 64));
       mbx::local_dangling_kernel<<<unsigned((rows + 31) / 32 / 256 + 1), 256, 0, st>>>(
@@ -584,6 +586,7 @@ MBX_API int mbx_shard_group_destroy(mbx_shard_group* G) {
     if (G->graph) cudaGraphExecDestroy(G->graph);
     for (mbx::Shard& s : G->shards) {
       for (void* p : {static_cast<void*>(s.cols_remap), static_cast<void*>(s.dangling),
+                      static_cast<void*>(s.view.cols_hub), static_cast<void*>(s.view.hub_cols),
                       static_cast<void*>(s.range_part), static_cast<void*>(s.block_part),
                       static_cast<void*>(s.counter), s.carry_ws})
         if (p) cudaFreeAsync(p, st);

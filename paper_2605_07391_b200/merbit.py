@@ -192,8 +192,8 @@ class Context:
         _check(_lib.lib().mbx_context_set_tuning(self.h, warps_per_cta, ctas_per_sm, max_hubs))
         if smem_per_sm is not None or prefetch is not None:
             _check(_lib.lib().mbx_context_set_tuning_ex(
-                self.h, 147456 if smem_per_sm is None else smem_per_sm,
-                1 if prefetch is None else prefetch))
+                self.h, 131072 if smem_per_sm is None else smem_per_sm,
+                0 if prefetch is None else prefetch))
 
     @property
     def launch_count(self) -> int:
@@ -480,15 +480,16 @@ class SpmvBackend:
 
 class MerbitB200Backend(SpmvBackend):
     """MerbitBackend (backend.hpp:112-136) on the GPU: the constructor uploads
-    the CSR once and builds the TILE (T_p = K1 device time); apply() returns an
-    internal buffer valid until the next apply()."""
+    the CSR once and builds the TILE and the x hub cache (T_p = their device
+    time); apply() returns an internal buffer valid until the next apply()."""
 
-    def __init__(self, a, c: SimtConfig, ctx: Context | None = None):
+    def __init__(self, a, c: SimtConfig, ctx: Context | None = None, xcache: bool = True):
         self.ctx = ctx or default_context()
         self.c = c
         self.matrix = DeviceMatrix.from_csr(self.ctx, a)
         self.tile_ = generate_tile_for(self.matrix, c)
-        self._preprocess_seconds = self.tile_.preprocess_seconds
+        xc = self.matrix.build_xcache() if xcache else 0.0
+        self._preprocess_seconds = self.tile_.preprocess_seconds + xc
         self.buffer = DualBuffer(self.matrix.n_rows, self.matrix.dtype)
 
     def apply(self, x):
