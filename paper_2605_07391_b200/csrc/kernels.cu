@@ -168,24 +168,37 @@ struct PrAcc {
   double resid = 0.0, dang = 0.0, mass = 0.0, err = 0.0;
 };
 
+// po = pi_old[row], dang = row is a dangling vertex (both may be preloaded).
+// With a constant yardstick s (reference_iters == 0) the accumulator holds
+// max|pi - s| and the division happens once in pr_block_finish: division by
+// a positive constant is monotone, so max(fl(|d|/s)) == fl(max|d| / s) and
+// ERR stays bitwise equal to rank_error's formula.
+template <typename T>
+__device__ __forceinline__ void pr_commit_v(const PrArgs& pr, T base, int64_t row, T w, T po,
+                                            bool dang, T* __restrict__ out, PrAcc& a) {
+  const T pn = static_cast<T>(pr.damping) * w + base;
+  out[row] = pn;
+  a.resid += fabs(static_cast<double>(pn) - static_cast<double>(po));
+  if (dang) a.dang += static_cast<double>(pn);
+  a.mass += fabs(static_cast<double>(pn));
+  if (pr.yardstick) {
+    const double s = static_cast<double>(reinterpret_cast<const T*>(pr.yardstick)[row]);
+    const double d = static_cast<double>(pn) - s;
+    if (s == 0.0) {
+      if (d != 0.0) a.err = INFINITY;
+    } else {
+      a.err = fmax(a.err, fabs(d / s));
+    }
+  } else {
+    a.err = fmax(a.err, fabs(static_cast<double>(pn) - pr.yard_const));
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void pr_commit(const PrArgs& pr, T base, int64_t row,
                                           T w, T* __restrict__ out, PrAcc& a) {
-  const T pn = static_cast<T>(pr.damping) * w + base;
-  const T po = reinterpret_cast<const T*>(pr.pi_old)[row];
-  out[row] = pn;
-  a.resid += fabs(static_cast<double>(pn) - static_cast<double>(po));
-  if ((pr.dangling[row >> 5] >> (row & 31)) & 1u) a.dang += static_cast<double>(pn);
-  a.mass += fabs(static_cast<double>(pn));
-  const double s = pr.yardstick ? static_cast<double>(
-                                      reinterpret_cast<const T*>(pr.yardstick)[row])
-                                : pr.yard_const;
-  const double d = static_cast<double>(pn) - s;
-  if (s == 0.0) {
-    if (d != 0.0) a.err = INFINITY;
-  } else {
-    a.err = fmax(a.err, fabs(d / s));
-  }
+  pr_commit_v<T>(pr, base, row, w, reinterpret_cast<const T*>(pr.pi_old)[row],
+                 (pr.dangling[row >> 5] >> (row & 31)) & 1u, out, a);
 }
 
 template <typename T>
@@ -260,6 +273,10 @@ __device__ void pr_block_finish(PrAcc a, const PrArgs& pr, double* block_part,
       d += sm[1][i];
       m += sm[2][i];
       e = fmax(e, sm[3][i]);
+    }
+    if (!pr.yardstick) {  // constant yardstick: e = max|pi - s| so far
+      const double s = pr.yard_const;
+      e = s == 0.0 ? (e != 0.0 ? INFINITY : 0.0) : e / s;
     }
     out->resid = r;
     out->dangling = d;
@@ -408,7 +425,20 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
       carry += warp_sum(s);
       continue;
     }
+    // PR: the tile's first 32 rows of pi_old and their dangling bits are
+    // loaded before the lane walk (after staging, off the register peak), so
+    // the commit does not wait on another memory round trip
+    T po_pre = T(0);
+    uint32_t dw_pre = 0u;
+    auto preload = [&]() {
+      if (PR && lid < nrows) {
+        const int64_t r = int64_t(y0) + lid;
+        po_pre = __ldg(reinterpret_cast<const T*>(p.pr.pi_old) + r);
+        dw_pre = __ldg(p.pr.dangling + (r >> 5));
+      }
+    };
     if (cnt == 0) {
+      preload();
       // no nonzero: every step closes a row (merbit_spmv.hpp:217-224); the
       // first closes the carried row, the rest are empty rows.
       for (int k = lid; k < nrows; k += 32) buf[k] = k == 0 ? carry : T(0);
@@ -420,6 +450,7 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
       const uint32_t d = valid ? ld_stream_u32(p.lane_desc + j, pol) : 0u;
       const int steps = valid ? static_cast<int>(imin64(sigma, total - j * sigma)) : 0;
       stage_products<T, false, MAXV, HUB>(p.vals, p.cols, p.x, hub, x0, x1, buf, lid, pol);
+      preload();
       __syncwarp();
       carry = lane_walk_and_scan<T, SIGMA>(buf, cnt, sigma, d, steps, ob, lid, carry,
                                            static_cast<int>(d & omask),
@@ -434,10 +465,14 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
         continue;
       }
       const int64_t row = int64_t(y0) + k;
-      if (PR)
-        pr_commit<T>(p.pr, base, row, w, p.y, acc);
-      else
+      if (PR) {
+        if (k < 32)
+          pr_commit_v<T>(p.pr, base, row, w, po_pre, (dw_pre >> (row & 31)) & 1u, p.y, acc);
+        else
+          pr_commit<T>(p.pr, base, row, w, p.y, acc);
+      } else {
         p.y[row] = w;
+      }
     }
     if (nrows > 0) head_open = false;
     __syncwarp();
