@@ -175,13 +175,15 @@ def time_device(stream, fn, reps):
     return e0.elapsed_time(e1) * 1e-3 / reps
 
 
-def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak):
-    """Plain SpMV (K2+K3) on an R-MAT matrix of the given precision."""
+def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak, make=None, label=None):
+    """Plain SpMV (K2+K3) on an R-MAT matrix (or make(ctx, dtype)) of the
+    given precision."""
     import numpy as np
     import torch
     t_dt = torch.float32 if dtype == np.float32 else torch.float64
     vs = 4 if dtype == np.float32 else 8
-    A = mb.DeviceMatrix.rmat(ctx, scale, 16, seed=1, transition=True, dtype=dtype)
+    A = (make(ctx, dtype) if make else
+         mb.DeviceMatrix.rmat(ctx, scale, 16, seed=1, transition=True, dtype=dtype))
     c = mb.SimtConfig.make(32, 14 if vs == 4 else 7, 128)
     t = mb.generate_tile_for(A, c)
     xc_s = A.build_xcache()
@@ -198,7 +200,12 @@ def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak):
            "preprocess_tile_ms": t.preprocess_seconds * 1e3, "preprocess_xcache_ms": xc_s * 1e3,
            "preprocess_over_spmv": (t.preprocess_seconds + xc_s) / ts,
            "xcache_hubs": A.xcache_info()[0], "xcache_coverage": A.xcache_info()[1]}
+    if label:
+        tr = mb.trace_counts(t)
+        out.update({"matrix": label, "n": n, "fast_tiles": tr.fast_tiles,
+                    "normal_tiles": tr.normal_tiles, "skipped_tiles": tr.skipped_tiles})
     del A, t, x, y
+    torch.cuda.synchronize()
     return out
 
 
@@ -352,6 +359,17 @@ def main():
                                               peak)
             extras["spmv_f64"] = spmv_numbers(mb, ctx, stream, scale, np.float64, args.spmv_reps,
                                               peak)
+            # BASELINE C3: fp64 power-law, long rows + exactly 10 % empty rows
+            extras["c3_powerlaw_f64"] = spmv_numbers(
+                mb, ctx, stream, 0, np.float64, args.spmv_reps, peak,
+                make=lambda cx, dt: mb.DeviceMatrix.powerlaw(cx, 22, seed=3, dtype=dt),
+                label="power-law 2^22 rows, 10% empty, rows up to 2^20 nnz")
+            # BASELINE C5: 27-point stencil, 64M rows (uniform sparsity)
+            for dt, key in ((np.float32, "c5_stencil_f32"), (np.float64, "c5_stencil_f64")):
+                extras[key] = spmv_numbers(
+                    mb, ctx, stream, 0, dt, max(5, args.spmv_reps // 3), peak,
+                    make=lambda cx, d: mb.DeviceMatrix.stencil27(cx, 400, d),
+                    label="27-point stencil 400^3 (64M rows)")
         if not args.no_cpu_baseline:
             import oracle as O
             if O.ref() is not None:

@@ -176,6 +176,17 @@ MBX_API int mbx_matrix_generate_rmat(mbx_context* ctx, int precision,
                                      uint64_t seed, int kind,
                                      uint64_t value_seed, double lo,
                                      double hi, mbx_matrix** out);
+/* BASELINE config C5: 27-point stencil on a grid_dim^3 grid (diagonal 26,
+ * neighbours -1; the 3-D five_point_laplacian, fixtures.hpp:40-56). */
+MBX_API int mbx_matrix_generate_stencil27(mbx_context* ctx, int precision,
+                                          int64_t grid_dim, mbx_matrix** out);
+/* BASELINE config C3: 2^log2_rows rows, power-law row lengths
+ * max(1, 2^20 / (rank+1)^0.8) by a seeded rank permutation, exactly
+ * n - floor(0.9 n) empty rows, strictly increasing columns spread over
+ * [0, n), values in [-1, 1). */
+MBX_API int mbx_matrix_generate_powerlaw(mbx_context* ctx, int precision,
+                                         int log2_rows, uint64_t seed,
+                                         mbx_matrix** out);
 MBX_API int mbx_matrix_info(const mbx_matrix* m, int* precision,
                             int64_t* n_rows, int64_t* n_cols, int64_t* nnz);
 /* Any output pointer may be NULL.  row_offsets as int64. */

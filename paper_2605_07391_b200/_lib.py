@@ -71,6 +71,8 @@ SIGNATURES = {
                               C.c_int),
     "mbx_matrix_generate_rmat": ([VP, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_uint64,
                                   C.c_double, C.c_double, C.POINTER(VP)], C.c_int),
+    "mbx_matrix_generate_stencil27": ([VP, C.c_int, C.c_int64, C.POINTER(VP)], C.c_int),
+    "mbx_matrix_generate_powerlaw": ([VP, C.c_int, C.c_int, C.c_uint64, C.POINTER(VP)], C.c_int),
     "mbx_matrix_info": ([VP, C.POINTER(C.c_int), I64P, I64P, I64P], C.c_int),
     "mbx_matrix_download": ([VP, VP, VP, VP], C.c_int),
     "mbx_matrix_device_ptrs": ([VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)], C.c_int),

@@ -57,10 +57,15 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   g.sigma = t->info.sigma;
   g.ob = t->offset_bits;
   g.num_chunks = (g.lane_num + 31) / 32;
-  g.chunks_per_range = std::max(1, std::min(31, block_size / 32));
-  g.num_ranges = (g.num_chunks + g.chunks_per_range - 1) / g.chunks_per_range;
   g.warps_per_cta = ctx->tuning.warps_per_cta;
   g.grid = ctx->sm_count * ctx->tuning.ctas_per_sm;
+  // b/32 tiles per warp range (the reference's block of b/omega tiles), but
+  // at least ~8 ranges per resident warp so small matrices do not leave the
+  // persistent grid with a long tail
+  const int64_t warps = int64_t(g.grid) * g.warps_per_cta;
+  const int64_t fit = std::max<int64_t>(1, g.num_chunks / (8 * warps));
+  g.chunks_per_range = int(std::max<int64_t>(1, std::min<int64_t>({31, block_size / 32, fit})));
+  g.num_ranges = (g.num_chunks + g.chunks_per_range - 1) / g.chunks_per_range;
   g.prefetch = ctx->tuning.prefetch;
   g.hub_count = 0;
   if (m->cols_hub && m->hub_avail > 0 && g.omega == 32 && ctx->tuning.max_hubs != 0 &&
@@ -448,6 +453,33 @@ MBX_API int mbx_matrix_generate_rmat(mbx_context* ctx, int precision, int scale,
     m->ctx = ctx;
     mbx::generate_rmat(ctx, precision, scale, edge_factor, seed, kind, value_seed, lo, hi,
                        m.get());
+    *out = m.release();
+  });
+}
+
+MBX_API int mbx_matrix_generate_stencil27(mbx_context* ctx, int precision, int64_t grid_dim,
+                                          mbx_matrix** out) {
+  return guarded([&] {
+    check_precision(precision);
+    require(grid_dim >= 1 && grid_dim * grid_dim * grid_dim < (int64_t(1) << 31),
+            MBX_CONFIG_ERROR, "stencil grid_dim^3 must be < 2^31");
+    Device dg(ctx->device);
+    auto m = std::make_unique<mbx_matrix>();
+    m->ctx = ctx;
+    mbx::generate_stencil27(ctx, precision, grid_dim, m.get());
+    *out = m.release();
+  });
+}
+
+MBX_API int mbx_matrix_generate_powerlaw(mbx_context* ctx, int precision, int log2_rows,
+                                         uint64_t seed, mbx_matrix** out) {
+  return guarded([&] {
+    check_precision(precision);
+    require(log2_rows >= 4 && log2_rows <= 30, MBX_CONFIG_ERROR, "log2_rows in [4, 30]");
+    Device dg(ctx->device);
+    auto m = std::make_unique<mbx_matrix>();
+    m->ctx = ctx;
+    mbx::generate_powerlaw(ctx, precision, log2_rows, seed, m.get());
     *out = m.release();
   });
 }

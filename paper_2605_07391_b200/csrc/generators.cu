@@ -99,6 +99,144 @@ __global__ void transition_values_kernel(const int32_t* __restrict__ cols, uint6
 
 unsigned grid(mbx_context* ctx) { return unsigned(ctx->sm_count) * 16; }
 
+// ---- C5: 27-point stencil on a g^3 grid (diagonal 26, neighbours -1), the
+// 3-D generalisation of five_point_laplacian (fixtures.hpp:40-56). ----------
+__host__ __device__ __forceinline__ uint32_t span3(int64_t i, int64_t g) {
+  return 3u - (i == 0) - (i == g - 1);
+}
+
+__global__ void stencil_counts_kernel(int64_t g, uint32_t* cnt) {
+  const int64_t n = g * g * g;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = r / (g * g), j = (r / g) % g, k = r % g;
+    cnt[r] = g == 1 ? 1u : span3(i, g) * span3(j, g) * span3(k, g);
+  }
+}
+
+template <typename T>
+__global__ void stencil_fill_kernel(int64_t g, const uint32_t* __restrict__ ro,
+                                    int32_t* __restrict__ cols, T* __restrict__ vals) {
+  const int64_t n = g * g * g;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = r / (g * g), j = (r / g) % g, k = r % g;
+    uint32_t p = ro[r];
+    for (int di = -1; di <= 1; ++di) {
+      if (i + di < 0 || i + di >= g) continue;
+      for (int dj = -1; dj <= 1; ++dj) {
+        if (j + dj < 0 || j + dj >= g) continue;
+        for (int dk = -1; dk <= 1; ++dk) {
+          if (k + dk < 0 || k + dk >= g) continue;
+          const int64_t c = ((i + di) * g + (j + dj)) * g + (k + dk);  // ascending
+          cols[p] = int32_t(c);
+          vals[p] = c == r ? T(26) : T(-1);
+          ++p;
+        }
+      }
+    }
+  }
+}
+
+// ---- C3: power-law rows, exactly 10 % empty rows (seeded permutation),
+// long rows scattered, strictly increasing columns spread over [0, n),
+// values in [-1, 1).  Row length by permuted rank q:
+//   L(q) = max(1, floor(2^20 / (q+1)^0.8))  for q < n - n/10, else 0. ------
+__host__ __device__ __forceinline__ uint64_t perm_bits(uint64_t v, int bits, uint64_t key) {
+  // bijection on [0, 2^bits): odd multiply + xor-shift rounds, masked
+  const uint64_t mask = (bits >= 64) ? ~0ULL : ((1ULL << bits) - 1);
+  for (int round = 0; round < 4; ++round) {
+    v = (v * 0x9E3779B97F4A7C15ULL + (key >> (round * 8))) & mask;
+    v ^= v >> ((bits + 1) / 2);
+    v &= mask;
+  }
+  return v;
+}
+
+__global__ void powerlaw_counts_kernel(int log2n, uint64_t key, uint32_t* cnt) {
+  const int64_t n = int64_t(1) << log2n;
+  const int64_t live = n - n / 10;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q = int64_t(perm_bits(uint64_t(r), log2n, key));
+    uint32_t L = 0;
+    if (q < live) {
+      const double l = floor(1048576.0 / pow(double(q + 1), 0.8));
+      L = uint32_t(l < 1.0 ? 1.0 : (l > double(n) ? double(n) : l));
+    }
+    cnt[r] = L;
+  }
+}
+
+template <typename T>
+__global__ void powerlaw_fill_kernel(int64_t n, const uint32_t* __restrict__ ro, uint64_t sm,
+                                     int32_t* __restrict__ cols, T* __restrict__ vals) {
+  // one warp per row (rows up to 2^20 long)
+  const int lid = threadIdx.x & 31;
+  const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = w; r < n; r += nw) {
+    const uint32_t b = ro[r], L = ro[r + 1] - b;
+    for (uint32_t t = lid; t < L; t += 32) {
+      const int64_t lo = int64_t(t) * n / L, hi = int64_t(t + 1) * n / L;  // [lo, hi) nonempty
+      const uint64_t h = smix(sm ^ (uint64_t(r) << 21) ^ t);
+      cols[b + t] = int32_t(lo + int64_t(h % uint64_t(hi - lo)));
+      const double u = double(smix(h) >> 11) * 0x1.0p-53;
+      vals[b + t] = T(__dadd_rn(-1.0, __dmul_rn(2.0, u)));
+    }
+  }
+}
+
+__global__ void widen_u32_kernel(const uint32_t* __restrict__ in, int64_t n,
+                                 uint64_t* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+
+__global__ void narrow_u64_kernel(const uint64_t* __restrict__ in, int64_t n,
+                                  uint32_t* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = uint32_t(in[i]);
+}
+
+// row offsets from per-row counts (64-bit inclusive scan), arrays allocated
+void csr_from_counts(mbx_context* ctx, int precision, int64_t n, uint32_t* cnt, mbx_matrix* m) {
+  cudaStream_t s = ctx->stream;
+  MBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&m->ro), (n + 1) * 4 + 64, s));
+  // 64-bit scan so an overflow of the 32-bit cursor is detected, not wrapped
+  uint64_t* ro64 = nullptr;
+  MBX_CUDA(cudaMallocAsync(&ro64, (n + 1) * 8, s));
+  MBX_CUDA(cudaMemsetAsync(ro64, 0, 8, s));
+  widen_u32_kernel<<<grid(ctx), 256, 0, s>>>(cnt, n, ro64 + 1);
+  ++ctx->launches;
+  size_t tb = 0;
+  MBX_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, ro64 + 1, ro64 + 1, n, s));
+  void* temp = nullptr;
+  MBX_CUDA(cudaMallocAsync(&temp, tb, s));
+  MBX_CUDA(cub::DeviceScan::InclusiveSum(temp, tb, ro64 + 1, ro64 + 1, n, s));
+  uint64_t nnz = 0;
+  MBX_CUDA(cudaMemcpyAsync(&nnz, ro64 + n, 8, cudaMemcpyDeviceToHost, s));
+  MBX_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(temp, s);
+  if (nnz > 0xFFFFFFFFULL) {
+    cudaFreeAsync(ro64, s);
+    fail(MBX_CAPACITY_ERROR, "generated nonzero count exceeds the 32-bit tile cursor");
+  }
+  narrow_u64_kernel<<<grid(ctx), 256, 0, s>>>(ro64, n + 1, m->ro);
+  ++ctx->launches;
+  cudaFreeAsync(ro64, s);
+  const size_t vs = value_size(precision);
+  m->precision = precision;
+  m->n_rows = m->n_cols = n;
+  m->nnz = int64_t(nnz);
+  MBX_CUDA(cudaMallocAsync(&m->vals, nnz * vs + 256, s));
+  MBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&m->cols), nnz * 4 + 256, s));
+  MBX_CUDA(cudaMemsetAsync(m->vals, 0, nnz * vs + 256, s));
+  MBX_CUDA(cudaMemsetAsync(m->cols, 0, nnz * 4 + 256, s));
+}
+
 }  // namespace
 
 void generate_rmat(mbx_context* ctx, int precision, int scale, int edge_factor, uint64_t seed,
@@ -166,6 +304,47 @@ void generate_rmat(mbx_context* ctx, int precision, int scale, int edge_factor, 
     MBX_CUDA(cudaFreeAsync(deg, s));
   }
   MBX_CUDA(cudaGetLastError());
+  MBX_CUDA(cudaStreamSynchronize(s));
+}
+
+void generate_stencil27(mbx_context* ctx, int precision, int64_t g, mbx_matrix* m) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = g * g * g;
+  uint32_t* cnt = nullptr;
+  MBX_CUDA(cudaMallocAsync(&cnt, n * 4 + 64, s));
+  stencil_counts_kernel<<<grid(ctx), 256, 0, s>>>(g, cnt);
+  ++ctx->launches;
+  csr_from_counts(ctx, precision, n, cnt, m);
+  if (precision == MBX_F32)
+    stencil_fill_kernel<float><<<grid(ctx), 256, 0, s>>>(g, m->ro, m->cols,
+                                                         static_cast<float*>(m->vals));
+  else
+    stencil_fill_kernel<double><<<grid(ctx), 256, 0, s>>>(g, m->ro, m->cols,
+                                                          static_cast<double*>(m->vals));
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+  cudaFreeAsync(cnt, s);
+  MBX_CUDA(cudaStreamSynchronize(s));
+}
+
+void generate_powerlaw(mbx_context* ctx, int precision, int log2n, uint64_t seed, mbx_matrix* m) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = int64_t(1) << log2n;
+  uint32_t* cnt = nullptr;
+  MBX_CUDA(cudaMallocAsync(&cnt, n * 4 + 64, s));
+  powerlaw_counts_kernel<<<grid(ctx), 256, 0, s>>>(log2n, smix(seed), cnt);
+  ++ctx->launches;
+  csr_from_counts(ctx, precision, n, cnt, m);
+  const uint64_t sm = smix(seed ^ 0x5851F42D4C957F2DULL);
+  if (precision == MBX_F32)
+    powerlaw_fill_kernel<float><<<grid(ctx), 256, 0, s>>>(n, m->ro, sm, m->cols,
+                                                          static_cast<float*>(m->vals));
+  else
+    powerlaw_fill_kernel<double><<<grid(ctx), 256, 0, s>>>(n, m->ro, sm, m->cols,
+                                                           static_cast<double*>(m->vals));
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+  cudaFreeAsync(cnt, s);
   MBX_CUDA(cudaStreamSynchronize(s));
 }
 

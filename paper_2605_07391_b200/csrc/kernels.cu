@@ -110,16 +110,19 @@ __device__ __forceinline__ T stage_products(const T* __restrict__ vals,
       for (int e = 0; e < N; ++e) col[it][e] = 0;
     }
   }
+  // element (it, e) sits at tile-relative position k = lead + (lid+32it)*N + e;
+  // it is live iff 0 <= k < cnt -- one unsigned compare
+  const int lead = static_cast<int>(a0 - x0);  // in (-N, 0]
+  const unsigned cnt = static_cast<unsigned>(x1 - x0);
   T xv[MAXV][N];
 #pragma unroll
   for (int it = 0; it < MAXV; ++it) {
 #pragma unroll
     for (int e = 0; e < N; ++e) {
-      const int64_t idx = a0 + int64_t(lid + 32 * it) * N + e;
-      const bool ok = idx >= x0 && idx < x1;
+      const unsigned k = static_cast<unsigned>(lead + (lid + 32 * it) * N + e);
       // hub columns (sign bit set) are served from shared memory; the rest
       // are gathered through the read-only path
-      if (!ok)
+      if (k >= cnt)
         xv[it][e] = T(0);
       else if (HUB && col[it][e] < 0)
         xv[it][e] = hub[col[it][e] & 0x7FFFFFFF];
@@ -144,13 +147,13 @@ __device__ __forceinline__ T stage_products(const T* __restrict__ vals,
   for (int it = 0; it < MAXV; ++it) {
 #pragma unroll
     for (int e = 0; e < N; ++e) {
-      const int64_t idx = a0 + int64_t(lid + 32 * it) * N + e;
-      if (idx >= x0 && idx < x1) {
+      const unsigned k = static_cast<unsigned>(lead + (lid + 32 * it) * N + e);
+      if (k < cnt) {
         const T p = val[it][e] * xv[it][e];
         if (ACCUM)
           acc += p;
         else
-          buf[idx - x0] = p;
+          buf[k] = p;
       }
     }
   }

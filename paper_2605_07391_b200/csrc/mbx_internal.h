@@ -165,5 +165,8 @@ void launch_narrow_rows(mbx_context* ctx, const int64_t* src, uint32_t* dst,
 void generate_rmat(mbx_context* ctx, int precision, int scale,
                    int edge_factor, uint64_t seed, int kind,
                    uint64_t value_seed, double lo, double hi, mbx_matrix* m);
+void generate_stencil27(mbx_context* ctx, int precision, int64_t g, mbx_matrix* m);
+void generate_powerlaw(mbx_context* ctx, int precision, int log2n, uint64_t seed,
+                       mbx_matrix* m);
 
 }  // namespace mbx

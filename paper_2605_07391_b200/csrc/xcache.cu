@@ -95,12 +95,17 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   std::vector<uint32_t> hc(cand);
   MBX_CUDA(cudaMemcpyAsync(hc.data(), cnt_sorted, size_t(cand) * 4, cudaMemcpyDeviceToHost, s));
   MBX_CUDA(cudaStreamSynchronize(s));
-  // a hub pays off only if it is referenced more often than it is loaded
-  // (once per resident CTA per SpMV)
-  const uint32_t min_refs = uint32_t(ctx->sm_count * tu.ctas_per_sm);
+  // A hub pays off only if it is referenced several times more often than
+  // it is loaded (once per resident CTA per SpMV), and the per-CTA table
+  // load (a serial preamble before any tile) must stay a small fraction
+  // (<= 2 %) of that CTA's share of the gathers -- small matrices get small
+  // tables (R-MAT s20: measured 10 % preamble with an uncapped table).
+  const int64_t ctas = int64_t(ctx->sm_count) * tu.ctas_per_sm;
+  const uint32_t min_refs = uint32_t(4 * ctas);
+  const int64_t cap = m->nnz / (ctas * 50);
   int h = 0;
   int64_t covered = 0;
-  while (h < cand && hc[h] > min_refs) covered += hc[h++];
+  while (h < cand && h < cap && hc[h] > min_refs) covered += hc[h++];
   if (h > 0) {
     MBX_CUDA(cudaMallocAsync(&m->hub_cols, size_t(h) * 4 + 64, s));
     MBX_CUDA(cudaMemcpyAsync(m->hub_cols, ids_sorted, size_t(h) * 4, cudaMemcpyDeviceToDevice, s));

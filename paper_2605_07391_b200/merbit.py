@@ -268,6 +268,22 @@ class DeviceMatrix:
                                                    value_seed, lo, hi, C.byref(h)))
         return cls(ctx, h)
 
+    @classmethod
+    def stencil27(cls, ctx: Context, grid_dim: int, dtype=np.float32):
+        """BASELINE C5: 27-point stencil on a grid_dim^3 grid."""
+        h = C.c_void_p()
+        _check(_lib.lib().mbx_matrix_generate_stencil27(ctx.h, _precision_of(dtype), grid_dim,
+                                                        C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def powerlaw(cls, ctx: Context, log2_rows: int, seed: int = 3, dtype=np.float64):
+        """BASELINE C3: power-law rows with long rows and exactly 10% empty rows."""
+        h = C.c_void_p()
+        _check(_lib.lib().mbx_matrix_generate_powerlaw(ctx.h, _precision_of(dtype), log2_rows,
+                                                       seed, C.byref(h)))
+        return cls(ctx, h)
+
     def download(self, want_values=True):
         ro = np.zeros(self.n_rows + 1, np.int64)
         cols = np.zeros(max(self.nnz, 1), np.int32)
