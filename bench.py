@@ -191,14 +191,16 @@ def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak, make=None, label=Non
     y = torch.empty(A.n_rows, device="cuda", dtype=t_dt)
     for _ in range(3):
         mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr())
+    slot_s = A.slot_info()[1]  # lane-major slot copy, built by the first SpMV
     ts = time_device(stream, lambda: mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr()), reps)
     m, n = A.nnz, A.n_rows
     b = m * (vs + 4) + 2 * n * vs + 4 * (n + 1)
     out = {"dtype": "f32" if vs == 4 else "f64", "ms": ts * 1e3, "gflops": 2 * m / ts / 1e9,
            "gbs": b / ts / 1e9, "frac": b / ts / 1e9 / peak, "bytes": b, "nnz": m,
-           "preprocess_ms": (t.preprocess_seconds + xc_s) * 1e3,
+           "preprocess_ms": (t.preprocess_seconds + xc_s + slot_s) * 1e3,
            "preprocess_tile_ms": t.preprocess_seconds * 1e3, "preprocess_xcache_ms": xc_s * 1e3,
-           "preprocess_over_spmv": (t.preprocess_seconds + xc_s) / ts,
+           "preprocess_slots_ms": slot_s * 1e3,
+           "preprocess_over_spmv": (t.preprocess_seconds + xc_s + slot_s) / ts,
            "xcache_hubs": A.xcache_info()[0], "xcache_coverage": A.xcache_info()[1]}
     if label:
         tr = mb.trace_counts(t)
@@ -273,10 +275,10 @@ def main():
     if world == 1:
         tile = mb.generate_tile_for(P, cfg)
         xc_s = P.build_xcache()  # x hub cache: preprocessing, next to the TILE
-        runner = mb.PageRankPlan(P, tile, cfg, prc)
+        runner = mb.PageRankPlan(P, tile, cfg, prc)  # builds the K2 slot copy once
         local_rows, local_nnz = n, m
         run = runner.run
-        pre_ms = (tile.preprocess_seconds + xc_s) * 1e3
+        pre_ms = (tile.preprocess_seconds + xc_s + P.slot_info()[1]) * 1e3
     else:
         ro_host, _, _ = P.download(want_values=False)
         bounds = mb.plan_row_shards(ro_host, n, m, world)

@@ -150,6 +150,10 @@ MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta,
  * prefetch of the next tile's streams (0/1).  Defaults 131072 / 0. */
 MBX_API int mbx_context_set_tuning_ex(mbx_context* ctx, int smem_per_sm,
                                       int prefetch);
+/* K2 data layout: 1 (default) = lane-major slot copy of the matrix, built
+ * once per TILE next to it (omega 32 with the default sigma: 14 for f32, 7
+ * for f64); 0 = CSR order staged through shared memory (any omega/sigma). */
+MBX_API int mbx_context_set_layout(mbx_context* ctx, int layout);
 /* Number of merbit kernels this context launched so far. */
 MBX_API int64_t mbx_context_launch_count(const mbx_context* ctx);
 
@@ -203,6 +207,9 @@ MBX_API int mbx_matrix_destroy(mbx_matrix* m);
  * the most referenced x entries in shared memory during SpMV.  Results are
  * bitwise identical with and without it.  max_hubs < 0: as many as the
  * shared-memory budget of the context tuning allows; 0: remove the cache. */
+/* Slot copy currently cached on the matrix: slots (0 if none) and the
+ * seconds its one-time build took (part of preprocessing). */
+MBX_API int mbx_matrix_slot_info(const mbx_matrix* m, int64_t* slots, double* seconds);
 MBX_API int mbx_matrix_build_xcache(mbx_context* ctx, mbx_matrix* m,
                                     int max_hubs, double* seconds);
 MBX_API int mbx_matrix_xcache_info(const mbx_matrix* m, int* hubs,

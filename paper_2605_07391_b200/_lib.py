@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmerbit_b200.so")
+# MBX_LIB_PATH: load an alternative build (kernel experiments only)
+LIB_PATH = os.environ.get("MBX_LIB_PATH") or os.path.join(_HERE, "libmerbit_b200.so")
 
 
 class mbx_simt_config(C.Structure):
@@ -63,6 +64,8 @@ SIGNATURES = {
     "mbx_context_launch_count": ([VP], C.c_int64),
     "mbx_context_set_tuning": ([VP, C.c_int, C.c_int, C.c_int], C.c_int),
     "mbx_context_set_tuning_ex": ([VP, C.c_int, C.c_int], C.c_int),
+    "mbx_context_set_layout": ([VP, C.c_int], C.c_int),
+    "mbx_matrix_slot_info": ([VP, C.POINTER(C.c_int64), C.POINTER(C.c_double)], C.c_int),
     "mbx_matrix_build_xcache": ([VP, VP, C.c_int, C.POINTER(C.c_double)], C.c_int),
     "mbx_matrix_xcache_info": ([VP, C.POINTER(C.c_int), C.POINTER(C.c_double)], C.c_int),
     "mbx_matrix_xcache_ptrs": ([VP, C.POINTER(VP), C.POINTER(VP)], C.c_int),

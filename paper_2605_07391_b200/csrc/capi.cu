@@ -2,6 +2,7 @@
 // device memory, host<->device staging, error translation, the PageRank
 // plan with its CUDA graph.  No CPU compute path exists: every SpMV /
 // TILE / PageRank result comes from the kernels in kernels.cu.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -73,6 +74,13 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
     const int slots = max_hub_slots(ctx, g.warps_per_cta, ctx->tuning.ctas_per_sm, g.sigma,
                                     m->precision);
     if (slots >= m->hub_avail) g.hub_count = m->hub_avail;
+  }
+  // lane-major slot copy for this TILE (built once, outside any capture)
+  g.slots = ensure_slots(const_cast<mbx_context*>(ctx), m, t, g) ? 1 : 0;
+  if (!g.slots && g.hub_count > 0) {
+    // the staged kernel needs more shared memory per warp than the slot one
+    const bool slot_budget = ctx->tuning.layout == 1 && g.sigma == default_sigma(m->precision);
+    if (slot_budget) g.hub_count = 0;
   }
   return g;
 }
@@ -174,8 +182,10 @@ void tile_counts(int64_t nnz, int64_t n, int omega, int sigma, int64_t* tn, int6
 }
 
 mbx_tile* new_tile(mbx_context* ctx, const mbx_simt_config& c, int64_t n_rows, int64_t nnz) {
+  static std::atomic<uint64_t> next_serial{1};
   auto t = std::make_unique<mbx_tile>();
   t->ctx = ctx;
+  t->serial = next_serial++;
   t->info.omega = c.omega;
   t->info.sigma = c.sigma;
   t->info.n_rows = n_rows;
@@ -542,6 +552,20 @@ MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta, int ctas
   });
 }
 
+MBX_API int mbx_context_set_layout(mbx_context* ctx, int layout) {
+  return guarded([&] {
+    require(layout == 0 || layout == 1, MBX_CONFIG_ERROR, "layout must be 0 or 1");
+    ctx->tuning.layout = layout;
+  });
+}
+
+MBX_API int mbx_matrix_slot_info(const mbx_matrix* m, int64_t* slots, double* seconds) {
+  return guarded([&] {
+    if (slots) *slots = m->slots.vals ? m->slots.count : 0;
+    if (seconds) *seconds = m->slots.vals ? m->slots.seconds : 0.0;
+  });
+}
+
 MBX_API int mbx_matrix_build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs,
                                     double* seconds) {
   return guarded([&] {
@@ -586,6 +610,7 @@ MBX_API int mbx_matrix_destroy(mbx_matrix* m) {
     dfree(ctx, m->ro);
     dfree(ctx, m->cols_hub);
     dfree(ctx, m->hub_cols);
+    mbx::free_slots(ctx, m);
     MBX_CUDA(cudaStreamSynchronize(ctx->stream));
     delete m;
   });

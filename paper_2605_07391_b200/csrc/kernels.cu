@@ -622,6 +622,398 @@ __global__ void __launch_bounds__(kThreads) spmv_generic_kernel(SpmvParams<T> p)
 }
 
 // ---------------------------------------------------------------------------
+// K2 over the lane-major slot layout (omega == 32, default sigma).
+//
+// The slot copy (built once per TILE by build_slots_kernel) stores, for
+// chunk c, the element lane l consumes at step i at
+//   c*32*SIGMA + (i/G)*32*G + l*G + i%G      (G = 8/sizeof(T) elements)
+// -- zero for Down steps; for marked tiles lane l step i holds element
+// 32*i + l, i.e. exactly the lane-strided order of fast_tile_reduce
+// (merbit_spmv.hpp:58-77).  Each lane therefore receives its own sigma
+// operands with coalesced 8-byte loads and walks them in registers: no
+// product staging, no shared-memory transposition (the L1 data pipe was
+// the co-limiter with the gather request port, profiles/).
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T mul_rn(T a, T b);
+template <>
+__device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+
+template <typename T, int SIGMA>
+__device__ __forceinline__ void load_slot_vals(const T* base, int lid, T (&v)[SIGMA],
+                                               uint64_t pol);
+template <>
+__device__ __forceinline__ void load_slot_vals<float, 14>(const float* base, int lid,
+                                                          float (&v)[14], uint64_t pol) {
+#pragma unroll
+  for (int g = 0; g < 7; ++g)
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+        : "=f"(v[2 * g]), "=f"(v[2 * g + 1])
+        : "l"(base + g * 64 + 2 * lid), "l"(pol));
+}
+template <>
+__device__ __forceinline__ void load_slot_vals<double, 7>(const double* base, int lid,
+                                                          double (&v)[7], uint64_t pol) {
+#pragma unroll
+  for (int i = 0; i < 7; ++i)
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+        : "=d"(v[i])
+        : "l"(base + i * 32 + lid), "l"(pol));
+}
+template <int SIGMA, int G>
+__device__ __forceinline__ void load_slot_cols(const int32_t* base, int lid, int (&c)[SIGMA],
+                                               uint64_t pol) {
+  if constexpr (G == 2) {
+#pragma unroll
+    for (int g = 0; g < SIGMA / 2; ++g)
+      asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+          : "=r"(c[2 * g]), "=r"(c[2 * g + 1])
+          : "l"(base + g * 64 + 2 * lid), "l"(pol));
+  } else {
+#pragma unroll
+    for (int i = 0; i < SIGMA; ++i)
+      asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+          : "=r"(c[i])
+          : "l"(base + i * 32 + lid), "l"(pol));
+  }
+}
+
+template <typename T>
+struct SlotParams {
+  const T* svals;
+  const int32_t* scols;
+  const T* x;
+  T* y;
+  const uint32_t* tile_x;
+  const uint32_t* tile_y;
+  const uint32_t* lane_desc;
+  const int32_t* hub_cols;
+  uint32_t* carry_row;
+  T* carry_val;
+  Geometry g;
+  PrArgs pr;
+};
+
+// gather x for the steps in `mask` (bit i: slot i is a live element)
+template <typename T, int SIGMA, bool HUB>
+__device__ __forceinline__ void gather_slots(const T* __restrict__ x, const T* hub,
+                                             const int (&col)[SIGMA], uint32_t mask,
+                                             T (&xv)[SIGMA]) {
+#pragma unroll
+  for (int i = 0; i < SIGMA; ++i) {
+    xv[i] = T(0);
+    if ((mask >> i) & 1u) {
+      const int c = col[i];
+      if (HUB && c < 0)
+        xv[i] = hub[c & 0x7FFFFFFF];
+      else
+        xv[i] = __ldg(x + c);
+    }
+  }
+}
+
+// Inclusive segmented scan of the lanes' trailing sums (Alg. 5,
+// merbit_spmv.hpp:85-117) with the previous tile's carry entering at lane 0;
+// returns the new carry (lane 31's run) and sets `headv` (the value of the
+// lane's first closed row, valid iff had_down).
+template <typename T>
+__device__ __forceinline__ T seg_scan(T sum, T head, bool had_down, int lid, T carry, T& headv) {
+  T tail = sum;
+  if (lid == 0) {
+    if (had_down)
+      head += carry;
+    else
+      tail += carry;
+  }
+  T S_ = tail;
+  bool F = had_down;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const T su = __shfl_up_sync(kFull, S_, off);
+    const bool fu = __shfl_up_sync(kFull, F, off);
+    if (lid >= off && !F) {
+      S_ += su;
+      F = fu;
+    }
+  }
+  const T prevS = __shfl_up_sync(kFull, S_, 1);
+  headv = head + (lid > 0 ? prevS : T(0));
+  return __shfl_sync(kFull, S_, 31);
+}
+
+template <typename T, bool PR>
+__device__ __forceinline__ void commit_row(const SlotParams<T>& p, T base, int64_t row, T w,
+                                           PrAcc& acc) {
+  if (PR)
+    pr_commit<T>(p.pr, base, row, w, p.y, acc);
+  else
+    p.y[row] = w;
+}
+
+template <typename T, int SIGMA, bool PR, bool HUB>
+__device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub, T* rowbuf,
+                                           int64_t range, int lid, uint64_t pol, T base) {
+  constexpr int G = 8 / int(sizeof(T));
+  constexpr int TS = 32 * SIGMA;
+  const Geometry& g = p.g;
+  const int64_t c0 = range * g.chunks_per_range;
+  const int nc = static_cast<int>(imin64(c0 + g.chunks_per_range, g.num_chunks) - c0);
+  const int64_t total = g.nnz + g.n_rows;
+  const int ob = g.ob;
+  const uint32_t omask = (1u << ob) - 1u;
+
+  uint32_t mtx = 0, mty = 0;
+  if (lid <= nc) {
+    mtx = ld_stream_u32(p.tile_x + c0 + lid, pol);
+    mty = ld_stream_u32(p.tile_y + c0 + lid, pol);
+  }
+  const uint32_t head_row = __shfl_sync(kFull, mty, 0) & ~kLongRowMask;
+  const uint32_t tail_row = __shfl_sync(kFull, mty, nc) & ~kLongRowMask;
+  T carry = T(0), head_val = T(0);
+  bool head_open = true;
+  PrAcc acc;
+
+  for (int ci = 0; ci < nc; ++ci) {
+    const int64_t c = c0 + ci;
+    const uint32_t x0 = __shfl_sync(kFull, mtx, ci);
+    const uint32_t x1 = __shfl_sync(kFull, mtx, ci + 1);
+    const uint32_t ty0 = __shfl_sync(kFull, mty, ci);
+    const uint32_t y0 = ty0 & ~kLongRowMask;
+    const uint32_t y1 = __shfl_sync(kFull, mty, ci + 1) & ~kLongRowMask;
+    const int cnt = static_cast<int>(x1 - x0);
+    const int nrows = static_cast<int>(y1 - y0);
+    const T* vb = p.svals + c * TS;
+    const int32_t* cb = p.scols + c * TS;
+    if (ty0 & kLongRowMask) {
+      // marked tile: one row; lane-strided subtotals + halving tree
+      // (fast_tile_reduce, merbit_spmv.hpp:58-77) -- the butterfly's lane 0
+      // adds exactly the halving tree's operand pairs
+      int col[SIGMA];
+      load_slot_cols<SIGMA, G>(cb, lid, col, pol);
+      uint32_t live = 0;
+#pragma unroll
+      for (int i = 0; i < SIGMA; ++i) live |= (32 * i + lid < cnt ? 1u : 0u) << i;
+      T xv[SIGMA], v[SIGMA];
+      gather_slots<T, SIGMA, HUB>(p.x, hub, col, live, xv);
+      load_slot_vals<T, SIGMA>(vb, lid, v, pol);
+      T s = T(0);
+#pragma unroll
+      for (int i = 0; i < SIGMA; ++i)
+        if ((live >> i) & 1u) s += mul_rn(v[i], xv[i]);
+      s = __shfl_sync(kFull, warp_sum(s), 0);
+      carry += s;
+      continue;
+    }
+    if (cnt == 0) {
+      // no nonzero: the first closure ends the carried row, the rest are
+      // empty rows (merbit_spmv.hpp:217-224)
+      for (int k = lid; k < nrows; k += 32) {
+        const T w = k == 0 ? carry : T(0);
+        if (k == 0 && head_open) {
+          head_val = w;
+          continue;
+        }
+        commit_row<T, PR>(p, base, int64_t(y0) + k, w, acc);
+      }
+      carry = T(0);
+      if (nrows > 0) head_open = false;
+      continue;
+    }
+    const int64_t j = c * 32 + lid;
+    const bool valid = j < g.lane_num;
+    const uint32_t d = valid ? ld_stream_u32(p.lane_desc + j, pol) : 0u;
+    const int steps = valid ? static_cast<int>(imin64(SIGMA, total - j * SIGMA)) : 0;
+    const uint32_t live = steps >= 32 ? kFull : ((1u << steps) - 1u);
+    const uint32_t dmask = (d >> (2 * ob)) & live;
+    const uint32_t rmask = ~(d >> (2 * ob)) & live;
+    const int r0 = static_cast<int>((d >> ob) & omask);
+    const bool direct = nrows > kSlotRowBuf;  // warp-uniform
+    int col[SIGMA];
+    load_slot_cols<SIGMA, G>(cb, lid, col, pol);
+    T xv[SIGMA], v[SIGMA];
+    gather_slots<T, SIGMA, HUB>(p.x, hub, col, rmask, xv);
+    load_slot_vals<T, SIGMA>(vb, lid, v, pol);
+    // per-lane walk (Alg. 4, merbit_spmv.hpp:251-297) in registers
+    int r = r0;
+    T sum = T(0), head = T(0);
+    bool had_down = false;
+#pragma unroll
+    for (int i = 0; i < SIGMA; ++i) {
+      if ((dmask >> i) & 1u) {
+        if (!had_down) {
+          head = sum;
+          had_down = true;
+        } else if (!direct) {
+          rowbuf[r] = sum;  // row opened and closed inside this lane
+        } else {
+          p.y[int64_t(y0) + r] = sum;  // raw row sum; PR update below
+        }
+        sum = T(0);
+        ++r;
+      } else if ((rmask >> i) & 1u) {
+        sum += mul_rn(v[i], xv[i]);
+      }
+    }
+    // pi_old / dangling words of the commit, in flight during the scan
+    T po_pre = T(0);
+    uint32_t dw_pre = 0u;
+    if (PR && !direct && lid < nrows) {
+      const int64_t pr_row = int64_t(y0) + lid;
+      po_pre = __ldg(reinterpret_cast<const T*>(p.pr.pi_old) + pr_row);
+      dw_pre = __ldg(p.pr.dangling + (pr_row >> 5));
+    }
+    T headv;
+    carry = seg_scan<T>(sum, head, had_down, lid, carry, headv);
+    if (!direct) {
+      if (had_down) rowbuf[r0] = headv;
+      __syncwarp();
+      // coalesced commit of the tile's rows (Alg. 6 load_mem)
+      for (int k = lid; k < nrows; k += 32) {
+        const T w = rowbuf[k];
+        if (k == 0 && head_open) {
+          head_val = w;
+          continue;
+        }
+        const int64_t row = int64_t(y0) + k;
+        if (PR) {
+          if (k < 32)
+            pr_commit_v<T>(p.pr, base, row, w, po_pre, (dw_pre >> (row & 31)) & 1u, p.y, acc);
+          else
+            pr_commit<T>(p.pr, base, row, w, p.y, acc);
+        } else {
+          p.y[row] = w;
+        }
+      }
+      __syncwarp();
+    } else {
+      // more rows than the row buffer: raw sums went straight to y; the
+      // PageRank update then runs over the tile's rows, coalesced
+      const bool opens = had_down && r0 == 0;  // this lane closes the tile's row 0
+      const unsigned who = __ballot_sync(kFull, opens);
+      const T hv = __shfl_sync(kFull, headv, who ? __ffs(who) - 1 : 0);
+      if (had_down && !(opens && head_open)) p.y[int64_t(y0) + r0] = headv;
+      __syncwarp();
+      if (PR) {
+        for (int k = lid; k < nrows; k += 32) {
+          if (k == 0 && head_open) continue;
+          const int64_t row = int64_t(y0) + k;
+          pr_commit<T>(p.pr, base, row, p.y[row], p.y, acc);
+        }
+        __syncwarp();
+      }
+      if (head_open && who) head_val = hv;
+    }
+    if (nrows > 0) head_open = false;
+  }
+  if (lid == 0) {
+    p.carry_row[2 * range] = head_row;
+    p.carry_val[2 * range] = head_open ? T(0) : head_val;
+    p.carry_row[2 * range + 1] = tail_row;
+    p.carry_val[2 * range + 1] = carry;
+  }
+  if (PR) {
+    acc.resid = warp_sum(acc.resid);
+    acc.dang = warp_sum(acc.dang);
+    acc.mass = warp_sum(acc.mass);
+    acc.err = warp_max(acc.err);
+    if (lid == 0) {
+      double* rp = p.pr.range_part + 4 * range;
+      rp[0] = acc.resid;
+      rp[1] = acc.dang;
+      rp[2] = acc.mass;
+      rp[3] = acc.err;
+    }
+  }
+}
+
+template <typename T, int SIGMA, bool PR, bool HUB>
+__global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geometry& g = p.g;
+  if (PR && *p.pr.stop) return;
+  const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
+  T* hub = reinterpret_cast<T*>(smem_raw);
+  const int hub_pad = HUB ? ((g.hub_count + 3) & ~3) : 0;
+  T* rowbuf = hub + hub_pad + size_t(warp) * kSlotRowBuf;
+  if (HUB) {
+    for (int i = threadIdx.x; i < g.hub_count; i += blockDim.x) hub[i] = __ldg(p.x + p.hub_cols[i]);
+    __syncthreads();
+  }
+  const uint64_t pol = evict_first_policy();
+  T base = T(0);
+  if (PR) base = pr_base<T>(p.pr);
+  const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t range = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp; range < g.num_ranges;
+       range += wstride)
+    slot_range<T, SIGMA, PR, HUB>(p, hub, rowbuf, range, lid, pol, base);
+}
+
+// One thread per (chunk, lane): writes that lane's sigma slots.
+template <typename T>
+__global__ void build_slots_kernel(const T* __restrict__ vals, const int32_t* __restrict__ cols,
+                                   const uint32_t* __restrict__ tile_x,
+                                   const uint32_t* __restrict__ tile_y,
+                                   const uint32_t* __restrict__ lane_desc, int64_t lane_num,
+                                   int64_t num_chunks, int64_t total, int sigma, int ob,
+                                   T* __restrict__ svals, int32_t* __restrict__ scols) {
+  constexpr int G = 8 / int(sizeof(T));
+  const uint32_t omask = (1u << ob) - 1u;
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < num_chunks * 32;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = j >> 5;
+    const int l = static_cast<int>(j & 31);
+    const int64_t x0 = tile_x[c], x1 = tile_x[c + 1];
+    const int64_t sb = c * 32 * sigma + int64_t(l) * G;
+    if (tile_y[c] & kLongRowMask) {
+      for (int i = 0; i < sigma; ++i) {
+        const int64_t e = x0 + int64_t(i) * 32 + l;
+        const int64_t pos = sb + int64_t(i / G) * 32 * G + (i % G);
+        const bool ok = e < x1;
+        svals[pos] = ok ? vals[e] : T(0);
+        scols[pos] = ok ? cols[e] : 0;
+      }
+    } else {
+      uint32_t d = 0;
+      int steps = 0;
+      if (j < lane_num) {
+        d = lane_desc[j];
+        steps = static_cast<int>(imin64(sigma, total - j * sigma));
+      }
+      int64_t x = x0 + (d & omask);
+      const uint32_t fl = d >> (2 * ob);
+      for (int i = 0; i < sigma; ++i) {
+        const int64_t pos = sb + int64_t(i / G) * 32 * G + (i % G);
+        if (i < steps && !((fl >> i) & 1u)) {
+          svals[pos] = vals[x];
+          scols[pos] = cols[x];
+          ++x;
+        } else {
+          svals[pos] = T(0);
+          scols[pos] = 0;
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int SIGMA, bool PR, bool HUB>
+void launch_slot(mbx_context* ctx, const SlotParams<T>& p, size_t smem) {
+  auto kern = spmv_slot_kernel<T, SIGMA, PR, HUB>;
+  static int configured = -1;
+  if (configured != ctx->device) {
+    int optin = 0;
+    MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    MBX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    configured = ctx->device;
+  }
+  const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
+  const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));
+  kern<<<grid, p.g.warps_per_cta * 32, smem, ctx->stream>>>(p);
+}
+
+// ---------------------------------------------------------------------------
 // K3: boundary rows.  Carries are ordered by range, rows nondecreasing; each
 // run of equal rows is summed left to right (ascending block order, exactly
 // the reference's fold order) and ASSIGNED; the terminal row n is dropped.
@@ -904,7 +1296,27 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
   const size_t row_bytes = ((ne * 4 + 255) / 256) * 256;
   p.carry_val = reinterpret_cast<T*>(static_cast<char*>(ws) + row_bytes);
   if (pr) p.pr = *pr;
-  if (g.omega == 32) {
+  if (g.slots) {
+    SlotParams<T> q;
+    q.svals = static_cast<const T*>(m->slots.vals);
+    q.scols = m->slots.cols;
+    q.x = p.x;
+    q.y = p.y;
+    q.tile_x = p.tile_x;
+    q.tile_y = p.tile_y;
+    q.lane_desc = p.lane_desc;
+    q.hub_cols = p.hub_cols;
+    q.carry_row = p.carry_row;
+    q.carry_val = p.carry_val;
+    q.g = g;
+    q.pr = p.pr;
+    constexpr int kDefSigma = sizeof(T) == 4 ? 14 : 7;
+    const size_t smem = spmv_smem_bytes(g, m->precision);
+    if (g.hub_count > 0)
+      launch_slot<T, kDefSigma, PR, true>(ctx, q, smem);
+    else
+      launch_slot<T, kDefSigma, PR, false>(ctx, q, smem);
+  } else if (g.omega == 32) {
     const size_t smem = spmv_smem_bytes(g, m->precision);
     constexpr int kDefSigma = sizeof(T) == 4 ? 14 : 7;
     if (g.hub_count > 0) {
@@ -939,8 +1351,11 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
 size_t spmv_smem_bytes(const Geometry& g, int precision) {
   const size_t vs = value_size(precision);
   const size_t hub = g.hub_count > 0 ? size_t((g.hub_count + 3) & ~3) : 0;
-  return (hub + size_t(g.warps_per_cta) * (32 * g.sigma + 1)) * vs;
+  const size_t per_warp = g.slots ? size_t(kSlotRowBuf) : size_t(32 * g.sigma + 1);
+  return (hub + size_t(g.warps_per_cta) * per_warp) * vs;
 }
+
+int default_sigma(int precision) { return precision == MBX_F32 ? 14 : 7; }
 
 int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, int sigma,
                   int precision) {
@@ -954,7 +1369,9 @@ int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, in
   int64_t per_cta = per_sm / ctas_per_sm - reserve;
   if (per_cta > optin) per_cta = optin;
   const int64_t vs = int64_t(value_size(precision));
-  const int64_t bufs = int64_t(warps_per_cta) * (32 * sigma + 1) * vs;
+  const bool slot_layout = ctx->tuning.layout == 1 && sigma == default_sigma(precision);
+  const int64_t bufs =
+      int64_t(warps_per_cta) * (slot_layout ? kSlotRowBuf : 32 * sigma + 1) * vs;
   const int64_t slots = (per_cta - bufs) / vs - 4;
   return slots > 0 ? int(slots & ~int64_t(3)) : 0;
 }
@@ -964,6 +1381,59 @@ size_t spmv_workspace_bytes(const Geometry& g, int precision, bool pagerank) {
   size_t b = ((ne * 4 + 255) / 256) * 256 + ((ne * value_size(precision) + 255) / 256) * 256;
   (void)pagerank;
   return b + 256;
+}
+
+void free_slots(mbx_context* ctx, const mbx_matrix* m) {
+  if (m->slots.vals) cudaFreeAsync(m->slots.vals, ctx->stream);
+  if (m->slots.cols) cudaFreeAsync(m->slots.cols, ctx->stream);
+  m->slots = mbx_matrix::SlotCache{};
+}
+
+bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, const Geometry& g) {
+  if (ctx->tuning.layout != 1 || g.omega != 32 || g.sigma != default_sigma(m->precision) ||
+      g.num_chunks == 0)
+    return false;
+  const int hub = g.hub_count > 0 ? 1 : 0;
+  mbx_matrix::SlotCache& sc = m->slots;
+  if (sc.vals && sc.tile_serial == t->serial && sc.version == m->version && sc.hub == hub)
+    return true;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  MBX_CUDA(cudaStreamIsCapturing(ctx->stream, &cap));
+  if (cap != cudaStreamCaptureStatusNone) return false;  // never build inside a capture
+  free_slots(ctx, m);
+  const int64_t count = g.num_chunks * 32 * g.sigma;
+  const size_t vs = value_size(m->precision);
+  cudaEvent_t e0, e1;
+  MBX_CUDA(cudaEventCreate(&e0));
+  MBX_CUDA(cudaEventCreate(&e1));
+  MBX_CUDA(cudaEventRecord(e0, ctx->stream));
+  MBX_CUDA(cudaMallocAsync(&sc.vals, count * vs + 256, ctx->stream));
+  MBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.cols), count * 4 + 256, ctx->stream));
+  const int32_t* src_cols = hub ? m->cols_hub : m->cols;
+  const unsigned grid = grid_for(g.num_chunks * 32, 256, int64_t(ctx->sm_count) * 16);
+  const int64_t total = g.nnz + g.n_rows;
+  if (m->precision == MBX_F32)
+    build_slots_kernel<float><<<grid, 256, 0, ctx->stream>>>(
+        static_cast<const float*>(m->vals), src_cols, t->tile_x, t->tile_y, t->lane_desc,
+        g.lane_num, g.num_chunks, total, g.sigma, g.ob, static_cast<float*>(sc.vals), sc.cols);
+  else
+    build_slots_kernel<double><<<grid, 256, 0, ctx->stream>>>(
+        static_cast<const double*>(m->vals), src_cols, t->tile_x, t->tile_y, t->lane_desc,
+        g.lane_num, g.num_chunks, total, g.sigma, g.ob, static_cast<double*>(sc.vals), sc.cols);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+  MBX_CUDA(cudaEventRecord(e1, ctx->stream));
+  MBX_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  MBX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  sc.tile_serial = t->serial;
+  sc.version = m->version;
+  sc.hub = hub;
+  sc.count = count;
+  sc.seconds = ms * 1e-3;
+  return true;
 }
 
 void launch_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, const Geometry& g,

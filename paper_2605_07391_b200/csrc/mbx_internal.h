@@ -42,6 +42,9 @@ struct Geometry {
   // are staged in shared memory; encoded columns (sign bit) address them.
   int hub_count = 0;
   int prefetch = 0;
+  // 1: K2 walks the lane-major slot copy of the matrix (slots.cu) instead of
+  // staging products through shared memory
+  int slots = 0;
 };
 
 // Launch tuning knobs (context-wide; see mbx_context_set_tuning).
@@ -55,7 +58,14 @@ struct Tuning {
   int smem_per_sm = 128 * 1024;
   int prefetch = 0;  // L2 prefetch of the next tile's value/column lines
                      // (measured: costs request-port slots, off by default)
+  // K2 data layout: 1 = lane-major slots (default, omega 32 with the
+  // default sigma), 0 = CSR order staged through shared memory
+  int layout = 1;
 };
+
+// Rows a slot-layout warp can commit through its shared-memory row buffer;
+// tiles closing more rows commit lane by lane.
+constexpr int kSlotRowBuf = 64;
 
 // Device-side reduction slots of one fused PageRank iteration.
 struct PrScalars {
@@ -116,6 +126,21 @@ struct mbx_matrix_s {
   int32_t* hub_cols = nullptr;
   int hub_avail = 0;
   double hub_coverage = 0.0;  // fraction of nonzeros that reference a hub
+  uint64_t version = 0;       // bumped whenever cols_hub is rebuilt
+  // Lane-major slot copy of (values, [hub-encoded] columns) for one TILE:
+  // slot (chunk c, step i, lane l) holds the element lane l consumes at step
+  // i (zero for Down steps); built once per (TILE, column encoding) and
+  // reused by every SpMV / PageRank iteration (slots.cu).
+  struct SlotCache {
+    void* vals = nullptr;
+    int32_t* cols = nullptr;
+    uint64_t tile_serial = 0;
+    uint64_t version = 0;
+    int hub = 0;
+    int64_t count = 0;
+    double seconds = 0.0;  // build time (preprocessing)
+  };
+  mutable SlotCache slots;
 };
 
 struct mbx_tile_s {
@@ -125,6 +150,7 @@ struct mbx_tile_s {
   uint32_t* tile_x = nullptr;
   uint32_t* tile_y = nullptr;
   uint32_t* lane_desc = nullptr;
+  uint64_t serial = 0;  // unique per TILE (slot-cache key)
 };
 
 namespace mbx {
@@ -138,6 +164,11 @@ size_t spmv_smem_bytes(const Geometry& g, int precision);
 int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, int sigma,
                   int precision);
 void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs);
+// slots.cu: make m->slots match (t, hub encoding of g); false if the slot
+// layout does not apply (then K2 uses the staged CSR order)
+bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, const Geometry& g);
+void free_slots(mbx_context* ctx, const mbx_matrix* m);
+int default_sigma(int precision);
 
 // ---- kernels (kernels.cu) ----
 void launch_generate_tile(mbx_context* ctx, const uint32_t* ro, int64_t n_rows,

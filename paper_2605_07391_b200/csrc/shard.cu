@@ -410,6 +410,7 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
         mbx::remap_cols_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, st>>>(
             m->cols, m->nnz, dbounds, world, G->chunk_elems, s.cols_remap);
       s.view = *m;
+      s.view.slots = mbx_matrix::SlotCache{};  // the view builds its own
       s.view.cols = s.cols_remap;
       s.view.cols_hub = nullptr;
       s.view.hub_cols = nullptr;
@@ -585,6 +586,7 @@ MBX_API int mbx_shard_group_destroy(mbx_shard_group* G) {
     cudaStream_t st = G->ctx->stream;
     if (G->graph) cudaGraphExecDestroy(G->graph);
     for (mbx::Shard& s : G->shards) {
+      mbx::free_slots(G->ctx, &s.view);
       for (void* p : {static_cast<void*>(s.cols_remap), static_cast<void*>(s.dangling),
                       static_cast<void*>(s.view.cols_hub), static_cast<void*>(s.view.hub_cols),
                       static_cast<void*>(s.range_part), static_cast<void*>(s.block_part),

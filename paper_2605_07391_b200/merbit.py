@@ -195,6 +195,10 @@ class Context:
                 self.h, 131072 if smem_per_sm is None else smem_per_sm,
                 0 if prefetch is None else prefetch))
 
+    def set_layout(self, layout: int):
+        """K2 data layout: 1 lane-major slots (default), 0 staged CSR order."""
+        _check(_lib.lib().mbx_context_set_layout(self.h, layout))
+
     @property
     def launch_count(self) -> int:
         return _lib.lib().mbx_context_launch_count(self.h)
@@ -302,6 +306,13 @@ class DeviceMatrix:
         hubs, cov = C.c_int(), C.c_double()
         _check(_lib.lib().mbx_matrix_xcache_info(self.h, C.byref(hubs), C.byref(cov)))
         return hubs.value, cov.value
+
+    def slot_info(self):
+        """(slots, build seconds) of the lane-major slot copy cached on this
+        matrix (built by the first SpMV / PageRank plan per TILE)."""
+        n, sec = C.c_int64(), C.c_double()
+        _check(_lib.lib().mbx_matrix_slot_info(self.h, C.byref(n), C.byref(sec)))
+        return n.value, sec.value
 
     def device_ptrs(self):
         v, c, r = C.c_void_p(), C.c_void_p(), C.c_void_p()

@@ -13,10 +13,15 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: large-scale case (R-MAT scale >= 20)")
 
 
-@pytest.fixture(scope="session")
-def ctx():
+@pytest.fixture(scope="session", params=[1, 0], ids=["slots", "staged"])
+def ctx(request):
+    """A device context per K2 data layout: 1 = lane-major slot copy
+    (default), 0 = CSR order staged through shared memory.  Every GPU parity
+    test runs under both."""
     import paper_2605_07391_b200 as mb
-    return mb.Context(0)
+    c = mb.Context(0)
+    c.set_layout(request.param)
+    return c
 
 
 @pytest.fixture(scope="session")

@@ -191,13 +191,67 @@ def test_power_law_long_and_empty_rows_fp64(ctx):
     assert not y[lens == 0].any()
 
 
+def _short_rows(n, seed, dt):
+    """Rows of 0-3 nonzeros (30 % forced empty): ~180 rows per 32x14 tile,
+    more than the slot kernel's 64-row commit buffer."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, 4, n)
+    lens[rng.random(n) < 0.3] = 0
+    ro = np.zeros(n + 1, np.int64)
+    ro[1:] = np.cumsum(lens)
+    cols = rng.integers(0, n, int(ro[-1])).astype(np.int32)
+    for r in range(0, n):  # CSR order: ascending columns within a row
+        a0, a1 = ro[r], ro[r + 1]
+        if a1 - a0 > 1:
+            cols[a0:a1] = np.sort(cols[a0:a1])
+    vals = rng.uniform(-1, 1, int(ro[-1])).astype(dt)
+    return O.Csr(n, n, ro, cols, vals)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_many_rows_per_tile(ctx, dt):
+    """Tiles closing more rows than the 64-row commit buffer commit lane by
+    lane (slot layout) -- same bound, zero on every empty row."""
+    a = _short_rows(30000, 21, dt)
+    x = O.seed_test_vector(a.n_cols, -1, 1, 5).astype(dt)
+    want = O.spmv_csr_f64(a.astype(np.float64), x.astype(np.float64))
+    bound = tolerance_bound(a, x, dt)
+    for (w, s, b) in [(32, 14 if dt == np.float32 else 7, 128), (32, 7, 32)]:
+        got = run(ctx, a, mb.SimtConfig.make(w, s, b), x)
+        assert first_violation(bound, want, got) == -1
+        assert not got[np.diff(a.row_offsets) == 0].any()
+
+
+def test_slot_and_staged_layouts_agree(ctx):
+    """Both K2 layouts on one R-MAT matrix: within 1e-5 of each other relative
+    to sum|a||x| (they differ only in the fast-tile summation order), and the
+    slot copy is cached on the matrix after the first SpMV."""
+    m = mb.DeviceMatrix.rmat(ctx, 16, 16, seed=8, dtype=np.float32)
+    ro, cols, vals = m.download()
+    a = O.Csr(m.n_rows, m.n_cols, ro, cols, vals)
+    x = O.hash_uniform(3, m.n_cols, -1.0, 1.0, np.float32)
+    c = mb.SimtConfig.make(32, 14, 128)
+    t = mb.generate_tile_for(m, c)
+    ys = []
+    for layout in (1, 0):
+        ctx.set_layout(layout)
+        ys.append(mb.spmv_merbit(m, t, c, x, mb.DualBuffer(m.n_rows, np.float32)).copy())
+        if layout == 1:
+            assert m.slot_info()[0] >= m.nnz
+    ctx.set_layout(1)
+    _, mag = O.spmv_csr_f32_acc64(a, x)
+    assert _rel_err(ys[0], ys[1].astype(np.float64), mag).max() <= 1e-5
+
+
 @pytest.mark.parametrize("tuning", [(32, 1, 0, 147456, 1), (16, 2, 0, 147456, 0),
                                     (8, 4, 0, 147456, 1), (32, 1, -1, 131072, 1),
                                     (16, 2, -1, 147456, 0)])
-def test_launch_shapes_and_hub_cache_are_bitwise_invariant(tuning):
+@pytest.mark.parametrize("layout", [1, 0])
+def test_launch_shapes_and_hub_cache_are_bitwise_invariant(tuning, layout):
     """Every K2 launch shape, the L2 prefetch and the shared-memory x hub cache
     change only speed: y is bitwise identical to the default launch."""
     ctx = mb.Context(0)
+    ctx.set_layout(layout)
     m = mb.DeviceMatrix.rmat(ctx, 16, 16, seed=4, dtype=np.float32)
     c = mb.SimtConfig.make(32, 14, 128)
     t = mb.generate_tile_for(m, c)
