@@ -882,8 +882,9 @@ MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, cons
     pl->ref_scal = static_cast<mbx::PrScalars*>(
         dmalloc(ctx, (cfg->reference_iters + 1) * sizeof(mbx::PrScalars)));
     MBX_CUDA(cudaMemsetAsync(pl->scal, 0, (cfg->max_iters + 1) * sizeof(mbx::PrScalars), ctx->stream));
-    pl->range_part = static_cast<double*>(dmalloc(ctx, (pl->g.num_ranges + 1) * 4 * sizeof(double)));
-    const int64_t k3_blocks = (pl->g.num_ranges + 255) / 256 + 1;
+    pl->range_part = static_cast<double*>(
+        dmalloc(ctx, (std::max(pl->g.num_ranges, mbx::pr_parts(pl->g)) + 1) * 4 * sizeof(double)));
+    const int64_t k3_blocks = mbx::fixup_blocks(pl->g) + 1;
     const int64_t nb = std::max<int64_t>({k3_blocks, int64_t(mbx::csr_pr_blocks(ctx, p)),
                                           int64_t(ctx->sm_count) * 4 + 1});
     pl->block_part = static_cast<double*>(dmalloc(ctx, nb * 4 * sizeof(double)));

@@ -80,6 +80,32 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// x hub table preamble: hub[i] = x[hub_cols[i]], eight independent gathers
+// in flight per thread (a one-at-a-time loop costs ~hubs/blockDim serial L2
+// round trips before the CTA's first tile).
+template <typename T>
+__device__ __forceinline__ void stage_hubs(T* hub, const T* __restrict__ x,
+                                           const int32_t* __restrict__ hub_cols, int hc) {
+  constexpr int U = 8;
+  for (int i0 = threadIdx.x; i0 < hc; i0 += blockDim.x * U) {
+    int idx[U];
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * blockDim.x;
+      idx[u] = i < hc ? __ldg(hub_cols + i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = idx[u] >= 0 ? __ldg(x + idx[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < hc) hub[i] = v[u];
+    }
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // Product staging: values[p] * x[col[p]] for p in [x0, x1).  ACCUM: return
 // this lane's running sum (fast path, merbit_spmv.hpp:58-77); else store
@@ -374,7 +400,8 @@ __device__ __forceinline__ T lane_walk_and_scan(T* buf, int cnt, int sigma, uint
 // One warp range: `chunks_per_range` consecutive tiles (chunk == tile here).
 template <typename T, int SIGMA, bool PR, bool HUB, bool PF>
 __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, T* buf,
-                                          int64_t range, int lid, uint64_t pol, T base) {
+                                          int64_t range, int lid, uint64_t pol, T base,
+                                          PrAcc& acc) {
   const Geometry& g = p.g;
   const int sigma = SIGMA > 0 ? SIGMA : g.sigma;
   const int64_t c0 = range * g.chunks_per_range;
@@ -394,7 +421,6 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
   const uint32_t tail_row = __shfl_sync(kFull, mty, nc) & ~kLongRowMask;
   T carry = T(0), head_val = T(0);
   bool head_open = true;
-  PrAcc acc;
 
   for (int ci = 0; ci < nc; ++ci) {
     const int64_t c = c0 + ci;
@@ -486,18 +512,21 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
     p.carry_row[2 * range + 1] = tail_row;
     p.carry_val[2 * range + 1] = carry;
   }
-  if (PR) {
-    acc.resid = warp_sum(acc.resid);
-    acc.dang = warp_sum(acc.dang);
-    acc.mass = warp_sum(acc.mass);
-    acc.err = warp_max(acc.err);
-    if (lid == 0) {
-      double* rp = p.pr.range_part + 4 * range;
-      rp[0] = acc.resid;
-      rp[1] = acc.dang;
-      rp[2] = acc.mass;
-      rp[3] = acc.err;
-    }
+}
+
+// Warp partials of the fused PageRank reductions: one slot per warp of the
+// persistent grid (fixed range->warp map, so the sums are deterministic).
+__device__ __forceinline__ void write_warp_part(PrAcc acc, double* parts, int lid) {
+  acc.resid = warp_sum(acc.resid);
+  acc.dang = warp_sum(acc.dang);
+  acc.mass = warp_sum(acc.mass);
+  acc.err = warp_max(acc.err);
+  if (lid == 0) {
+    double* rp = parts + 4 * (int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5));
+    rp[0] = acc.resid;
+    rp[1] = acc.dang;
+    rp[2] = acc.mass;
+    rp[3] = acc.err;
   }
 }
 
@@ -513,17 +542,16 @@ __global__ void __launch_bounds__(1024) spmv_w32_kernel(SpmvParams<T> p) {
   T* hub = reinterpret_cast<T*>(smem_raw);
   const int hub_pad = HUB ? ((g.hub_count + 3) & ~3) : 0;
   T* buf = hub + hub_pad + size_t(warp) * (32 * sigma + 1);
-  if (HUB) {
-    for (int i = threadIdx.x; i < g.hub_count; i += blockDim.x) hub[i] = __ldg(p.x + p.hub_cols[i]);
-    __syncthreads();
-  }
+  if (HUB) stage_hubs<T>(hub, p.x, p.hub_cols, g.hub_count);
   const uint64_t pol = evict_first_policy();
   T base = T(0);
   if (PR) base = pr_base<T>(p.pr);
   const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
+  PrAcc acc;
   for (int64_t range = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp; range < g.num_ranges;
        range += wstride)
-    w32_range<T, SIGMA, PR, HUB, PF>(p, hub, buf, range, lid, pol, base);
+    w32_range<T, SIGMA, PR, HUB, PF>(p, hub, buf, range, lid, pol, base, acc);
+  if (PR) write_warp_part(acc, p.pr.range_part, lid);
 }
 
 // ---------------------------------------------------------------------------
@@ -743,6 +771,47 @@ __device__ __forceinline__ T seg_scan(T sum, T head, bool had_down, int lid, T c
   return __shfl_sync(kFull, S_, 31);
 }
 
+// Asynchronous global->shared copies (LDGSTS): the commit's pi_old rows and
+// dangling words are fetched at the start of a tile without holding
+// registers through the gather phase.
+__device__ __forceinline__ void cp_async(void* smem, const float* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(g));
+}
+__device__ __forceinline__ void cp_async(void* smem, const double* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(g));
+}
+__device__ __forceinline__ void cp_async(void* smem, const uint32_t* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(g));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// Per-lane PageRank accumulators parked in shared memory between commits
+// ([field][lane] per warp, conflict-free): keeps the 8 fp64 registers out of
+// the gather phase, where the 64-register budget of a 1024-thread CTA is
+// spent on the lane's sigma operands.
+__device__ __forceinline__ PrAcc load_acc(const double* wa, int lid) {
+  PrAcc a;
+  a.resid = wa[lid];
+  a.dang = wa[32 + lid];
+  a.mass = wa[64 + lid];
+  a.err = wa[96 + lid];
+  return a;
+}
+__device__ __forceinline__ void store_acc(double* wa, int lid, const PrAcc& a) {
+  wa[lid] = a.resid;
+  wa[32 + lid] = a.dang;
+  wa[64 + lid] = a.mass;
+  wa[96 + lid] = a.err;
+}
+
 template <typename T, bool PR>
 __device__ __forceinline__ void commit_row(const SlotParams<T>& p, T base, int64_t row, T w,
                                            PrAcc& acc) {
@@ -754,7 +823,8 @@ __device__ __forceinline__ void commit_row(const SlotParams<T>& p, T base, int64
 
 template <typename T, int SIGMA, bool PR, bool HUB>
 __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub, T* rowbuf,
-                                           int64_t range, int lid, uint64_t pol, T base) {
+                                           int64_t range, int lid, uint64_t pol, T base,
+                                           double* wacc) {
   constexpr int G = 8 / int(sizeof(T));
   constexpr int TS = 32 * SIGMA;
   const Geometry& g = p.g;
@@ -773,7 +843,6 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
   const uint32_t tail_row = __shfl_sync(kFull, mty, nc) & ~kLongRowMask;
   T carry = T(0), head_val = T(0);
   bool head_open = true;
-  PrAcc acc;
 
   for (int ci = 0; ci < nc; ++ci) {
     const int64_t c = c0 + ci;
@@ -809,6 +878,8 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
     if (cnt == 0) {
       // no nonzero: the first closure ends the carried row, the rest are
       // empty rows (merbit_spmv.hpp:217-224)
+      PrAcc acc;
+      if (PR) acc = load_acc(wacc, lid);
       for (int k = lid; k < nrows; k += 32) {
         const T w = k == 0 ? carry : T(0);
         if (k == 0 && head_open) {
@@ -817,6 +888,7 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
         }
         commit_row<T, PR>(p, base, int64_t(y0) + k, w, acc);
       }
+      if (PR) store_acc(wacc, lid, acc);
       carry = T(0);
       if (nrows > 0) head_open = false;
       continue;
@@ -830,6 +902,14 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
     const uint32_t rmask = ~(d >> (2 * ob)) & live;
     const int r0 = static_cast<int>((d >> ob) & omask);
     const bool direct = nrows > kSlotRowBuf;  // warp-uniform
+    T* pobuf = rowbuf + kSlotRowBuf;                            // pi_old of the rows
+    uint32_t* dwbuf = reinterpret_cast<uint32_t*>(pobuf + kSlotRowBuf);  // dangling words
+    if (PR && !direct) {
+      const T* po = reinterpret_cast<const T*>(p.pr.pi_old) + y0;
+      if (lid < nrows) cp_async(pobuf + lid, po + lid);
+      if (lid + 32 < nrows) cp_async(pobuf + lid + 32, po + lid + 32);
+      if (lid < 3) cp_async(dwbuf + lid, p.pr.dangling + (y0 >> 5) + lid);  // padded array
+    }
     int col[SIGMA];
     load_slot_cols<SIGMA, G>(cb, lid, col, pol);
     T xv[SIGMA], v[SIGMA];
@@ -856,19 +936,14 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
         sum += mul_rn(v[i], xv[i]);
       }
     }
-    // pi_old / dangling words of the commit, in flight during the scan
-    T po_pre = T(0);
-    uint32_t dw_pre = 0u;
-    if (PR && !direct && lid < nrows) {
-      const int64_t pr_row = int64_t(y0) + lid;
-      po_pre = __ldg(reinterpret_cast<const T*>(p.pr.pi_old) + pr_row);
-      dw_pre = __ldg(p.pr.dangling + (pr_row >> 5));
-    }
     T headv;
     carry = seg_scan<T>(sum, head, had_down, lid, carry, headv);
     if (!direct) {
       if (had_down) rowbuf[r0] = headv;
+      if (PR) cp_async_wait_all();
       __syncwarp();
+      PrAcc acc;
+      if (PR) acc = load_acc(wacc, lid);
       // coalesced commit of the tile's rows (Alg. 6 load_mem)
       for (int k = lid; k < nrows; k += 32) {
         const T w = rowbuf[k];
@@ -878,14 +953,13 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
         }
         const int64_t row = int64_t(y0) + k;
         if (PR) {
-          if (k < 32)
-            pr_commit_v<T>(p.pr, base, row, w, po_pre, (dw_pre >> (row & 31)) & 1u, p.y, acc);
-          else
-            pr_commit<T>(p.pr, base, row, w, p.y, acc);
+          const uint32_t dw = dwbuf[(uint32_t(row) >> 5) - (y0 >> 5)];
+          pr_commit_v<T>(p.pr, base, row, w, pobuf[k], (dw >> (row & 31)) & 1u, p.y, acc);
         } else {
           p.y[row] = w;
         }
       }
+      if (PR) store_acc(wacc, lid, acc);
       __syncwarp();
     } else {
       // more rows than the row buffer: raw sums went straight to y; the
@@ -896,11 +970,13 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
       if (had_down && !(opens && head_open)) p.y[int64_t(y0) + r0] = headv;
       __syncwarp();
       if (PR) {
+        PrAcc acc = load_acc(wacc, lid);
         for (int k = lid; k < nrows; k += 32) {
           if (k == 0 && head_open) continue;
           const int64_t row = int64_t(y0) + k;
           pr_commit<T>(p.pr, base, row, p.y[row], p.y, acc);
         }
+        store_acc(wacc, lid, acc);
         __syncwarp();
       }
       if (head_open && who) head_val = hv;
@@ -913,19 +989,6 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
     p.carry_row[2 * range + 1] = tail_row;
     p.carry_val[2 * range + 1] = carry;
   }
-  if (PR) {
-    acc.resid = warp_sum(acc.resid);
-    acc.dang = warp_sum(acc.dang);
-    acc.mass = warp_sum(acc.mass);
-    acc.err = warp_max(acc.err);
-    if (lid == 0) {
-      double* rp = p.pr.range_part + 4 * range;
-      rp[0] = acc.resid;
-      rp[1] = acc.dang;
-      rp[2] = acc.mass;
-      rp[3] = acc.err;
-    }
-  }
 }
 
 template <typename T, int SIGMA, bool PR, bool HUB>
@@ -936,18 +999,23 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
   T* hub = reinterpret_cast<T*>(smem_raw);
   const int hub_pad = HUB ? ((g.hub_count + 3) & ~3) : 0;
-  T* rowbuf = hub + hub_pad + size_t(warp) * kSlotRowBuf;
-  if (HUB) {
-    for (int i = threadIdx.x; i < g.hub_count; i += blockDim.x) hub[i] = __ldg(p.x + p.hub_cols[i]);
-    __syncthreads();
-  }
+  // per warp: row buffer (64 T), pi_old rows (64 T), dangling words (4 u32)
+  constexpr size_t kWarpBytes = 2 * kSlotRowBuf * sizeof(T) + 16;
+  unsigned char* wbase = reinterpret_cast<unsigned char*>(hub + hub_pad);
+  T* rowbuf = reinterpret_cast<T*>(wbase + size_t(warp) * kWarpBytes);
+  double* wacc = reinterpret_cast<double*>(wbase + size_t(blockDim.x >> 5) * kWarpBytes) +
+                 size_t(warp) * 128;
+  if (PR) store_acc(wacc, lid, PrAcc());
+  if (HUB) stage_hubs<T>(hub, p.x, p.hub_cols, g.hub_count);
   const uint64_t pol = evict_first_policy();
   T base = T(0);
   if (PR) base = pr_base<T>(p.pr);
   const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t range = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp; range < g.num_ranges;
        range += wstride)
-    slot_range<T, SIGMA, PR, HUB>(p, hub, rowbuf, range, lid, pol, base);
+    slot_range<T, SIGMA, PR, HUB>(p, hub, rowbuf, range, lid, pol, base, wacc);
+  __syncwarp();
+  if (PR) write_warp_part(load_acc(wacc, lid), p.pr.range_part, lid);
 }
 
 // One thread per (chunk, lane): writes that lane's sigma slots.
@@ -1018,41 +1086,70 @@ void launch_slot(mbx_context* ctx, const SlotParams<T>& p, size_t smem) {
 // run of equal rows is summed left to right (ascending block order, exactly
 // the reference's fold order) and ASSIGNED; the terminal row n is dropped.
 // ---------------------------------------------------------------------------
+constexpr int kFixupRun = 32;  // carries one thread folds before the warp takes over
+
 template <typename T, bool PR>
 __global__ void __launch_bounds__(256) fixup_kernel(const uint32_t* __restrict__ crow,
                                                     const T* __restrict__ cval,
                                                     int64_t num_ranges, int64_t n_rows,
-                                                    T* __restrict__ y, PrArgs pr) {
+                                                    T* __restrict__ y, PrArgs pr,
+                                                    int64_t num_parts) {
   if (PR && *pr.stop) return;
-  const int64_t rg = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  // one thread per carry entry; the first entry of each run of equal rows
+  // folds the run left to right (merbit_spmv.hpp:330-337) -- runs longer
+  // than kFixupRun (rows spanning many ranges) are folded by the whole warp
+  // in a fixed lane-strided order + butterfly
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lid = threadIdx.x & 31;
   const int64_t ne = 2 * num_ranges;
   PrAcc acc;
   T base = T(0);
   if (PR) base = pr_base<T>(pr);
-  if (rg < num_ranges) {
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int64_t e = 2 * rg + s;
-      const uint32_t r = crow[e];
-      if (e > 0 && crow[e - 1] == r) continue;
-      T sum = T(0);
-      for (int64_t k = e; k < ne && crow[k] == r; ++k) sum += cval[k];
-      if (int64_t(r) < n_rows) {
-        if (PR)
-          pr_commit<T>(pr, base, r, sum, y, acc);
-        else
-          y[r] = sum;
-      }
+  uint32_t r = 0;
+  bool start = false, lng = false;
+  T sum = T(0);
+  if (e < ne) {
+    r = crow[e];
+    start = e == 0 || crow[e - 1] != r;
+    if (start) {
+      int64_t k = e;
+      const int64_t lim = imin64(ne, e + kFixupRun);
+      for (; k < lim && crow[k] == r; ++k) sum += cval[k];
+      lng = k == lim && k < ne && crow[k] == r;
     }
-    if (PR) {
-      const double* rp = pr.range_part + 4 * rg;
+  }
+  unsigned long_lanes = __ballot_sync(kFull, lng);
+  while (long_lanes) {
+    const int src = __ffs(long_lanes) - 1;
+    long_lanes &= long_lanes - 1;
+    const int64_t e0 = __shfl_sync(kFull, e, src);
+    const uint32_t rr = __shfl_sync(kFull, r, src);
+    T part = T(0);
+    for (int64_t w = e0;; w += 32) {
+      const int64_t k = w + lid;
+      const bool in = k < ne && crow[k] == rr;
+      if (in) part += cval[k];
+      if (__ballot_sync(kFull, in) != kFull) break;
+    }
+    part = __shfl_sync(kFull, warp_sum(part), 0);
+    if (lid == src) sum = part;
+  }
+  if (start && int64_t(r) < n_rows) {
+    if (PR)
+      pr_commit<T>(pr, base, r, sum, y, acc);
+    else
+      y[r] = sum;
+  }
+  if (PR) {
+    if (e < num_parts) {
+      const double* rp = pr.range_part + 4 * e;
       acc.resid += rp[0];
       acc.dang += rp[1];
       acc.mass += rp[2];
       acc.err = fmax(acc.err, rp[3]);
     }
+    pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, pr.check_stop != 0);
   }
-  if (PR) pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, pr.check_stop != 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1339,9 +1436,9 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
   }
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
-  const unsigned fgrid = static_cast<unsigned>((g.num_ranges + 255) / 256);
-  fixup_kernel<T, PR><<<fgrid, 256, 0, ctx->stream>>>(p.carry_row, p.carry_val,
-                                                     g.num_ranges, g.n_rows, p.y, p.pr);
+  const unsigned fgrid = static_cast<unsigned>(fixup_blocks(g));
+  fixup_kernel<T, PR><<<fgrid, 256, 0, ctx->stream>>>(p.carry_row, p.carry_val, g.num_ranges,
+                                                     g.n_rows, p.y, p.pr, pr_parts(g));
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
 }
@@ -1351,8 +1448,9 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
 size_t spmv_smem_bytes(const Geometry& g, int precision) {
   const size_t vs = value_size(precision);
   const size_t hub = g.hub_count > 0 ? size_t((g.hub_count + 3) & ~3) : 0;
-  const size_t per_warp = g.slots ? size_t(kSlotRowBuf) : size_t(32 * g.sigma + 1);
-  return (hub + size_t(g.warps_per_cta) * per_warp) * vs;
+  if (g.slots)  // hub | per warp: rows, pi_old rows, dangling words | parked accumulators
+    return hub * vs + size_t(g.warps_per_cta) * (2 * kSlotRowBuf * vs + 16 + 128 * sizeof(double));
+  return (hub + size_t(g.warps_per_cta) * (32 * g.sigma + 1)) * vs;
 }
 
 int default_sigma(int precision) { return precision == MBX_F32 ? 14 : 7; }
@@ -1370,10 +1468,23 @@ int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, in
   if (per_cta > optin) per_cta = optin;
   const int64_t vs = int64_t(value_size(precision));
   const bool slot_layout = ctx->tuning.layout == 1 && sigma == default_sigma(precision);
-  const int64_t bufs =
-      int64_t(warps_per_cta) * (slot_layout ? kSlotRowBuf : 32 * sigma + 1) * vs;
+  const int64_t bufs = slot_layout
+                           ? int64_t(warps_per_cta) * (2 * kSlotRowBuf * vs + 16 + 128 * 8)
+                           : int64_t(warps_per_cta) * (32 * sigma + 1) * vs;
   const int64_t slots = (per_cta - bufs) / vs - 4;
   return slots > 0 ? int(slots & ~int64_t(3)) : 0;
+}
+
+int64_t pr_parts(const Geometry& g) {
+  if (g.omega != 32) return g.num_ranges;  // spmv_generic_kernel: one per range
+  const int64_t need = (g.num_ranges + g.warps_per_cta - 1) / g.warps_per_cta;
+  return imin64(g.grid, need) * g.warps_per_cta;  // persistent: one per warp
+}
+
+int64_t fixup_blocks(const Geometry& g) {
+  const int64_t ne = 2 * g.num_ranges;
+  const int64_t n = ne > pr_parts(g) ? ne : pr_parts(g);
+  return n > 0 ? (n + 255) / 256 : 1;
 }
 
 size_t spmv_workspace_bytes(const Geometry& g, int precision, bool pagerank) {

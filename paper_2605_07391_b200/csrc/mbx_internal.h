@@ -84,7 +84,7 @@ struct PrArgs {
   double inv_n = 0.0;
   const PrScalars* prev = nullptr;  // scalars of pi_old (dangling mass)
   PrScalars* next = nullptr;        // scalars of pi_new (written by K3)
-  double* range_part = nullptr;     // 4 doubles per range (K2 -> K3)
+  double* range_part = nullptr;     // 4 doubles per K2 part (K2 -> K3), see pr_parts
   double* block_part = nullptr;     // 4 doubles per K3 block
   unsigned int* done_counter = nullptr;
   int* stop = nullptr;         // set once converged / failed
@@ -177,6 +177,11 @@ void launch_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
                  const Geometry& g, const void* x, void* y, void* carry_ws,
                  const PrArgs* pr);
 size_t spmv_workspace_bytes(const Geometry& g, int precision, bool pagerank);
+// PageRank partial sums K2 hands to K3: one per warp of the persistent
+// omega-32 kernels, one per range otherwise.
+int64_t pr_parts(const Geometry& g);
+// K3 blocks of one SpMV / PageRank iteration (block_part slots it needs).
+int64_t fixup_blocks(const Geometry& g);
 void launch_trace_counts(mbx_context* ctx, const mbx_tile* t,
                          unsigned long long* counters_dev);
 void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,

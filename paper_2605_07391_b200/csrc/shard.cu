@@ -423,9 +423,10 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
       mbx::local_dangling_kernel<<<unsigned((rows + 31) / 32 / 256 + 1), 256, 0, st>>>(
           seen, s.r0, rows, s.dangling);
       s.geo = mbx::make_geometry(ctx, &s.view, s.tile, c->block_size);
-      s.range_part = static_cast<double*>(dm(ctx, (s.geo.num_ranges + 1) * 4 * sizeof(double)));
+      s.range_part = static_cast<double*>(
+          dm(ctx, (std::max(s.geo.num_ranges, mbx::pr_parts(s.geo)) + 1) * 4 * sizeof(double)));
       // K3 blocks, or the pr_init grid (sm_count * 4) when a start vector is given
-      const int64_t nblk = std::max<int64_t>((s.geo.num_ranges + 255) / 256 + 1, ctx->sm_count * 4 + 1);
+      const int64_t nblk = std::max<int64_t>(mbx::fixup_blocks(s.geo) + 1, ctx->sm_count * 4 + 1);
       s.block_part = static_cast<double*>(dm(ctx, nblk * 4 * sizeof(double)));
       s.counter = static_cast<unsigned int*>(dm(ctx, 64));
       MBX_CUDA(cudaMemsetAsync(s.counter, 0, 64, st));
