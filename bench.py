@@ -50,6 +50,18 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def traffic_per_launch():
+    """DRAM bytes (read + write) of one fused PageRank iteration (K2 + K3) at
+    scale 24, from the committed `ncu --set full` capture summarised in
+    profiles/ncu_traffic.json (null when absent)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d["pagerank_iteration_s24_f32"]["dram_bytes"]
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -398,8 +410,8 @@ def main():
                    "l2": "inputs (values+cols %.1f GB per GPU) larger than L2; no flush"
                          % (8 * local_nnz / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "fused PageRank iteration (spmv_w32_kernel<float,14,PR> + "
+                     "frac": achieved / peak, "traffic": traffic_per_launch(), "peak_kind": peak_kind,
+                     "kernel": "fused PageRank iteration (spmv_slot_kernel<float,14,PR,HUB> + "
                                "fixup_kernel) on rank 0",
                      "bytes_per_launch": b_iter, "us_per_iteration": t_iter_local * 1e6},
         "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d,

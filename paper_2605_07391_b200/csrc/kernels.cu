@@ -1517,9 +1517,9 @@ bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, cons
   cudaEvent_t e0, e1;
   MBX_CUDA(cudaEventCreate(&e0));
   MBX_CUDA(cudaEventCreate(&e1));
-  MBX_CUDA(cudaEventRecord(e0, ctx->stream));
   MBX_CUDA(cudaMallocAsync(&sc.vals, count * vs + 256, ctx->stream));
   MBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.cols), count * 4 + 256, ctx->stream));
+  MBX_CUDA(cudaEventRecord(e0, ctx->stream));  // build time, not the allocation
   const int32_t* src_cols = hub ? m->cols_hub : m->cols;
   const unsigned grid = grid_for(g.num_chunks * 32, 256, int64_t(ctx->sm_count) * 16);
   const int64_t total = g.nnz + g.n_rows;
