@@ -186,6 +186,13 @@ __device__ __forceinline__ T stage_products(const T* __restrict__ vals,
   return acc;
 }
 
+template <typename T>
+__device__ __forceinline__ T mul_rn(T a, T b);
+template <>
+__device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+
 // ---------------------------------------------------------------------------
 // PageRank commit of one finished row w = (P pi_old)[row]:
 //   pi_new = damping * w + base  (rank_update, solvers.hpp:99-115)
@@ -205,9 +212,13 @@ struct PrAcc {
 template <typename T>
 __device__ __forceinline__ void pr_commit_v(const PrArgs& pr, T base, int64_t row, T w, T po,
                                             bool dang, T* __restrict__ out, PrAcc& a) {
-  const T pn = static_cast<T>(pr.damping) * w + base;
+  // c * w + base with the product rounded first, as rank_update computes it
+  // (solvers.hpp:110-112; no contraction into an FMA)
+  const T pn = mul_rn(static_cast<T>(pr.damping), w) + base;
   out[row] = pn;
-  a.resid += fabs(static_cast<double>(pn) - static_cast<double>(po));
+  // |pn - po| is formed in T (the reference's own precision for pi) and
+  // accumulated in fp64
+  a.resid += static_cast<double>(fabs(pn - po));
   if (dang) a.dang += static_cast<double>(pn);
   a.mass += fabs(static_cast<double>(pn));
   if (pr.yardstick) {
@@ -662,13 +673,6 @@ __global__ void __launch_bounds__(kThreads) spmv_generic_kernel(SpmvParams<T> p)
 // product staging, no shared-memory transposition (the L1 data pipe was
 // the co-limiter with the gather request port, profiles/).
 // ---------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ T mul_rn(T a, T b);
-template <>
-__device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
-template <>
-__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
-
 template <typename T, int SIGMA>
 __device__ __forceinline__ void load_slot_vals(const T* base, int lid, T (&v)[SIGMA],
                                                uint64_t pol);
