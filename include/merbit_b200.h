@@ -98,6 +98,23 @@ typedef struct {
   double dangling_mass;      /* sum of pi_k over dangling vertices */
 } mbx_pagerank_result;
 
+/* BicgstabConfig (solvers.hpp:224-228). */
+typedef struct {
+  double tol;        /* 1e-10 (converted to T like BicgstabConfig<T>) */
+  int64_t max_iters; /* 20000 */
+} mbx_bicgstab_config;
+
+/* BicgstabResult (solvers.hpp:230-240); x and the residual history are
+ * returned through the caller's buffers. */
+typedef struct {
+  int64_t iterations;
+  double final_residual;     /* ||A x - b|| / ||b|| of the last pass */
+  int32_t status;            /* 0 converged, 1 max_iterations, 2 breakdown */
+  char breakdown_reason[32]; /* "rho", "rhat_dot_v", "t_dot_t", "omega", "diverged" */
+  double preprocess_seconds; /* T_p of the TILE used */
+  double iterate_seconds;    /* device time of the iteration loop */
+} mbx_bicgstab_result;
+
 typedef struct mbx_context_s mbx_context;
 typedef struct mbx_matrix_s mbx_matrix;
 typedef struct mbx_tile_s mbx_tile;
@@ -296,6 +313,19 @@ MBX_API const void* mbx_pagerank_plan_pi(const mbx_pagerank_plan* plan);
 MBX_API const void* mbx_pagerank_plan_reference_pi(
     const mbx_pagerank_plan* plan);
 MBX_API int mbx_pagerank_plan_destroy(mbx_pagerank_plan* plan);
+
+/* ---- BiCGSTAB (K2/K3 SpMVs + device dot/axpy kernels) ------------------- */
+/* bicgstab<T>(a, b, cfg, backend) (solvers.hpp:268-373): unpreconditioned
+ * BiCGSTAB, three SpMVs per pass (the third for the true-residual stopping
+ * test), breakdown reported with the reference's reason string.  Inner
+ * products accumulate in fp64 (rounded to T once); vector updates round in T
+ * exactly as written.  dimension_error on a non-square system, config_error
+ * on a TILE that does not belong to the matrix.  residual_history_host
+ * (max_iters doubles) may be NULL. */
+MBX_API int mbx_bicgstab(mbx_context* ctx, const mbx_matrix* a, const mbx_tile* t,
+                         const mbx_simt_config* c, const mbx_bicgstab_config* cfg,
+                         const void* b_host, void* x_host,
+                         double* residual_history_host, mbx_bicgstab_result* result);
 
 /* ---- multi-GPU row-sharded PageRank (one process per GPU) ---------------- */
 /* GPU g owns rows [row_bounds[g], row_bounds[g+1]) of P (mbx_plan_row_shards)

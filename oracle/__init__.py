@@ -112,6 +112,11 @@ def lib():
                                       C.c_float, C.c_int64, C.c_int64, f32p, f32p,
                                       C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                       C.POINTER(C.c_int)]
+        for name, fp, tt in (("mo_bicgstab_f64", f64p, C.c_double),
+                             ("mo_bicgstab_f32", f32p, C.c_float)):
+            getattr(L, name).argtypes = [C.c_int64, i64p, i32p, fp, fp, tt, C.c_int64, fp,
+                                         f64p, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.mo_free.argtypes = [C.c_void_p]
         alloc_args = [C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int32)),
                       C.POINTER(C.POINTER(C.c_double))]
@@ -288,9 +293,65 @@ def pagerank(p: Csr, damping=0.85, err_tol=1e-10, max_iters=210, reference_iters
                 status="converged" if st.value == 0 else "max_iterations")
 
 
+_SOLVE_STATUS = {0: "converged", 1: "max_iterations", 2: "breakdown"}
+_BREAKDOWN = {0: "", 1: "rho", 2: "rhat_dot_v", 3: "t_dot_t", 4: "omega", 5: "diverged"}
+
+
+def bicgstab(a: Csr, b, tol=1e-10, max_iters=20000):
+    """bicgstab<T> over the csr backend (solvers.hpp:268-373) in a.values' dtype
+    (dot products sequential in T, residual norm in fp64)."""
+    n = a.n_rows
+    dt = a.values.dtype
+    x = np.zeros(n, dt)
+    hist = np.zeros(max(max_iters, 1), np.float64)
+    it, fr, st, why = C.c_int64(), C.c_double(), C.c_int(), C.c_int()
+    fn = lib().mo_bicgstab_f64 if dt == np.float64 else lib().mo_bicgstab_f32
+    _check(fn(n, a.row_offsets, _vals_or_dummy(a.col_indices), _vals_or_dummy(a.values),
+              np.ascontiguousarray(b, dt), tol, max_iters, x, hist, C.byref(it), C.byref(fr),
+              C.byref(st), C.byref(why)), "bicgstab")
+    reason = _BREAKDOWN[why.value]
+    return dict(x=x, residual_history=hist[:_hist_len(it.value, st.value, reason)],
+                iterations=it.value, final_residual=fr.value, status=_SOLVE_STATUS[st.value],
+                breakdown_reason=reason)
+
+
+def _hist_len(iterations, status, reason):
+    """residual_history gets one entry per completed pass: a breakdown before
+    the stopping test (every reason but "diverged") leaves the pass out."""
+    return iterations - 1 if status == 2 and reason != "diverged" else iterations
+
+
 # --------------------------------------------------------------------------
 # fixtures / generators
 # --------------------------------------------------------------------------
+def five_point_laplacian(grid_dim, dtype=np.float64) -> Csr:
+    """five_point_laplacian<T>(grid_dim) (fixtures.hpp:41-56): 4 on the
+    diagonal, -1 to the grid neighbours, CSR columns ascending."""
+    n = grid_dim * grid_dim
+    ro, cols, vals = [0], [], []
+    for i in range(grid_dim):
+        for j in range(grid_dim):
+            v = i * grid_dim + j
+            ent = [(v, 4.0)]
+            if i > 0:
+                ent.append((v - grid_dim, -1.0))
+            if i + 1 < grid_dim:
+                ent.append((v + grid_dim, -1.0))
+            if j > 0:
+                ent.append((v - 1, -1.0))
+            if j + 1 < grid_dim:
+                ent.append((v + 1, -1.0))
+            ent.sort()
+            cols += [c for c, _ in ent]
+            vals += [w for _, w in ent]
+            ro.append(len(cols))
+    return Csr(n, n, np.array(ro, np.int64), np.array(cols, np.int32), np.array(vals, dtype))
+
+
+def singular_diagonal(dtype=np.float64) -> Csr:
+    """singular_diagonal_fixture<T>() (fixtures.hpp:83-91): diag(1, 0)."""
+    return Csr(2, 2, np.array([0, 1, 1], np.int64), np.array([0], np.int32),
+               np.array([1.0], dtype))
 def _alloc_ptrs():
     return C.POINTER(C.c_int64)(), C.POINTER(C.c_int32)(), C.POINTER(C.c_double)()
 
@@ -407,6 +468,11 @@ class _Ref:
                                            C.c_double, C.c_int64, C.c_int64, f32p,
                                            C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                            C.POINTER(C.c_int)]
+        for name, fp in (("ref_bicgstab_csr_f64", f64p), ("ref_bicgstab_csr_f32", f32p)):
+            getattr(L, name).argtypes = [C.c_int64, i64p, i32p, fp, fp, C.c_double, C.c_int64,
+                                         fp, f64p, C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                         C.c_char_p, C.c_int]
         L.ref_build_transition_f64.argtypes = [C.c_int64, i64p, i32p, i64p, i32p, f64p]
         alloc_args = [C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int32)),
                       C.POINTER(C.POINTER(C.c_double))]
@@ -470,6 +536,23 @@ class _Ref:
             a.n_rows, a.n_cols, a.row_offsets, _vals_or_dummy(a.col_indices),
             _vals_or_dummy(a.values), _vals_or_dummy(np.ascontiguousarray(x, dt)), y))
         return y[:a.n_rows]
+
+    def bicgstab_csr(self, a: Csr, b, tol=1e-10, max_iters=20000):
+        """The reference's own bicgstab<T> over CsrReferenceBackend."""
+        n = a.n_rows
+        dt = a.values.dtype
+        x = np.zeros(n, dt)
+        hist = np.zeros(max(max_iters, 1), np.float64)
+        it, fr, st = C.c_int64(), C.c_double(), C.c_int()
+        why = C.create_string_buffer(32)
+        fn = self.L.ref_bicgstab_csr_f64 if dt == np.float64 else self.L.ref_bicgstab_csr_f32
+        self._check(fn(n, a.row_offsets, _vals_or_dummy(a.col_indices), _vals_or_dummy(a.values),
+                       np.ascontiguousarray(b, dt), tol, max_iters, x, hist, C.byref(it),
+                       C.byref(fr), C.byref(st), why, 32))
+        reason = why.value.decode()
+        return dict(x=x, residual_history=hist[:_hist_len(it.value, st.value, reason)],
+                    iterations=it.value, final_residual=fr.value,
+                    status=_SOLVE_STATUS[st.value], breakdown_reason=reason)
 
     def pagerank_csr(self, p: Csr, damping=0.85, err_tol=1e-10, max_iters=210,
                      reference_iters=210):

@@ -892,3 +892,102 @@ void mo_hash_uniform_f32(uint64_t seed, int64_t count, double lo, double hi,
 
 DEFINE_TVALS(float, mo_transition_values_f32)
 DEFINE_TVALS(double, mo_transition_values_f64)
+
+/* ========================================================================
+ * bicgstab over the csr backend -- include/merbit/solvers.hpp:268-373
+ * (dot: sequential sum in T, 243-248; norm2: fp64, 250-255).  status: 0
+ * converged, 1 max_iterations, 2 breakdown; reason 1 rho, 2 rhat_dot_v,
+ * 3 t_dot_t, 4 omega, 5 diverged.
+ * ======================================================================== */
+#define MO_BICGSTAB(T, SUFFIX, SPMV)                                              \
+  static T mo_dot_##SUFFIX(int64_t n, const T* a, const T* b) {                  \
+    T s = (T)0;                                                                   \
+    for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];                             \
+    return s;                                                                     \
+  }                                                                               \
+  int mo_bicgstab_##SUFFIX(int64_t n, const int64_t* ro, const int32_t* cols,    \
+                           const T* vals, const T* b, T tol, int64_t max_iters,   \
+                           T* x, double* hist, int64_t* iterations,               \
+                           double* final_residual, int* status, int* reason) {    \
+    double bb = 0.0;                                                              \
+    for (int64_t i = 0; i < n; ++i) bb += (double)b[i] * (double)b[i];            \
+    const double b_norm = sqrt(bb);                                               \
+    for (int64_t i = 0; i < n; ++i) x[i] = (T)0;                                  \
+    *iterations = 0;                                                              \
+    *final_residual = INFINITY;                                                   \
+    *status = 1;                                                                  \
+    *reason = 0;                                                                  \
+    if (b_norm == 0.0) {                                                          \
+      *status = 0;                                                                \
+      *final_residual = 0.0;                                                      \
+      return MO_OK;                                                               \
+    }                                                                             \
+    T* r = (T*)malloc(sizeof(T) * (n + 1));                                       \
+    T* rh = (T*)malloc(sizeof(T) * (n + 1));                                      \
+    T* p = (T*)calloc(n + 1, sizeof(T));                                          \
+    T* v = (T*)calloc(n + 1, sizeof(T));                                          \
+    T* s = (T*)calloc(n + 1, sizeof(T));                                          \
+    T* t = (T*)calloc(n + 1, sizeof(T));                                          \
+    T* ax = (T*)calloc(n + 1, sizeof(T));                                         \
+    memcpy(r, b, sizeof(T) * n);                                                  \
+    memcpy(rh, b, sizeof(T) * n);                                                 \
+    T rho = (T)1, alpha = (T)1, omega = (T)1;                                     \
+    for (int64_t iter = 1; iter <= max_iters; ++iter) {                           \
+      const T rho_new = mo_dot_##SUFFIX(n, rh, r);                                \
+      if (rho_new == (T)0 || !isfinite((double)rho_new)) {                        \
+        *status = 2; *reason = 1; *iterations = iter; break;                      \
+      }                                                                           \
+      if (iter == 1) {                                                            \
+        memcpy(p, r, sizeof(T) * n);                                              \
+      } else {                                                                    \
+        const T beta = (rho_new / rho) * (alpha / omega);                         \
+        for (int64_t i = 0; i < n; ++i) p[i] = r[i] + beta * (p[i] - omega * v[i]); \
+      }                                                                           \
+      SPMV(n, ro, cols, vals, p, v);                                              \
+      const T rhat_v = mo_dot_##SUFFIX(n, rh, v);                                 \
+      if (rhat_v == (T)0 || !isfinite((double)rhat_v)) {                          \
+        *status = 2; *reason = 2; *iterations = iter; break;                      \
+      }                                                                           \
+      alpha = rho_new / rhat_v;                                                   \
+      for (int64_t i = 0; i < n; ++i) s[i] = r[i] - alpha * v[i];                 \
+      SPMV(n, ro, cols, vals, s, t);                                              \
+      const T t_t = mo_dot_##SUFFIX(n, t, t);                                     \
+      if (t_t == (T)0 || !isfinite((double)t_t)) {                                \
+        *status = 2; *reason = 3; *iterations = iter; break;                      \
+      }                                                                           \
+      omega = mo_dot_##SUFFIX(n, t, s) / t_t;                                     \
+      if (omega == (T)0 || !isfinite((double)omega)) {                            \
+        *status = 2; *reason = 4; *iterations = iter; break;                      \
+      }                                                                           \
+      for (int64_t i = 0; i < n; ++i) {                                           \
+        x[i] += alpha * p[i] + omega * s[i];                                      \
+        r[i] = s[i] - omega * t[i];                                               \
+      }                                                                           \
+      rho = rho_new;                                                              \
+      SPMV(n, ro, cols, vals, x, ax);                                             \
+      double rr = 0.0;                                                            \
+      for (int64_t i = 0; i < n; ++i) {                                           \
+        const double d = (double)ax[i] - (double)b[i];                            \
+        rr += d * d;                                                              \
+      }                                                                           \
+      const double resid = sqrt(rr) / b_norm;                                     \
+      if (hist) hist[iter - 1] = resid;                                           \
+      *iterations = iter;                                                         \
+      *final_residual = resid;                                                    \
+      if (!isfinite(resid)) { *status = 2; *reason = 5; break; }                  \
+      if (resid < (double)tol) { *status = 0; break; }                            \
+    }                                                                             \
+    free(r); free(rh); free(p); free(v); free(s); free(t); free(ax);              \
+    return MO_OK;                                                                 \
+  }
+
+static void mo_spmv_ref_f64(int64_t n, const int64_t* ro, const int32_t* cols,
+                            const double* vals, const double* x, double* y) {
+  mo_spmv_csr_f64(n, ro, cols, vals, x, y, NULL, 1);
+}
+static void mo_spmv_ref_f32(int64_t n, const int64_t* ro, const int32_t* cols,
+                            const float* vals, const float* x, float* y) {
+  mo_spmv_csr_f32(n, ro, cols, vals, x, y);
+}
+MO_BICGSTAB(double, f64, mo_spmv_ref_f64)
+MO_BICGSTAB(float, f32, mo_spmv_ref_f32)

@@ -135,6 +135,20 @@ void mo_transition_values_f32(int64_t n, int64_t nnz, const int32_t* cols,
 void mo_transition_values_f64(int64_t n, int64_t nnz, const int32_t* cols,
                               double* vals);
 
+/* bicgstab over the csr backend (solvers.hpp:268-373).  status 0 converged,
+ * 1 max_iterations, 2 breakdown; reason 0 none, 1 rho, 2 rhat_dot_v,
+ * 3 t_dot_t, 4 omega, 5 diverged.  hist (max_iters doubles) may be NULL. */
+int mo_bicgstab_f64(int64_t n, const int64_t* ro, const int32_t* cols,
+                    const double* vals, const double* b, double tol,
+                    int64_t max_iters, double* x, double* hist,
+                    int64_t* iterations, double* final_residual, int* status,
+                    int* reason);
+int mo_bicgstab_f32(int64_t n, const int64_t* ro, const int32_t* cols,
+                    const float* vals, const float* b, float tol,
+                    int64_t max_iters, float* x, double* hist,
+                    int64_t* iterations, double* final_residual, int* status,
+                    int* reason);
+
 #ifdef __cplusplus
 }
 #endif

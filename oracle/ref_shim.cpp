@@ -9,6 +9,7 @@
 // restatement (oracle/merbit_oracle.c), to write tests/golden/, and as the
 // CPU arm of bench.py (--impl reference and the cpu_baseline field).
 #include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -227,6 +228,38 @@ int ref_generate_tile(const int64_t* ro, int64_t n_rows, int64_t nnz,
 
 REF_SPMV(double, f64)
 REF_SPMV(float, f32)
+
+// bicgstab<T> over the csr backend (solvers.hpp:268-373); status 0/1/2 as
+// SolveStatus converged / max_iterations / breakdown.
+#define REF_BICGSTAB(T, SUFFIX)                                                   \
+  int ref_bicgstab_csr_##SUFFIX(int64_t n, const int64_t* ro, const int32_t* cols, \
+                                const T* vals, const T* b, double tol,            \
+                                int64_t max_iters, T* x, double* hist,            \
+                                int64_t* iterations, double* final_residual,      \
+                                int* status, char* reason, int reason_len) {      \
+    return guarded([&] {                                                          \
+      const CsrMatrix<T> a = make_csr<T>(n, n, ro, cols, vals);                   \
+      CsrReferenceBackend<T> backend(a);                                          \
+      BicgstabConfig<T> cfg;                                                      \
+      cfg.tol = static_cast<T>(tol);                                              \
+      cfg.max_iters = max_iters;                                                  \
+      const auto r = bicgstab<T>(a, std::span<const T>(b, b + n), cfg, backend);  \
+      std::memcpy(x, r.x.data(), sizeof(T) * n);                                  \
+      for (std::size_t i = 0; i < r.residual_history.size(); ++i)                 \
+        hist[i] = r.residual_history[i];                                          \
+      *iterations = r.iterations;                                                 \
+      *final_residual = r.final_residual;                                         \
+      *status = r.status == SolveStatus::converged       ? 0                      \
+                : r.status == SolveStatus::max_iterations ? 1                     \
+                                                          : 2;                    \
+      std::snprintf(reason, reason_len, "%s", r.breakdown_reason.c_str());        \
+    });                                                                           \
+  }
+
+extern "C" {
+REF_BICGSTAB(double, f64)
+REF_BICGSTAB(float, f32)
+}
 
 // pagerank<T> over the csr backend (solvers.hpp:154-218); status 0/1 as
 // SolveStatus converged / max_iterations.

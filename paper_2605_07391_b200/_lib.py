@@ -43,6 +43,16 @@ class mbx_pagerank_result(C.Structure):
                 ("dangling_mass", C.c_double)]
 
 
+class mbx_bicgstab_config(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iters", C.c_int64)]
+
+
+class mbx_bicgstab_result(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("final_residual", C.c_double),
+                ("status", C.c_int32), ("breakdown_reason", C.c_char * 32),
+                ("preprocess_seconds", C.c_double), ("iterate_seconds", C.c_double)]
+
+
 VP = C.c_void_p
 I64P = C.POINTER(C.c_int64)
 SIGNATURES = {
@@ -65,6 +75,8 @@ SIGNATURES = {
     "mbx_context_set_tuning": ([VP, C.c_int, C.c_int, C.c_int], C.c_int),
     "mbx_context_set_tuning_ex": ([VP, C.c_int, C.c_int], C.c_int),
     "mbx_context_set_layout": ([VP, C.c_int], C.c_int),
+    "mbx_bicgstab": ([VP, VP, VP, C.POINTER(mbx_simt_config), C.POINTER(mbx_bicgstab_config),
+                      VP, VP, C.POINTER(C.c_double), C.POINTER(mbx_bicgstab_result)], C.c_int),
     "mbx_matrix_slot_info": ([VP, C.POINTER(C.c_int64), C.POINTER(C.c_double)], C.c_int),
     "mbx_matrix_build_xcache": ([VP, VP, C.c_int, C.POINTER(C.c_double)], C.c_int),
     "mbx_matrix_xcache_info": ([VP, C.POINTER(C.c_int), C.POINTER(C.c_double)], C.c_int),

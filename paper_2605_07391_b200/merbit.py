@@ -11,6 +11,7 @@ libmerbit_b200.so on the GPU; nothing here computes on the CPU.
     SpmvBackend / MerbitB200Backend         backend.hpp:22-34, 112-136
     make_backend / BackendKind              backend.hpp:138-169
     pagerank -> PageRankResult              solvers.hpp:76-218
+    bicgstab -> BicgstabResult              solvers.hpp:224-373
 """
 from __future__ import annotations
 
@@ -21,8 +22,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from ._lib import (mbx_pagerank_config, mbx_pagerank_result, mbx_simt_config,
-                   mbx_spmv_trace, mbx_tile_info)
+from ._lib import (mbx_bicgstab_config, mbx_bicgstab_result, mbx_pagerank_config,
+                   mbx_pagerank_result, mbx_simt_config, mbx_spmv_trace, mbx_tile_info)
 
 F32, F64 = 0, 1
 
@@ -592,6 +593,71 @@ def pagerank(p, cfg: PageRankConfig, backend: MerbitB200Backend | None = None,
                           iterate_seconds=res.iterate_seconds, l1_residual=res.l1_residual,
                           mass=res.mass, dangling_mass=res.dangling_mass,
                           residual_history=hist[:res.iterations])
+
+
+# ---------------------------------------------------------------------------
+# BiCGSTAB (solvers.hpp:224-373)
+# ---------------------------------------------------------------------------
+_SOLVE_STATUS = {0: "converged", 1: "max_iterations", 2: "breakdown"}
+
+
+def solve_status_name(status: str) -> str:
+    """solve_status_name (solvers.hpp): the status strings are the names."""
+    return status
+
+
+@dataclass
+class BicgstabConfig:
+    tol: float = 1e-10
+    max_iters: int = 20000
+
+    def _c(self):
+        return mbx_bicgstab_config(self.tol, self.max_iters)
+
+
+@dataclass
+class BicgstabResult:
+    x: np.ndarray
+    residual_history: np.ndarray
+    iterations: int
+    final_residual: float
+    status: str
+    breakdown_reason: str
+    preprocess_seconds: float
+    iterate_seconds: float
+
+
+def bicgstab(a, b, cfg: BicgstabConfig | None = None,
+             backend: MerbitB200Backend | None = None) -> BicgstabResult:
+    """bicgstab<T>(a, b, cfg, backend): unpreconditioned BiCGSTAB with every
+    SpMV, inner product and vector update on the device (K2/K3 + fused
+    dot/axpy kernels).  `a` is the host CSR when `backend` is None."""
+    cfg = cfg or BicgstabConfig()
+    if backend is None:
+        dt = np.asarray(a.values).dtype
+        c = SimtConfig.make(32, select_sigma("f64" if dt == np.float64 else "f32"), 128)
+        backend = MerbitB200Backend(a, c)
+    m, t, c = backend.matrix, backend.tile_, backend.c
+    if m.n_rows != m.n_cols:
+        raise DimensionError("bicgstab needs a square system")
+    b = np.ascontiguousarray(b, m.dtype)
+    if b.shape != (m.n_rows,):
+        raise DimensionError(f"bicgstab: right-hand side has {b.size} entries for "
+                             f"{m.n_rows} rows")
+    x = np.zeros(m.n_rows, m.dtype)
+    hist = np.zeros(max(cfg.max_iters, 1), np.float64)
+    res = mbx_bicgstab_result()
+    cc, bc = c._c(), cfg._c()
+    _check(_lib.lib().mbx_bicgstab(m.ctx.h, m.h, t.h, C.byref(cc), C.byref(bc), _ptr(b), _ptr(x),
+                                   hist.ctypes.data_as(C.POINTER(C.c_double)), C.byref(res)))
+    reason = res.breakdown_reason.decode()
+    hl = res.iterations - (1 if res.status == 2 and reason != "diverged" else 0)
+    return BicgstabResult(x=x, residual_history=hist[:hl].copy(),
+                          iterations=res.iterations, final_residual=res.final_residual,
+                          status=_SOLVE_STATUS[res.status],
+                          breakdown_reason=reason,
+                          preprocess_seconds=res.preprocess_seconds,
+                          iterate_seconds=res.iterate_seconds)
 
 
 class PageRankPlan:

@@ -157,3 +157,29 @@ def test_restatement_vs_live_reference_f32():
                 y2, c2 = R.spmv_merbit(m, x, w, s, b)
                 assert np.array_equal(y1.view(np.uint32), y2.view(np.uint32))
                 assert np.array_equal(c1, c2)
+
+
+@pytest.mark.skipif(O.ref() is None, reason="oracle/_ref (the compiled reference) not built")
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_bicgstab_restatement_is_the_reference(dt):
+    """mo_bicgstab (C restatement of solvers.hpp:268-373) == the reference's own
+    bicgstab<T> over CsrReferenceBackend, bitwise: x, history, counts, reason."""
+    cases = []
+    a = O.five_point_laplacian(8, dt)
+    cases.append((a, O.seed_test_vector(a.n_rows, -1, 1, 97).astype(dt), 1e-10))
+    a = O.five_point_laplacian(32, dt)
+    xt = O.seed_test_vector(a.n_rows, -1, 1, 77)
+    cases.append((a, O.spmv_csr_f64(a.astype(np.float64), xt).astype(dt),
+                  1e-10 if dt == np.float64 else 1e-6))
+    cases.append((O.singular_diagonal(dt), np.ones(2, dt), 1e-10))
+    cases.append((O.five_point_laplacian(3, dt), np.zeros(9, dt), 1e-10))
+    for a, b, tol in cases:
+        got = O.bicgstab(a, b, tol, 500)
+        want = O.ref().bicgstab_csr(a, b, tol, 500)
+        assert got["iterations"] == want["iterations"]
+        assert got["status"] == want["status"]
+        assert got["breakdown_reason"] == want["breakdown_reason"]
+        assert np.array_equal(got["x"], want["x"])
+        assert np.array_equal(got["residual_history"], want["residual_history"])
+        assert got["final_residual"] == want["final_residual"] or (
+            np.isinf(got["final_residual"]) and np.isinf(want["final_residual"]))
