@@ -115,6 +115,17 @@ typedef struct {
   double iterate_seconds;    /* device time of the iteration loop */
 } mbx_bicgstab_result;
 
+/* CooTriples (include/merbit/csr.hpp:22-26) as three host arrays in entry
+ * order; arrays returned by the library are freed with mbx_coo_free. */
+typedef struct {
+  int64_t n_rows;
+  int64_t n_cols;
+  int64_t nnz;
+  int64_t* rows;
+  int64_t* cols;
+  double* vals;
+} mbx_coo;
+
 typedef struct mbx_context_s mbx_context;
 typedef struct mbx_matrix_s mbx_matrix;
 typedef struct mbx_tile_s mbx_tile;
@@ -326,6 +337,43 @@ MBX_API int mbx_bicgstab(mbx_context* ctx, const mbx_matrix* a, const mbx_tile* 
                          const mbx_simt_config* c, const mbx_bicgstab_config* cfg,
                          const void* b_host, void* x_host,
                          double* residual_history_host, mbx_bicgstab_result* result);
+
+/* ---- file formats (host) ------------------------------- */
+/* MBTL TILE cache, byte-identical to write_tile_cache / read_tile_cache
+ * (src/tile.cpp:161-234).  precision: MBX_F32 / MBX_F64 (header byte). */
+MBX_API int mbx_tile_cache_write_host(const char* path, const mbx_tile_info* info,
+                                      const uint32_t* tile_x, const uint32_t* tile_y,
+                                      const uint32_t* lane_desc, int precision);
+/* Arrays are allocated by the library (free with mbx_free); counts follow
+ * from the header (tile.cpp:214-218).  io_error / parse_error /
+ * corruption_error as the reference. */
+MBX_API int mbx_tile_cache_read_host(const char* path, mbx_tile_info* info,
+                                     uint32_t** tile_x, uint32_t** tile_y,
+                                     uint32_t** lane_desc, int* precision);
+/* Device TILE <-> MBTL file. */
+MBX_API int mbx_tile_cache_write(const mbx_tile* t, const char* path, int precision);
+MBX_API int mbx_tile_cache_load(mbx_context* ctx, const char* path, mbx_tile** out,
+                                int* precision);
+/* Matrix Market coordinate text (parse_matrix_market, matrix_market.cpp:
+ * 47-133): real / integer / pattern, general / symmetric; parse_error
+ * "origin:line: what" on malformed input. */
+MBX_API int mbx_mm_read(const char* path, mbx_coo* out);
+MBX_API int mbx_mm_parse(const char* text, int64_t len, const char* origin, mbx_coo* out);
+/* "coordinate real general", 1-based, shortest round-trip values
+ * (write_matrix_market, matrix_market.cpp:156-168). */
+MBX_API int mbx_mm_write(const char* path, const mbx_coo* coo);
+/* MBMX binary matrix cache (write/read_matrix_cache, matrix_market.cpp:
+ * 178-225) and the magic-sniffing loader (load_matrix_any, 227-238). */
+MBX_API int mbx_matrix_cache_write(const char* path, const mbx_coo* coo);
+MBX_API int mbx_matrix_cache_read(const char* path, mbx_coo* out);
+MBX_API int mbx_matrix_load_any(const char* path, mbx_coo* out);
+MBX_API void mbx_coo_free(mbx_coo* coo);
+MBX_API void mbx_free(void* p);
+/* coo_to_csr<T> (csr.hpp:43-88) on the device: bounds check
+ * (dimension_error), stable row-major sort, duplicates summed in fp64 in
+ * entry order, one rounding to T -- the result is a resident matrix. */
+MBX_API int mbx_matrix_from_coo(mbx_context* ctx, int precision, const mbx_coo* coo,
+                                mbx_matrix** out);
 
 /* ---- multi-GPU row-sharded PageRank (one process per GPU) ---------------- */
 /* GPU g owns rows [row_bounds[g], row_bounds[g+1]) of P (mbx_plan_row_shards)

@@ -400,4 +400,63 @@ PageRankResult<T> pagerank(MerbitB200Backend<T>& backend, const PageRankConfig<T
   return r;
 }
 
+// ---- BiCGSTAB (solvers.hpp:224-373) -------------------------------------------
+template <typename T>
+struct BicgstabConfig {
+  T tol = T(1e-10);  // on ||A*x - b|| / ||b||, recomputed each pass
+  index_t max_iters = 20000;
+};
+
+template <typename T>
+struct BicgstabResult {
+  std::vector<T> x;
+  std::vector<double> residual_history;  // true relative residual per pass
+  index_t iterations = 0;
+  double final_residual = std::numeric_limits<double>::infinity();
+  SolveStatus status = SolveStatus::max_iterations;
+  std::string breakdown_reason;
+  double preprocess_seconds = 0.0;
+  double iterate_seconds = 0.0;
+};
+
+inline const char* solve_status_name(SolveStatus s) {
+  switch (s) {
+    case SolveStatus::converged: return "converged";
+    case SolveStatus::max_iterations: return "max_iterations";
+    case SolveStatus::breakdown: return "breakdown";
+  }
+  return "unknown";
+}
+
+// bicgstab<T>(a, b, cfg, backend): every SpMV, inner product and vector
+// update runs on the device (mbx_bicgstab); x reaches the host once.
+template <typename T>
+BicgstabResult<T> bicgstab(MerbitB200Backend<T>& backend, std::span<const T> b,
+                           const BicgstabConfig<T>& cfg = {}) {
+  const auto& a = backend.matrix();
+  if (a.n_rows() != a.n_cols()) throw dimension_error("bicgstab needs a square system");
+  if (static_cast<index_t>(b.size()) != a.n_rows())
+    throw dimension_error("bicgstab: right-hand side has " + std::to_string(b.size()) +
+                          " entries for " + std::to_string(a.n_rows()) + " rows");
+  const mbx_simt_config cc = backend.config().c();
+  BicgstabResult<T> r;
+  r.x.resize(a.n_rows());
+  r.residual_history.assign(std::max<index_t>(cfg.max_iters, 1), 0.0);
+  const mbx_bicgstab_config bc{double(cfg.tol), cfg.max_iters};
+  mbx_bicgstab_result res{};
+  check(mbx_bicgstab(a.context().get(), a.get(), backend.tile().get(), &cc, &bc, b.data(),
+                     r.x.data(), r.residual_history.data(), &res));
+  r.iterations = res.iterations;
+  r.final_residual = res.final_residual;
+  r.status = res.status == 0   ? SolveStatus::converged
+             : res.status == 1 ? SolveStatus::max_iterations
+                               : SolveStatus::breakdown;
+  r.breakdown_reason = res.breakdown_reason;
+  const bool early = r.status == SolveStatus::breakdown && r.breakdown_reason != "diverged";
+  r.residual_history.resize(r.iterations - (early ? 1 : 0));
+  r.preprocess_seconds = backend.preprocess_seconds();
+  r.iterate_seconds = res.iterate_seconds;
+  return r;
+}
+
 }  // namespace merbit_b200

@@ -473,6 +473,23 @@ class _Ref:
                                          fp, f64p, C.POINTER(C.c_int64),
                                          C.POINTER(C.c_double), C.POINTER(C.c_int),
                                          C.c_char_p, C.c_int]
+        u32pp = C.POINTER(C.POINTER(C.c_uint32))
+        L.ref_tile_cache_write.argtypes = [C.c_char_p, C.c_int64, C.c_int64, i64p, C.c_int,
+                                           C.c_int, C.c_int]
+        L.ref_tile_cache_read.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                          u32pp, u32pp, u32pp, C.POINTER(C.c_int)]
+        coo_out = [C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                   C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int64)),
+                   C.POINTER(C.POINTER(C.c_double))]
+        L.ref_matrix_read.argtypes = [C.c_char_p, C.c_int] + coo_out
+        L.ref_matrix_write.argtypes = [C.c_char_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                       i64p, i64p, f64p]
+        L.ref_coo_to_csr_f64.argtypes = [C.c_int64, C.c_int64, C.c_int64, i64p, i64p, f64p,
+                                         C.POINTER(C.c_int64), C.POINTER(C.POINTER(C.c_int64)),
+                                         C.POINTER(C.POINTER(C.c_int32)),
+                                         C.POINTER(C.POINTER(C.c_double))]
         L.ref_build_transition_f64.argtypes = [C.c_int64, i64p, i32p, i64p, i32p, f64p]
         alloc_args = [C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int32)),
                       C.POINTER(C.POINTER(C.c_double))]
@@ -536,6 +553,57 @@ class _Ref:
             a.n_rows, a.n_cols, a.row_offsets, _vals_or_dummy(a.col_indices),
             _vals_or_dummy(a.values), _vals_or_dummy(np.ascontiguousarray(x, dt)), y))
         return y[:a.n_rows]
+
+    # ---- file formats --------------------------------------------------
+    def tile_cache_write(self, path, ro, n_rows, nnz, omega, sigma, f64=False):
+        self._check(self.L.ref_tile_cache_write(os.fsencode(path), n_rows, nnz,
+                                                np.ascontiguousarray(ro, np.int64), omega, sigma,
+                                                1 if f64 else 0))
+
+    def tile_cache_read(self, path):
+        om, sg, f64 = C.c_int(), C.c_int(), C.c_int()
+        nr, nz, tn, ln = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        tx, ty, ld = (C.POINTER(C.c_uint32)() for _ in range(3))
+        self._check(self.L.ref_tile_cache_read(os.fsencode(path), C.byref(om), C.byref(sg),
+                                               C.byref(nr), C.byref(nz), C.byref(tn),
+                                               C.byref(ln), C.byref(tx), C.byref(ty),
+                                               C.byref(ld), C.byref(f64)))
+        take = lambda p, n: self._take(p, n, np.uint32)  # noqa: E731
+        return dict(omega=om.value, sigma=sg.value, n_rows=nr.value, nnz=nz.value,
+                    tile_x=take(tx, tn.value + 1), tile_y=take(ty, tn.value + 1),
+                    lane_desc=take(ld, ln.value), f64=bool(f64.value))
+
+    def matrix_read(self, path, which=0):
+        """which: 0 parse_matrix_market_file, 1 read_matrix_cache, 2 load_matrix_any."""
+        nr, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+        r, c = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
+        v = C.POINTER(C.c_double)()
+        self._check(self.L.ref_matrix_read(os.fsencode(path), which, C.byref(nr), C.byref(nc),
+                                           C.byref(nz), C.byref(r), C.byref(c), C.byref(v)))
+        n = nz.value
+        return dict(n_rows=nr.value, n_cols=nc.value, rows=self._take(r, n, np.int64),
+                    cols=self._take(c, n, np.int64), vals=self._take(v, n, np.float64))
+
+    def matrix_write(self, path, coo, which=0):
+        """which: 0 write_matrix_market_file, 1 write_matrix_cache."""
+        self._check(self.L.ref_matrix_write(os.fsencode(path), which, coo["n_rows"],
+                                            coo["n_cols"], len(coo["rows"]),
+                                            np.ascontiguousarray(coo["rows"], np.int64),
+                                            np.ascontiguousarray(coo["cols"], np.int64),
+                                            np.ascontiguousarray(coo["vals"], np.float64)))
+
+    def coo_to_csr(self, coo) -> Csr:
+        m = C.c_int64()
+        ro, cols = C.POINTER(C.c_int64)(), C.POINTER(C.c_int32)()
+        vals = C.POINTER(C.c_double)()
+        self._check(self.L.ref_coo_to_csr_f64(coo["n_rows"], coo["n_cols"], len(coo["rows"]),
+                                              np.ascontiguousarray(coo["rows"], np.int64),
+                                              np.ascontiguousarray(coo["cols"], np.int64),
+                                              np.ascontiguousarray(coo["vals"], np.float64),
+                                              C.byref(m), C.byref(ro), C.byref(cols),
+                                              C.byref(vals)))
+        return Csr(coo["n_rows"], coo["n_cols"], self._take(ro, coo["n_rows"] + 1, np.int64),
+                   self._take(cols, m.value, np.int32), self._take(vals, m.value, np.float64))
 
     def bicgstab_csr(self, a: Csr, b, tol=1e-10, max_iters=20000):
         """The reference's own bicgstab<T> over CsrReferenceBackend."""

@@ -20,6 +20,7 @@
 #include "merbit/config.hpp"
 #include "merbit/fixtures.hpp"
 #include "merbit/merbit_spmv.hpp"
+#include "merbit/matrix_market.hpp"
 #include "merbit/merge_path.hpp"
 #include "merbit/random.hpp"
 #include "merbit/reference.hpp"
@@ -259,6 +260,105 @@ REF_SPMV(float, f32)
 extern "C" {
 REF_BICGSTAB(double, f64)
 REF_BICGSTAB(float, f32)
+
+// ---- file formats (tile.cpp:161-234, matrix_market.cpp) -----------------
+// generate_tile on the given rows + write_tile_cache
+int ref_tile_cache_write(const char* path, int64_t n_rows, int64_t nnz, const int64_t* ro,
+                         int omega, int sigma, int f64) {
+  return guarded([&] {
+    const SimtConfig c = SimtConfig::make(omega, sigma, omega);
+    const TileMetadata t = generate_tile(std::span<const index_t>(ro, ro + n_rows + 1), n_rows,
+                                         nnz, c);
+    write_tile_cache(path, t, f64 ? ScalarPrecision::f64 : ScalarPrecision::f32);
+  });
+}
+
+// read_tile_cache: counts + arrays (malloc'd, ref_free)
+int ref_tile_cache_read(const char* path, int* omega, int* sigma, int64_t* n_rows,
+                        int64_t* nnz, int64_t* tile_num, int64_t* lane_num, uint32_t** tx,
+                        uint32_t** ty, uint32_t** ld, int* f64) {
+  return guarded([&] {
+    const TileCacheContents c = read_tile_cache(path);
+    const TileMetadata& t = c.tile;
+    *omega = t.omega;
+    *sigma = t.sigma;
+    *n_rows = t.n_rows;
+    *nnz = t.nnz;
+    *tile_num = t.tile_num;
+    *lane_num = t.lane_num;
+    *f64 = c.precision == ScalarPrecision::f64 ? 1 : 0;
+    auto dup = [](const std::vector<uint32_t>& v) {
+      auto* p = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * (v.size() + 1)));
+      std::memcpy(p, v.data(), sizeof(uint32_t) * v.size());
+      return p;
+    };
+    *tx = dup(t.tile_x);
+    *ty = dup(t.tile_y);
+    *ld = dup(t.lane_desc);
+  });
+}
+
+static void export_coo_arrays(const CooTriples& coo, int64_t* n_rows, int64_t* n_cols,
+                              int64_t* nnz, int64_t** rows, int64_t** cols, double** vals) {
+  const std::size_t n = coo.entries.size();
+  *n_rows = coo.n_rows;
+  *n_cols = coo.n_cols;
+  *nnz = static_cast<int64_t>(n);
+  *rows = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (n + 1)));
+  *cols = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (n + 1)));
+  *vals = static_cast<double*>(std::malloc(sizeof(double) * (n + 1)));
+  for (std::size_t k = 0; k < n; ++k) {
+    (*rows)[k] = coo.entries[k].row;
+    (*cols)[k] = coo.entries[k].col;
+    (*vals)[k] = coo.entries[k].value;
+  }
+}
+
+static CooTriples import_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* rows,
+                             const int64_t* cols, const double* vals) {
+  CooTriples coo;
+  coo.n_rows = n_rows;
+  coo.n_cols = n_cols;
+  coo.entries.reserve(static_cast<std::size_t>(nnz));
+  for (int64_t k = 0; k < nnz; ++k) coo.entries.push_back({rows[k], cols[k], vals[k]});
+  return coo;
+}
+
+// 0 = Matrix Market text, 1 = MBMX cache, 2 = load_matrix_any
+int ref_matrix_read(const char* path, int which, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,
+                    int64_t** rows, int64_t** cols, double** vals) {
+  return guarded([&] {
+    const CooTriples coo = which == 0   ? parse_matrix_market_file(path)
+                           : which == 1 ? read_matrix_cache(path)
+                                        : load_matrix_any(path);
+    export_coo_arrays(coo, n_rows, n_cols, nnz, rows, cols, vals);
+  });
+}
+
+// 0 = Matrix Market text, 1 = MBMX cache
+int ref_matrix_write(const char* path, int which, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                     const int64_t* rows, const int64_t* cols, const double* vals) {
+  return guarded([&] {
+    const CooTriples coo = import_coo(n_rows, n_cols, nnz, rows, cols, vals);
+    if (which == 0)
+      write_matrix_market_file(path, coo);
+    else
+      write_matrix_cache(path, coo);
+  });
+}
+
+// coo_to_csr<T> (csr.hpp:70-88): CSR arrays (malloc'd)
+int ref_coo_to_csr_f64(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* rows,
+                       const int64_t* cols, const double* vals, int64_t* out_nnz, int64_t** ro,
+                       int32_t** ocols, double** ovals) {
+  return guarded([&] {
+    const CsrMatrix<double> a = coo_to_csr<double>(import_coo(n_rows, n_cols, nnz, rows, cols,
+                                                              vals));
+    int64_t nr, nc, m;
+    export_csr(a, &nr, &nc, &m, ro, ocols, ovals);
+    *out_nnz = m;
+  });
+}
 }
 
 // pagerank<T> over the csr backend (solvers.hpp:154-218); status 0/1 as

@@ -53,6 +53,12 @@ class mbx_bicgstab_result(C.Structure):
                 ("preprocess_seconds", C.c_double), ("iterate_seconds", C.c_double)]
 
 
+class mbx_coo(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64),
+                ("rows", C.POINTER(C.c_int64)), ("cols", C.POINTER(C.c_int64)),
+                ("vals", C.POINTER(C.c_double))]
+
+
 VP = C.c_void_p
 I64P = C.POINTER(C.c_int64)
 SIGNATURES = {
@@ -75,6 +81,24 @@ SIGNATURES = {
     "mbx_context_set_tuning": ([VP, C.c_int, C.c_int, C.c_int], C.c_int),
     "mbx_context_set_tuning_ex": ([VP, C.c_int, C.c_int], C.c_int),
     "mbx_context_set_layout": ([VP, C.c_int], C.c_int),
+    "mbx_free": ([VP], None),
+    "mbx_coo_free": ([C.POINTER(mbx_coo)], None),
+    "mbx_mm_read": ([C.c_char_p, C.POINTER(mbx_coo)], C.c_int),
+    "mbx_mm_parse": ([C.c_char_p, C.c_int64, C.c_char_p, C.POINTER(mbx_coo)], C.c_int),
+    "mbx_mm_write": ([C.c_char_p, C.POINTER(mbx_coo)], C.c_int),
+    "mbx_matrix_cache_write": ([C.c_char_p, C.POINTER(mbx_coo)], C.c_int),
+    "mbx_matrix_cache_read": ([C.c_char_p, C.POINTER(mbx_coo)], C.c_int),
+    "mbx_matrix_load_any": ([C.c_char_p, C.POINTER(mbx_coo)], C.c_int),
+    "mbx_matrix_from_coo": ([VP, C.c_int, C.POINTER(mbx_coo), C.POINTER(VP)], C.c_int),
+    "mbx_tile_cache_write_host": ([C.c_char_p, C.POINTER(mbx_tile_info),
+                                   C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                   C.POINTER(C.c_uint32), C.c_int], C.c_int),
+    "mbx_tile_cache_read_host": ([C.c_char_p, C.POINTER(mbx_tile_info),
+                                  C.POINTER(C.POINTER(C.c_uint32)),
+                                  C.POINTER(C.POINTER(C.c_uint32)),
+                                  C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_int)], C.c_int),
+    "mbx_tile_cache_write": ([VP, C.c_char_p, C.c_int], C.c_int),
+    "mbx_tile_cache_load": ([VP, C.c_char_p, C.POINTER(VP), C.POINTER(C.c_int)], C.c_int),
     "mbx_bicgstab": ([VP, VP, VP, C.POINTER(mbx_simt_config), C.POINTER(mbx_bicgstab_config),
                       VP, VP, C.POINTER(C.c_double), C.POINTER(mbx_bicgstab_result)], C.c_int),
     "mbx_matrix_slot_info": ([VP, C.POINTER(C.c_int64), C.POINTER(C.c_double)], C.c_int),

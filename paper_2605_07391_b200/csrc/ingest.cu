@@ -1,0 +1,264 @@
+// ingest.cu -- device side of the file formats:
+//
+//  * mbx_matrix_from_coo: coo_to_csr<T> (include/merbit/csr.hpp:43-88) on the
+//    GPU for Matrix Market / MBMX inputs of any size.  normalize_coo's
+//    contract is kept exactly: bounds check (dimension_error), stable
+//    row-major order, duplicates summed in fp64 in their stable order (one
+//    sequential run per key), one rounding to T at the end.  Stable LSD
+//    radix sort of (row * n_cols + col) gives the same permutation as
+//    std::stable_sort on (row, col).
+//  * mbx_tile_cache_write / mbx_tile_cache_load: MBTL files straight from /
+//    into a device TILE (layout in io.cpp).
+#include <cub/cub.cuh>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mbx_internal.h"
+
+namespace mbx {
+
+void write_tile_cache_host(const std::string& path, const mbx_tile_info& info,
+                           const uint32_t* tx, const uint32_t* ty, const uint32_t* ld,
+                           int precision);
+void read_tile_cache_host(const std::string& path, mbx_tile_info* info, uint32_t** tx,
+                          uint32_t** ty, uint32_t** ld, int* precision);
+
+namespace {
+
+__global__ void coo_keys_kernel(const int64_t* __restrict__ r, const int64_t* __restrict__ c,
+                                int64_t n, int64_t n_rows, int64_t n_cols,
+                                unsigned long long* __restrict__ keys, int64_t* __restrict__ idx,
+                                int* bad) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = r[k], col = c[k];
+    if (row < 0 || row >= n_rows || col < 0 || col >= n_cols) atomicExch(bad, 1);
+    keys[k] = (unsigned long long)(row) * (unsigned long long)(n_cols) +
+              (unsigned long long)(col);
+    idx[k] = k;
+  }
+}
+
+__global__ void run_heads_kernel(const unsigned long long* __restrict__ keys, int64_t n,
+                                 int64_t* __restrict__ head) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += int64_t(gridDim.x) * blockDim.x)
+    head[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1 : 0;
+}
+
+// one thread per run head: the run's values summed left to right in fp64
+// (normalize_coo: merged.back().value += e.value), then rounded to T once
+template <typename T>
+__global__ void merge_runs_kernel(const unsigned long long* __restrict__ keys,
+                                  const int64_t* __restrict__ idx, const double* __restrict__ v,
+                                  const int64_t* __restrict__ head,
+                                  const int64_t* __restrict__ pos,
+                                  int64_t n, int64_t n_cols, int64_t* __restrict__ out_row,
+                                  int32_t* __restrict__ out_col, T* __restrict__ out_val) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    if (!head[k]) continue;
+    const unsigned long long key = keys[k];
+    double s = v[idx[k]];
+    for (int64_t j = k + 1; j < n && keys[j] == key; ++j) s += v[idx[j]];
+    const int64_t p = pos[k];
+    out_row[p] = int64_t(key / (unsigned long long)n_cols);
+    out_col[p] = int32_t(key % (unsigned long long)n_cols);
+    out_val[p] = static_cast<T>(s);
+  }
+}
+
+// row_offsets[r] = first merged entry with row >= r (rows are sorted)
+__global__ void row_offsets_kernel(const int64_t* __restrict__ rows, int64_t m, int64_t n_rows,
+                                   uint32_t* __restrict__ ro) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r <= n_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (rows[mid] < r)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    ro[r] = uint32_t(lo);
+  }
+}
+
+template <typename F>
+int iguard(F&& f) {
+  try {
+    f();
+    return MBX_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return MBX_ERROR;
+  }
+}
+
+unsigned grid_of(int64_t n, const mbx_context* ctx) {
+  const int64_t b = (n + 255) / 256;
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>(b, int64_t(ctx->sm_count) * 16)));
+}
+
+}  // namespace
+}  // namespace mbx
+
+extern "C" {
+
+MBX_API int mbx_matrix_from_coo(mbx_context* ctx, int precision, const mbx_coo* coo,
+                                mbx_matrix** out) {
+  return mbx::iguard([&] {
+    using mbx::fail;
+    if (precision != MBX_F32 && precision != MBX_F64)
+      fail(MBX_CONFIG_ERROR, "precision must be MBX_F32 or MBX_F64");
+    if (coo->n_rows < 0 || coo->n_cols < 0 || coo->nnz < 0)
+      fail(MBX_DIMENSION_ERROR, "negative COO dimensions");
+    if (coo->n_cols >= (int64_t(1) << 31))
+      fail(MBX_CAPACITY_ERROR, "n_cols must be < 2^31 (int32 device column indices)");
+    if (coo->nnz > 0 && (!coo->rows || !coo->cols || !coo->vals))
+      fail(MBX_DIMENSION_ERROR, "null COO arrays");
+    MBX_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int64_t n = coo->nnz, nr = coo->n_rows, nc = coo->n_cols;
+    auto dm = [&](size_t b) {
+      void* p = nullptr;
+      MBX_CUDA(cudaMallocAsync(&p, std::max<size_t>(b, 256), s));
+      return p;
+    };
+    std::vector<void*> tmp;
+    auto tm = [&](size_t b) {
+      void* p = dm(b);
+      tmp.push_back(p);
+      return p;
+    };
+    auto release = [&] {
+      for (void* p : tmp) cudaFreeAsync(p, s);
+      tmp.clear();
+    };
+    auto m = std::make_unique<mbx_matrix>();
+    m->ctx = ctx;
+    m->precision = precision;
+    m->n_rows = nr;
+    m->n_cols = nc;
+    const size_t vs = mbx::value_size(precision);
+    try {
+      int64_t merged = 0;
+      int64_t* mrow = nullptr;
+      if (n > 0) {
+        auto* rows = static_cast<int64_t*>(tm(n * 8));
+        auto* cols = static_cast<int64_t*>(tm(n * 8));
+        auto* vals = static_cast<double*>(tm(n * 8));
+        MBX_CUDA(cudaMemcpyAsync(rows, coo->rows, n * 8, cudaMemcpyHostToDevice, s));
+        MBX_CUDA(cudaMemcpyAsync(cols, coo->cols, n * 8, cudaMemcpyHostToDevice, s));
+        MBX_CUDA(cudaMemcpyAsync(vals, coo->vals, n * 8, cudaMemcpyHostToDevice, s));
+        auto* keys = static_cast<unsigned long long*>(tm(n * 8));
+        auto* keys2 = static_cast<unsigned long long*>(tm(n * 8));
+        auto* idx = static_cast<int64_t*>(tm(n * 8));
+        auto* idx2 = static_cast<int64_t*>(tm(n * 8));
+        int* bad = static_cast<int*>(tm(64));
+        MBX_CUDA(cudaMemsetAsync(bad, 0, 4, s));
+        mbx::coo_keys_kernel<<<mbx::grid_of(n, ctx), 256, 0, s>>>(rows, cols, n, nr, nc, keys,
+                                                                   idx, bad);
+        ++ctx->launches;
+        int hbad = 0;
+        MBX_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s));
+        MBX_CUDA(cudaStreamSynchronize(s));
+        if (hbad) {
+          // normalize_coo reports the first offending entry (csr.hpp:44-51)
+          for (int64_t k = 0; k < n; ++k)
+            if (coo->rows[k] < 0 || coo->rows[k] >= nr || coo->cols[k] < 0 || coo->cols[k] >= nc)
+              fail(MBX_DIMENSION_ERROR, "coo entry (" + std::to_string(coo->rows[k]) + ", " +
+                                            std::to_string(coo->cols[k]) + ") outside " +
+                                            std::to_string(nr) + "x" + std::to_string(nc));
+        }
+        const unsigned long long span =
+            (unsigned long long)std::max<int64_t>(nr, 1) * (unsigned long long)std::max<int64_t>(nc, 1);
+        int bits = 1;
+        while (bits < 64 && (1ull << bits) < span) ++bits;
+        size_t tb = 0;
+        MBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, idx, idx2, n, 0, bits, s));
+        void* temp = tm(tb);
+        MBX_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys2, idx, idx2, n, 0, bits, s));
+        auto* head = static_cast<int64_t*>(tm(n * 8 + 8));
+        auto* pos = static_cast<int64_t*>(tm(n * 8 + 8));
+        mbx::run_heads_kernel<<<mbx::grid_of(n, ctx), 256, 0, s>>>(keys2, n, head);
+        size_t sb = 0;
+        MBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, head, pos, n, s));
+        void* st = tm(sb);
+        MBX_CUDA(cub::DeviceScan::ExclusiveSum(st, sb, head, pos, n, s));
+        int64_t last[2];
+        MBX_CUDA(cudaMemcpyAsync(&last[0], pos + n - 1, 8, cudaMemcpyDeviceToHost, s));
+        MBX_CUDA(cudaMemcpyAsync(&last[1], head + n - 1, 8, cudaMemcpyDeviceToHost, s));
+        MBX_CUDA(cudaStreamSynchronize(s));
+        merged = last[0] + last[1];
+        if (merged > int64_t(0xFFFFFFFF))
+          fail(MBX_CAPACITY_ERROR, "nonzero count " + std::to_string(merged) +
+                                       " exceeds the 32-bit tile cursor");
+        m->nnz = merged;
+        m->vals = dm(merged * vs + 256);
+        m->cols = static_cast<int32_t*>(dm(merged * 4 + 256));
+        MBX_CUDA(cudaMemsetAsync(m->vals, 0, merged * vs + 256, s));
+        MBX_CUDA(cudaMemsetAsync(m->cols, 0, merged * 4 + 256, s));
+        mrow = static_cast<int64_t*>(tm(merged * 8));
+        if (precision == MBX_F32)
+          mbx::merge_runs_kernel<float><<<mbx::grid_of(n, ctx), 256, 0, s>>>(
+              keys2, idx2, vals, head, pos, n, nc, mrow, m->cols, static_cast<float*>(m->vals));
+        else
+          mbx::merge_runs_kernel<double><<<mbx::grid_of(n, ctx), 256, 0, s>>>(
+              keys2, idx2, vals, head, pos, n, nc, mrow, m->cols, static_cast<double*>(m->vals));
+        ctx->launches += 2;
+      } else {
+        m->vals = dm(256);
+        m->cols = static_cast<int32_t*>(dm(256));
+        MBX_CUDA(cudaMemsetAsync(m->vals, 0, 256, s));
+        MBX_CUDA(cudaMemsetAsync(m->cols, 0, 256, s));
+        mrow = static_cast<int64_t*>(tm(8));
+      }
+      m->ro = static_cast<uint32_t*>(dm((nr + 1) * 4 + 64));
+      mbx::row_offsets_kernel<<<mbx::grid_of(nr + 1, ctx), 256, 0, s>>>(mrow, merged, nr, m->ro);
+      ++ctx->launches;
+      MBX_CUDA(cudaGetLastError());
+      MBX_CUDA(cudaStreamSynchronize(s));
+      release();
+    } catch (...) {
+      release();
+      cudaStreamSynchronize(s);
+      for (void* p : {m->vals, static_cast<void*>(m->cols), static_cast<void*>(m->ro)})
+        if (p) cudaFree(p);
+      throw;
+    }
+    *out = m.release();
+  });
+}
+
+MBX_API int mbx_tile_cache_write(const mbx_tile* t, const char* path, int precision) {
+  return mbx::iguard([&] {
+    std::vector<uint32_t> tx(t->info.tile_num + 1), ty(t->info.tile_num + 1),
+        ld(std::max<int64_t>(t->info.lane_num, 1));
+    const int rc = mbx_tile_download(t, tx.data(), ty.data(), ld.data());
+    if (rc) mbx::fail(rc, mbx_last_error());
+    mbx::write_tile_cache_host(path, t->info, tx.data(), ty.data(), ld.data(), precision);
+  });
+}
+
+MBX_API int mbx_tile_cache_load(mbx_context* ctx, const char* path, mbx_tile** out,
+                                int* precision) {
+  return mbx::iguard([&] {
+    mbx_tile_info info{};
+    uint32_t *tx = nullptr, *ty = nullptr, *ld = nullptr;
+    mbx::read_tile_cache_host(path, &info, &tx, &ty, &ld, precision);
+    const int rc = mbx_tile_upload(ctx, &info, tx, ty, ld, out);
+    std::free(tx);
+    std::free(ty);
+    std::free(ld);
+    if (rc) mbx::fail(rc, mbx_last_error());
+  });
+}
+
+}  // extern "C"

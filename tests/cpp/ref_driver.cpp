@@ -106,7 +106,39 @@ int main() {
            "reference pagerank<double> over B200Backend: " + std::to_string(run.iterations) +
                " iterations, max |pi - pi_csr| = " + std::to_string(dev));
   }
-  // 4. error taxonomy survives the boundary (test_kernel.cpp:241-267)
+  // 4. the reference's bicgstab driver over the GPU backend (acceptance c10),
+  //    and the device-resident merbit_b200::bicgstab on the same system
+  {
+    const auto a = five_point_laplacian<double>(32);
+    const auto x_true = seed_test_vector<double>(a.n_rows, -1.0, 1.0, 77);
+    const auto b = spmv_csr_reference(a, std::span<const double>(x_true));
+    const SimtConfig c = SimtConfig::make(32, 7, 128);
+    B200Backend<double> gpu(a, c);
+    const auto run = bicgstab<double>(a, std::span<const double>(b), {}, gpu);
+    CsrReferenceBackend<double> csr(a);
+    const auto want = bicgstab<double>(a, std::span<const double>(b), {}, csr);
+    report(run.status == SolveStatus::converged && run.final_residual < 1e-10 &&
+               std::llabs(static_cast<long long>(run.iterations - want.iterations)) <= 2,
+           "reference bicgstab<double> over B200Backend: " + std::to_string(run.iterations) +
+               " passes (csr backend " + std::to_string(want.iterations) + ")");
+    merbit_b200::Context dctx(0);
+    const auto bc = merbit_b200::SimtConfig::make(32, 7, 128);
+    merbit_b200::MerbitB200Backend<double> eng(dctx, a, bc);
+    const auto dev = merbit_b200::bicgstab<double>(eng, std::span<const double>(b));
+    report(dev.status == merbit_b200::SolveStatus::converged && dev.final_residual < 1e-10 &&
+               dev.residual_history.size() == static_cast<std::size_t>(dev.iterations),
+           "device-resident merbit_b200::bicgstab: " + std::to_string(dev.iterations) +
+               " passes, residual " + std::to_string(dev.final_residual));
+    const auto singular = singular_diagonal_fixture<double>();
+    merbit_b200::MerbitB200Backend<double> sg(dctx, singular,
+                                              merbit_b200::SimtConfig::make(4, 4, 4));
+    const std::vector<double> ones = {1.0, 1.0};
+    const auto broken = merbit_b200::bicgstab<double>(sg, std::span<const double>(ones));
+    report(broken.status == merbit_b200::SolveStatus::breakdown &&
+               broken.breakdown_reason == "rhat_dot_v" && broken.iterations == 2,
+           "device bicgstab breakdown on diag(1, 0): " + broken.breakdown_reason);
+  }
+  // 5. error taxonomy survives the boundary (test_kernel.cpp:241-267)
   {
     const auto a = walkthrough_fixture<double>();
     B200Backend<double> gpu(a, SimtConfig::make(4, 4, 4));

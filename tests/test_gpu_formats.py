@@ -1,0 +1,97 @@
+"""GPU side of the file formats: coo_to_csr<T> on the
+device (mbx_matrix_from_coo) against the reference's own coo_to_csr, and MBTL
+caches written from / loaded into device TILEs."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2605_07391_b200 as mb
+from paper_2605_07391_b200 import formats as F
+
+pytestmark = pytest.mark.gpu
+needs_ref = pytest.mark.skipif(O.ref() is None, reason="oracle/_ref not built")
+
+
+def _dup_heavy_coo(seed, n_rows=300, n_cols=200, n=6000):
+    rng = np.random.default_rng(seed)
+    rows = rng.integers(0, n_rows, n)
+    cols = rng.integers(0, n_cols, n)
+    # force long duplicate runs with values of very different magnitude, so
+    # a different summation order would change the low bits
+    rows[:600] = 5
+    cols[:600] = 7
+    vals = rng.uniform(-1, 1, n) * 10.0 ** rng.integers(-8, 9, n)
+    return F.CooTriples(n_rows, n_cols, rows, cols, vals)
+
+
+@needs_ref
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_from_coo_matches_reference_coo_to_csr(ctx, dt):
+    for seed in range(3):
+        coo = _dup_heavy_coo(seed)
+        m = F.matrix_from_coo(coo, dt, ctx)
+        ro, cols, vals = m.download()
+        want = O.ref().coo_to_csr(dict(n_rows=coo.n_rows, n_cols=coo.n_cols, rows=coo.rows,
+                                       cols=coo.cols, vals=coo.vals))
+        assert (m.n_rows, m.n_cols, m.nnz) == (want.n_rows, want.n_cols, want.nnz)
+        assert np.array_equal(ro, want.row_offsets)
+        assert np.array_equal(cols, want.col_indices)
+        # coo_to_csr<T>: the fp64 duplicate sum, rounded to T once
+        assert np.array_equal(vals, want.values.astype(dt))
+
+
+def test_from_coo_edges_and_errors(ctx):
+    empty = F.CooTriples(4, 3, np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    m = F.matrix_from_coo(empty, np.float64, ctx)
+    ro, cols, _ = m.download()
+    assert m.nnz == 0 and ro.tolist() == [0, 0, 0, 0, 0]
+    trailing = F.CooTriples(6, 6, np.array([0, 2]), np.array([1, 5]), np.array([1.0, 2.0]))
+    ro, cols, vals = F.matrix_from_coo(trailing, np.float64, ctx).download()
+    assert ro.tolist() == [0, 1, 1, 2, 2, 2, 2] and cols.tolist() == [1, 5]
+    bad = F.CooTriples(2, 2, np.array([0, 3]), np.array([1, 1]), np.array([1.0, 1.0]))
+    with pytest.raises(mb.DimensionError, match=r"coo entry \(3, 1\) outside 2x2"):
+        F.matrix_from_coo(bad, np.float64, ctx)
+
+
+def test_matrix_market_to_spmv(ctx, tmp_path):
+    """Matrix Market file -> device CSR -> TILE -> SpMV within the reference's
+    ToleranceBound of the CSR oracle."""
+    lap = O.five_point_laplacian(20)
+    rows = np.repeat(np.arange(lap.n_rows), np.diff(lap.row_offsets))
+    coo = F.CooTriples(lap.n_rows, lap.n_cols, rows, lap.col_indices.astype(np.int64),
+                       lap.values)
+    path = str(tmp_path / "lap.mtx")
+    F.write_matrix_market_file(path, coo)
+    m = F.matrix_from_coo(F.load_matrix_any(path), np.float64, ctx)
+    c = mb.SimtConfig.make(32, 7, 128)
+    t = mb.generate_tile_for(m, c)
+    x = O.seed_test_vector(m.n_cols, -1, 1, 3)
+    y = mb.spmv_merbit(m, t, c, x, mb.DualBuffer(m.n_rows))
+    assert np.allclose(y, O.spmv_csr_f64(lap, x), rtol=0, atol=1e-13)
+
+
+@needs_ref
+def test_tile_cache_device_round_trip(ctx, tmp_path):
+    m = mb.DeviceMatrix.rmat(ctx, 14, 16, seed=2, dtype=np.float32)
+    ro, _, _ = m.download(want_values=False)
+    for (w, s) in ((32, 14), (32, 7), (4, 4)):
+        c = mb.SimtConfig.make(w, s, 128 if w == 32 else 16)
+        t = mb.generate_tile_for(m, c)
+        path = str(tmp_path / f"t{w}_{s}.mbtl")
+        F.write_tile_cache(path, t, "f32")
+        # the reference's reader sees exactly its own generate_tile
+        got = O.ref().tile_cache_read(path)
+        want = O.generate_tile(ro, m.n_rows, m.nnz, w, s)
+        for k, v in zip(("tile_x", "tile_y", "lane_desc"), want):
+            assert np.array_equal(got[k], v)
+        # and the reference's file loads back into an identical device TILE
+        ref_path = str(tmp_path / f"r{w}_{s}.mbtl")
+        O.ref().tile_cache_write(ref_path, ro, m.n_rows, m.nnz, w, s, False)
+        t2, prec = F.load_tile_cache(ref_path, ctx)
+        assert prec == "f32"
+        for a, b in zip(t.download(), t2.download()):
+            assert np.array_equal(a, b)
+        x = O.hash_uniform(4, m.n_cols, -1, 1, np.float32)
+        y1 = mb.spmv_merbit(m, t, c, x, mb.DualBuffer(m.n_rows, np.float32)).copy()
+        y2 = mb.spmv_merbit(m, t2, c, x, mb.DualBuffer(m.n_rows, np.float32))
+        assert np.array_equal(y1.view(np.uint32), y2.view(np.uint32))
