@@ -214,6 +214,21 @@ def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak, make=None, label=Non
            "preprocess_slots_ms": slot_s * 1e3,
            "preprocess_over_spmv": (t.preprocess_seconds + xc_s + slot_s) / ts,
            "xcache_hubs": A.xcache_info()[0], "xcache_coverage": A.xcache_info()[1]}
+    # the paper's comparators on the same device and inputs
+    from paper_2605_07391_b200.merbit import spmv_baseline_device
+    base = {}
+    for kind in ("coo_atomic", "csr_vector", "merge_runtime", "merge_cub"):
+        try:
+            fn = (lambda k=kind: spmv_baseline_device(A, k, x.data_ptr(), y.data_ptr(), c.sigma))
+            fn()
+            tb = time_device(stream, fn, max(3, reps // 3))
+            base[kind] = {"ms": tb * 1e3, "gflops": 2 * A.nnz / tb / 1e9,
+                          "merbit_speedup": tb / ts}
+        except Exception as e:  # e.g. merge_cub's int32 offsets at > 2^31 nonzeros
+            base[kind] = {"unavailable": str(e)[:120]}
+    out["comparators"] = base
+    if "ms" in base.get("coo_atomic", {}):
+        out["speedup_vs_coo"] = base["coo_atomic"]["ms"] * 1e-3 / ts  # BenchRecord.speedup
     if label:
         tr = mb.trace_counts(t)
         out.update({"matrix": label, "n": n, "fast_tiles": tr.fast_tiles,

@@ -292,6 +292,13 @@ MBX_API int mbx_spmv_trace_counts(mbx_context* ctx, const mbx_tile* t,
 MBX_API int mbx_spmv_csr_device(mbx_context* ctx, const mbx_matrix* m,
                                 const void* x_dev, void* y_dev);
 
+/* The paper's baselines on the same device: kind 0
+ * csr_vector (warp per row), 1 coo_atomic (CooReferenceBackend, backend.hpp:
+ * 67-84), 2 merge_runtime (spmv_merge_runtime, merge_spmv.hpp:21-82, with
+ * this sigma), 3 merge_cub (cub::DeviceSpmv::CsrMV, library). */
+MBX_API int mbx_spmv_baseline_device(mbx_context* ctx, const mbx_matrix* m, int kind,
+                                     int sigma, const void* x_dev, void* y_dev);
+
 /* ---- PageRank (K2/K3 in fused mode) --------------------------------------- */
 /* One-shot pagerank<T>(p, cfg, backend) (solvers.hpp:154-218): yardstick,
  * power loop with the damping/teleport update, dangling redistribution, L1

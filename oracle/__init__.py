@@ -473,6 +473,8 @@ class _Ref:
                                          fp, f64p, C.POINTER(C.c_int64),
                                          C.POINTER(C.c_double), C.POINTER(C.c_int),
                                          C.c_char_p, C.c_int]
+        for name, fp in (("ref_spmv_merge_runtime_f64", f64p), ("ref_spmv_merge_runtime_f32", f32p)):
+            getattr(L, name).argtypes = [C.c_int64, C.c_int64, i64p, i32p, fp, fp, C.c_int, fp]
         u32pp = C.POINTER(C.POINTER(C.c_uint32))
         L.ref_tile_cache_write.argtypes = [C.c_char_p, C.c_int64, C.c_int64, i64p, C.c_int,
                                            C.c_int, C.c_int]
@@ -553,6 +555,17 @@ class _Ref:
             a.n_rows, a.n_cols, a.row_offsets, _vals_or_dummy(a.col_indices),
             _vals_or_dummy(a.values), _vals_or_dummy(np.ascontiguousarray(x, dt)), y))
         return y[:a.n_rows]
+
+    def spmv_merge_runtime(self, a: Csr, x, sigma):
+        """The reference's spmv_merge_runtime<T> (merge_spmv.hpp:21-82)."""
+        dt = a.values.dtype
+        y = np.zeros(a.n_rows, dt)
+        fn = (self.L.ref_spmv_merge_runtime_f64 if dt == np.float64
+              else self.L.ref_spmv_merge_runtime_f32)
+        self._check(fn(a.n_rows, a.n_cols, a.row_offsets, _vals_or_dummy(a.col_indices),
+                       _vals_or_dummy(a.values), np.ascontiguousarray(x, dt), sigma,
+                       y if a.n_rows else np.zeros(1, dt)))
+        return y
 
     # ---- file formats --------------------------------------------------
     def tile_cache_write(self, path, ro, n_rows, nnz, omega, sigma, f64=False):

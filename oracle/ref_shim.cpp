@@ -22,6 +22,7 @@
 #include "merbit/merbit_spmv.hpp"
 #include "merbit/matrix_market.hpp"
 #include "merbit/merge_path.hpp"
+#include "merbit/merge_spmv.hpp"
 #include "merbit/random.hpp"
 #include "merbit/reference.hpp"
 #include "merbit/solvers.hpp"
@@ -257,7 +258,22 @@ REF_SPMV(float, f32)
     });                                                                           \
   }
 
+// spmv_merge_runtime<T> (merge_spmv.hpp:21-82), single-threaded
+#define REF_MERGE_RUNTIME(T, SUFFIX)                                              \
+  int ref_spmv_merge_runtime_##SUFFIX(int64_t n_rows, int64_t n_cols,             \
+                                      const int64_t* ro, const int32_t* cols,     \
+                                      const T* vals, const T* x, int sigma, T* y) { \
+    return guarded([&] {                                                          \
+      const CsrMatrix<T> a = make_csr<T>(n_rows, n_cols, ro, cols, vals);         \
+      const SimtConfig c = SimtConfig::make(32, sigma, 32);                       \
+      const auto out = spmv_merge_runtime<T>(a, std::span<const T>(x, x + n_cols), c); \
+      std::memcpy(y, out.data(), sizeof(T) * out.size());                        \
+    });                                                                           \
+  }
+
 extern "C" {
+REF_MERGE_RUNTIME(double, f64)
+REF_MERGE_RUNTIME(float, f32)
 REF_BICGSTAB(double, f64)
 REF_BICGSTAB(float, f32)
 

@@ -611,6 +611,7 @@ MBX_API int mbx_matrix_destroy(mbx_matrix* m) {
     dfree(ctx, m->cols_hub);
     dfree(ctx, m->hub_cols);
     mbx::free_slots(ctx, m);
+    dfree(ctx, m->coo_rows);
     MBX_CUDA(cudaStreamSynchronize(ctx->stream));
     delete m;
   });

@@ -825,7 +825,7 @@ __device__ __forceinline__ void commit_row(const SlotParams<T>& p, T base, int64
     p.y[row] = w;
 }
 
-template <typename T, int SIGMA, bool PR, bool HUB>
+template <typename T, int SIGMA, bool PR, bool HUB, bool PF>
 __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub, T* rowbuf,
                                            int64_t range, int lid, uint64_t pol, T base,
                                            double* wacc) {
@@ -859,6 +859,14 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
     const int nrows = static_cast<int>(y1 - y0);
     const T* vb = p.svals + c * TS;
     const int32_t* cb = p.scols + c * TS;
+    if (PF && lid == 0 && ci + 1 < nc) {
+      // one bulk L2 prefetch per stream for the next tile: its column and
+      // value slots then arrive at L2 latency instead of DRAM latency
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cb + TS),
+                   "r"(unsigned(TS * 4)));
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vb + TS),
+                   "r"(unsigned(TS * sizeof(T))));
+    }
     if (ty0 & kLongRowMask) {
       // marked tile: one row; lane-strided subtotals + halving tree
       // (fast_tile_reduce, merbit_spmv.hpp:58-77) -- the butterfly's lane 0
@@ -995,7 +1003,7 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
   }
 }
 
-template <typename T, int SIGMA, bool PR, bool HUB>
+template <typename T, int SIGMA, bool PR, bool HUB, bool PF>
 __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geometry& g = p.g;
@@ -1017,7 +1025,7 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t range = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp; range < g.num_ranges;
        range += wstride)
-    slot_range<T, SIGMA, PR, HUB>(p, hub, rowbuf, range, lid, pol, base, wacc);
+    slot_range<T, SIGMA, PR, HUB, PF>(p, hub, rowbuf, range, lid, pol, base, wacc);
   __syncwarp();
   if (PR) write_warp_part(load_acc(wacc, lid), p.pr.range_part, lid);
 }
@@ -1072,13 +1080,14 @@ __global__ void build_slots_kernel(const T* __restrict__ vals, const int32_t* __
 
 template <typename T, int SIGMA, bool PR, bool HUB>
 void launch_slot(mbx_context* ctx, const SlotParams<T>& p, size_t smem) {
-  auto kern = spmv_slot_kernel<T, SIGMA, PR, HUB>;
-  static int configured = -1;
-  if (configured != ctx->device) {
+  auto kern = p.g.prefetch ? spmv_slot_kernel<T, SIGMA, PR, HUB, true>
+                           : spmv_slot_kernel<T, SIGMA, PR, HUB, false>;
+  static int configured[2] = {-1, -1};
+  if (configured[p.g.prefetch ? 1 : 0] != ctx->device) {
     int optin = 0;
     MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     MBX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    configured = ctx->device;
+    configured[p.g.prefetch ? 1 : 0] = ctx->device;
   }
   const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
   const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));

@@ -141,6 +141,7 @@ struct mbx_matrix_s {
     double seconds = 0.0;  // build time (preprocessing)
   };
   mutable SlotCache slots;
+  mutable int32_t* coo_rows = nullptr;  // COO row array of the coo_atomic comparator
 };
 
 struct mbx_tile_s {

@@ -480,6 +480,18 @@ def spmv_device(m: DeviceMatrix, t: Tile, c: SimtConfig, x_ptr: int, y_ptr: int)
     _check(_lib.lib().mbx_spmv_device(m.ctx.h, m.h, t.h, C.byref(cc), x_ptr, y_ptr))
 
 
+BASELINE_KINDS = {"csr_vector": 0, "coo_atomic": 1, "merge_runtime": 2, "merge_cub": 3}
+
+
+def spmv_baseline_device(m: DeviceMatrix, kind: str, x_ptr: int, y_ptr: int, sigma: int = 0):
+    """The paper's comparators on the GPU (csr_vector, coo_atomic,
+    merge_runtime with `sigma`, merge_cub); device pointers in and out."""
+    if sigma <= 0:
+        sigma = 14 if m.dtype == np.float32 else 7
+    _check(_lib.lib().mbx_spmv_baseline_device(m.ctx.h, m.h, BASELINE_KINDS[kind], sigma,
+                                               x_ptr, y_ptr))
+
+
 def trace_counts(t: Tile) -> SpmvTrace:
     tr = mbx_spmv_trace()
     _check(_lib.lib().mbx_spmv_trace_counts(t.ctx.h, t.h, C.byref(tr)))

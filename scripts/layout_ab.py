@@ -16,7 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=24)
 ap.add_argument("--dtype", default="f32")
 ap.add_argument("--variants", default="1:131072:32,0:131072:32",
-                help="layout:smem_per_sm:warps,...")
+                help="layout:smem_per_sm:warps[:prefetch],...")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--iters", type=int, default=20)
 args = ap.parse_args()
@@ -47,9 +47,10 @@ def timed(fn, reps):
 
 
 for v in args.variants.split(","):
-    layout, smem, warps = (int(f) for f in v.split(":"))
+    fs = [int(f) for f in v.split(":")] + [0]
+    layout, smem, warps, pf = fs[:4]
     ctx.set_layout(layout)
-    ctx.set_tuning(warps, 1, -1, smem, 0)
+    ctx.set_tuning(warps, 1, -1, smem, pf)
     xs = P.build_xcache()
     y = torch.empty_like(x)
     ms = timed(lambda: mb.spmv_device(P, t, c, x.data_ptr(), y.data_ptr()), args.reps)
@@ -63,7 +64,7 @@ for v in args.variants.split(","):
     m, n = P.nnz, P.n_rows
     vs = 4 if dt == np.float32 else 8
     b = m * (vs + 4) + 2 * n * vs + 4 * (n + 1)
-    print(json.dumps({"layout": layout, "smem_per_sm": smem, "warps": warps,
+    print(json.dumps({"layout": layout, "smem_per_sm": smem, "warps": warps, "prefetch": pf,
                       "hubs": P.xcache_info()[0], "coverage": P.xcache_info()[1],
                       "slot_build_s": P.slot_info()[1], "spmv_ms": ms, "spmv_gbs": b / ms / 1e6,
                       "pr_ms_per_iter": pr_ms, "pr_it_s": 1e3 / pr_ms,
