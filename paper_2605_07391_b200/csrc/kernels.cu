@@ -216,6 +216,10 @@ __device__ __forceinline__ void pr_commit_v(const PrArgs& pr, T base, int64_t ro
   // (solvers.hpp:110-112; no contraction into an FMA)
   const T pn = mul_rn(static_cast<T>(pr.damping), w) + base;
   out[row] = pn;
+  if (pr.xout) {  // row shards: the exchange copy of a non-dangling vertex
+    const int32_t q = pr.xmap[row];
+    if (q >= 0) static_cast<T*>(pr.xout)[q] = pn;
+  }
   // |pn - po| is formed in T (the reference's own precision for pi) and
   // accumulated in fp64
   a.resid += static_cast<double>(fabs(pn - po));

@@ -94,6 +94,10 @@ struct PrArgs {
   // 1: K3's last block decides convergence.  0 (row shards): the scalars are
   // partial; the combine kernel after the exchange decides.
   int check_stop = 1;
+  // Row shards: pi_new of a non-dangling row is also written to its slot
+  // xmap[row] (>= 0) of the compacted exchange buffer xout.
+  void* xout = nullptr;
+  const int32_t* xmap = nullptr;
 };
 
 }  // namespace mbx

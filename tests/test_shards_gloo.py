@@ -1,7 +1,9 @@
 """CPU, world_size 2 over gloo: the multi-GPU exchange protocol of shard.cu
-(merge-path row bounds from the product's mbx_plan_row_shards, padded chunks
-with an fp64 scalar tail, one all-gather per iteration, rank-order combine)
-reproduces the single-process PageRank.  The per-shard multiply here is the
+(merge-path row bounds from the product's mbx_plan_row_shards, compacted
+chunks holding only the NON-DANGLING entries of each rank's rows plus an fp64
+scalar tail, columns remapped to pos(v) = owner * chunk + #non-dangling before
+v in the owner's rows, one all-gather per iteration, rank-order combine, full
+rows kept locally) reproduces the single-process PageRank.  The per-shard multiply here is the
 CPU oracle (the checker) -- this test covers the host logic and layout; the
 device kernels of the same protocol are covered by tests/test_gpu_shards.py."""
 import os
@@ -34,37 +36,49 @@ def _worker(rank, world, port, q):
     n = p.n_rows
     vals = O.transition_values(n, p.col_indices, np.float64)
     b = mb.plan_row_shards(p.row_offsets, n, p.nnz, world)  # product host logic
-    rows_max = int(np.diff(b).max())
-    chunk = rows_max + 4  # pi rows, then 4 fp64 scalars (dangling, resid, mass, err)
     r0, r1 = int(b[rank]), int(b[rank + 1])
     ro = p.row_offsets[r0:r1 + 1] - p.row_offsets[r0]
     cols = p.col_indices[p.row_offsets[r0]:p.row_offsets[r1]]
     v = vals[p.row_offsets[r0]:p.row_offsets[r1]]
-    local = O.Csr(r1 - r0, n, ro, cols, v)
     seen = torch.zeros(n, dtype=torch.uint8)
     seen[torch.from_numpy(cols.astype(np.int64))] = 1
-    dist.all_reduce(seen, op=dist.ReduceOp.MAX)  # global empty columns
-    dang = (seen.numpy() == 0)[r0:r1]
-    # padded exchange buffer [world][chunk]
+    dist.all_reduce(seen, op=dist.ReduceOp.MAX)  # global empty columns = dangling
+    nd = seen.numpy().astype(bool)
+    gpre = np.concatenate([[0], np.cumsum(nd)])  # non-dangling before v
+    nd_max = max(int(gpre[b[g + 1]] - gpre[b[g]]) for g in range(world))
+    chunk = nd_max + 4  # non-dangling pi entries, then 4 fp64 scalars
+    owner = np.searchsorted(np.asarray(b), np.arange(n), side="right") - 1
+    pos = owner * chunk + (gpre[:n] - gpre[np.asarray(b)[owner]])
+    assert nd[cols].all()  # only non-dangling columns are ever gathered
+    local = O.Csr(r1 - r0, world * chunk, ro, pos[cols].astype(np.int32), v)
+    dang = ~nd[r0:r1]
+    xmap = np.where(nd[r0:r1], pos[r0:r1] - rank * chunk, -1)
+
+    def pack(pi):
+        mine = torch.zeros(chunk, dtype=torch.float64)
+        mine[torch.from_numpy(xmap[xmap >= 0])] = torch.from_numpy(pi[xmap >= 0])
+        return mine
     buf = torch.zeros(world * chunk, dtype=torch.float64)
     pi_local = np.full(r1 - r0, 1.0 / n)
-    mine = torch.zeros(chunk, dtype=torch.float64)
-    mine[:r1 - r0] = torch.from_numpy(pi_local)
-    mine[rows_max] = pi_local[dang].sum()
+    mine = pack(pi_local)
+    mine[nd_max] = pi_local[dang].sum()
     dist.all_gather_into_tensor(buf, mine)
     for _ in range(ITERS):
-        full = np.concatenate([buf[g * chunk:g * chunk + (b[g + 1] - b[g])].numpy()
-                               for g in range(world)])
-        dm = sum(float(buf[g * chunk + rows_max]) for g in range(world))  # rank order
-        w = O.spmv_csr_f64(local, full)
+        dm = sum(float(buf[g * chunk + nd_max]) for g in range(world))  # rank order
+        w = O.spmv_csr_f64(local, buf.numpy())
         new = C_ * w + (C_ * dm + 1 - C_) / n
-        mine = torch.zeros(chunk, dtype=torch.float64)
-        mine[:r1 - r0] = torch.from_numpy(new)
-        mine[rows_max] = new[dang].sum()
-        mine[rows_max + 1] = np.abs(new - pi_local).sum()
+        mine = pack(new)
+        mine[nd_max] = new[dang].sum()
+        mine[nd_max + 1] = np.abs(new - pi_local).sum()
         pi_local = new
         dist.all_gather_into_tensor(buf, mine)
-    full = np.concatenate([buf[g * chunk:g * chunk + (b[g + 1] - b[g])].numpy()
+    # the full answer: one gather of the local rows (mbx_shard_group_gather_pi)
+    rows_max = int(np.diff(np.asarray(b)).max())
+    lbuf = torch.zeros(world * rows_max, dtype=torch.float64)
+    lmine = torch.zeros(rows_max, dtype=torch.float64)
+    lmine[:r1 - r0] = torch.from_numpy(pi_local)
+    dist.all_gather_into_tensor(lbuf, lmine)
+    full = np.concatenate([lbuf[g * rows_max:g * rows_max + (b[g + 1] - b[g])].numpy()
                            for g in range(world)])
     q.put((rank, full, [int(x) for x in b]))
     dist.destroy_process_group()
