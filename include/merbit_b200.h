@@ -299,6 +299,12 @@ MBX_API int mbx_spmv_csr_device(mbx_context* ctx, const mbx_matrix* m,
 MBX_API int mbx_spmv_baseline_device(mbx_context* ctx, const mbx_matrix* m, int kind,
                                      int sigma, const void* x_dev, void* y_dev);
 
+/* Mean device time of one multiply (CUDA events; x uploaded once, warm-up
+ * untimed): kind -1 = MERBIT (K2+K3 with t), 0..3 = the comparators above. */
+MBX_API int mbx_bench_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                           const mbx_simt_config* c, int kind, int iters, int warmup,
+                           const void* x_host, double* mean_seconds);
+
 /* ---- PageRank (K2/K3 in fused mode) --------------------------------------- */
 /* One-shot pagerank<T>(p, cfg, backend) (solvers.hpp:154-218): yardstick,
  * power loop with the damping/teleport update, dangling redistribution, L1
@@ -381,6 +387,11 @@ MBX_API void mbx_free(void* p);
  * entry order, one rounding to T -- the result is a resident matrix. */
 MBX_API int mbx_matrix_from_coo(mbx_context* ctx, int precision, const mbx_coo* coo,
                                 mbx_matrix** out);
+/* build_transition (solvers.hpp:36-74) on the device: P[i][j] = T(1)/T(outdeg j)
+ * for every adjacency entry j -> i, rows in ascending source order, dangling
+ * columns empty; dimension_error on a non-square adjacency. */
+MBX_API int mbx_matrix_build_transition(mbx_context* ctx, const mbx_matrix* adjacency,
+                                        mbx_matrix** out);
 
 /* ---- multi-GPU row-sharded PageRank (one process per GPU) ---------------- */
 /* GPU g owns rows [row_bounds[g], row_bounds[g+1]) of P (mbx_plan_row_shards)

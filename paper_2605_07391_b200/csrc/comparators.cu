@@ -244,4 +244,51 @@ MBX_API int mbx_spmv_baseline_device(mbx_context* ctx, const mbx_matrix* m, int 
   });
 }
 
+// Device-resident timing of one multiply kind on this matrix (CUDA events on
+// the context stream): kind -1 = MERBIT (K2+K3 with the given TILE), 0..3 the
+// comparators above.  x is uploaded once; warm-up launches are untimed.
+MBX_API int mbx_bench_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                           const mbx_simt_config* c, int kind, int iters, int warmup,
+                           const void* x_host, double* mean_seconds) {
+  return mbx::cguard([&] {
+    if (iters < 1) mbx::fail(MBX_CONFIG_ERROR, "--iters must be at least 1");
+    MBX_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const size_t vs = mbx::value_size(m->precision);
+    void *x = nullptr, *y = nullptr;
+    MBX_CUDA(cudaMallocAsync(&x, m->n_cols * vs + 256, s));
+    MBX_CUDA(cudaMallocAsync(&y, m->n_rows * vs + 256, s));
+    if (m->n_cols) MBX_CUDA(cudaMemcpyAsync(x, x_host, m->n_cols * vs, cudaMemcpyHostToDevice, s));
+    auto once = [&] {
+      const int rc = kind < 0 ? mbx_spmv_device(ctx, m, t, c, x, y)
+                              : mbx_spmv_baseline_device(ctx, m, kind, c->sigma, x, y);
+      if (rc) mbx::fail(rc, mbx_last_error());
+    };
+    cudaEvent_t e0, e1;
+    MBX_CUDA(cudaEventCreate(&e0));
+    MBX_CUDA(cudaEventCreate(&e1));
+    try {
+      for (int i = 0; i < warmup; ++i) once();
+      MBX_CUDA(cudaEventRecord(e0, s));
+      for (int i = 0; i < iters; ++i) once();
+      MBX_CUDA(cudaEventRecord(e1, s));
+      MBX_CUDA(cudaEventSynchronize(e1));
+    } catch (...) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      cudaFreeAsync(x, s);
+      cudaFreeAsync(y, s);
+      throw;
+    }
+    float ms = 0.f;
+    MBX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *mean_seconds = double(ms) * 1e-3 / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(x, s);
+    cudaFreeAsync(y, s);
+    MBX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 }  // extern "C"

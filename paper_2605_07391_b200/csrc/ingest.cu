@@ -87,6 +87,36 @@ __global__ void row_offsets_kernel(const int64_t* __restrict__ rows, int64_t m, 
   }
 }
 
+// build_transition (solvers.hpp:36-74): every adjacency entry j -> i becomes
+// the key (i * n + j) of P with the weight T(1) / T(outdeg(j)) computed in T
+template <typename T>
+__global__ void transition_keys_kernel(const uint32_t* __restrict__ ro,
+                                       const int32_t* __restrict__ cols, int64_t n,
+                                       unsigned long long* __restrict__ keys,
+                                       T* __restrict__ w) {
+  const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lid = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = wid; j < n; j += nw) {
+    const uint32_t b = ro[j], e = ro[j + 1];
+    const T weight = e > b ? T(1) / static_cast<T>(e - b) : T(0);
+    for (uint32_t k = b + lid; k < e; k += 32) {
+      keys[k] = (unsigned long long)(cols[k]) * (unsigned long long)(n) + (unsigned long long)(j);
+      w[k] = weight;
+    }
+  }
+}
+
+__global__ void split_keys_kernel(const unsigned long long* __restrict__ keys, int64_t m,
+                                  int64_t n, int64_t* __restrict__ rows,
+                                  int32_t* __restrict__ cols) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    rows[k] = int64_t(keys[k] / (unsigned long long)n);
+    cols[k] = int32_t(keys[k] % (unsigned long long)n);
+  }
+}
+
 template <typename F>
 int iguard(F&& f) {
   try {
@@ -234,6 +264,80 @@ MBX_API int mbx_matrix_from_coo(mbx_context* ctx, int precision, const mbx_coo* 
       throw;
     }
     *out = m.release();
+  });
+}
+
+MBX_API int mbx_matrix_build_transition(mbx_context* ctx, const mbx_matrix* a,
+                                        mbx_matrix** out) {
+  return mbx::iguard([&] {
+    using mbx::fail;
+    if (a->n_rows != a->n_cols)
+      fail(MBX_DIMENSION_ERROR, "transition matrix needs a square adjacency (" +
+                                    std::to_string(a->n_rows) + "x" + std::to_string(a->n_cols) +
+                                    ")");
+    MBX_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int64_t n = a->n_rows, m = a->nnz;
+    const size_t vs = mbx::value_size(a->precision);
+    auto dm = [&](size_t b) {
+      void* p = nullptr;
+      MBX_CUDA(cudaMallocAsync(&p, std::max<size_t>(b, 256), s));
+      return p;
+    };
+    auto p = std::make_unique<mbx_matrix>();
+    p->ctx = ctx;
+    p->precision = a->precision;
+    p->n_rows = p->n_cols = n;
+    p->nnz = m;
+    p->vals = dm(m * vs + 256);
+    p->cols = static_cast<int32_t*>(dm(m * 4 + 256));
+    p->ro = static_cast<uint32_t*>(dm((n + 1) * 4 + 64));
+    MBX_CUDA(cudaMemsetAsync(p->vals, 0, m * vs + 256, s));
+    MBX_CUDA(cudaMemsetAsync(p->cols, 0, m * 4 + 256, s));
+    auto* keys = static_cast<unsigned long long*>(dm(m * 8 + 8));
+    auto* keys2 = static_cast<unsigned long long*>(dm(m * 8 + 8));
+    void* w = dm(m * vs + 8);
+    auto* rows = static_cast<int64_t*>(dm(m * 8 + 8));
+    const unsigned grid = unsigned(ctx->sm_count) * 16;
+    if (m > 0) {
+      if (a->precision == MBX_F32)
+        mbx::transition_keys_kernel<float><<<grid, 256, 0, s>>>(a->ro, a->cols, n, keys,
+                                                               static_cast<float*>(w));
+      else
+        mbx::transition_keys_kernel<double><<<grid, 256, 0, s>>>(a->ro, a->cols, n, keys,
+                                                                static_cast<double*>(w));
+      const unsigned long long span = (unsigned long long)n * (unsigned long long)n;
+      int bits = 1;
+      while (bits < 64 && (1ull << bits) < span) ++bits;
+      // stable: equal (i, j) pairs keep their order, rows keep ascending sources
+      size_t tb = 0;
+      if (a->precision == MBX_F32) {
+        MBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, static_cast<float*>(w),
+                                                 static_cast<float*>(p->vals), m, 0, bits, s));
+        void* tmp = dm(tb);
+        MBX_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, static_cast<float*>(w),
+                                                 static_cast<float*>(p->vals), m, 0, bits, s));
+        cudaFreeAsync(tmp, s);
+      } else {
+        MBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2,
+                                                 static_cast<double*>(w),
+                                                 static_cast<double*>(p->vals), m, 0, bits, s));
+        void* tmp = dm(tb);
+        MBX_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, static_cast<double*>(w),
+                                                 static_cast<double*>(p->vals), m, 0, bits, s));
+        cudaFreeAsync(tmp, s);
+      }
+      mbx::split_keys_kernel<<<grid, 256, 0, s>>>(keys2, m, n, rows, p->cols);
+      ctx->launches += 3;
+    }
+    mbx::row_offsets_kernel<<<mbx::grid_of(n + 1, ctx), 256, 0, s>>>(rows, m, n, p->ro);
+    ++ctx->launches;
+    MBX_CUDA(cudaGetLastError());
+    for (void* q : {static_cast<void*>(keys), static_cast<void*>(keys2), w,
+                    static_cast<void*>(rows)})
+      cudaFreeAsync(q, s);
+    MBX_CUDA(cudaStreamSynchronize(s));
+    *out = p.release();
   });
 }
 

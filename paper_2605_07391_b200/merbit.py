@@ -308,6 +308,13 @@ class DeviceMatrix:
         _check(_lib.lib().mbx_matrix_xcache_info(self.h, C.byref(hubs), C.byref(cov)))
         return hubs.value, cov.value
 
+    def build_transition(self) -> "DeviceMatrix":
+        """build_transition (solvers.hpp:36-74) on the device: P = A^T D^-1 of
+        this adjacency pattern, in this matrix's precision."""
+        h = C.c_void_p()
+        _check(_lib.lib().mbx_matrix_build_transition(self.ctx.h, self.h, C.byref(h)))
+        return DeviceMatrix(self.ctx, h)
+
     def slot_info(self):
         """(slots, build seconds) of the lane-major slot copy cached on this
         matrix (built by the first SpMV / PageRank plan per TILE)."""

@@ -95,3 +95,23 @@ def test_tile_cache_device_round_trip(ctx, tmp_path):
         y1 = mb.spmv_merbit(m, t, c, x, mb.DualBuffer(m.n_rows, np.float32)).copy()
         y2 = mb.spmv_merbit(m, t2, c, x, mb.DualBuffer(m.n_rows, np.float32))
         assert np.array_equal(y1.view(np.uint32), y2.view(np.uint32))
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_build_transition_is_the_reference(ctx, dt):
+    """build_transition on the device == the oracle's restatement (pinned to
+    the reference), bitwise: pattern, ascending sources, T(1)/T(outdeg)."""
+    g = mb.DeviceMatrix.rmat(ctx, 12, 16, seed=5, dtype=np.float64)
+    ro, cols, vals = g.download()
+    rmat12 = O.Csr(g.n_rows, g.n_cols, ro, cols, vals)
+    for adj in (O.ring_with_chords(100, 260, 42), rmat12, O.walkthrough()):
+        a = adj.astype(dt)
+        P = mb.DeviceMatrix.from_csr(ctx, a).build_transition()
+        ro, cols, vals = P.download()
+        want = O.build_transition(a, dt)
+        assert np.array_equal(ro, want.row_offsets)
+        assert np.array_equal(cols, want.col_indices)
+        assert np.array_equal(vals, want.values)
+    rect = O.single_dense_row(4, 1)
+    with pytest.raises(mb.DimensionError):
+        mb.DeviceMatrix.from_csr(ctx, rect).build_transition()
