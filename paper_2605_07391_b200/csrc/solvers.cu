@@ -129,12 +129,30 @@ __global__ void __launch_bounds__(kThreads)
     is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (!is_last || threadIdx.x != 0) return;
+  if (!is_last) return;
   __threadfence();
+  // the last block folds the block partials: fixed thread->block map, warp
+  // butterflies, warps in order (deterministic); L2-coherent loads in flight
+  // together instead of one serial round trip per block
+  double q0 = 0.0, q1 = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(part) + i);
+    q0 += v.x;
+    q1 += v.y;
+  }
+  q0 = warp_sum_d(q0);
+  q1 = warp_sum_d(q1);
+  __syncthreads();
+  if (l == 0) {
+    sm[0][w] = q0;
+    sm[1][w] = q1;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   double d0 = 0.0, d1 = 0.0;
-  for (unsigned i = 0; i < gridDim.x; ++i) {
-    d0 += reinterpret_cast<volatile double*>(part)[2 * i];
-    d1 += reinterpret_cast<volatile double*>(part)[2 * i + 1];
+  for (int i = 0; i < nw; ++i) {
+    d0 += sm[0][i];
+    d1 += sm[1][i];
   }
   *counter = 0;
   if (MODE == kBnorm) {
