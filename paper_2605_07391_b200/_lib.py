@@ -86,6 +86,7 @@ SIGNATURES = {
     "mbx_bench_spmv": ([VP, VP, VP, C.POINTER(mbx_simt_config), C.c_int, C.c_int, C.c_int, VP,
                         C.POINTER(C.c_double)], C.c_int),
     "mbx_matrix_build_transition": ([VP, VP, C.POINTER(VP)], C.c_int),
+    "mbx_matrix_relabel_by_degree": ([VP, VP, C.POINTER(VP), VP], C.c_int),
     "mbx_coo_free": ([C.POINTER(mbx_coo)], None),
     "mbx_mm_read": ([C.c_char_p, C.POINTER(mbx_coo)], C.c_int),
     "mbx_mm_parse": ([C.c_char_p, C.c_int64, C.c_char_p, C.POINTER(mbx_coo)], C.c_int),

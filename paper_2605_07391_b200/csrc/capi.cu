@@ -612,6 +612,7 @@ MBX_API int mbx_matrix_destroy(mbx_matrix* m) {
     dfree(ctx, m->hub_cols);
     mbx::free_slots(ctx, m);
     dfree(ctx, m->coo_rows);
+    dfree(ctx, m->vmap);
     MBX_CUDA(cudaStreamSynchronize(ctx->stream));
     delete m;
   });
@@ -1034,22 +1035,33 @@ MBX_API int mbx_pagerank(mbx_context* ctx, const mbx_matrix* p, const mbx_tile* 
     if (rc) fail(rc, g_last_error);
     std::unique_ptr<mbx_pagerank_plan, int (*)(mbx_pagerank_plan*)> guard(pl, mbx_pagerank_plan_destroy);
     Device dg(ctx->device);
+    // a degree-relabelled matrix keeps its vertex map: pi0 / pi / the
+    // yardstick cross the boundary in the ORIGINAL vertex order
     void* pi0 = nullptr;
+    void* tmp = p->vmap ? dmalloc(ctx, pl->n * pl->vs + 256) : nullptr;
     if (pi0_host) {
       pi0 = dmalloc(ctx, pl->n * pl->vs);
-      MBX_CUDA(cudaMemcpyAsync(pi0, pi0_host, pl->n * pl->vs, cudaMemcpyHostToDevice, ctx->stream));
+      MBX_CUDA(cudaMemcpyAsync(p->vmap ? tmp : pi0, pi0_host, pl->n * pl->vs,
+                               cudaMemcpyHostToDevice, ctx->stream));
+      if (p->vmap) mbx::launch_vertex_map(ctx, p->precision, pl->n, p->vmap, tmp, pi0, true);
     }
     rc = mbx_pagerank_plan_run(pl, pi0);
     if (rc) fail(rc, g_last_error);
     rc = mbx_pagerank_plan_result(pl, result, history);
     if (rc) fail(rc, g_last_error);
-    if (pi_host)
-      MBX_CUDA(cudaMemcpyAsync(pi_host, pl->pi[result->iterations & 1], pl->n * pl->vs,
-                               cudaMemcpyDeviceToHost, ctx->stream));
+    auto download = [&](void* host, const void* dev) {
+      const void* src = dev;
+      if (p->vmap) {
+        mbx::launch_vertex_map(ctx, p->precision, pl->n, p->vmap, dev, tmp, false);
+        src = tmp;
+      }
+      MBX_CUDA(cudaMemcpyAsync(host, src, pl->n * pl->vs, cudaMemcpyDeviceToHost, ctx->stream));
+      MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    };
+    if (pi_host) download(pi_host, pl->pi[result->iterations & 1]);
     if (ref_host) {
       if (cfg->reference_iters > 0) {
-        MBX_CUDA(cudaMemcpyAsync(ref_host, pl->ref[cfg->reference_iters & 1], pl->n * pl->vs,
-                                 cudaMemcpyDeviceToHost, ctx->stream));
+        download(ref_host, pl->ref[cfg->reference_iters & 1]);
       } else {
         // zero-iteration yardstick: the uniform start vector
         if (p->precision == MBX_F32) {
@@ -1062,6 +1074,7 @@ MBX_API int mbx_pagerank(mbx_context* ctx, const mbx_matrix* p, const mbx_tile* 
       }
     }
     dfree(ctx, pi0);
+    dfree(ctx, tmp);
     MBX_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

@@ -117,6 +117,52 @@ __global__ void split_keys_kernel(const unsigned long long* __restrict__ keys, i
   }
 }
 
+// ---- degree relabelling (a locality preprocessing for graphs whose x
+// does not fit L2): vertex v gets the rank of its column count, descending
+// (ties: ascending id), applied to rows and columns alike
+__global__ void count_columns_kernel(const int32_t* __restrict__ cols, int64_t nnz,
+                                     uint32_t* __restrict__ cnt) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
+       k += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(cnt + cols[k], 1u);
+}
+
+__global__ void iota32_kernel(int32_t* v, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    v[i] = int32_t(i);
+}
+
+__global__ void invert_order_kernel(const int32_t* __restrict__ order, int64_t n,
+                                    int32_t* __restrict__ rank) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    rank[order[i]] = int32_t(i);
+}
+
+// vertex v -> inner[v] -> outer[inner[v]]
+__global__ void compose_map_kernel(const int32_t* __restrict__ inner,
+                                   const int32_t* __restrict__ outer, int64_t n,
+                                   int32_t* __restrict__ out) {
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
+       v += int64_t(gridDim.x) * blockDim.x)
+    out[v] = outer[inner[v]];
+}
+
+__global__ void relabel_keys_kernel(const uint32_t* __restrict__ ro,
+                                    const int32_t* __restrict__ cols, int64_t n,
+                                    const int32_t* __restrict__ rank,
+                                    unsigned long long* __restrict__ keys) {
+  const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lid = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < n; r += nw) {
+    const unsigned long long rr = (unsigned long long)rank[r] * (unsigned long long)n;
+    for (uint32_t k = ro[r] + lid; k < ro[r + 1]; k += 32)
+      keys[k] = rr + (unsigned long long)rank[cols[k]];
+  }
+}
+
 template <typename F>
 int iguard(F&& f) {
   try {
@@ -336,6 +382,94 @@ MBX_API int mbx_matrix_build_transition(mbx_context* ctx, const mbx_matrix* a,
     for (void* q : {static_cast<void*>(keys), static_cast<void*>(keys2), w,
                     static_cast<void*>(rows)})
       cudaFreeAsync(q, s);
+    MBX_CUDA(cudaStreamSynchronize(s));
+    *out = p.release();
+  });
+}
+
+MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
+                                         mbx_matrix** out, int32_t* rank_host) {
+  return mbx::iguard([&] {
+    using mbx::fail;
+    if (a->n_rows != a->n_cols) fail(MBX_DIMENSION_ERROR, "relabelling needs a square matrix");
+    MBX_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int64_t n = a->n_rows, m = a->nnz;
+    const size_t vs = mbx::value_size(a->precision);
+    std::vector<void*> tmp;
+    auto dm = [&](size_t b, bool keep = false) {
+      void* p = nullptr;
+      MBX_CUDA(cudaMallocAsync(&p, std::max<size_t>(b, 256), s));
+      if (!keep) tmp.push_back(p);
+      return p;
+    };
+    const unsigned grid = unsigned(ctx->sm_count) * 16;
+    auto* cnt = static_cast<uint32_t*>(dm(n * 4 + 64));
+    auto* cnt2 = static_cast<uint32_t*>(dm(n * 4 + 64));
+    auto* ids = static_cast<int32_t*>(dm(n * 4 + 64));
+    auto* order = static_cast<int32_t*>(dm(n * 4 + 64));
+    auto* rank = static_cast<int32_t*>(dm(n * 4 + 64));
+    MBX_CUDA(cudaMemsetAsync(cnt, 0, n * 4 + 64, s));
+    if (m) mbx::count_columns_kernel<<<grid, 256, 0, s>>>(a->cols, m, cnt);
+    mbx::iota32_kernel<<<grid, 256, 0, s>>>(ids, n);
+    size_t tb = 0;
+    MBX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt, cnt2, ids, order, n, 0,
+                                                        32, s));
+    void* t1 = dm(tb);
+    MBX_CUDA(cub::DeviceRadixSort::SortPairsDescending(t1, tb, cnt, cnt2, ids, order, n, 0, 32,
+                                                        s));
+    mbx::invert_order_kernel<<<grid, 256, 0, s>>>(order, n, rank);
+    auto p = std::make_unique<mbx_matrix>();
+    p->ctx = ctx;
+    p->precision = a->precision;
+    p->n_rows = p->n_cols = n;
+    p->nnz = m;
+    p->vals = dm(m * vs + 256, true);
+    p->cols = static_cast<int32_t*>(dm(m * 4 + 256, true));
+    p->ro = static_cast<uint32_t*>(dm((n + 1) * 4 + 64, true));
+    MBX_CUDA(cudaMemsetAsync(p->vals, 0, m * vs + 256, s));
+    MBX_CUDA(cudaMemsetAsync(p->cols, 0, m * 4 + 256, s));
+    auto* rows = static_cast<int64_t*>(dm(m * 8 + 8));
+    if (m) {
+      auto* keys = static_cast<unsigned long long*>(dm(m * 8 + 8));
+      auto* keys2 = static_cast<unsigned long long*>(dm(m * 8 + 8));
+      mbx::relabel_keys_kernel<<<grid, 256, 0, s>>>(a->ro, a->cols, n, rank, keys);
+      const unsigned long long span = (unsigned long long)n * (unsigned long long)n;
+      int bits = 1;
+      while (bits < 64 && (1ull << bits) < span) ++bits;
+      size_t tb2 = 0;
+      if (a->precision == MBX_F32) {
+        const float* v = static_cast<const float*>(a->vals);
+        MBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, keys, keys2, v,
+                                                 static_cast<float*>(p->vals), m, 0, bits, s));
+        void* t2 = dm(tb2);
+        MBX_CUDA(cub::DeviceRadixSort::SortPairs(t2, tb2, keys, keys2, v,
+                                                 static_cast<float*>(p->vals), m, 0, bits, s));
+      } else {
+        const double* v = static_cast<const double*>(a->vals);
+        MBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, keys, keys2, v,
+                                                 static_cast<double*>(p->vals), m, 0, bits, s));
+        void* t2 = dm(tb2);
+        MBX_CUDA(cub::DeviceRadixSort::SortPairs(t2, tb2, keys, keys2, v,
+                                                 static_cast<double*>(p->vals), m, 0, bits, s));
+      }
+      mbx::split_keys_kernel<<<grid, 256, 0, s>>>(keys2, m, n, rows, p->cols);
+    }
+    mbx::row_offsets_kernel<<<mbx::grid_of(n + 1, ctx), 256, 0, s>>>(rows, m, n, p->ro);
+    ctx->launches += 6;
+    MBX_CUDA(cudaGetLastError());
+    if (rank_host && n)
+      MBX_CUDA(cudaMemcpyAsync(rank_host, rank, n * 4, cudaMemcpyDeviceToHost, s));
+    // the new matrix keeps the vertex map (composed with the input's own)
+    p->vmap = static_cast<int32_t*>(dm(n * 4 + 64, true));
+    if (a->vmap) {
+      mbx::compose_map_kernel<<<grid, 256, 0, s>>>(a->vmap, rank, n, p->vmap);
+      ++ctx->launches;
+    } else if (n) {
+      MBX_CUDA(cudaMemcpyAsync(p->vmap, rank, n * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    MBX_CUDA(cudaStreamSynchronize(s));
+    for (void* q : tmp) cudaFreeAsync(q, s);
     MBX_CUDA(cudaStreamSynchronize(s));
     *out = p.release();
   });

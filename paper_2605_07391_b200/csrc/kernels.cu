@@ -1689,6 +1689,32 @@ void launch_dangling_mask(mbx_context* ctx, const mbx_matrix* m, uint32_t* mask)
   MBX_CUDA(cudaGetLastError());
 }
 
+template <typename T>
+__global__ void vertex_map_kernel(int64_t n, const int32_t* __restrict__ map,
+                                  const T* __restrict__ src, T* __restrict__ dst, bool to_new) {
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
+       v += int64_t(gridDim.x) * blockDim.x) {
+    if (to_new)
+      dst[map[v]] = src[v];
+    else
+      dst[v] = src[map[v]];
+  }
+}
+
+void launch_vertex_map(mbx_context* ctx, int precision, int64_t n, const int32_t* map,
+                       const void* src, void* dst, bool to_new) {
+  if (n == 0) return;
+  const unsigned grid = grid_for(n, 256, int64_t(ctx->sm_count) * 8);
+  if (precision == MBX_F32)
+    vertex_map_kernel<float><<<grid, 256, 0, ctx->stream>>>(
+        n, map, static_cast<const float*>(src), static_cast<float*>(dst), to_new);
+  else
+    vertex_map_kernel<double><<<grid, 256, 0, ctx->stream>>>(
+        n, map, static_cast<const double*>(src), static_cast<double*>(dst), to_new);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
 void launch_narrow_cols(mbx_context* ctx, const int64_t* src, int32_t* dst, int64_t n,
                         int64_t limit, int* bad) {
   if (n == 0) return;

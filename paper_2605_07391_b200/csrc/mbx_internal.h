@@ -146,6 +146,10 @@ struct mbx_matrix_s {
   };
   mutable SlotCache slots;
   mutable int32_t* coo_rows = nullptr;  // COO row array of the coo_atomic comparator
+  // Set on a matrix made by mbx_matrix_relabel_by_degree: vertex v of the
+  // original graph is vertex vmap[v] here.  Host-facing PageRank I/O
+  // (pi0 in, pi / yardstick out) stays in the ORIGINAL vertex order.
+  int32_t* vmap = nullptr;
 };
 
 struct mbx_tile_s {
@@ -197,6 +201,9 @@ void launch_pr_init(mbx_context* ctx, int precision, int64_t n,
                     PrScalars* out, double* block_part, unsigned int* counter);
 void launch_dangling_mask(mbx_context* ctx, const mbx_matrix* m,
                           uint32_t* mask_words);
+// dst[map[v]] = src[v] (to_new) or dst[v] = src[map[v]] (back), T = precision
+void launch_vertex_map(mbx_context* ctx, int precision, int64_t n, const int32_t* map,
+                       const void* src, void* dst, bool to_new);
 void launch_narrow_cols(mbx_context* ctx, const int64_t* src, int32_t* dst,
                         int64_t n, int64_t limit, int* bad_flag);
 void launch_narrow_rows(mbx_context* ctx, const int64_t* src, uint32_t* dst,

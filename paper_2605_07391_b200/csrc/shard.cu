@@ -484,6 +484,7 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
       s.view = *m;
       s.view.slots = mbx_matrix::SlotCache{};  // the view builds its own
       s.view.coo_rows = nullptr;
+      s.view.vmap = nullptr;
       s.view.cols = s.cols_remap;
       s.view.cols_hub = nullptr;
       s.view.hub_cols = nullptr;

@@ -315,6 +315,16 @@ class DeviceMatrix:
         _check(_lib.lib().mbx_matrix_build_transition(self.ctx.h, self.h, C.byref(h)))
         return DeviceMatrix(self.ctx, h)
 
+    def relabel_by_degree(self):
+        """(P', rank): the symmetric degree relabelling P' = Q P Q^T on the
+        device (vertex v -> rank[v], by descending column count) -- a locality
+        preprocessing for graphs whose x exceeds L2."""
+        h = C.c_void_p()
+        rank = np.zeros(max(self.n_rows, 1), np.int32)
+        _check(_lib.lib().mbx_matrix_relabel_by_degree(self.ctx.h, self.h, C.byref(h),
+                                                       rank.ctypes.data))
+        return DeviceMatrix(self.ctx, h), rank[:self.n_rows]
+
     def slot_info(self):
         """(slots, build seconds) of the lane-major slot copy cached on this
         matrix (built by the first SpMV / PageRank plan per TILE)."""

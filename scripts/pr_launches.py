@@ -15,6 +15,8 @@ torch.cuda.set_stream(s)
 ctx = mb.Context(0)
 ctx.set_stream(s.cuda_stream)
 P = mb.DeviceMatrix.rmat(ctx, scale, 16, seed=1, transition=True, dtype=np.float32)
+if os.environ.get("MBX_VERTEX_ORDER", "degree") == "degree":  # as bench.py
+    P, _ = P.relabel_by_degree()
 c = mb.SimtConfig.make(32, 14, 128)
 t = mb.generate_tile_for(P, c)
 P.build_xcache()
