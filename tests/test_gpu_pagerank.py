@@ -117,7 +117,7 @@ def test_degree_relabel_preprocessing(ctx):
     byte-identical to the oracle's, and PageRank through the relabelled
     matrix returns pi in the ORIGINAL vertex order within 1e-6 L1 of the fp64
     oracle on P."""
-    P = mb.DeviceMatrix.rmat(ctx, 13, 16, seed=6, transition=True, dtype=np.float32)
+    P = mb.DeviceMatrix.rmat(ctx, 18, 16, seed=6, transition=True, dtype=np.float32)
     ro, cols, vals = P.download()
     n = P.n_rows
     Q, rank = P.relabel_by_degree()
