@@ -396,9 +396,10 @@ MBX_API int mbx_matrix_build_transition(mbx_context* ctx, const mbx_matrix* adja
  * P' = Q P Q^T with vertex v -> rank of its column count (descending, ties by
  * id), rows sorted, columns ascending -- hot columns of x become contiguous
  * (R-MAT s27 PageRank: 1.9x).  PageRank on P' gives pi'[rank[v]] = pi[v] up
- * to summation order.  The new matrix keeps the vertex map: mbx_pagerank's
- * pi0 / pi / yardstick stay in the ORIGINAL vertex order; device-pointer
- * entry points (mbx_spmv*, plans, shard groups) work in the new order.
+ * to summation order.  The new matrix keeps the vertex map: the host-facing
+ * mbx_spmv (x, y) and mbx_pagerank (pi0, pi, yardstick) stay in the ORIGINAL
+ * vertex order; device-pointer entry points (mbx_spmv_device, plans, shard
+ * groups) work in the new order.
  * rank_host (n int32) may be NULL. */
 MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* m,
                                          mbx_matrix** out, int32_t* rank_host);

@@ -761,13 +761,22 @@ MBX_API int mbx_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
     const size_t vs = mbx::value_size(m->precision);
     void* x = dmalloc(ctx, m->n_cols * vs + 256);
     void* y = dmalloc(ctx, m->n_rows * vs + 256);
-    if (m->n_cols) MBX_CUDA(cudaMemcpyAsync(x, x_host, m->n_cols * vs, cudaMemcpyHostToDevice, ctx->stream));
+    // a degree-relabelled matrix takes x and gives y in the original order
+    void* tmp = m->vmap ? dmalloc(ctx, std::max(m->n_rows, m->n_cols) * vs + 256) : nullptr;
+    if (m->n_cols)
+      MBX_CUDA(cudaMemcpyAsync(m->vmap ? tmp : x, x_host, m->n_cols * vs, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    if (m->vmap) mbx::launch_vertex_map(ctx, m->precision, m->n_cols, m->vmap, tmp, x, true);
     const mbx::Geometry g = mbx::make_geometry(ctx, m, t, c->block_size);
     void* ws = mbx::scratch(ctx, mbx::spmv_workspace_bytes(g, m->precision, false));
     mbx::launch_spmv(ctx, m, t, g, x, y, ws, nullptr);
-    if (m->n_rows) MBX_CUDA(cudaMemcpyAsync(y_host, y, m->n_rows * vs, cudaMemcpyDeviceToHost, ctx->stream));
+    if (m->vmap) mbx::launch_vertex_map(ctx, m->precision, m->n_rows, m->vmap, y, tmp, false);
+    if (m->n_rows)
+      MBX_CUDA(cudaMemcpyAsync(y_host, m->vmap ? tmp : y, m->n_rows * vs, cudaMemcpyDeviceToHost,
+                               ctx->stream));
     dfree(ctx, x);
     dfree(ctx, y);
+    dfree(ctx, tmp);
     MBX_CUDA(cudaStreamSynchronize(ctx->stream));
     if (trace) {
       int rc = mbx_spmv_trace_counts(ctx, t, trace);

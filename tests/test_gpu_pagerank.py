@@ -137,6 +137,11 @@ def test_degree_relabel_preprocessing(ctx):
     t = mb.generate_tile_for(Q, c)
     for got, want in zip(t.download(), O.generate_tile(qro, n, Q.nnz, 32, 14)):
         assert np.array_equal(got, want)
+    # host-facing SpMV on the relabelled matrix: x and y in the original order
+    x = O.hash_uniform(2, n, -1.0, 1.0, np.float32)
+    y = mb.spmv_merbit(Q, t, c, x, mb.DualBuffer(n, np.float32))
+    wy, mag = O.spmv_csr_f32_acc64(O.Csr(n, n, ro, cols, vals), x)
+    assert (np.abs(y.astype(np.float64) - wy) / np.where(mag > 0, mag, 1)).max() <= 1e-5
     be = type("B", (), {})()
     be.matrix, be.tile_, be.c = Q, t, c
     r = mb.pagerank(None, mb.PageRankConfig(0.85, 1e-30, 50, 0), backend=be)
