@@ -936,27 +936,32 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
     T xv[SIGMA], v[SIGMA];
     gather_slots<T, SIGMA, HUB>(p.x, hub, col, rmask, xv);
     load_slot_vals<T, SIGMA>(vb, lid, v, pol);
-    // per-lane walk (Alg. 4, merbit_spmv.hpp:251-297) in registers
-    int r = r0;
+    // per-lane walk (Alg. 4, merbit_spmv.hpp:251-297) in registers, as
+    // predicated selects (no divergent branches per step): a Down step
+    // closes a row -- the lane's first closure is its head, later ones are
+    // rows opened and closed inside the lane -- and a Right step adds its
+    // product; rows beyond the commit buffer go straight to y (raw sums,
+    // PageRank update below)
     T sum = T(0), head = T(0);
     bool had_down = false;
+    auto walk = [&](T* sink) {
+      int r = r0;
 #pragma unroll
-    for (int i = 0; i < SIGMA; ++i) {
-      if ((dmask >> i) & 1u) {
-        if (!had_down) {
-          head = sum;
-          had_down = true;
-        } else if (!direct) {
-          rowbuf[r] = sum;  // row opened and closed inside this lane
-        } else {
-          p.y[int64_t(y0) + r] = sum;  // raw row sum; PR update below
-        }
-        sum = T(0);
-        ++r;
-      } else if ((rmask >> i) & 1u) {
-        sum += mul_rn(v[i], xv[i]);
+      for (int i = 0; i < SIGMA; ++i) {
+        const bool dn = (dmask >> i) & 1u;
+        const bool rt = (rmask >> i) & 1u;
+        const T prod = mul_rn(v[i], xv[i]);
+        if (dn && had_down) sink[r] = sum;
+        head = (dn && !had_down) ? sum : head;
+        had_down = had_down || dn;
+        sum = dn ? T(0) : (rt ? sum + prod : sum);
+        r += dn ? 1 : 0;
       }
-    }
+    };
+    if (!direct)
+      walk(rowbuf);
+    else
+      walk(p.y + y0);
     T headv;
     carry = seg_scan<T>(sum, head, had_down, lid, carry, headv);
     if (!direct) {
