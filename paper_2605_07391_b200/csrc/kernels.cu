@@ -1151,12 +1151,26 @@ __global__ void __launch_bounds__(256) fixup_kernel(const uint32_t* __restrict__
     long_lanes &= long_lanes - 1;
     const int64_t e0 = __shfl_sync(kFull, e, src);
     const uint32_t rr = __shfl_sync(kFull, r, src);
+    // 128 carries per round trip: four independent loads per lane in
+    // flight, folded in a fixed (lane, round) order -> deterministic
     T part = T(0);
-    for (int64_t w = e0;; w += 32) {
-      const int64_t k = w + lid;
-      const bool in = k < ne && crow[k] == rr;
-      if (in) part += cval[k];
-      if (__ballot_sync(kFull, in) != kFull) break;
+    for (int64_t w = e0;; w += 128) {
+      uint32_t rk[4];
+      T vk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t k = w + 32 * j + lid;
+        rk[j] = k < ne ? crow[k] : ~rr;
+        vk[j] = k < ne ? cval[k] : T(0);
+      }
+      bool all_in = true;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool in = rk[j] == rr;
+        if (in) part += vk[j];
+        all_in = all_in && in;
+      }
+      if (__ballot_sync(kFull, all_in) != kFull) break;
     }
     part = __shfl_sync(kFull, warp_sum(part), 0);
     if (lid == src) sum = part;
