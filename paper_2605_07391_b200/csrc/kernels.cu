@@ -1,20 +1,26 @@
 // kernels.cu -- the sm_100a kernels of the MERBIT hot path.
 //
 //  K1 gen_tile_kernel      generate_tile (src/tile.cpp:17-85; paper Alg. 2)
-//  K2 spmv_w32_kernel      spmv_merbit tile loop (merbit_spmv.hpp:182-324;
-//     spmv_generic_kernel  paper Alg. 3-5), commit fused with the PageRank
-//                          update (solvers.hpp:99-115) in PR mode
+//  K2 spmv_slot_kernel     spmv_merbit tile loop (merbit_spmv.hpp:182-324;
+//                          paper Alg. 3-5) over the lane-major slot copy
+//                          (default: omega 32, default sigma)
+//     spmv_w32_kernel      the same over CSR order staged through shared
+//                          memory (any sigma at omega 32; layout 0)
+//     spmv_generic_kernel  any omega (the reference's small test configs)
+//                          -- all three fuse the PageRank update
+//                          (solvers.hpp:99-115) into the commit in PR mode
 //  K3 fixup_kernel         ordered boundary-carry fold (merbit_spmv.hpp:
 //                          328-337) + PageRank scalar finalisation
 //  csr_kernel              spmv_csr_reference (reference.hpp:15-46): the
 //                          pagerank yardstick (solvers.hpp:178-191)
 //
-// Design: SpMV is HBM-bound integer/fp gather work, so no
-// tensor cores.  Values/columns stream once with 128-bit non-allocating
-// loads tagged L2 evict-first; x is gathered through the read-only path and
-// kept L2-resident (evict-normal); every row of y is ASSIGNED exactly once
-// (interior rows by the warp that closes them, boundary rows by K3), so no
-// zero-fill, no atomics, and bitwise run-to-run determinism.
+// Design: SpMV is gather-bound integer/fp work, so no tensor
+// cores.  Values/columns stream once with non-allocating loads tagged L2
+// evict-first; x is gathered through the read-only path and kept
+// L2-resident, its most referenced entries staged in shared memory (the hub
+// table); every row of y is ASSIGNED exactly once (interior rows by the warp
+// that closes them, boundary rows by K3), so no zero-fill, no atomics, and
+// bitwise run-to-run determinism.
 #include <cfloat>
 #include <cmath>
 
