@@ -266,7 +266,8 @@ def main():
 
     import paper_2605_07391_b200 as mb
     from paper_2605_07391_b200 import _lib
-    from paper_2605_07391_b200.merbit import ShardGroup, nccl_unique_id, row_slice
+    from paper_2605_07391_b200.merbit import (ShardGroup, nccl_unique_id, pagerank_row_weight,
+                                              row_slice)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -322,7 +323,8 @@ def main():
         pre_ms = (relabel_s + tile.preprocess_seconds + xc_s + P.slot_info()[1]) * 1e3
     else:
         ro_host, _, _ = P.download(want_values=False)
-        bounds = mb.plan_row_shards(ro_host, n, m, world)
+        row_w = pagerank_row_weight(n, 4)
+        bounds = mb.plan_row_shards(ro_host, n, m, world, row_w)
         Lm = row_slice(P, int(bounds[rank]), int(bounds[rank + 1]))
         del P, P_natural
         P_natural = None
@@ -447,7 +449,8 @@ def main():
                                + ("degree-relabelled on the device as preprocessing, pi "
                                   "returned in the original order" if args.vertex_order ==
                                   "degree" else "natural") + "), preprocessing amortised"
-                               + (f", {world} row shards + NCCL all-gather" if world > 1 else ""),
+                               + (f", {world} row shards (row weight {row_w}) + NCCL all-gather"
+                                  if world > 1 else ""),
                    "scale": scale, "n": n, "nnz": m, "omega": 32, "sigma": 14,
                    "block_size": args.block_size,
                    "l2": "inputs (values+cols %.1f GB per GPU) larger than L2; no flush"

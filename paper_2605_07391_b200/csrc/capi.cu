@@ -360,6 +360,34 @@ MBX_API int mbx_plan_row_shards(const int64_t* ro, int64_t n_rows, int64_t nnz, 
   });
 }
 
+MBX_API int mbx_plan_row_shards_weighted(const int64_t* ro, int64_t n_rows, int64_t nnz,
+                                         int parts, double row_weight, int64_t* bounds) {
+  if (row_weight == 1.0) return mbx_plan_row_shards(ro, n_rows, nnz, parts, bounds);
+  return guarded([&] {
+    require(parts >= 1, MBX_CONFIG_ERROR, "parts must be >= 1");
+    require(row_weight >= 0.0 && row_weight < 1e9, MBX_CONFIG_ERROR,
+            "row_weight must be in [0, 1e9)");
+    require(n_rows >= 0 && ro[n_rows] == nnz, MBX_DIMENSION_ERROR,
+            "row_offsets[n_rows] != nnz");
+    const double total = static_cast<double>(nnz) + row_weight * static_cast<double>(n_rows);
+    bounds[0] = 0;
+    for (int g = 1; g < parts; ++g) {
+      const double target = total * g / parts;
+      // smallest r with ro[r] + w*r >= target (cost is nondecreasing in r)
+      int64_t lo = 0, hi = n_rows;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (static_cast<double>(ro[mid]) + row_weight * static_cast<double>(mid) < target)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      bounds[g] = std::max(bounds[g - 1], lo);
+    }
+    bounds[parts] = n_rows;
+  });
+}
+
 MBX_API int mbx_device_count(int* count) {
   return guarded([&] {
     int n = 0;

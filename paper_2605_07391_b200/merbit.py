@@ -151,10 +151,27 @@ def merge_search(row_offsets, n_rows: int, nnz: int, diag: int):
     return x.value, y.value
 
 
-def plan_row_shards(row_offsets, n_rows: int, nnz: int, parts: int) -> np.ndarray:
+# Cost of one row's PageRank commit in nonzeros: least-squares fit of per-shard
+# K2 times at R-MAT s24 over 32 shards (t ~ 3.2 ns/nnz + 10.9 ns/row + 20 us).
+PAGERANK_ROW_WEIGHT = 3.4
+
+
+def pagerank_row_weight(n_vertices: int, value_bytes: int = 4) -> float:
+    """Row weight for plan_row_shards.  Once pi no longer sits in L2 (s27:
+    512 MB) each gathered nonzero costs more relative to a row's commit; the
+    measured best cut there is ~2.5 (slowest of 8 shards 1.37 ms vs 1.43 ms at
+    3.4), at s24 (64 MB of pi) 3.4 (0.159 ms vs 0.257 ms at the merge-path 1.0)."""
+    return PAGERANK_ROW_WEIGHT if n_vertices * value_bytes <= (96 << 20) else 2.5
+
+
+def plan_row_shards(row_offsets, n_rows: int, nnz: int, parts: int,
+                    row_weight: float = 1.0) -> np.ndarray:
+    """Row bounds of `parts` shards.  row_weight 1.0 is the merge-path cut
+    (mbx_plan_row_shards); other weights cut ro[r] + row_weight * r evenly."""
     ro = np.ascontiguousarray(row_offsets, np.int64)
     out = np.zeros(parts + 1, np.int64)
-    _check(_lib.lib().mbx_plan_row_shards(_ptr(ro), n_rows, nnz, parts, _ptr(out)))
+    _check(_lib.lib().mbx_plan_row_shards_weighted(_ptr(ro), n_rows, nnz, parts,
+                                                   float(row_weight), _ptr(out)))
     return out
 
 

@@ -1,4 +1,5 @@
-"""L2 hot-head probe: PageRank fp32 on the degree-relabelled R-MAT at a scale
+"""(Historical: needs the mbx_context_set_l2_hot knob, measured and reverted.)
+L2 hot-head probe: PageRank fp32 on the degree-relabelled R-MAT at a scale
 with the x gathers of the first H columns marked L2 evict_last (the rest
 evict_first), for several H (0 = plain gathers, -1 = auto)."""
 import argparse

@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=27)
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--parts", default="2,4,8")
+ap.add_argument("--row-weight", type=float, default=0.0, help="0: pagerank_row_weight(n)")
 args = ap.parse_args()
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
@@ -45,6 +46,24 @@ def timed(fn):
     return e0.elapsed_time(e1) / args.iters
 
 
+def shard_kernel_ms(fn, g):
+    """Per-shard device time of one iteration (its K2 + K3 + the shared
+    combine), from CUPTI kernel records of a warm run (not replayed)."""
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    ev.sort(key=lambda e: e.time_range.start)
+    names = [e.name for e in ev]
+    dur = [e.time_range.elapsed_us() / 1e3 for e in ev]
+    # last iteration: the final combine and the g (K2, K3) pairs before it
+    last = max(i for i, nm in enumerate(names) if "combine" in nm)
+    k = [i for i in range(last) if "spmv_slot" in names[i] or "fixup" in names[i]][-2 * g:]
+    comb = dur[last]
+    return [dur[k[2 * r]] + dur[k[2 * r + 1]] + comb for r in range(g)]
+
+
 t = mb.generate_tile_for(P, c)
 P.build_xcache()
 plan = mb.PageRankPlan(P, t, c, cfg)
@@ -57,20 +76,25 @@ del cols
 out = {"scale": args.scale, "n": n, "nnz": m, "single_gpu_ms_per_iter": single,
        "nondangling_vertices": nondangling}
 for g in [int(x) for x in args.parts.split(",")]:
-    bounds = mb.plan_row_shards(ro, n, m, g)
+    w = args.row_weight or mb.merbit.pagerank_row_weight(n)
+    bounds = mb.plan_row_shards(ro, n, m, g, w)
     shards = []
     for r in range(g):
         L = row_slice(P, int(bounds[r]), int(bounds[r + 1]))
         shards.append((L, mb.generate_tile_for(L, c)))
     grp = ShardGroup(ctx, n, g, bounds, 0, shards, c, cfg, None)
     virt = timed(grp.run)
+    per_shard = shard_kernel_ms(grp.run, g)
     grp.close()
     del grp, shards
     torch.cuda.synchronize()
     xbytes = nondangling * 4 * (g - 1) / g  # received per GPU per iteration
     exch = xbytes / 770e9 * 1e3
-    proj = virt / g + exch + 0.02  # + NCCL/launch latency allowance
-    out[f"G{g}"] = {"virtual_all_shards_ms_per_iter": virt, "per_gpu_compute_ms": virt / g,
+    slowest = max(per_shard)
+    proj = slowest + exch + 0.02  # + NCCL/launch latency allowance
+    out[f"G{g}"] = {"virtual_all_shards_ms_per_iter": virt, "mean_gpu_compute_ms": virt / g,
+                    "shard_kernel_ms": [round(v, 4) for v in per_shard],
+                    "per_gpu_compute_ms": slowest,
                     "exchange_ms_at_770GBps": exch, "projected_ms_per_iter": proj,
                     "projected_speedup": single / proj}
 print(json.dumps(out))

@@ -113,6 +113,23 @@ def test_row_shards_are_merge_path_balanced(parts):
     assert max(abs(w - target) for w in work) <= longest  # off by at most one row
 
 
+@pytest.mark.parametrize("weight", [0.0, 1.0, 3.4, 16.0])
+@pytest.mark.parametrize("parts", [1, 2, 5, 8])
+def test_weighted_row_shards(parts, weight):
+    p = O.rmat(14, 16, 5, transposed=True)
+    ro = p.row_offsets
+    b = mb.plan_row_shards(ro, p.n_rows, p.nnz, parts, weight)
+    assert b[0] == 0 and b[-1] == p.n_rows and np.all(np.diff(b) >= 0)
+    if weight == 1.0:  # exactly the merge-path cut
+        assert np.array_equal(b, mb.plan_row_shards(ro, p.n_rows, p.nnz, parts))
+    cost = [(ro[b[g + 1]] - ro[b[g]]) + weight * (b[g + 1] - b[g]) for g in range(parts)]
+    target = (p.nnz + weight * p.n_rows) / parts
+    longest = int(np.diff(ro).max()) + weight
+    assert max(abs(c - target) for c in cost) <= longest + 1e-9
+    with pytest.raises(mb.ConfigError):
+        mb.plan_row_shards(ro, p.n_rows, p.nnz, parts, -1.0)
+
+
 def test_no_gpu_means_loud_failure():
     try:
         import torch

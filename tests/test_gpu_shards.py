@@ -13,9 +13,9 @@ from paper_2605_07391_b200.merbit import ShardGroup, row_slice
 pytestmark = pytest.mark.gpu
 
 
-def sharded_pagerank(ctx, P, parts, iters, c):
+def sharded_pagerank(ctx, P, parts, iters, c, row_weight=1.0):
     ro, _, _ = P.download(want_values=False)
-    b = mb.plan_row_shards(ro, P.n_rows, P.nnz, parts)
+    b = mb.plan_row_shards(ro, P.n_rows, P.nnz, parts, row_weight)
     shards = []
     for g in range(parts):
         m = row_slice(P, int(b[g]), int(b[g + 1]))
@@ -27,12 +27,13 @@ def sharded_pagerank(ctx, P, parts, iters, c):
     return grp.gather_pi(), res, hist, b
 
 
+@pytest.mark.parametrize("row_weight", [1.0, mb.merbit.PAGERANK_ROW_WEIGHT])
 @pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
-def test_sharded_matches_fp64_oracle_and_single_gpu(ctx, parts):
+def test_sharded_matches_fp64_oracle_and_single_gpu(ctx, parts, row_weight):
     P = mb.DeviceMatrix.rmat(ctx, 14, 16, seed=7, transition=True, dtype=np.float32)
     ro, cols, _ = P.download(want_values=False)
     c = mb.SimtConfig.make(32, 14, 128)
-    pi, res, hist, b = sharded_pagerank(ctx, P, parts, 60, c)
+    pi, res, hist, b = sharded_pagerank(ctx, P, parts, 60, c, row_weight)
     assert res.iterations == 60
     p64 = O.Csr(P.n_rows, P.n_cols, ro, cols, O.transition_values(P.n_rows, cols, np.float64))
     want = O.pagerank(p64, 0.85, 1e-300, 60, 0, nthreads=8)
@@ -49,7 +50,7 @@ def test_sharded_matches_fp64_oracle_and_single_gpu(ctx, parts):
         # one shard is the single-GPU computation: bitwise identical
         assert np.array_equal(pi.view(np.uint32), single.pi.view(np.uint32))
     # deterministic run to run
-    pi2, _, _, _ = sharded_pagerank(ctx, P, parts, 60, c)
+    pi2, _, _, _ = sharded_pagerank(ctx, P, parts, 60, c, row_weight)
     assert np.array_equal(pi.view(np.uint32), pi2.view(np.uint32))
 
 
