@@ -62,6 +62,21 @@ def traffic_per_launch():
         return None
 
 
+def gather_ceiling():
+    """Measured ceiling of scattered 4-byte gathers from an L2-resident array
+    (scripts/micro/dsmem_gather.cu, case global_64MB, all 148 SMs) -- the
+    bound of an SpMV whose x is gathered at random (null when absent)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1s2_dsmem_gather.jsonl")) as f:
+            for line in f:
+                d = json.loads(line)
+                if d.get("case") == "global_64MB":
+                    return float(d["gathers_per_s"])
+    except Exception:
+        pass
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -317,6 +332,7 @@ def main():
     if world == 1:
         tile = mb.generate_tile_for(P, cfg)
         xc_s = P.build_xcache()  # x hub cache: preprocessing, next to the TILE
+        hub_cov = P.xcache_info()[1]
         runner = mb.PageRankPlan(P, tile, cfg, prc)  # builds the K2 slot copy once
         local_rows, local_nnz = n, m
         run = runner.run
@@ -324,6 +340,7 @@ def main():
     else:
         ro_host, _, _ = P.download(want_values=False)
         row_w = pagerank_row_weight(n, 4)
+        hub_cov = None  # the shard group builds its own hub tables
         bounds = mb.plan_row_shards(ro_host, n, m, world, row_w)
         Lm = row_slice(P, int(bounds[rank]), int(bounds[rank + 1]))
         del P, P_natural
@@ -361,6 +378,17 @@ def main():
     t_iter_local = ms_local * 1e-3 / (args.iters * args.steps)
     b_iter = 8 * local_nnz + 16 * local_rows + 4
     achieved = b_iter / t_iter_local / 1e9
+    ceil = gather_ceiling()
+    gather_bound = None
+    if hub_cov is not None and ceil:
+        # every nonzero outside the shared-memory hub table is one scattered
+        # x gather (one 32-B L1->L2 request); this, not DRAM, bounds K2 on R-MAT
+        g_iter = local_nnz * (1.0 - hub_cov)
+        gather_bound = {"gathers_per_iteration": g_iter, "hub_coverage": hub_cov,
+                        "achieved_per_s": g_iter / t_iter_local, "ceiling_per_s": ceil,
+                        "frac": g_iter / t_iter_local / ceil,
+                        "ceiling_source": "profiles/r1s2_dsmem_gather.jsonl global_64MB "
+                                          "(scattered 4-B gathers, L2-resident, 148 SMs)"}
 
     # e2e with pinned host buffers inside the timed region
     if world == 1:
@@ -459,7 +487,8 @@ def main():
                      "frac": achieved / peak, "traffic": traffic_per_launch(), "peak_kind": peak_kind,
                      "kernel": "fused PageRank iteration (spmv_slot_kernel<float,14,PR,HUB> + "
                                "fixup_kernel) on rank 0",
-                     "bytes_per_launch": b_iter, "us_per_iteration": t_iter_local * 1e6},
+                     "bytes_per_launch": b_iter, "us_per_iteration": t_iter_local * 1e6,
+                     "gather_bound": gather_bound},
         "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "mass": mass},
         "gpu_launches": launches,
