@@ -429,9 +429,11 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
     p->ro = static_cast<uint32_t*>(dm((n + 1) * 4 + 64, true));
     MBX_CUDA(cudaMemsetAsync(p->vals, 0, m * vs + 256, s));
     MBX_CUDA(cudaMemsetAsync(p->cols, 0, m * 4 + 256, s));
-    auto* rows = static_cast<int64_t*>(dm(m * 8 + 8));
+    // the sort's input keys are dead after the sort: their buffer takes the
+    // decoded row ids (2 GB less to allocate at s24)
+    auto* keys = static_cast<unsigned long long*>(dm(m * 8 + 8));
+    auto* rows = reinterpret_cast<int64_t*>(keys);
     if (m) {
-      auto* keys = static_cast<unsigned long long*>(dm(m * 8 + 8));
       auto* keys2 = static_cast<unsigned long long*>(dm(m * 8 + 8));
       mbx::relabel_keys_kernel<<<grid, 256, 0, s>>>(a->ro, a->cols, n, rank, keys);
       const unsigned long long span = (unsigned long long)n * (unsigned long long)n;
