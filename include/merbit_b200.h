@@ -318,13 +318,19 @@ MBX_API int mbx_bench_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile
  * power loop with the damping/teleport update, dangling redistribution, L1
  * residual, mass check and ERR fused into the SpMV commit; early exit when
  * ERR < err_tol.  pi0_host may be NULL (uniform 1/n, as the reference).
- * reference_pi_host / residual_history_host (max_iters doubles) may be NULL. */
+ * reference_pi_host / residual_history_host (max_iters doubles) may be NULL.
+ * The context keeps the call's plan (2 pi buffers, scalars, the captured
+ * power-loop graph) for the next call with the same matrix, TILE and configs;
+ * it is dropped when the matrix or TILE is destroyed, the tuning changes, or
+ * by mbx_context_release_cache. */
 MBX_API int mbx_pagerank(mbx_context* ctx, const mbx_matrix* p,
                          const mbx_tile* t, const mbx_simt_config* c,
                          const mbx_pagerank_config* cfg, const void* pi0_host,
                          void* pi_host, void* reference_pi_host,
                          double* residual_history_host,
                          mbx_pagerank_result* result);
+/* Free the plan mbx_pagerank keeps between calls (no-op when none). */
+MBX_API int mbx_context_release_cache(mbx_context* ctx);
 /* Reusable plan: device buffers, dangling mask and the CUDA graph of the
  * power loop are built once. */
 MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p,

@@ -70,6 +70,7 @@ SIGNATURES = {
     "mbx_metadata_footprint": ([C.c_int64, C.c_int64, C.POINTER(mbx_simt_config), C.c_double],
                                C.c_double),
     "mbx_merge_search": ([VP, C.c_int64, C.c_int64, C.c_int64, I64P, I64P], C.c_int),
+    "mbx_context_release_cache": ([VP], C.c_int),
     "mbx_plan_row_shards": ([VP, C.c_int64, C.c_int64, C.c_int, VP], C.c_int),
     "mbx_plan_row_shards_weighted": ([VP, C.c_int64, C.c_int64, C.c_int, C.c_double, VP], C.c_int),
     "mbx_device_count": ([C.POINTER(C.c_int)], C.c_int),

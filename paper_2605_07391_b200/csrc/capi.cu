@@ -90,6 +90,11 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
 using mbx::fail;
 
 namespace {
+void drop_pr_cache(mbx_context* ctx);
+bool pr_cache_refs(const mbx_context* ctx, const void* obj);
+}  // namespace
+
+namespace {
 
 template <typename F>
 int guarded(F&& f) {
@@ -430,6 +435,7 @@ MBX_API int mbx_context_destroy(mbx_context* ctx) {
   return guarded([&] {
     if (!ctx) return;
     Device dg(ctx->device);
+    drop_pr_cache(ctx);
     if (ctx->scratch) cudaFreeAsync(ctx->scratch, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
@@ -566,6 +572,8 @@ MBX_API int mbx_context_set_tuning_ex(mbx_context* ctx, int smem_per_sm, int pre
   return guarded([&] {
     ctx->tuning.smem_per_sm = smem_per_sm;
     ctx->tuning.prefetch = prefetch;
+    ++ctx->tuning_epoch;
+    drop_pr_cache(ctx);
   });
 }
 
@@ -577,6 +585,8 @@ MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta, int ctas
     ctx->tuning.warps_per_cta = warps_per_cta;
     ctx->tuning.ctas_per_sm = ctas_per_sm;
     ctx->tuning.max_hubs = max_hubs;
+    ++ctx->tuning_epoch;
+    drop_pr_cache(ctx);
   });
 }
 
@@ -584,6 +594,8 @@ MBX_API int mbx_context_set_layout(mbx_context* ctx, int layout) {
   return guarded([&] {
     require(layout == 0 || layout == 1, MBX_CONFIG_ERROR, "layout must be 0 or 1");
     ctx->tuning.layout = layout;
+    ++ctx->tuning_epoch;
+    drop_pr_cache(ctx);
   });
 }
 
@@ -633,6 +645,7 @@ MBX_API int mbx_matrix_destroy(mbx_matrix* m) {
     if (!m) return;
     mbx_context* ctx = m->ctx;
     Device dg(ctx->device);
+    if (pr_cache_refs(ctx, m)) drop_pr_cache(ctx);
     dfree(ctx, m->vals);
     dfree(ctx, m->cols);
     dfree(ctx, m->ro);
@@ -743,6 +756,7 @@ MBX_API int mbx_tile_destroy(mbx_tile* t) {
     if (!t) return;
     mbx_context* ctx = t->ctx;
     Device dg(ctx->device);
+    if (pr_cache_refs(ctx, t)) drop_pr_cache(ctx);
     dfree(ctx, t->tile_x);
     dfree(ctx, t->tile_y);
     dfree(ctx, t->lane_desc);
@@ -848,7 +862,37 @@ struct mbx_pagerank_plan_s {
   int64_t graph_launches = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   bool ran = false;
+  // cache key (mbx_pagerank): what the plan was built from
+  uint64_t p_version = 0, t_serial = 0, tuning_epoch = 0;
+  mbx_pagerank_config cfg_in{};
 };
+
+namespace {
+
+// drop the context's cached mbx_pagerank plan (if any)
+void drop_pr_cache(mbx_context* ctx) {
+  if (ctx->pr_cache) {
+    mbx_pagerank_plan* pl = ctx->pr_cache;
+    ctx->pr_cache = nullptr;
+    mbx_pagerank_plan_destroy(pl);
+  }
+}
+
+bool pr_cache_refs(const mbx_context* ctx, const void* obj) {
+  return ctx->pr_cache && (static_cast<const void*>(ctx->pr_cache->p) == obj ||
+                           static_cast<const void*>(ctx->pr_cache->t) == obj);
+}
+
+bool same_config(const mbx_simt_config& a, const mbx_simt_config& b) {
+  return a.omega == b.omega && a.sigma == b.sigma && a.block_size == b.block_size;
+}
+
+bool same_config(const mbx_pagerank_config& a, const mbx_pagerank_config& b) {
+  return a.damping == b.damping && a.err_tol == b.err_tol && a.max_iters == b.max_iters &&
+         a.reference_iters == b.reference_iters;
+}
+
+}  // namespace
 
 namespace {
 
@@ -1067,10 +1111,24 @@ MBX_API int mbx_pagerank(mbx_context* ctx, const mbx_matrix* p, const mbx_tile* 
                          const void* pi0_host, void* pi_host, void* ref_host, double* history,
                          mbx_pagerank_result* result) {
   return guarded([&] {
-    mbx_pagerank_plan* pl = nullptr;
-    int rc = mbx_pagerank_plan_create(ctx, p, t, c, cfg, &pl);
-    if (rc) fail(rc, g_last_error);
+    // reuse the context's plan when nothing it was built from has changed
+    mbx_pagerank_plan* pl = ctx->pr_cache;
+    if (!(pl && pl->p == p && pl->p_version == p->version && pl->t == t &&
+          pl->t_serial == t->serial && pl->tuning_epoch == ctx->tuning_epoch &&
+          same_config(pl->c, *c) && same_config(pl->cfg_in, *cfg))) {
+      drop_pr_cache(ctx);
+      pl = nullptr;
+      int rc = mbx_pagerank_plan_create(ctx, p, t, c, cfg, &pl);
+      if (rc) fail(rc, g_last_error);
+      pl->p_version = p->version;
+      pl->t_serial = t->serial;
+      pl->tuning_epoch = ctx->tuning_epoch;
+      pl->cfg_in = *cfg;
+    } else {
+      ctx->pr_cache = nullptr;  // owned by this call until it succeeds
+    }
     std::unique_ptr<mbx_pagerank_plan, int (*)(mbx_pagerank_plan*)> guard(pl, mbx_pagerank_plan_destroy);
+    int rc = 0;
     Device dg(ctx->device);
     // a degree-relabelled matrix keeps its vertex map: pi0 / pi / the
     // yardstick cross the boundary in the ORIGINAL vertex order
@@ -1113,6 +1171,16 @@ MBX_API int mbx_pagerank(mbx_context* ctx, const mbx_matrix* p, const mbx_tile* 
     dfree(ctx, pi0);
     dfree(ctx, tmp);
     MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    // kept for the next call (only for objects of this context: their
+    // destroy calls are what invalidate it)
+    if (p->ctx == ctx && t->ctx == ctx) ctx->pr_cache = guard.release();
+  });
+}
+
+MBX_API int mbx_context_release_cache(mbx_context* ctx) {
+  return guarded([&] {
+    Device dg(ctx->device);
+    drop_pr_cache(ctx);
   });
 }
 

@@ -114,6 +114,11 @@ struct mbx_context_s {
   void* host_scratch = nullptr;  // pinned staging
   size_t host_scratch_bytes = 0;
   mbx::Tuning tuning;
+  uint64_t tuning_epoch = 0;  // bumped by every tuning / layout change
+  // mbx_pagerank keeps its last plan (pi buffers, scalars, the captured
+  // power-loop graph) for the next call on the same matrix, TILE and
+  // configs; dropped when either is destroyed or by mbx_context_release_cache
+  struct mbx_pagerank_plan_s* pr_cache = nullptr;
 };
 
 struct mbx_matrix_s {

@@ -196,6 +196,10 @@ class Context:
     def set_stream(self, stream_ptr: int | None):
         _check(_lib.lib().mbx_context_set_stream(self.h, stream_ptr))
 
+    def release_cache(self):
+        """Free the plan pagerank() keeps between calls."""
+        _check(_lib.lib().mbx_context_release_cache(self.h))
+
     @property
     def stream(self) -> int:
         return _lib.lib().mbx_context_stream(self.h) or 0

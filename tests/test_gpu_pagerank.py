@@ -148,3 +148,45 @@ def test_degree_relabel_preprocessing(ctx):
     p64 = O.Csr(n, n, ro, cols, O.transition_values(n, cols, np.float64))
     want = O.pagerank(p64, 0.85, 1e-300, 50, 0)
     assert np.abs(r.pi.astype(np.float64) - want["pi"]).sum() <= 1e-6
+
+
+def test_pagerank_plan_cache(ctx):
+    """mbx_pagerank keeps its plan between calls: repeated calls are bitwise
+    equal, a changed config / tuning / matrix rebuilds it, and a destroyed
+    matrix never leaves a stale plan behind."""
+    def backend(P, c):
+        be = type("B", (), {})()
+        be.matrix, be.tile_, be.c = P, mb.generate_tile_for(P, c), c
+        return be
+
+    c = mb.SimtConfig.make(32, 14, 128)
+    P = mb.DeviceMatrix.rmat(ctx, 12, 16, seed=3, transition=True, dtype=np.float32)
+    be = backend(P, c)
+    cfg = mb.PageRankConfig(0.85, 1e-30, 30, 0)
+    a = mb.pagerank(None, cfg, backend=be)
+    b = mb.pagerank(None, cfg, backend=be)  # cached plan
+    assert np.array_equal(a.pi.view(np.uint32), b.pi.view(np.uint32))
+    assert a.iterations == b.iterations == 30
+    pi0 = np.random.default_rng(1).random(P.n_rows).astype(np.float32)
+    pi0 /= pi0.sum()
+    c0 = mb.pagerank(None, cfg, backend=be, pi0=pi0)  # same plan, other start
+    ctx.release_cache()
+    c1 = mb.pagerank(None, cfg, backend=be, pi0=pi0)  # fresh plan
+    assert np.array_equal(c0.pi.view(np.uint32), c1.pi.view(np.uint32))
+    d = mb.pagerank(None, mb.PageRankConfig(0.5, 1e-30, 7, 2), backend=be)  # new config
+    ctx.release_cache()
+    e = mb.pagerank(None, mb.PageRankConfig(0.5, 1e-30, 7, 2), backend=be)
+    assert d.iterations == e.iterations and np.array_equal(d.pi, e.pi)
+    ctx.set_tuning(32, 1, 0)  # no hub table: plan rebuilt, result unchanged
+    f = mb.pagerank(None, cfg, backend=be)
+    ctx.set_tuning(32, 1, -1)
+    assert np.array_equal(a.pi.view(np.uint32), f.pi.view(np.uint32))
+    # a new matrix (possibly at the freed address) gets its own plan
+    del be, P
+    Q = mb.DeviceMatrix.rmat(ctx, 11, 16, seed=4, transition=True, dtype=np.float32)
+    beq = backend(Q, c)
+    g = mb.pagerank(None, cfg, backend=beq)
+    ctx.release_cache()
+    h = mb.pagerank(None, cfg, backend=beq)
+    assert g.pi.shape == (Q.n_rows,)
+    assert np.array_equal(g.pi.view(np.uint32), h.pi.view(np.uint32))
