@@ -62,6 +62,16 @@ def test_s24_pagerank_l1_vs_fp64_oracle(ctx, s24):
     l1 = float(np.abs(r.pi.astype(np.float64) - want["pi"]).sum())
     assert r.iterations == 100 and l1 <= 1e-6, l1
     assert abs(r.mass - 1.0) <= 1e-5
+    # bench.py's own configuration: degree-relabelled on the device + hub
+    # table; pi comes back in the original vertex order, same gate
+    Q, _ = P.relabel_by_degree()
+    tq = mb.generate_tile_for(Q, c)
+    Q.build_xcache()
+    be.matrix, be.tile_ = Q, tq
+    rq = mb.pagerank(None, mb.PageRankConfig(0.85, 1e-30, 100, 0), backend=be)
+    l1q = float(np.abs(rq.pi.astype(np.float64) - want["pi"]).sum())
+    assert rq.iterations == 100 and l1q <= 1e-6, l1q
+    assert abs(rq.mass - 1.0) <= 1e-5
 
 
 def test_s24_spmv_f64_within_1e12(ctx):
@@ -115,3 +125,23 @@ def test_c5_stencil_64m_rows_exact_row_sums(ctx, dtype):
         total = si * kj * kk + sj * ki * kk + sk * ki * kj  # sum of all neighbour indices
         want = 27.0 * i.double() - total  # 26 * i - (total - i)
         assert torch.equal(y, want)
+
+
+def test_c3_powerlaw_fp64_full_size_within_1e12(ctx):
+    """BASELINE C3 at the bench's size (2^22 rows, fp64, Zipf rows up to n
+    nonzeros, exactly 10 % empty): y within 1e-12 of the fp64 CSR oracle
+    relative to sum |a||x| per row; empty rows exactly zero."""
+    log2n = 22
+    A = mb.DeviceMatrix.powerlaw(ctx, log2n, seed=3, dtype=np.float64)
+    ro, cols, vals = A.download()
+    n = 1 << log2n
+    c = mb.SimtConfig.make(32, 7, 128)
+    t = mb.generate_tile_for(A, c)
+    A.build_xcache()
+    x = O.hash_uniform(5, n, -1.0, 1.0, np.float64)
+    y = mb.spmv_merbit(A, t, c, x, mb.DualBuffer(n, np.float64))
+    want, mag = O.spmv_csr_f64(O.Csr(n, n, ro, cols, vals), x, nthreads=NT, want_abs=True)
+    assert (np.abs(y - want) / np.where(mag > 0, mag, 1.0)).max() <= 1e-12
+    lens = np.diff(ro)
+    assert int((lens == 0).sum()) == n // 10  # exactly 10 % empty rows
+    assert not y[lens == 0].any()
