@@ -444,6 +444,33 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global,
                                    const mbx_pagerank_config* cfg,
                                    const void* nccl_id,
                                    mbx_shard_group** out);
+/* Fused compute + exchange (no collective library on the iteration path):
+ * the PageRank commit of K2/K3 stores every non-dangling pi_new -- and K3
+ * the rank's scalar tail -- straight into every peer's exchange buffer
+ * (CUDA IPC mappings, NVLink/NVSwitch P2P stores), so the transfer overlaps
+ * the SpMV tile by tile; one device barrier per iteration (system-scope
+ * release/acquire epochs in peer memory, bounded: a missing peer fails the
+ * run instead of hanging) replaces the all-gather.  Setup is two-phase
+ * through the caller's bootstrap (MPI, torch.distributed, ...):
+ *   create_peer -> export (MBX_SHARD_BLOB_BYTES) -> all-gather the world's
+ *   blobs in rank order -> connect.
+ * One shard per group (this rank's rows).  Ranks may share a device (the
+ * 2-process test) or a process (peers of the same pid use raw pointers).
+ * run / result / gather_pi / download_local / destroy as above; destroy is
+ * collective (a final barrier). */
+#define MBX_SHARD_BLOB_BYTES 512
+MBX_API int mbx_shard_group_create_peer(mbx_context* ctx, int64_t n_global,
+                                        int world, const int64_t* row_bounds_host,
+                                        int rank, mbx_matrix* local_matrix,
+                                        mbx_tile* local_tile,
+                                        const mbx_simt_config* c,
+                                        const mbx_pagerank_config* cfg,
+                                        mbx_shard_group** out);
+MBX_API int mbx_shard_group_export(mbx_shard_group* group, void* blob);
+MBX_API int mbx_shard_group_connect(mbx_shard_group* group, const void* blobs);
+/* Peer groups: enqueue the final barrier without waiting (destroy does it
+ * and then waits); lets one thread retire several ranks' groups. */
+MBX_API int mbx_shard_group_quiesce(mbx_shard_group* group);
 /* pi0_dev: optional start vector (n_global entries on this device; each
  * shard reads its own rows); NULL = uniform 1/n like the reference. */
 MBX_API int mbx_shard_group_run(mbx_shard_group* group, const void* pi0_dev);

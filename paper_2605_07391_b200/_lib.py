@@ -149,6 +149,11 @@ SIGNATURES = {
     "mbx_shard_group_create": ([VP, C.c_int64, C.c_int, VP, C.c_int, C.c_int, VP, VP,
                                 C.POINTER(mbx_simt_config), C.POINTER(mbx_pagerank_config), VP,
                                 C.POINTER(VP)], C.c_int),
+    "mbx_shard_group_create_peer": ([VP, C.c_int64, C.c_int, VP, C.c_int, VP, VP, VP, VP, VP],
+                                    C.c_int),
+    "mbx_shard_group_export": ([VP, VP], C.c_int),
+    "mbx_shard_group_connect": ([VP, VP], C.c_int),
+    "mbx_shard_group_quiesce": ([VP], C.c_int),
     "mbx_shard_group_run": ([VP, VP], C.c_int),
     "mbx_shard_group_result": ([VP, C.POINTER(mbx_pagerank_result), VP], C.c_int),
     "mbx_shard_group_gather_pi": ([VP, VP], C.c_int),

@@ -224,7 +224,10 @@ __device__ __forceinline__ void pr_commit_v(const PrArgs& pr, T base, int64_t ro
   out[row] = pn;
   if (pr.xout) {  // row shards: the exchange copy of a non-dangling vertex
     const int32_t q = pr.xmap[row];
-    if (q >= 0) static_cast<T*>(pr.xout)[q] = pn;
+    if (q >= 0) {
+      static_cast<T*>(pr.xout)[q] = pn;
+      for (int k = 0; k < pr.npeer; ++k) static_cast<T*>(pr.xpeer[k])[q] = pn;  // NVLink
+    }
   }
   // |pn - po| is formed in T (the reference's own precision for pi) and
   // accumulated in fp64
@@ -337,6 +340,15 @@ __device__ void pr_block_finish(PrAcc a, const PrArgs& pr, double* block_part,
     out->dangling = d;
     out->mass = m;
     out->err = e;
+    for (int k = 0; k < pr.npeer; ++k) {  // the tail travels with the chunk
+      PrScalars* o = reinterpret_cast<PrScalars*>(
+          static_cast<char*>(pr.xpeer[k]) +
+          (reinterpret_cast<char*>(out) - static_cast<char*>(pr.xout)));
+      o->resid = r;
+      o->dangling = d;
+      o->mass = m;
+      o->err = e;
+    }
     if (check_stop && pr.stop) {
       if (m == 0.0) {
         *pr.stop = 2;  // zero-norm iterate (solvers.hpp:202-205)

@@ -98,6 +98,12 @@ struct PrArgs {
   // xmap[row] (>= 0) of the compacted exchange buffer xout.
   void* xout = nullptr;
   const int32_t* xmap = nullptr;
+  // Fused exchange (peer shard groups): the same store goes to the npeer
+  // peers' exchange buffers (same layout as xout, mapped over NVLink with
+  // CUDA IPC), and K3's scalar tail follows at the same offset.
+  static constexpr int kMaxPeers = 7;
+  int npeer = 0;
+  void* xpeer[kMaxPeers] = {};
 };
 
 }  // namespace mbx

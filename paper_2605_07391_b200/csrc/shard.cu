@@ -23,6 +23,7 @@
 // GPU (tests/test_gpu_shards.py).
 #include <cub/cub.cuh>
 #include <dlfcn.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -213,6 +214,65 @@ __global__ void slice_rows_kernel(const uint32_t* __restrict__ ro, int64_t r0, i
     out[i] = ro[r0 + i] - ro[r0];
 }
 
+// ---- fused exchange (peer shard groups) ------------------------------------
+struct PeerFlags {
+  uint64_t* f[8];  // every rank's epoch array (own included), mapped
+  int world = 1;
+  int rank = 0;
+};
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Device barrier across the group: publish this rank's epoch in every
+// rank's flag array (release, system scope: the NVLink stores of the
+// preceding K2/K3 are ordered before it), then wait until every rank has
+// published it here (acquire).  Skipped once the run has stopped -- every
+// rank reaches the same stop decision at the same iteration.  Bounded: a
+// peer that never arrives sets *err instead of hanging the GPU.
+__global__ void peer_barrier_kernel(PeerFlags pf, const uint64_t* __restrict__ base, int slot,
+                                    const int* stop, int* err) {
+  if (threadIdx.x != 0) return;
+  if (stop && *stop) return;
+  const uint64_t epoch = *base + uint64_t(slot);
+  __threadfence_system();
+  for (int k = 0; k < pf.world; ++k)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pf.f[k] + pf.rank), "l"(epoch)
+                 : "memory");
+  const uint64_t t0 = globaltimer_ns();
+  for (int k = 0; k < pf.world; ++k) {
+    while (true) {
+      uint64_t v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(pf.f[pf.rank] + k)
+                   : "memory");
+      if (v >= epoch) break;
+      if (globaltimer_ns() - t0 > 30ull * 1000000000ull) {
+        atomicExch(err, 1);
+        return;
+      }
+      __nanosleep(128);
+    }
+  }
+}
+
+__global__ void bump_epoch_kernel(uint64_t* base, uint64_t step) { *base += step; }
+
+// global column flags = OR over the ranks' own flags (read over NVLink)
+struct SeenPtrs {
+  const uint8_t* p[8];
+};
+__global__ void seen_or_kernel(SeenPtrs sp, int world, int64_t n, uint8_t* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    uint8_t v = 0;
+    for (int k = 0; k < world; ++k) v |= sp.p[k][i];
+    out[i] = v;
+  }
+}
+
 struct Shard {
   int g = 0;
   int li = 0;  // local index (slot in the group's local-row buffers)
@@ -253,6 +313,20 @@ struct mbx_shard_group_s {
   mbx_pagerank_config cfg{};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   bool ran = false;
+  // ---- fused exchange (mbx_shard_group_create_peer / _connect) ----
+  bool peer = false, connected = false, quiesced = false;
+  mbx_matrix* pmat = nullptr;  // the rank's shard, kept for connect
+  mbx_tile* ptile = nullptr;
+  uint8_t* seen = nullptr;     // this rank's column flags (shared with the peers)
+  uint64_t* pflags = nullptr;  // epochs published by the world (shared)
+  uint64_t* run_base = nullptr;
+  int* perr = nullptr;
+  void* xpeer[2][8] = {};      // every rank's exchange buffer (own = pi[i])
+  void* lpeer[2][8] = {};      // every rank's local rows (own = loc[i])
+  uint8_t* speer[8] = {};
+  mbx::PeerFlags pf{};
+  std::vector<void*> opened;   // IPC mappings to close
+  int64_t epoch_step = 0;
 };
 
 namespace {
@@ -277,10 +351,30 @@ void* dm(mbx_context* ctx, size_t b) {
   return p;
 }
 
+// IPC-shareable allocation (cudaIpcGetMemHandle needs a cudaMalloc base)
+void* dm_shared(size_t b) {
+  void* p = nullptr;
+  MBX_CUDA(cudaMalloc(&p, std::max<size_t>(b, 256)));
+  MBX_CUDA(cudaMemset(p, 0, std::max<size_t>(b, 256)));
+  return p;
+}
+
+// barrier slots of one run: 0 = entry, 1 + r = after iteration r (r >= 0)
+void peer_barrier(mbx_shard_group* G, int slot) {
+  mbx_context* ctx = G->ctx;
+  mbx::peer_barrier_kernel<<<1, 32, 0, ctx->stream>>>(G->pf, G->run_base, slot,
+                                                      slot > 1 ? G->flags : nullptr, G->perr);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
 void exchange_and_combine(mbx_shard_group* G, int slot, int iter) {
   mbx_context* ctx = G->ctx;
   unsigned char* base = static_cast<unsigned char*>(G->pi[slot]);
-  if (G->comm) {
+  if (G->peer) {
+    // the chunk already went out with the commit: wait for every rank's
+    peer_barrier(G, 1 + iter);
+  } else if (G->comm) {
     // in-place all-gather: each rank's chunk (pi rows + scalar tail)
     MBX_NCCL(mbx::nccl().AllGather(base + int64_t(G->rank0) * G->chunk_bytes, base, G->chunk_bytes,
                            ncclUint8, G->comm, ctx->stream));
@@ -310,6 +404,9 @@ void launch_iteration(mbx_shard_group* G, int64_t r) {
     a.next = reinterpret_cast<mbx::PrScalars*>(xnew + G->tail_off);
     a.xout = G->pi[dst];
     a.xmap = s.xmap;
+    if (G->peer)
+      for (int k = 0; k < G->world; ++k)
+        if (k != G->rank0) a.xpeer[a.npeer++] = G->xpeer[dst][k];
     a.range_part = s.range_part;
     a.block_part = s.block_part;
     a.done_counter = s.counter;
@@ -321,6 +418,240 @@ void launch_iteration(mbx_shard_group* G, int64_t r) {
     mbx::launch_spmv(ctx, &s.view, s.tile, s.geo, G->pi[src], pnew, s.carry_ws, &a);
   }
   exchange_and_combine(G, dst, int(r));
+}
+
+// validation + the fields and buffers every mode shares
+void group_init(mbx_shard_group* G, mbx_context* ctx, int64_t n_global, int world,
+                const int64_t* bounds, int rank0, int nlocal, mbx_matrix* const* mats,
+                const mbx_simt_config* c, const mbx_pagerank_config* cfg, bool peer) {
+  if (world < 1 || nlocal < 1 || rank0 < 0 || rank0 + nlocal > world)
+    mbx::fail(MBX_CONFIG_ERROR, "shard group: bad world/rank/nlocal");
+  if (cfg->reference_iters != 0)
+    mbx::fail(MBX_UNSUPPORTED, "shard group: the yardstick run (reference_iters > 0) is "
+                               "single-GPU only");
+  if (!(cfg->damping >= 0.0 && cfg->damping <= 1.0))
+    mbx::fail(MBX_CONFIG_ERROR, "damping must lie in [0, 1]");
+  if (!(cfg->err_tol > 0.0)) mbx::fail(MBX_CONFIG_ERROR, "err_tol must be positive");
+  if (cfg->max_iters < 0) mbx::fail(MBX_CONFIG_ERROR, "iteration counts must be >= 0");
+  if (bounds[0] != 0 || bounds[world] != n_global)
+    mbx::fail(MBX_DIMENSION_ERROR, "row bounds must cover [0, n)");
+  for (int g = 0; g < world; ++g)
+    if (bounds[g + 1] < bounds[g]) mbx::fail(MBX_DIMENSION_ERROR, "row bounds must not decrease");
+  G->ctx = ctx;
+  G->precision = mats[0]->precision;
+  G->vs = mbx::value_size(G->precision);
+  G->world = world;
+  G->rank0 = rank0;
+  G->nlocal = nlocal;
+  G->n = n_global;
+  G->peer = peer;
+  G->bounds.assign(bounds, bounds + world + 1);
+  G->c = *c;
+  G->cfg = *cfg;
+  if (G->precision == MBX_F32) {
+    G->cfg.damping = double(float(cfg->damping));
+    G->cfg.err_tol = double(float(cfg->err_tol));
+  }
+  int64_t rows_max = 0;
+  for (int g = 0; g < world; ++g) rows_max = std::max(rows_max, bounds[g + 1] - bounds[g]);
+  G->lchunk_bytes = ((rows_max * int64_t(G->vs) + 255) / 256) * 256 + 256;
+  cudaStream_t st = ctx->stream;
+  for (int i = 0; i < 2; ++i) {
+    if (peer) {
+      G->loc[i] = dm_shared(G->lchunk_bytes * nlocal);
+    } else {
+      G->loc[i] = dm(ctx, G->lchunk_bytes * nlocal);
+      MBX_CUDA(cudaMemsetAsync(G->loc[i], 0, G->lchunk_bytes * nlocal, st));
+    }
+  }
+  G->gscal = static_cast<mbx::PrScalars*>(dm(ctx, (cfg->max_iters + 1) * sizeof(mbx::PrScalars)));
+  MBX_CUDA(cudaMemsetAsync(G->gscal, 0, (cfg->max_iters + 1) * sizeof(mbx::PrScalars), st));
+  G->flags = static_cast<int*>(dm(ctx, 64));
+  MBX_CUDA(cudaMemsetAsync(G->flags, 0, 64, st));
+}
+
+// column flags of this process's shards (dangling = no rank sets the flag)
+void local_seen(mbx_shard_group* G, mbx_matrix* const* mats, uint8_t* seen) {
+  mbx_context* ctx = G->ctx;
+  for (int i = 0; i < G->nlocal; ++i)
+    if (mats[i]->nnz)
+      mbx::seen_flags_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, ctx->stream>>>(
+          mats[i]->cols, mats[i]->nnz, seen);
+  ctx->launches += G->nlocal;
+  MBX_CUDA(cudaGetLastError());
+}
+
+// compacted exchange layout from the GLOBAL column flags, then every local
+// shard's remapped view, TILE geometry and PageRank workspaces.  chunk_fixed
+// > 0 (peer mode): the chunk stride was fixed before the flags were known.
+void group_layout(mbx_shard_group* G, mbx_matrix* const* mats, mbx_tile* const* tiles,
+                  const uint8_t* seen, int64_t chunk_fixed) {
+  mbx_context* ctx = G->ctx;
+  cudaStream_t st = ctx->stream;
+  const int world = G->world;
+  const int64_t n_global = G->n;
+  const mbx_simt_config* c = &G->c;
+  int64_t* dbounds = static_cast<int64_t*>(dm(ctx, (world + 1) * 8));
+  MBX_CUDA(cudaMemcpyAsync(dbounds, G->bounds.data(), (world + 1) * 8, cudaMemcpyHostToDevice, st));
+  // gpre = exclusive scan of the global flags
+  int64_t* gpre = static_cast<int64_t*>(dm(ctx, (n_global + 1) * 8));
+  {
+    int64_t* cnt = static_cast<int64_t*>(dm(ctx, (n_global + 1) * 8));
+    MBX_CUDA(cudaMemsetAsync(cnt, 0, (n_global + 1) * 8, st));
+    mbx::seen_to_count_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, st>>>(seen, n_global, cnt);
+    size_t tb = 0;
+    MBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, gpre, n_global + 1, st));
+    void* tmp = dm(ctx, tb);
+    MBX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, gpre, n_global + 1, st));
+    cudaFreeAsync(tmp, st);
+    cudaFreeAsync(cnt, st);
+    ctx->launches += 2;
+  }
+  if (chunk_fixed > 0) {
+    G->chunk_bytes = chunk_fixed;
+    G->tail_off = chunk_fixed - 256;
+  } else {
+    // chunk = the largest per-rank non-dangling count (+ the scalar tail)
+    std::vector<int64_t> gb(world + 1);
+    for (int g = 0; g <= world; ++g)
+      MBX_CUDA(cudaMemcpyAsync(&gb[g], gpre + G->bounds[g], 8, cudaMemcpyDeviceToHost, st));
+    MBX_CUDA(cudaStreamSynchronize(st));
+    int64_t nd_max = 0;
+    for (int g = 0; g < world; ++g) nd_max = std::max(nd_max, gb[g + 1] - gb[g]);
+    G->tail_off = ((nd_max * int64_t(G->vs) + 255) / 256) * 256;
+    G->chunk_bytes = G->tail_off + 256;
+  }
+  G->chunk_elems = G->chunk_bytes / int64_t(G->vs);
+  if (G->chunk_elems * world >= (int64_t(1) << 31))
+    mbx::fail(MBX_CAPACITY_ERROR, "exchange layout exceeds int32 column indices");
+  if (!G->peer) {
+    for (int i = 0; i < 2; ++i) {
+      G->pi[i] = dm(ctx, G->chunk_bytes * world);
+      MBX_CUDA(cudaMemsetAsync(G->pi[i], 0, G->chunk_bytes * world, st));
+    }
+  }
+  for (int i = 0; i < G->nlocal; ++i) {
+    mbx_matrix* m = mats[i];
+    const int g = G->rank0 + i;
+    if (m->n_rows != G->bounds[g + 1] - G->bounds[g] || m->n_cols != n_global)
+      mbx::fail(MBX_DIMENSION_ERROR, "shard matrix shape does not match its row bounds");
+    if (tiles[i]->info.n_rows != m->n_rows || tiles[i]->info.nnz != m->nnz ||
+        tiles[i]->info.omega != c->omega || tiles[i]->info.sigma != c->sigma)
+      mbx::fail(MBX_CONFIG_ERROR, "shard TILE does not match its matrix / config");
+    mbx::Shard s;
+    s.g = g;
+    s.li = i;
+    s.r0 = G->bounds[g];
+    s.r1 = G->bounds[g + 1];
+    s.tile = tiles[i];
+    s.cols_remap = static_cast<int32_t*>(dm(ctx, m->nnz * 4 + 256));
+    MBX_CUDA(cudaMemsetAsync(s.cols_remap, 0, m->nnz * 4 + 256, st));
+    if (m->nnz)
+      mbx::remap_cols_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, st>>>(
+          m->cols, m->nnz, dbounds, world, G->chunk_elems, gpre, s.cols_remap);
+    s.view = *m;
+    s.view.slots = mbx_matrix::SlotCache{};  // the view builds its own
+    s.view.coo_rows = nullptr;
+    s.view.vmap = nullptr;
+    s.view.cols = s.cols_remap;
+    s.view.cols_hub = nullptr;
+    s.view.hub_cols = nullptr;
+    s.view.hub_avail = 0;
+    s.view.n_cols = G->chunk_elems * world;
+    // x hub cache over the remapped columns (owned by the group)
+    mbx::build_xcache(ctx, &s.view, ctx->tuning.max_hubs);
+    const int64_t rows = s.r1 - s.r0;
+    s.xmap = static_cast<int32_t*>(dm(ctx, rows * 4 + 64));
+    if (rows)
+      mbx::xmap_kernel<<<unsigned(ctx->sm_count) * 4, 256, 0, st>>>(
+          seen, s.r0, rows, dbounds, world, G->chunk_elems, gpre, s.xmap);
+    s.dangling = static_cast<uint32_t*>(dm(ctx, ((rows + 31) / 32) * 4 + 64));
+    mbx::local_dangling_kernel<<<unsigned((rows + 31) / 32 / 256 + 1), 256, 0, st>>>(
+        seen, s.r0, rows, s.dangling);
+    s.geo = mbx::make_geometry(ctx, &s.view, s.tile, c->block_size);
+    s.range_part = static_cast<double*>(
+        dm(ctx, (std::max(s.geo.num_ranges, mbx::pr_parts(s.geo)) + 1) * 4 * sizeof(double)));
+    // K3 blocks, or the pr_init grid (sm_count * 4) when a start vector is given
+    const int64_t nblk = std::max<int64_t>(mbx::fixup_blocks(s.geo) + 1, ctx->sm_count * 4 + 1);
+    s.block_part = static_cast<double*>(dm(ctx, nblk * 4 * sizeof(double)));
+    s.counter = static_cast<unsigned int*>(dm(ctx, 64));
+    MBX_CUDA(cudaMemsetAsync(s.counter, 0, 64, st));
+    s.carry_ws = dm(ctx, mbx::spmv_workspace_bytes(s.geo, G->precision, true));
+    ctx->launches += 2;
+    G->shards.push_back(s);
+  }
+  MBX_CUDA(cudaGetLastError());
+  MBX_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(dbounds, st);
+  cudaFreeAsync(gpre, st);
+  MBX_CUDA(cudaStreamSynchronize(st));
+}
+
+// the fixed-count loop as one CUDA graph
+void group_capture(mbx_shard_group* G) {
+  mbx_context* ctx = G->ctx;
+  cudaStream_t st = ctx->stream;
+  MBX_CUDA(cudaEventCreate(&G->e0));
+  MBX_CUDA(cudaEventCreate(&G->e1));
+  if (G->cfg.max_iters > 0 && G->cfg.max_iters <= 4096) {
+    MBX_CUDA(cudaStreamSynchronize(st));
+    const int64_t before = ctx->launches;
+    cudaGraph_t graph;
+    MBX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      for (int64_t r = 1; r <= G->cfg.max_iters; ++r) launch_iteration(G, r);
+    } catch (...) {
+      cudaStreamEndCapture(st, &graph);
+      throw;
+    }
+    MBX_CUDA(cudaStreamEndCapture(st, &graph));
+    MBX_CUDA(cudaGraphInstantiate(&G->graph, graph, 0));
+    cudaGraphDestroy(graph);
+    G->graph_launches = ctx->launches - before;
+    ctx->launches = before;
+  }
+}
+
+// Blob one rank publishes for the others (mbx_shard_group_export)
+constexpr uint32_t kBlobMagic = 0x4d425850u;  // "MBXP"
+struct PeerBlob {
+  uint32_t magic;
+  int32_t rank, world, pid, device;
+  int32_t pad;
+  uint64_t ptr[6];  // pi0, pi1, loc0, loc1, seen, pflags (same-process peers)
+  cudaIpcMemHandle_t h[6];
+};
+static_assert(sizeof(PeerBlob) <= MBX_SHARD_BLOB_BYTES, "blob size");
+
+void group_free(mbx_shard_group* G) {
+  cudaStream_t st = G->ctx->stream;
+  if (G->graph) cudaGraphExecDestroy(G->graph);
+  for (mbx::Shard& s : G->shards) {
+    mbx::free_slots(G->ctx, &s.view);
+    for (void* p : {static_cast<void*>(s.cols_remap), static_cast<void*>(s.dangling),
+                    static_cast<void*>(s.xmap),
+                    static_cast<void*>(s.view.cols_hub), static_cast<void*>(s.view.hub_cols),
+                    static_cast<void*>(s.range_part), static_cast<void*>(s.block_part),
+                    static_cast<void*>(s.counter), s.carry_ws})
+      if (p) cudaFreeAsync(p, st);
+  }
+  for (void* p : {static_cast<void*>(G->gscal), static_cast<void*>(G->flags),
+                  static_cast<void*>(G->run_base), static_cast<void*>(G->perr)})
+    if (p) cudaFreeAsync(p, st);
+  if (G->e0) cudaEventDestroy(G->e0);
+  if (G->e1) cudaEventDestroy(G->e1);
+  cudaStreamSynchronize(st);
+  if (G->peer) {
+    for (void* p : G->opened) cudaIpcCloseMemHandle(p);
+    for (void* p : {G->pi[0], G->pi[1], G->loc[0], G->loc[1], static_cast<void*>(G->seen),
+                    static_cast<void*>(G->pflags)})
+      if (p) cudaFree(p);
+  } else {
+    for (void* p : {G->pi[0], G->pi[1], G->loc[0], G->loc[1]})
+      if (p) cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
+  }
+  if (G->comm) mbx::nccl().CommDestroy(G->comm);
 }
 
 }  // namespace
@@ -371,60 +702,24 @@ MBX_API int mbx_matrix_row_slice(mbx_context* ctx, const mbx_matrix* m, int64_t 
   });
 }
 
+
 MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world,
                                    const int64_t* bounds, int rank0, int nlocal,
                                    mbx_matrix* const* mats, mbx_tile* const* tiles,
                                    const mbx_simt_config* c, const mbx_pagerank_config* cfg,
                                    const void* nccl_id, mbx_shard_group** out) {
-  return sguard([&] {
-    if (world < 1 || nlocal < 1 || rank0 < 0 || rank0 + nlocal > world)
-      mbx::fail(MBX_CONFIG_ERROR, "shard group: bad world/rank/nlocal");
+  mbx_shard_group* raw = nullptr;
+  const int rc = sguard([&] {
     if (!nccl_id && nlocal != world)
       mbx::fail(MBX_CONFIG_ERROR, "shard group: without NCCL every shard must be local");
-    if (cfg->reference_iters != 0)
-      mbx::fail(MBX_UNSUPPORTED, "shard group: the yardstick run (reference_iters > 0) is "
-                                 "single-GPU only");
-    if (!(cfg->damping >= 0.0 && cfg->damping <= 1.0))
-      mbx::fail(MBX_CONFIG_ERROR, "damping must lie in [0, 1]");
-    if (!(cfg->err_tol > 0.0)) mbx::fail(MBX_CONFIG_ERROR, "err_tol must be positive");
-    if (bounds[0] != 0 || bounds[world] != n_global)
-      mbx::fail(MBX_DIMENSION_ERROR, "row bounds must cover [0, n)");
     auto G = std::make_unique<mbx_shard_group_s>();
-    G->ctx = ctx;
-    G->precision = mats[0]->precision;
-    G->vs = mbx::value_size(G->precision);
-    G->world = world;
-    G->rank0 = rank0;
-    G->nlocal = nlocal;
-    G->n = n_global;
-    G->bounds.assign(bounds, bounds + world + 1);
-    G->c = *c;
-    G->cfg = *cfg;
-    if (G->precision == MBX_F32) {
-      G->cfg.damping = double(float(cfg->damping));
-      G->cfg.err_tol = double(float(cfg->err_tol));
-    }
-    int64_t rows_max = 0;
-    for (int g = 0; g < world; ++g) rows_max = std::max(rows_max, bounds[g + 1] - bounds[g]);
-    G->lchunk_bytes = ((rows_max * int64_t(G->vs) + 255) / 256) * 256 + 256;
+    raw = G.get();
+    group_init(G.get(), ctx, n_global, world, bounds, rank0, nlocal, mats, c, cfg, false);
     cudaStream_t st = ctx->stream;
-    for (int i = 0; i < 2; ++i) {
-      G->loc[i] = dm(ctx, G->lchunk_bytes * nlocal);
-      MBX_CUDA(cudaMemsetAsync(G->loc[i], 0, G->lchunk_bytes * nlocal, st));
-    }
-    G->gscal = static_cast<mbx::PrScalars*>(dm(ctx, (cfg->max_iters + 1) * sizeof(mbx::PrScalars)));
-    MBX_CUDA(cudaMemsetAsync(G->gscal, 0, (cfg->max_iters + 1) * sizeof(mbx::PrScalars), st));
-    G->flags = static_cast<int*>(dm(ctx, 64));
-    int64_t* dbounds = static_cast<int64_t*>(dm(ctx, (world + 1) * 8));
-    MBX_CUDA(cudaMemcpyAsync(dbounds, bounds, (world + 1) * 8, cudaMemcpyHostToDevice, st));
     // dangling vertices = empty columns of the GLOBAL P
     uint8_t* seen = static_cast<uint8_t*>(dm(ctx, n_global + 64));
     MBX_CUDA(cudaMemsetAsync(seen, 0, n_global + 64, st));
-    for (int i = 0; i < nlocal; ++i) {
-      if (mats[i]->nnz)
-        mbx::seen_flags_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, st>>>(mats[i]->cols,
-                                                                            mats[i]->nnz, seen);
-    }
+    local_seen(G.get(), mats, seen);
     if (nccl_id) {
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
@@ -432,119 +727,143 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
       MBX_NCCL(mbx::nccl().CommInitRank(&G->comm, world, id, rank0));
       MBX_NCCL(mbx::nccl().AllReduce(seen, seen, n_global, ncclUint8, ncclMax, G->comm, st));
     }
-    // compacted exchange layout: gpre = exclusive scan of the global flags,
-    // chunk = the largest per-rank non-dangling count (+ the scalar tail)
-    int64_t* gpre = static_cast<int64_t*>(dm(ctx, (n_global + 1) * 8));
-    {
-      int64_t* cnt = static_cast<int64_t*>(dm(ctx, (n_global + 1) * 8));
-      MBX_CUDA(cudaMemsetAsync(cnt, 0, (n_global + 1) * 8, st));
-      mbx::seen_to_count_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, st>>>(seen, n_global, cnt);
-      size_t tb = 0;
-      MBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, gpre, n_global + 1, st));
-      void* tmp = dm(ctx, tb);
-      MBX_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, gpre, n_global + 1, st));
-      cudaFreeAsync(tmp, st);
-      cudaFreeAsync(cnt, st);
-      ctx->launches += 2;
-    }
-    std::vector<int64_t> gb(world + 1);
-    for (int g = 0; g <= world; ++g)
-      MBX_CUDA(cudaMemcpyAsync(&gb[g], gpre + bounds[g], 8, cudaMemcpyDeviceToHost, st));
-    MBX_CUDA(cudaStreamSynchronize(st));
-    int64_t nd_max = 0;
-    for (int g = 0; g < world; ++g) nd_max = std::max(nd_max, gb[g + 1] - gb[g]);
-    G->tail_off = ((nd_max * int64_t(G->vs) + 255) / 256) * 256;
-    G->chunk_bytes = G->tail_off + 256;
-    G->chunk_elems = G->chunk_bytes / int64_t(G->vs);
-    if (G->chunk_elems * world >= (int64_t(1) << 31))
-      mbx::fail(MBX_CAPACITY_ERROR, "exchange layout exceeds int32 column indices");
-    for (int i = 0; i < 2; ++i) {
-      G->pi[i] = dm(ctx, G->chunk_bytes * world);
-      MBX_CUDA(cudaMemsetAsync(G->pi[i], 0, G->chunk_bytes * world, st));
-    }
-    for (int i = 0; i < nlocal; ++i) {
-      mbx_matrix* m = mats[i];
-      const int g = rank0 + i;
-      if (m->n_rows != bounds[g + 1] - bounds[g] || m->n_cols != n_global)
-        mbx::fail(MBX_DIMENSION_ERROR, "shard matrix shape does not match its row bounds");
-      if (tiles[i]->info.n_rows != m->n_rows || tiles[i]->info.nnz != m->nnz ||
-          tiles[i]->info.omega != c->omega || tiles[i]->info.sigma != c->sigma)
-        mbx::fail(MBX_CONFIG_ERROR, "shard TILE does not match its matrix / config");
-      mbx::Shard s;
-      s.g = g;
-      s.li = i;
-      s.r0 = bounds[g];
-      s.r1 = bounds[g + 1];
-      s.tile = tiles[i];
-      s.cols_remap = static_cast<int32_t*>(dm(ctx, m->nnz * 4 + 256));
-      MBX_CUDA(cudaMemsetAsync(s.cols_remap, 0, m->nnz * 4 + 256, st));
-      if (m->nnz)
-        mbx::remap_cols_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, st>>>(
-            m->cols, m->nnz, dbounds, world, G->chunk_elems, gpre, s.cols_remap);
-      s.view = *m;
-      s.view.slots = mbx_matrix::SlotCache{};  // the view builds its own
-      s.view.coo_rows = nullptr;
-      s.view.vmap = nullptr;
-      s.view.cols = s.cols_remap;
-      s.view.cols_hub = nullptr;
-      s.view.hub_cols = nullptr;
-      s.view.hub_avail = 0;
-      s.view.n_cols = G->chunk_elems * world;
-      // x hub cache over the remapped columns (owned by the group)
-      mbx::build_xcache(ctx, &s.view, ctx->tuning.max_hubs);
-      const int64_t rows = s.r1 - s.r0;
-      s.xmap = static_cast<int32_t*>(dm(ctx, rows * 4 + 64));
-      if (rows)
-        mbx::xmap_kernel<<<unsigned(ctx->sm_count) * 4, 256, 0, st>>>(
-            seen, s.r0, rows, dbounds, world, G->chunk_elems, gpre, s.xmap);
-      s.dangling = static_cast<uint32_t*>(dm(ctx, ((rows + 31) / 32) * 4 + 64));
-      mbx::local_dangling_kernel<<<unsigned((rows + 31) / 32 / 256 + 1), 256, 0, st>>>(
-          seen, s.r0, rows, s.dangling);
-      s.geo = mbx::make_geometry(ctx, &s.view, s.tile, c->block_size);
-      s.range_part = static_cast<double*>(
-          dm(ctx, (std::max(s.geo.num_ranges, mbx::pr_parts(s.geo)) + 1) * 4 * sizeof(double)));
-      // K3 blocks, or the pr_init grid (sm_count * 4) when a start vector is given
-      const int64_t nblk = std::max<int64_t>(mbx::fixup_blocks(s.geo) + 1, ctx->sm_count * 4 + 1);
-      s.block_part = static_cast<double*>(dm(ctx, nblk * 4 * sizeof(double)));
-      s.counter = static_cast<unsigned int*>(dm(ctx, 64));
-      MBX_CUDA(cudaMemsetAsync(s.counter, 0, 64, st));
-      s.carry_ws = dm(ctx, mbx::spmv_workspace_bytes(s.geo, G->precision, true));
-      ctx->launches += 2;
-      G->shards.push_back(s);
-    }
-    MBX_CUDA(cudaGetLastError());
-    MBX_CUDA(cudaStreamSynchronize(st));
+    group_layout(G.get(), mats, tiles, seen, 0);
     cudaFreeAsync(seen, st);
-    cudaFreeAsync(dbounds, st);
-    cudaFreeAsync(gpre, st);
-    MBX_CUDA(cudaEventCreate(&G->e0));
-    MBX_CUDA(cudaEventCreate(&G->e1));
-    if (cfg->max_iters > 0 && cfg->max_iters <= 4096) {
-      MBX_CUDA(cudaStreamSynchronize(st));
-      const int64_t before = ctx->launches;
-      cudaGraph_t graph;
-      MBX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      try {
-        for (int64_t r = 1; r <= cfg->max_iters; ++r) launch_iteration(G.get(), r);
-      } catch (...) {
-        cudaStreamEndCapture(st, &graph);
-        throw;
-      }
-      MBX_CUDA(cudaStreamEndCapture(st, &graph));
-      MBX_CUDA(cudaGraphInstantiate(&G->graph, graph, 0));
-      cudaGraphDestroy(graph);
-      G->graph_launches = ctx->launches - before;
-      ctx->launches = before;
-    }
+    group_capture(G.get());
+    raw = nullptr;
     *out = G.release();
+  });
+  if (rc && raw) group_free(raw);
+  return rc;
+}
+
+MBX_API int mbx_shard_group_create_peer(mbx_context* ctx, int64_t n_global, int world,
+                                        const int64_t* bounds, int rank, mbx_matrix* local,
+                                        mbx_tile* tile, const mbx_simt_config* c,
+                                        const mbx_pagerank_config* cfg, mbx_shard_group** out) {
+  return sguard([&] {
+    if (world < 1 || world > 8)
+      mbx::fail(MBX_CONFIG_ERROR, "peer shard group: world must be in [1, 8]");
+    auto G = std::make_unique<mbx_shard_group_s>();
+    mbx_matrix* const mats[1] = {local};
+    group_init(G.get(), ctx, n_global, world, bounds, rank, 1, mats, c, cfg, true);
+    G->pmat = local;
+    G->ptile = tile;
+    // the exchange stride is fixed before the global flags are known: every
+    // row of the largest shard could be non-dangling (+ the scalar tail)
+    int64_t rows_max = 0;
+    for (int g = 0; g < world; ++g) rows_max = std::max(rows_max, bounds[g + 1] - bounds[g]);
+    G->chunk_bytes = ((rows_max * int64_t(G->vs) + 255) / 256) * 256 + 256;
+    if (G->chunk_bytes / int64_t(G->vs) * world >= (int64_t(1) << 31))
+      mbx::fail(MBX_CAPACITY_ERROR, "exchange layout exceeds int32 column indices");
+    for (int i = 0; i < 2; ++i) G->pi[i] = dm_shared(G->chunk_bytes * world);
+    G->seen = static_cast<uint8_t*>(dm_shared(n_global + 64));
+    G->pflags = static_cast<uint64_t*>(dm_shared(8 * 8));
+    G->run_base = static_cast<uint64_t*>(dm(ctx, 64));
+    G->perr = static_cast<int*>(dm(ctx, 64));
+    MBX_CUDA(cudaMemsetAsync(G->run_base, 0, 64, ctx->stream));
+    MBX_CUDA(cudaMemsetAsync(G->perr, 0, 64, ctx->stream));
+    G->epoch_step = G->cfg.max_iters + 3;  // entry + iterations 0..max + the final barrier
+    local_seen(G.get(), mats, G->seen);
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = G.release();
+  });
+}
+
+MBX_API int mbx_shard_group_export(mbx_shard_group* G, void* blob) {
+  return sguard([&] {
+    if (!G->peer) mbx::fail(MBX_CONFIG_ERROR, "export: not a peer shard group");
+    PeerBlob b;
+    std::memset(&b, 0, sizeof(b));
+    b.magic = kBlobMagic;
+    b.rank = G->rank0;
+    b.world = G->world;
+    b.pid = int32_t(getpid());
+    b.device = G->ctx->device;
+    void* bufs[6] = {G->pi[0], G->pi[1], G->loc[0], G->loc[1], G->seen, G->pflags};
+    for (int i = 0; i < 6; ++i) {
+      b.ptr[i] = reinterpret_cast<uint64_t>(bufs[i]);
+      MBX_CUDA(cudaIpcGetMemHandle(&b.h[i], bufs[i]));
+    }
+    std::memset(blob, 0, MBX_SHARD_BLOB_BYTES);
+    std::memcpy(blob, &b, sizeof(b));
+  });
+}
+
+MBX_API int mbx_shard_group_connect(mbx_shard_group* G, const void* blobs) {
+  return sguard([&] {
+    if (!G->peer) mbx::fail(MBX_CONFIG_ERROR, "connect: not a peer shard group");
+    if (G->connected) mbx::fail(MBX_CONFIG_ERROR, "connect: already connected");
+    mbx_context* ctx = G->ctx;
+    const int world = G->world;
+    const int mypid = int(getpid());
+    for (int k = 0; k < world; ++k) {
+      PeerBlob b;
+      std::memcpy(&b, static_cast<const char*>(blobs) + int64_t(k) * MBX_SHARD_BLOB_BYTES,
+                  sizeof(b));
+      if (b.magic != kBlobMagic || b.rank != k || b.world != world)
+        mbx::fail(MBX_CONFIG_ERROR, "connect: blob " + std::to_string(k) +
+                                        " is not rank " + std::to_string(k) + " of this group");
+      void* p[6];
+      if (k == G->rank0) {
+        void* own[6] = {G->pi[0], G->pi[1], G->loc[0], G->loc[1], G->seen, G->pflags};
+        std::copy(own, own + 6, p);
+      } else if (b.pid == mypid) {
+        // a peer group of this process: its device pointers are valid here
+        if (b.device != ctx->device) {
+          const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            mbx::fail(MBX_CUDA_ERROR, std::string("peer access: ") + cudaGetErrorString(e));
+          cudaGetLastError();
+        }
+        for (int i = 0; i < 6; ++i) p[i] = reinterpret_cast<void*>(b.ptr[i]);
+      } else {
+        for (int i = 0; i < 6; ++i) {
+          MBX_CUDA(cudaIpcOpenMemHandle(&p[i], b.h[i], cudaIpcMemLazyEnablePeerAccess));
+          G->opened.push_back(p[i]);
+        }
+      }
+      G->xpeer[0][k] = p[0];
+      G->xpeer[1][k] = p[1];
+      G->lpeer[0][k] = p[2];
+      G->lpeer[1][k] = p[3];
+      G->speer[k] = static_cast<uint8_t*>(p[4]);
+      G->pf.f[k] = static_cast<uint64_t*>(p[5]);
+    }
+    G->pf.world = world;
+    G->pf.rank = G->rank0;
+    // global column flags: OR of every rank's own (all computed before the
+    // caller's all-gather of the blobs)
+    cudaStream_t st = ctx->stream;
+    uint8_t* gseen = static_cast<uint8_t*>(dm(ctx, G->n + 64));
+    mbx::SeenPtrs sp{};
+    for (int k = 0; k < world; ++k) sp.p[k] = G->speer[k];
+    mbx::seen_or_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, st>>>(sp, world, G->n, gseen);
+    ++ctx->launches;
+    MBX_CUDA(cudaGetLastError());
+    mbx_matrix* const mats[1] = {G->pmat};
+    mbx_tile* const tiles[1] = {G->ptile};
+    group_layout(G, mats, tiles, gseen, G->chunk_bytes);
+    cudaFreeAsync(gseen, st);
+    group_capture(G);
+    G->connected = true;
   });
 }
 
 MBX_API int mbx_shard_group_run(mbx_shard_group* G, const void* pi0_dev) {
   return sguard([&] {
+    if (G->peer && !G->connected) mbx::fail(MBX_CONFIG_ERROR, "peer shard group not connected");
+    if (G->quiesced) mbx::fail(MBX_CONFIG_ERROR, "peer shard group already quiesced");
     mbx_context* ctx = G->ctx;
     cudaStream_t st = ctx->stream;
     MBX_CUDA(cudaMemsetAsync(G->flags, 0, 8, st));
+    if (G->peer) {
+      // a new epoch range; every rank's previous run (its combines, the
+      // caller's reads of its rows) is over once all have entered this one
+      mbx::bump_epoch_kernel<<<1, 1, 0, st>>>(G->run_base, uint64_t(G->epoch_step));
+      ++ctx->launches;
+      peer_barrier(G, 0);
+    }
     for (mbx::Shard& s : G->shards) {
       unsigned char* x0 = static_cast<unsigned char*>(G->pi[0]) + int64_t(s.g) * G->chunk_bytes;
       unsigned char* p0 = static_cast<unsigned char*>(G->loc[0]) + int64_t(s.li) * G->lchunk_bytes;
@@ -566,26 +885,34 @@ MBX_API int mbx_shard_group_run(mbx_shard_group* G, const void* pi0_dev) {
                 reinterpret_cast<const double*>(p0), rows, s.xmap, static_cast<double*>(G->pi[0]));
           ++ctx->launches;
         }
-        continue;
-      }
-      auto* cnt = reinterpret_cast<unsigned long long*>(s.counter + 8);
-      MBX_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
-      const unsigned grid = unsigned(ctx->sm_count) * 4;
-      double val;
-      if (G->precision == MBX_F32) {
-        const float v = 1.0f / float(G->n);  // T(1)/static_cast<T>(n) (solvers.hpp:193)
-        val = double(v);
-        mbx::shard_init_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<float*>(p0), rows, v,
-                                                            s.dangling, cnt, s.xmap,
-                                                            static_cast<float*>(G->pi[0]));
       } else {
-        val = 1.0 / double(G->n);
-        mbx::shard_init_kernel<double><<<grid, 256, 0, st>>>(reinterpret_cast<double*>(p0), rows,
-                                                             val, s.dangling, cnt, s.xmap,
-                                                             static_cast<double*>(G->pi[0]));
+        auto* cnt = reinterpret_cast<unsigned long long*>(s.counter + 8);
+        MBX_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
+        const unsigned grid = unsigned(ctx->sm_count) * 4;
+        double val;
+        if (G->precision == MBX_F32) {
+          const float v = 1.0f / float(G->n);  // T(1)/static_cast<T>(n) (solvers.hpp:193)
+          val = double(v);
+          mbx::shard_init_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<float*>(p0), rows,
+                                                              v, s.dangling, cnt, s.xmap,
+                                                              static_cast<float*>(G->pi[0]));
+        } else {
+          val = 1.0 / double(G->n);
+          mbx::shard_init_kernel<double><<<grid, 256, 0, st>>>(reinterpret_cast<double*>(p0),
+                                                               rows, val, s.dangling, cnt, s.xmap,
+                                                               static_cast<double*>(G->pi[0]));
+        }
+        mbx::shard_init_tail_kernel<<<1, 1, 0, st>>>(cnt, rows, val, tail);
+        ctx->launches += 2;
       }
-      mbx::shard_init_tail_kernel<<<1, 1, 0, st>>>(cnt, rows, val, tail);
-      ctx->launches += 2;
+      if (G->peer) {
+        // the start chunk (values + tail) out to every peer, then barrier 1
+        for (int k = 0; k < G->world; ++k)
+          if (k != G->rank0)
+            MBX_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(G->xpeer[0][k]) +
+                                         int64_t(s.g) * G->chunk_bytes,
+                                     x0, G->chunk_bytes, cudaMemcpyDeviceToDevice, st));
+      }
     }
     MBX_CUDA(cudaGetLastError());
     exchange_and_combine(G, 0, 0);
@@ -607,11 +934,15 @@ MBX_API int mbx_shard_group_result(mbx_shard_group* G, mbx_pagerank_result* res,
     if (!G->ran) mbx::fail(MBX_ERROR, "shard group has not run");
     cudaStream_t st = G->ctx->stream;
     int flags[2];
+    int perr = 0;
     MBX_CUDA(cudaMemcpyAsync(flags, G->flags, 8, cudaMemcpyDeviceToHost, st));
+    if (G->perr) MBX_CUDA(cudaMemcpyAsync(&perr, G->perr, 4, cudaMemcpyDeviceToHost, st));
     std::vector<mbx::PrScalars> sc(G->cfg.max_iters + 1);
     MBX_CUDA(cudaMemcpyAsync(sc.data(), G->gscal, sc.size() * sizeof(mbx::PrScalars),
                              cudaMemcpyDeviceToHost, st));
     MBX_CUDA(cudaStreamSynchronize(st));
+    if (perr)
+      mbx::fail(MBX_NCCL_ERROR, "peer shard group: a rank did not reach the barrier in 30 s");
     const int64_t iters = flags[0] ? flags[1] : G->cfg.max_iters;
     if (flags[0] == 2)
       mbx::fail(MBX_ERROR, "pagerank: zero-norm iterate at iteration " + std::to_string(iters));
@@ -639,9 +970,12 @@ MBX_API int mbx_shard_group_gather_pi(mbx_shard_group* G, void* pi_host) {
     MBX_CUDA(cudaMemcpyAsync(flags, G->flags, 8, cudaMemcpyDeviceToHost, st));
     MBX_CUDA(cudaStreamSynchronize(st));
     const int64_t iters = flags[0] ? flags[1] : G->cfg.max_iters;
-    const unsigned char* base = static_cast<const unsigned char*>(G->loc[iters & 1]);
+    const int slot = int(iters & 1);
+    const unsigned char* base = static_cast<const unsigned char*>(G->loc[slot]);
     // the full rows live with their owners: one all-gather of the local
-    // chunks (the exchange buffers hold only the non-dangling entries)
+    // chunks (the exchange buffers hold only the non-dangling entries), or
+    // direct reads of the peers' rows (peer groups; every rank finished the
+    // last iteration before this rank's final barrier)
     unsigned char* all = nullptr;
     if (G->comm) {
       all = static_cast<unsigned char*>(dm(G->ctx, G->lchunk_bytes * G->world));
@@ -649,11 +983,13 @@ MBX_API int mbx_shard_group_gather_pi(mbx_shard_group* G, void* pi_host) {
     }
     for (int g = 0; g < G->world; ++g) {
       const int64_t rows = G->bounds[g + 1] - G->bounds[g];
-      const unsigned char* src = all ? all + int64_t(g) * G->lchunk_bytes
-                                     : base + int64_t(g - G->rank0) * G->lchunk_bytes;
+      const unsigned char* src =
+          G->peer ? static_cast<const unsigned char*>(G->lpeer[slot][g])
+                  : all ? all + int64_t(g) * G->lchunk_bytes
+                        : base + int64_t(g - G->rank0) * G->lchunk_bytes;
       if (rows)
         MBX_CUDA(cudaMemcpyAsync(static_cast<char*>(pi_host) + G->bounds[g] * int64_t(G->vs), src,
-                                 rows * G->vs, cudaMemcpyDeviceToHost, st));
+                                 rows * G->vs, cudaMemcpyDefault, st));
     }
     MBX_CUDA(cudaStreamSynchronize(st));
     if (all) cudaFreeAsync(all, st);
@@ -682,27 +1018,27 @@ MBX_API int mbx_shard_group_download_local(mbx_shard_group* G, void* pi_local_ho
   });
 }
 
+// Peer groups: enqueue the final barrier (asynchronous).  Its completion
+// means no peer can still read or write this rank's buffers.
+MBX_API int mbx_shard_group_quiesce(mbx_shard_group* G) {
+  return sguard([&] {
+    if (!G->peer || !G->connected || G->quiesced) return;
+    MBX_CUDA(cudaMemsetAsync(G->flags, 0, 8, G->ctx->stream));  // stop must not skip it
+    peer_barrier(G, int(G->epoch_step - 1));
+    G->quiesced = true;
+  });
+}
+
+// Collective for peer groups (quiesce, then wait for the final barrier).
 MBX_API int mbx_shard_group_destroy(mbx_shard_group* G) {
   return sguard([&] {
     if (!G) return;
-    cudaStream_t st = G->ctx->stream;
-    if (G->graph) cudaGraphExecDestroy(G->graph);
-    for (mbx::Shard& s : G->shards) {
-      mbx::free_slots(G->ctx, &s.view);
-      for (void* p : {static_cast<void*>(s.cols_remap), static_cast<void*>(s.dangling),
-                      static_cast<void*>(s.xmap),
-                      static_cast<void*>(s.view.cols_hub), static_cast<void*>(s.view.hub_cols),
-                      static_cast<void*>(s.range_part), static_cast<void*>(s.block_part),
-                      static_cast<void*>(s.counter), s.carry_ws})
-        if (p) cudaFreeAsync(p, st);
+    if (G->peer && G->connected) {
+      const int rc = mbx_shard_group_quiesce(G);
+      if (rc) mbx::fail(rc, "quiesce failed");
+      MBX_CUDA(cudaStreamSynchronize(G->ctx->stream));
     }
-    for (void* p : {G->pi[0], G->pi[1], G->loc[0], G->loc[1], static_cast<void*>(G->gscal),
-                    static_cast<void*>(G->flags)})
-      if (p) cudaFreeAsync(p, st);
-    if (G->e0) cudaEventDestroy(G->e0);
-    if (G->e1) cudaEventDestroy(G->e1);
-    cudaStreamSynchronize(st);
-    if (G->comm) mbx::nccl().CommDestroy(G->comm);
+    group_free(G);
     delete G;
   });
 }

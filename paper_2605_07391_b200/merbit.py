@@ -810,3 +810,45 @@ class ShardGroup:
             self.close()
         except Exception:
             pass
+
+
+SHARD_BLOB_BYTES = 512
+
+
+class PeerShardGroup(ShardGroup):
+    """This rank's row shard joined to its peers by the FUSED exchange: the
+    PageRank commit stores pi_new straight into every peer's exchange buffer
+    (CUDA IPC, NVLink P2P) and a device barrier ends each iteration -- no
+    collective library on the iteration path.  Setup through any bootstrap:
+        g = PeerShardGroup(...); blobs = all_gather(g.export()); g.connect(blobs)
+    close() is collective (final barrier)."""
+
+    def __init__(self, ctx: Context, n_global: int, world: int, bounds, rank: int,
+                 matrix: DeviceMatrix, tile: Tile, c: SimtConfig, cfg: PageRankConfig):
+        self.ctx, self.n, self.world, self.cfg = ctx, n_global, world, cfg
+        self.keep = [(matrix, tile)]
+        self.bounds = np.ascontiguousarray(bounds, np.int64)
+        self.dtype = matrix.dtype
+        cc, pc = c._c(), cfg._c()
+        h = C.c_void_p()
+        _check(_lib.lib().mbx_shard_group_create_peer(ctx.h, n_global, world, _ptr(self.bounds),
+                                                      rank, matrix.h, tile.h, C.byref(cc),
+                                                      C.byref(pc), C.byref(h)))
+        self.h = h
+
+    def export(self) -> bytes:
+        b = C.create_string_buffer(SHARD_BLOB_BYTES)
+        _check(_lib.lib().mbx_shard_group_export(self.h, b))
+        return b.raw
+
+    def connect(self, blobs):
+        """blobs: the world's export() results in rank order."""
+        allb = b"".join(blobs)
+        if len(allb) != SHARD_BLOB_BYTES * self.world:
+            raise ConfigError(f"connect: expected {self.world} blobs of {SHARD_BLOB_BYTES} bytes")
+        buf = C.create_string_buffer(allb, len(allb))
+        _check(_lib.lib().mbx_shard_group_connect(self.h, buf))
+
+    def quiesce(self):
+        """Enqueue the final barrier without waiting (close() waits)."""
+        _check(_lib.lib().mbx_shard_group_quiesce(self.h))
