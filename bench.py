@@ -266,6 +266,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the spmv f32/f64 extras")
     ap.add_argument("--spmv-reps", type=int, default=30)
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="N > 1: fused = the commit stores into the peers' buffers (P2P, "
+                         "one device barrier per iteration); nccl = one ncclAllGather")
     ap.add_argument("--vertex-order", default="degree", choices=["degree", "natural"],
                     help="degree: relabel vertices by column count on the device "
                          "(preprocessing); natural: R-MAT's own numbering")
@@ -281,12 +284,14 @@ def main():
 
     import paper_2605_07391_b200 as mb
     from paper_2605_07391_b200 import _lib
-    from paper_2605_07391_b200.merbit import (ShardGroup, nccl_unique_id, pagerank_row_weight,
-                                              row_slice)
+    from paper_2605_07391_b200.merbit import (PeerShardGroup, ShardGroup, nccl_unique_id,
+                                              pagerank_row_weight, row_slice)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("MBX_BENCH_ONE_DEVICE") == "1":
+        local = 0  # plumbing check of N > 1 on a one-GPU box (fused exchange only)
     if world > 1:
         # gloo only bootstraps (NCCL id broadcast, barriers, max-over-ranks);
         # the pi exchange is the library's own NCCL all-gather
@@ -346,9 +351,17 @@ def main():
         del P, P_natural
         P_natural = None
         tile = mb.generate_tile_for(Lm, cfg)
-        ids = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(ids, src=0)
-        runner = ShardGroup(ctx, n, world, bounds, rank, [(Lm, tile)], cfg, prc, ids[0])
+        if args.exchange == "fused":
+            # the commit stores pi_new into every peer's buffer over NVLink
+            # (CUDA IPC); gloo only carries the setup blobs
+            runner = PeerShardGroup(ctx, n, world, bounds, rank, Lm, tile, cfg, prc)
+            blobs = [None] * world
+            dist.all_gather_object(blobs, runner.export())
+            runner.connect(blobs)
+        else:
+            ids = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(ids, src=0)
+            runner = ShardGroup(ctx, n, world, bounds, rank, [(Lm, tile)], cfg, prc, ids[0])
         local_rows, local_nnz = int(bounds[rank + 1] - bounds[rank]), Lm.nnz
         run = runner.run
         pre_ms = (relabel_s + tile.preprocess_seconds) * 1e3
@@ -477,14 +490,16 @@ def main():
                                + ("degree-relabelled on the device as preprocessing, pi "
                                   "returned in the original order" if args.vertex_order ==
                                   "degree" else "natural") + "), preprocessing amortised"
-                               + (f", {world} row shards (row weight {row_w}) + NCCL all-gather"
-                                  if world > 1 else ""),
+                               + (f", {world} row shards (row weight {row_w}), exchange: "
+                                  + ("fused P2P stores in the commit" if args.exchange == "fused"
+                                     else "ncclAllGather") if world > 1 else ""),
                    "scale": scale, "n": n, "nnz": m, "omega": 32, "sigma": 14,
                    "block_size": args.block_size,
                    "l2": "inputs (values+cols %.1f GB per GPU) larger than L2; no flush"
                          % (8 * local_nnz / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_per_launch(), "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic_per_launch() if scale == 24 and world == 1 else None,
+                     "peak_kind": peak_kind,
                      "kernel": "fused PageRank iteration (spmv_slot_kernel<float,14,PR,HUB> + "
                                "fixup_kernel) on rank 0",
                      "bytes_per_launch": b_iter, "us_per_iteration": t_iter_local * 1e6,
