@@ -17,6 +17,12 @@
 // decides convergence.  Iteration = K2 + K3 (PR mode, local rows) ->
 // ncclAllGather -> combine, captured once as a CUDA graph.
 //
+// Fused mode (mbx_shard_group_create_peer / export / connect): no all-gather.
+// The commit itself stores each non-dangling pi_new (and K3 the scalar tail)
+// into every peer's exchange buffer through CUDA IPC mappings -- P2P stores
+// over NVLink spread across the whole SpMV -- and peer_barrier_kernel
+// (system-scope release/acquire epochs, bounded wait) ends the iteration.
+//
 // Virtual mode (nccl_id == NULL, nlocal == world): all shards live in one
 // process on one device and write into one shared buffer, so no exchange is
 // needed -- the sharded kernels, remap and combine are verified on a single
