@@ -430,6 +430,8 @@ void launch_iteration(mbx_shard_group* G, int64_t r) {
 void group_init(mbx_shard_group* G, mbx_context* ctx, int64_t n_global, int world,
                 const int64_t* bounds, int rank0, int nlocal, mbx_matrix* const* mats,
                 const mbx_simt_config* c, const mbx_pagerank_config* cfg, bool peer) {
+  G->ctx = ctx;
+  G->peer = peer;
   if (world < 1 || nlocal < 1 || rank0 < 0 || rank0 + nlocal > world)
     mbx::fail(MBX_CONFIG_ERROR, "shard group: bad world/rank/nlocal");
   if (cfg->reference_iters != 0)
@@ -630,6 +632,7 @@ struct PeerBlob {
 static_assert(sizeof(PeerBlob) <= MBX_SHARD_BLOB_BYTES, "blob size");
 
 void group_free(mbx_shard_group* G) {
+  if (!G->ctx) return;  // failed before any allocation
   cudaStream_t st = G->ctx->stream;
   if (G->graph) cudaGraphExecDestroy(G->graph);
   for (mbx::Shard& s : G->shards) {
@@ -659,6 +662,15 @@ void group_free(mbx_shard_group* G) {
   }
   if (G->comm) mbx::nccl().CommDestroy(G->comm);
 }
+
+// owns a group under construction: a failed create releases what it got
+struct GroupDeleter {
+  void operator()(mbx_shard_group* G) const {
+    group_free(G);
+    delete G;
+  }
+};
+using GroupPtr = std::unique_ptr<mbx_shard_group, GroupDeleter>;
 
 }  // namespace
 
@@ -714,12 +726,10 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
                                    mbx_matrix* const* mats, mbx_tile* const* tiles,
                                    const mbx_simt_config* c, const mbx_pagerank_config* cfg,
                                    const void* nccl_id, mbx_shard_group** out) {
-  mbx_shard_group* raw = nullptr;
-  const int rc = sguard([&] {
+  return sguard([&] {
     if (!nccl_id && nlocal != world)
       mbx::fail(MBX_CONFIG_ERROR, "shard group: without NCCL every shard must be local");
-    auto G = std::make_unique<mbx_shard_group_s>();
-    raw = G.get();
+    GroupPtr G(new mbx_shard_group_s);
     group_init(G.get(), ctx, n_global, world, bounds, rank0, nlocal, mats, c, cfg, false);
     cudaStream_t st = ctx->stream;
     // dangling vertices = empty columns of the GLOBAL P
@@ -736,11 +746,8 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
     group_layout(G.get(), mats, tiles, seen, 0);
     cudaFreeAsync(seen, st);
     group_capture(G.get());
-    raw = nullptr;
     *out = G.release();
   });
-  if (rc && raw) group_free(raw);
-  return rc;
 }
 
 MBX_API int mbx_shard_group_create_peer(mbx_context* ctx, int64_t n_global, int world,
@@ -750,7 +757,7 @@ MBX_API int mbx_shard_group_create_peer(mbx_context* ctx, int64_t n_global, int 
   return sguard([&] {
     if (world < 1 || world > 8)
       mbx::fail(MBX_CONFIG_ERROR, "peer shard group: world must be in [1, 8]");
-    auto G = std::make_unique<mbx_shard_group_s>();
+    GroupPtr G(new mbx_shard_group_s);
     mbx_matrix* const mats[1] = {local};
     group_init(G.get(), ctx, n_global, world, bounds, rank, 1, mats, c, cfg, true);
     G->pmat = local;
