@@ -415,6 +415,19 @@ MBX_API int mbx_matrix_build_transition(mbx_context* ctx, const mbx_matrix* adja
  * vertex order; device-pointer entry points (mbx_spmv_device, plans, shard
  * groups) work in the new order.
  * rank_host (n int32) may be NULL. */
+/* DegreeStats (include/merbit/csr.hpp:108-140): mean degree nnz/n_rows,
+ * low_degree = mean <= sigma_threshold (callers pass select_sigma), the
+ * longest row and the number of empty rows -- one reduction over the
+ * resident row offsets.  dimension_error for a matrix with no rows. */
+typedef struct {
+  double mean_degree;
+  int32_t low_degree;
+  int32_t pad_;
+  int64_t max_degree;
+  int64_t empty_rows;
+} mbx_degree_stats;
+MBX_API int mbx_matrix_degree_stats(mbx_context* ctx, const mbx_matrix* m,
+                                    int sigma_threshold, mbx_degree_stats* out);
 MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* m,
                                          mbx_matrix** out, int32_t* rank_host);
 

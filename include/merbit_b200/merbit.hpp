@@ -178,6 +178,21 @@ class DeviceCsr {
   std::unique_ptr<mbx_matrix, Del> h_;
 };
 
+// ---- DegreeStats (csr.hpp:108-140), reduced on the device --------------------
+struct DegreeStats {
+  double mean_degree = 0.0;
+  bool low_degree = false;
+  index_t max_degree = 0;
+  index_t empty_rows = 0;
+};
+
+template <typename T>
+DegreeStats degree_stats(const DeviceCsr<T>& a, int sigma_threshold) {
+  mbx_degree_stats d{};
+  check(mbx_matrix_degree_stats(a.context().get(), a.get(), sigma_threshold, &d));
+  return DegreeStats{d.mean_degree, d.low_degree != 0, d.max_degree, d.empty_rows};
+}
+
 // ---- TileMetadata (tile.hpp:27-44) -------------------------------------------
 struct TileMetadata {
   int omega = 0;

@@ -43,6 +43,11 @@ class mbx_pagerank_result(C.Structure):
                 ("dangling_mass", C.c_double)]
 
 
+class mbx_degree_stats(C.Structure):
+    _fields_ = [("mean_degree", C.c_double), ("low_degree", C.c_int32), ("pad_", C.c_int32),
+                ("max_degree", C.c_int64), ("empty_rows", C.c_int64)]
+
+
 class mbx_bicgstab_config(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iters", C.c_int64)]
 
@@ -71,6 +76,7 @@ SIGNATURES = {
                                C.c_double),
     "mbx_merge_search": ([VP, C.c_int64, C.c_int64, C.c_int64, I64P, I64P], C.c_int),
     "mbx_context_release_cache": ([VP], C.c_int),
+    "mbx_matrix_degree_stats": ([VP, VP, C.c_int, C.POINTER(mbx_degree_stats)], C.c_int),
     "mbx_plan_row_shards": ([VP, C.c_int64, C.c_int64, C.c_int, VP], C.c_int),
     "mbx_plan_row_shards_weighted": ([VP, C.c_int64, C.c_int64, C.c_int, C.c_double, VP], C.c_int),
     "mbx_device_count": ([C.POINTER(C.c_int)], C.c_int),

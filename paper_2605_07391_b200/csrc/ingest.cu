@@ -117,6 +117,27 @@ __global__ void split_keys_kernel(const unsigned long long* __restrict__ keys, i
   }
 }
 
+// ---- degree_stats (csr.hpp:119-140): longest row and empty rows
+__global__ void degree_stats_kernel(const uint32_t* __restrict__ ro, int64_t n,
+                                    unsigned long long* out /* [0] max, [1] empty */) {
+  unsigned long long mx = 0, empty = 0;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long d = ro[r + 1] - ro[r];
+    mx = d > mx ? d : mx;
+    empty += d == 0;
+  }
+  for (int o = 16; o >= 1; o >>= 1) {
+    const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = m2 > mx ? m2 : mx;
+    empty += __shfl_xor_sync(0xffffffffu, empty, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, mx);
+    if (empty) atomicAdd(out + 1, empty);
+  }
+}
+
 // ---- degree relabelling (a locality preprocessing for graphs whose x
 // does not fit L2): vertex v gets the rank of its column count, descending
 // (ties: ascending id), applied to rows and columns alike
@@ -384,6 +405,30 @@ MBX_API int mbx_matrix_build_transition(mbx_context* ctx, const mbx_matrix* a,
       cudaFreeAsync(q, s);
     MBX_CUDA(cudaStreamSynchronize(s));
     *out = p.release();
+  });
+}
+
+MBX_API int mbx_matrix_degree_stats(mbx_context* ctx, const mbx_matrix* m, int sigma_threshold,
+                                    mbx_degree_stats* out) {
+  return mbx::iguard([&] {
+    if (m->n_rows <= 0) mbx::fail(MBX_DIMENSION_ERROR, "degree stats of a matrix with no rows");
+    MBX_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    unsigned long long* d = nullptr;
+    MBX_CUDA(cudaMallocAsync(&d, 16, s));
+    MBX_CUDA(cudaMemsetAsync(d, 0, 16, s));
+    mbx::degree_stats_kernel<<<mbx::grid_of(m->n_rows, ctx), 256, 0, s>>>(m->ro, m->n_rows, d);
+    ++ctx->launches;
+    MBX_CUDA(cudaGetLastError());
+    unsigned long long h[2];
+    MBX_CUDA(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(d, s);
+    MBX_CUDA(cudaStreamSynchronize(s));
+    out->mean_degree = double(m->nnz) / double(m->n_rows);
+    out->low_degree = out->mean_degree <= sigma_threshold ? 1 : 0;
+    out->pad_ = 0;
+    out->max_degree = int64_t(h[0]);
+    out->empty_rows = int64_t(h[1]);
   });
 }
 

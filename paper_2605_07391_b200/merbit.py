@@ -247,6 +247,15 @@ def default_context() -> Context:
     return _default_ctx
 
 
+@dataclass
+class DegreeStats:
+    """DegreeStats (include/merbit/csr.hpp:108-113)."""
+    mean_degree: float
+    low_degree: bool
+    max_degree: int
+    empty_rows: int
+
+
 class DeviceMatrix:
     """A CsrMatrix<T> (csr.hpp:29-38) resident on the device."""
 
@@ -335,6 +344,13 @@ class DeviceMatrix:
         h = C.c_void_p()
         _check(_lib.lib().mbx_matrix_build_transition(self.ctx.h, self.h, C.byref(h)))
         return DeviceMatrix(self.ctx, h)
+
+    def degree_stats(self, sigma_threshold: int):
+        """DegreeStats (csr.hpp:108-140) of the resident matrix."""
+        d = _lib.mbx_degree_stats()
+        _check(_lib.lib().mbx_matrix_degree_stats(self.ctx.h, self.h, int(sigma_threshold),
+                                                  C.byref(d)))
+        return DegreeStats(d.mean_degree, bool(d.low_degree), d.max_degree, d.empty_rows)
 
     def relabel_by_degree(self):
         """(P', rank): the symmetric degree relabelling P' = Q P Q^T on the

@@ -115,3 +115,21 @@ def test_build_transition_is_the_reference(ctx, dt):
     rect = O.single_dense_row(4, 1)
     with pytest.raises(mb.DimensionError):
         mb.DeviceMatrix.from_csr(ctx, rect).build_transition()
+
+
+def test_degree_stats_reference_cases(ctx):
+    """test_sparse_core.cpp:95-113: the walkthrough fixture (34 nonzeros over
+    8 rows) and a 2-row matrix with 16 nonzeros; no rows -> dimension_error."""
+    a = O.walkthrough()
+    m = mb.DeviceMatrix.from_csr(ctx, a)
+    single = m.degree_stats(14)
+    assert abs(single.mean_degree - 4.25) <= 1e-12 and single.low_degree
+    dbl = m.degree_stats(7)
+    assert dbl.low_degree and dbl.max_degree == 7 and dbl.empty_rows == 1
+    cols = np.array(list(range(0, 16, 2)) + list(range(1, 16, 2)), np.int32)
+    wide = O.Csr(2, 16, np.array([0, 8, 16], np.int64), cols, np.ones(16))
+    assert not mb.DeviceMatrix.from_csr(ctx, wide).degree_stats(7).low_degree
+    empty = mb.DeviceMatrix.from_csr(ctx, O.Csr(0, 4, np.zeros(1, np.int64),
+                                                np.zeros(0, np.int32), np.zeros(0)))
+    with pytest.raises(mb.DimensionError):
+        empty.degree_stats(7)

@@ -470,8 +470,9 @@ int cmd_bench(mbx_context* ctx, const Args& a) {
   Loaded L;
   load(ctx, path, k.precision, L);
   const auto x = as_precision(seed_vector(L.n_cols, -1.0, 1.0, k.seed), k.precision);
-  const bool low = L.n_rows > 0 &&
-                   double(L.nnz) / double(L.n_rows) <= double(mbx_select_sigma(k.precision, 0));
+  mbx_degree_stats degrees{};  // degree_stats(a, select_sigma(p)) (merbit_cli.cpp:270)
+  check(mbx_matrix_degree_stats(ctx, L.a.h, mbx_select_sigma(k.precision, 0), &degrees));
+  const bool low = degrees.low_degree != 0;
   // the COO baseline is always measured in-process (every speedup refers to it)
   const double coo = time_kernel(ctx, L, c, 1, iters, warmup, x).mean;
   std::vector<BenchRecord> rows;
