@@ -21,6 +21,7 @@ import sys
 import numpy as np
 import pytest
 
+import oracle as O
 import paper_2605_07391_b200 as mb
 from paper_2605_07391_b200.merbit import PeerShardGroup, ShardGroup, row_slice
 
@@ -134,3 +135,51 @@ def test_peer_groups_across_two_processes(tmp_path):
         assert np.array_equal(pi.view(np.uint32), want.view(np.uint32)), r
         resid = float(np.load(tmp_path / f"resid{r}.npy"))
         assert resid == wres.l1_residual
+
+
+def test_peer_groups_early_stop_and_start_vector():
+    """Convergence decided after the barrier: on a directed ring pi stays
+    uniform, so ERR against the uniform yardstick (reference_iters = 0) drops
+    below err_tol at iteration 1 and every rank must stop there and skip the
+    remaining barriers consistently (the final barrier still meets).  The
+    start vector comes from the caller (its chunk pushed to the peers before
+    the first barrier)."""
+    import torch
+    parts, iters, n = 3, 50, 3000
+    ring = O.Csr(n, n, np.arange(n + 1, dtype=np.int64),
+                 np.array([(i - 1) % n for i in range(n)], np.int32), np.ones(n))
+    base = mb.Context(0)
+    c = mb.SimtConfig.make(32, 7, 128)
+    cfg = mb.PageRankConfig(0.85, 1e-9, iters, 0)
+    b = np.array([0, 700, 2100, n], np.int64)
+    P = mb.DeviceMatrix.from_csr(base, ring)
+    vs = [(m, mb.generate_tile_for(m, c)) for m in
+          (row_slice(P, int(b[g]), int(b[g + 1])) for g in range(parts))]
+    virt = ShardGroup(base, n, parts, b, 0, vs, c, cfg)
+    pi0_dev = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    virt.run(pi0_dev.data_ptr())
+    wres, whist = virt.result(want_history=True)
+    want = virt.gather_pi()
+    assert wres.status == 0 and wres.iterations == 1  # converged at once
+    groups = []
+    for r in range(parts):
+        cx = mb.Context(0)
+        Q = mb.DeviceMatrix.from_csr(cx, ring)
+        L = row_slice(Q, int(b[r]), int(b[r + 1]))
+        groups.append(PeerShardGroup(cx, n, parts, b, r, L, mb.generate_tile_for(L, c), c, cfg))
+    blobs = [g.export() for g in groups]
+    for g in groups:
+        g.connect(blobs)
+    for rep in range(2):
+        for g in groups:
+            g.run(pi0_dev.data_ptr())
+        for g in groups:
+            res, hist = g.result(want_history=True)
+            assert res.status == 0 and res.iterations == 1
+            assert res.final_err == wres.final_err and np.array_equal(hist, whist)
+            assert np.array_equal(g.gather_pi(), want)
+    for g in groups:
+        g.quiesce()
+    for g in groups:
+        g.close()
