@@ -266,6 +266,9 @@ __device__ void pr_block_finish(PrAcc a, const PrArgs& pr, double* block_part,
                                 unsigned int* counter, PrScalars* out, bool check_stop) {
   __shared__ double sm[4][32];
   __shared__ bool is_last;
+  // fused exchange: this thread's NVLink stores are performed system-wide
+  // before the grid completes (the peer barrier that follows publishes them)
+  if (pr.npeer) __threadfence_system();
   a.resid = warp_sum(a.resid);
   a.dang = warp_sum(a.dang);
   a.mass = warp_sum(a.mass);
@@ -349,6 +352,7 @@ __device__ void pr_block_finish(PrAcc a, const PrArgs& pr, double* block_part,
       o->mass = m;
       o->err = e;
     }
+    if (pr.npeer) __threadfence_system();
     if (check_stop && pr.stop) {
       if (m == 0.0) {
         *pr.stop = 2;  // zero-norm iterate (solvers.hpp:202-205)
@@ -589,6 +593,7 @@ __global__ void __launch_bounds__(1024) spmv_w32_kernel(SpmvParams<T> p) {
   for (int64_t range = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp; range < g.num_ranges;
        range += wstride)
     w32_range<T, SIGMA, PR, HUB, PF>(p, hub, buf, range, lid, pol, base, acc);
+  if (PR && p.pr.npeer) __threadfence_system();  // NVLink stores performed (fused exchange)
   if (PR) write_warp_part(acc, p.pr.range_part, lid);
 }
 
@@ -673,6 +678,7 @@ __global__ void __launch_bounds__(kThreads) spmv_generic_kernel(SpmvParams<T> p)
     p.carry_val[2 * range + 1] = carry;
   }
   if (PR) {
+    if (p.pr.npeer) __threadfence_system();  // NVLink stores performed (fused exchange)
     acc.resid = warp_sum(acc.resid);
     acc.dang = warp_sum(acc.dang);
     acc.mass = warp_sum(acc.mass);
@@ -1059,6 +1065,7 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
        range += wstride)
     slot_range<T, SIGMA, PR, HUB, PF>(p, hub, rowbuf, range, lid, pol, base, wacc);
   __syncwarp();
+  if (PR && p.pr.npeer) __threadfence_system();  // NVLink stores performed (fused exchange)
   if (PR) write_warp_part(load_acc(wacc, lid), p.pr.range_part, lid);
 }
 
