@@ -329,6 +329,20 @@ MBX_API int mbx_pagerank(mbx_context* ctx, const mbx_matrix* p,
                          void* pi_host, void* reference_pi_host,
                          double* residual_history_host,
                          mbx_pagerank_result* result);
+/* pagerank with the reference's on_iteration hook (solvers.hpp:157-158, 209):
+ * iteration by iteration (no graph), each iterate copied to the host in the
+ * original vertex order and handed to observer(r, pi, ERR, user) after the
+ * mass check and before the convergence test -- a test / monitoring path.
+ * Results as mbx_pagerank (bitwise: the same kernels run). */
+typedef int (*mbx_pagerank_observer)(int64_t iteration, const void* pi_host, double err,
+                                     void* user);  /* nonzero: abort the run (MBX_ERROR) */
+MBX_API int mbx_pagerank_observed(mbx_context* ctx, const mbx_matrix* p,
+                                  const mbx_tile* t, const mbx_simt_config* c,
+                                  const mbx_pagerank_config* cfg, const void* pi0_host,
+                                  void* pi_host, void* reference_pi_host,
+                                  double* residual_history_host,
+                                  mbx_pagerank_observer observer, void* user,
+                                  mbx_pagerank_result* result);
 /* Free the plan mbx_pagerank keeps between calls (no-op when none). */
 MBX_API int mbx_context_release_cache(mbx_context* ctx);
 /* Reusable plan: device buffers, dangling mask and the CUDA graph of the

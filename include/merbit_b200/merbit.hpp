@@ -17,10 +17,13 @@
 // once from a host CsrMatrix-like triple of vectors); apply() returns a host
 // vector that stays valid until the next apply(), exactly the reference's
 // lifetime rule (backend.hpp:17-21).  The PageRank power loop runs fused on
-// the device; on_iteration, when set, copies each iterate to the host.
+// the device; on_iteration, when set, copies each iterate to the host
+// (mbx_pagerank_observed).
 #pragma once
 
 #include <cstdint>
+#include <cstring>
+#include <exception>
 #include <functional>
 #include <limits>
 #include <memory>
@@ -384,14 +387,16 @@ struct PageRankResult {
   double l1_residual = 0.0;  // ||pi_k - pi_{k-1}||_1, fused on the device
 };
 
-// pagerank<T>(p, cfg, backend): yardstick, damping/teleport update, dangling
-// redistribution, mass check, ERR and early exit -- all fused into the SpMV
-// commit on the device; pi reaches the host once, at the end.  Callers that
-// need the reference's per-iterate on_iteration callback run the
-// reference's own pagerank() over MerbitB200Backend::apply.
+// pagerank<T>(p, cfg, backend, on_iteration): yardstick, damping/teleport
+// update, dangling redistribution, mass check, ERR and early exit -- all fused
+// into the SpMV commit on the device; pi reaches the host once, at the end,
+// or after every iteration when on_iteration is set (solvers.hpp:157-158,
+// 209: called after the mass check, before the convergence test).
 template <typename T>
-PageRankResult<T> pagerank(MerbitB200Backend<T>& backend, const PageRankConfig<T>& cfg,
-                           std::vector<double>* residual_history = nullptr) {
+PageRankResult<T> pagerank(
+    MerbitB200Backend<T>& backend, const PageRankConfig<T>& cfg,
+    std::vector<double>* residual_history = nullptr,
+    const std::function<void(index_t, const std::vector<T>&, double)>& on_iteration = {}) {
   const auto& a = backend.matrix();
   if (a.n_rows() != a.n_cols()) throw dimension_error("pagerank needs a square transition matrix");
   const mbx_simt_config cc = backend.config().c();
@@ -402,9 +407,34 @@ PageRankResult<T> pagerank(MerbitB200Backend<T>& backend, const PageRankConfig<T
   const mbx_pagerank_config pc{double(cfg.damping), double(cfg.err_tol), cfg.max_iters,
                                cfg.reference_iters};
   if (residual_history) residual_history->assign(std::max<index_t>(cfg.max_iters, 1), 0.0);
-  check(mbx_pagerank(a.context().get(), a.get(), backend.tile().get(), &cc, &pc, nullptr,
-                     r.pi.data(), r.reference_pi.data(),
-                     residual_history ? residual_history->data() : nullptr, &res));
+  if (!on_iteration) {
+    check(mbx_pagerank(a.context().get(), a.get(), backend.tile().get(), &cc, &pc, nullptr,
+                       r.pi.data(), r.reference_pi.data(),
+                       residual_history ? residual_history->data() : nullptr, &res));
+  } else {
+    struct Obs {
+      const std::function<void(index_t, const std::vector<T>&, double)>* fn;
+      std::vector<T> it;
+      std::exception_ptr failure;
+    } obs{&on_iteration, std::vector<T>(a.n_rows()), nullptr};
+    auto tramp = [](int64_t iter, const void* pi, double err, void* user) -> int {
+      auto* o = static_cast<Obs*>(user);
+      try {
+        std::memcpy(o->it.data(), pi, o->it.size() * sizeof(T));
+        (*o->fn)(index_t(iter), o->it, err);
+        return 0;
+      } catch (...) {  // stops the run; rethrown once the C call has returned
+        o->failure = std::current_exception();
+        return 1;
+      }
+    };
+    const int rc = mbx_pagerank_observed(
+        a.context().get(), a.get(), backend.tile().get(), &cc, &pc, nullptr, r.pi.data(),
+        r.reference_pi.data(), residual_history ? residual_history->data() : nullptr, tramp, &obs,
+        &res);
+    if (obs.failure) std::rethrow_exception(obs.failure);
+    check(rc);
+  }
   if (residual_history) residual_history->resize(res.iterations);
   r.iterations = res.iterations;
   r.final_err = res.final_err;

@@ -43,6 +43,9 @@ class mbx_pagerank_result(C.Structure):
                 ("dangling_mass", C.c_double)]
 
 
+PAGERANK_OBSERVER = C.CFUNCTYPE(C.c_int, C.c_int64, C.c_void_p, C.c_double, C.c_void_p)
+
+
 class mbx_degree_stats(C.Structure):
     _fields_ = [("mean_degree", C.c_double), ("low_degree", C.c_int32), ("pad_", C.c_int32),
                 ("max_degree", C.c_int64), ("empty_rows", C.c_int64)]
@@ -77,6 +80,8 @@ SIGNATURES = {
     "mbx_merge_search": ([VP, C.c_int64, C.c_int64, C.c_int64, I64P, I64P], C.c_int),
     "mbx_context_release_cache": ([VP], C.c_int),
     "mbx_matrix_degree_stats": ([VP, VP, C.c_int, C.POINTER(mbx_degree_stats)], C.c_int),
+    "mbx_pagerank_observed": ([VP, VP, VP, VP, VP, VP, VP, VP, VP, PAGERANK_OBSERVER, VP,
+                               C.POINTER(mbx_pagerank_result)], C.c_int),
     "mbx_plan_row_shards": ([VP, C.c_int64, C.c_int64, C.c_int, VP], C.c_int),
     "mbx_plan_row_shards_weighted": ([VP, C.c_int64, C.c_int64, C.c_int, C.c_double, VP], C.c_int),
     "mbx_device_count": ([C.POINTER(C.c_int)], C.c_int),

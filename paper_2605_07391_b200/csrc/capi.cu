@@ -999,10 +999,35 @@ MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, cons
   });
 }
 
+namespace {
+
+// yardstick + pi_0 of a run (everything before the power loop)
+void plan_prologue(mbx_pagerank_plan* pl, const void* pi0);
+
+}  // namespace
+
 MBX_API int mbx_pagerank_plan_run(mbx_pagerank_plan* pl, const void* pi0) {
   return guarded([&] {
     mbx_context* ctx = pl->ctx;
     Device dg(ctx->device);
+    plan_prologue(pl, pi0);
+    MBX_CUDA(cudaEventRecord(pl->e0, ctx->stream));
+    if (pl->graph) {
+      MBX_CUDA(cudaGraphLaunch(pl->graph, ctx->stream));
+      ctx->launches += pl->graph_launches;
+    } else {
+      launch_power_loop(pl);
+    }
+    MBX_CUDA(cudaEventRecord(pl->e1, ctx->stream));
+    pl->ran = true;
+  });
+}
+
+namespace {
+
+void plan_prologue(mbx_pagerank_plan* pl, const void* pi0) {
+  {
+    mbx_context* ctx = pl->ctx;
     MBX_CUDA(cudaMemsetAsync(pl->flags, 0, 8, ctx->stream));
     // Yardstick: fixed-count power run on the plain CSR kernel (178-191).
     if (pl->cfg.reference_iters > 0) {
@@ -1023,17 +1048,10 @@ MBX_API int mbx_pagerank_plan_run(mbx_pagerank_plan* pl, const void* pi0) {
     }
     mbx::launch_pr_init(ctx, pl->p->precision, pl->n, pi0, pl->pi[0], pl->dangling, pl->scal,
                         pl->block_part, pl->counter);
-    MBX_CUDA(cudaEventRecord(pl->e0, ctx->stream));
-    if (pl->graph) {
-      MBX_CUDA(cudaGraphLaunch(pl->graph, ctx->stream));
-      ctx->launches += pl->graph_launches;
-    } else {
-      launch_power_loop(pl);
-    }
-    MBX_CUDA(cudaEventRecord(pl->e1, ctx->stream));
-    pl->ran = true;
-  });
+  }
 }
+
+}  // namespace
 
 MBX_API int mbx_pagerank_plan_result(mbx_pagerank_plan* pl, mbx_pagerank_result* res,
                                      double* history) {
@@ -1174,6 +1192,95 @@ MBX_API int mbx_pagerank(mbx_context* ctx, const mbx_matrix* p, const mbx_tile* 
     // kept for the next call (only for objects of this context: their
     // destroy calls are what invalidate it)
     if (p->ctx == ctx && t->ctx == ctx) ctx->pr_cache = guard.release();
+  });
+}
+
+MBX_API int mbx_pagerank_observed(mbx_context* ctx, const mbx_matrix* p, const mbx_tile* t,
+                                  const mbx_simt_config* c, const mbx_pagerank_config* cfg,
+                                  const void* pi0_host, void* pi_host, void* ref_host,
+                                  double* history, mbx_pagerank_observer observer, void* user,
+                                  mbx_pagerank_result* result) {
+  return guarded([&] {
+    require(observer != nullptr, MBX_CONFIG_ERROR, "observer must not be NULL");
+    mbx_pagerank_plan* pl = nullptr;
+    int rc = mbx_pagerank_plan_create(ctx, p, t, c, cfg, &pl);
+    if (rc) fail(rc, g_last_error);
+    std::unique_ptr<mbx_pagerank_plan, int (*)(mbx_pagerank_plan*)> guard(pl,
+                                                                         mbx_pagerank_plan_destroy);
+    Device dg(ctx->device);
+    cudaStream_t st = ctx->stream;
+    void* pi0 = nullptr;
+    void* tmp = dmalloc(ctx, pl->n * pl->vs + 256);
+    struct Bufs {  // released on every exit, the observer's abort included
+      mbx_context* ctx;
+      void** a;
+      void** b;
+      ~Bufs() {
+        dfree(ctx, *a);
+        dfree(ctx, *b);
+        *a = *b = nullptr;
+      }
+    } bufs{ctx, &pi0, &tmp};
+    if (pi0_host) {
+      pi0 = dmalloc(ctx, pl->n * pl->vs);
+      MBX_CUDA(cudaMemcpyAsync(p->vmap ? tmp : pi0, pi0_host, pl->n * pl->vs,
+                               cudaMemcpyHostToDevice, st));
+      if (p->vmap) mbx::launch_vertex_map(ctx, p->precision, pl->n, p->vmap, tmp, pi0, true);
+    }
+    plan_prologue(pl, pi0);
+    std::vector<unsigned char> iterate(size_t(pl->n) * pl->vs);
+    MBX_CUDA(cudaEventRecord(pl->e0, st));
+    const void* yard = pl->cfg.reference_iters > 0 ? pl->ref[pl->cfg.reference_iters & 1]
+                                                   : nullptr;
+    for (int64_t r = 1; r <= pl->cfg.max_iters; ++r) {
+      // one iteration, then the iterate and its scalars reach the host
+      // (solvers.hpp:197-213: mass check, ERR, on_iteration, convergence)
+      const mbx::PrArgs a = pr_args(pl, r, yard);
+      mbx::launch_spmv(ctx, pl->p, pl->t, pl->g, pl->pi[(r - 1) & 1], pl->pi[r & 1],
+                       pl->carry_ws, &a);
+      const void* src = pl->pi[r & 1];
+      if (p->vmap) {
+        mbx::launch_vertex_map(ctx, p->precision, pl->n, p->vmap, src, tmp, false);
+        src = tmp;
+      }
+      int flags[2];
+      mbx::PrScalars sc;
+      MBX_CUDA(cudaMemcpyAsync(iterate.data(), src, iterate.size(), cudaMemcpyDeviceToHost, st));
+      MBX_CUDA(cudaMemcpyAsync(flags, pl->flags, 8, cudaMemcpyDeviceToHost, st));
+      MBX_CUDA(cudaMemcpyAsync(&sc, pl->scal + r, sizeof(sc), cudaMemcpyDeviceToHost, st));
+      MBX_CUDA(cudaStreamSynchronize(st));
+      if (flags[0] == 2) break;  // zero-norm iterate: reported by plan_result, no callback
+      if (observer(r, iterate.data(), sc.err, user) != 0)
+        fail(MBX_ERROR, "pagerank: aborted by the on_iteration observer at iteration " +
+                            std::to_string(r));
+      if (flags[0] == 1) break;
+    }
+    MBX_CUDA(cudaEventRecord(pl->e1, st));
+    pl->ran = true;
+    rc = mbx_pagerank_plan_result(pl, result, history);
+    if (rc) fail(rc, g_last_error);
+    auto download = [&](void* host, const void* dev) {
+      const void* s2 = dev;
+      if (p->vmap) {
+        mbx::launch_vertex_map(ctx, p->precision, pl->n, p->vmap, dev, tmp, false);
+        s2 = tmp;
+      }
+      MBX_CUDA(cudaMemcpyAsync(host, s2, pl->n * pl->vs, cudaMemcpyDeviceToHost, st));
+      MBX_CUDA(cudaStreamSynchronize(st));
+    };
+    if (pi_host) download(pi_host, pl->pi[result->iterations & 1]);
+    if (ref_host) {
+      if (cfg->reference_iters > 0) {
+        download(ref_host, pl->ref[cfg->reference_iters & 1]);
+      } else if (p->precision == MBX_F32) {
+        float* r = static_cast<float*>(ref_host);
+        for (int64_t i = 0; i < pl->n; ++i) r[i] = 1.0f / float(pl->n);
+      } else {
+        double* r = static_cast<double*>(ref_host);
+        for (int64_t i = 0; i < pl->n; ++i) r[i] = 1.0 / double(pl->n);
+      }
+    }
+    MBX_CUDA(cudaStreamSynchronize(st));
   });
 }
 

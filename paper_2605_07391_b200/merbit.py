@@ -634,11 +634,14 @@ class PageRankResult:
 
 
 def pagerank(p, cfg: PageRankConfig, backend: MerbitB200Backend | None = None,
-             c: SimtConfig | None = None, pi0=None) -> PageRankResult:
-    """pagerank<T>(p, cfg, backend): the power loop runs fused on the device.
+             c: SimtConfig | None = None, pi0=None, on_iteration=None) -> PageRankResult:
+    """pagerank<T>(p, cfg, backend, on_iteration): the power loop runs fused on
+    the device.
 
     `p` is the transition matrix (host CSR) when `backend` is None; otherwise the
-    backend's resident matrix and TILE are used."""
+    backend's resident matrix and TILE are used.  on_iteration(r, pi, err), when
+    given, observes every iterate (solvers.hpp:157-158, 209) -- the loop then
+    runs iteration by iteration with a host copy of each iterate."""
     if backend is None:
         dt = np.asarray(p.values).dtype
         c = c or SimtConfig.make(32, select_sigma("f64" if dt == np.float64 else "f32"), 128)
@@ -650,8 +653,29 @@ def pagerank(p, cfg: PageRankConfig, backend: MerbitB200Backend | None = None,
     res = mbx_pagerank_result()
     cc, pc = c._c(), cfg._c()
     p0 = None if pi0 is None else np.ascontiguousarray(pi0, m.dtype)
-    _check(_lib.lib().mbx_pagerank(m.ctx.h, m.h, t.h, C.byref(cc), C.byref(pc), _ptr(p0),
-                                   _ptr(pi), _ptr(ref), _ptr(hist), C.byref(res)))
+    if on_iteration is None:
+        _check(_lib.lib().mbx_pagerank(m.ctx.h, m.h, t.h, C.byref(cc), C.byref(pc), _ptr(p0),
+                                       _ptr(pi), _ptr(ref), _ptr(hist), C.byref(res)))
+    else:
+        n, dt = m.n_rows, m.dtype
+        failure = []
+
+        def trampoline(r, pi_host, err, _user):
+            try:
+                it = np.ctypeslib.as_array(C.cast(pi_host, C.POINTER(
+                    C.c_float if dt == np.float32 else C.c_double)), shape=(n,))
+                on_iteration(int(r), it.copy(), float(err))
+                return 0
+            except BaseException as e:  # stops the run; re-raised after the C call
+                failure.append(e)
+                return 1
+        cb = _lib.PAGERANK_OBSERVER(trampoline)
+        rc = _lib.lib().mbx_pagerank_observed(m.ctx.h, m.h, t.h, C.byref(cc), C.byref(pc),
+                                              _ptr(p0), _ptr(pi), _ptr(ref), _ptr(hist), cb,
+                                              None, C.byref(res))
+        if failure:
+            raise failure[0]
+        _check(rc)
     return PageRankResult(pi=pi, reference_pi=ref, iterations=res.iterations,
                           final_err=res.final_err,
                           status="converged" if res.status == 0 else "max_iterations",

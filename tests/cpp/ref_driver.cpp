@@ -106,6 +106,34 @@ int main() {
            "reference pagerank<double> over B200Backend: " + std::to_string(run.iterations) +
                " iterations, max |pi - pi_csr| = " + std::to_string(dev));
   }
+  // 3b. the device-resident merbit_b200::pagerank with on_iteration: the hook
+  //     sees every iterate (mass invariant, solvers.hpp:157-158, 209) and the
+  //     observed run equals the fused graph run bitwise
+  {
+    const auto p = build_transition(ring_with_chords<double>(100, 260, 42));
+    merbit_b200::Context dctx(0);
+    merbit_b200::MerbitB200Backend<double> eng(dctx, p, merbit_b200::SimtConfig::make(32, 7, 128));
+    merbit_b200::PageRankConfig<double> cfg;
+    index_t calls = 0, last = 0;
+    double worst_mass = 0.0;
+    const auto watch = [&](index_t r, const std::vector<double>& pi, double) {
+      ++calls;
+      last = r;
+      double mass = 0.0;
+      for (double v : pi) mass += std::abs(v);
+      worst_mass = std::max(worst_mass, std::abs(mass - 1.0));
+    };
+    const auto seen = merbit_b200::pagerank<double>(eng, cfg, nullptr, watch);
+    const auto fused = merbit_b200::pagerank<double>(eng, cfg);
+    CsrReferenceBackend<double> csr(p);
+    const auto want = pagerank<double>(p, {}, csr);
+    double dev = 0.0;
+    for (std::size_t i = 0; i < seen.pi.size(); ++i) dev = std::max(dev, std::abs(seen.pi[i] - want.pi[i]));
+    report(calls == seen.iterations && last == seen.iterations &&
+               seen.iterations == fused.iterations && seen.pi == fused.pi && worst_mass <= 1e-12 &&
+               dev <= 1e-12,
+           "merbit_b200::pagerank on_iteration: " + std::to_string(calls) + " iterates observed");
+  }
   // 4. the reference's bicgstab driver over the GPU backend (acceptance c10),
   //    and the device-resident merbit_b200::bicgstab on the same system
   {

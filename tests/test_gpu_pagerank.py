@@ -190,3 +190,41 @@ def test_pagerank_plan_cache(ctx):
     h = mb.pagerank(None, cfg, backend=beq)
     assert g.pi.shape == (Q.n_rows,)
     assert np.array_equal(g.pi.view(np.uint32), h.pi.view(np.uint32))
+
+
+@pytest.mark.parametrize("relabel", [False, True])
+def test_pagerank_on_iteration_observes_every_iterate(ctx, relabel):
+    """on_iteration (solvers.hpp:157-158, 209): called once per iteration
+    with the iterate in the ORIGINAL vertex order and its ERR; the mass
+    invariant holds for each; the observed run equals the fused one bitwise;
+    an exception in the hook propagates."""
+    c = mb.SimtConfig.make(32, 14, 128)
+    P = mb.DeviceMatrix.rmat(ctx, 12, 16, seed=6, transition=True, dtype=np.float32)
+    if relabel:
+        P, _ = P.relabel_by_degree()
+    be = type("B", (), {})()
+    be.matrix, be.tile_, be.c = P, mb.generate_tile_for(P, c), c
+    cfg = mb.PageRankConfig(0.85, 1e-30, 25, 0)
+    seen = []
+
+    def hook(r, pi, err):
+        seen.append((r, pi, err))
+    a = mb.pagerank(None, cfg, backend=be, on_iteration=hook)
+    b = mb.pagerank(None, cfg, backend=be)
+    assert [r for r, _, _ in seen] == list(range(1, 26))
+    assert np.array_equal(a.pi.view(np.uint32), b.pi.view(np.uint32))
+    assert np.array_equal(seen[-1][1].view(np.uint32), b.pi.view(np.uint32))
+    for r, pi, err in seen:
+        assert abs(pi.astype(np.float64).sum() - 1.0) <= 1e-5
+        assert err >= 0.0
+    assert np.array_equal(a.residual_history, b.residual_history)
+
+    calls = []
+
+    def boom(r, pi, err):
+        calls.append(r)
+        if r == 3:
+            raise RuntimeError("stop here")
+    with pytest.raises(RuntimeError, match="stop here"):
+        mb.pagerank(None, cfg, backend=be, on_iteration=boom)
+    assert calls == [1, 2, 3]  # the run stops at the raising iterate
