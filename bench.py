@@ -499,7 +499,7 @@ def main():
                          % (8 * local_nnz / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_per_launch() if scale == 24 and world == 1 else None,
-                     "peak_kind": peak_kind,
+                     "peak_kind": peak_kind, "frac_of_nominal_8tbs": achieved / 8000.0,
                      "kernel": "fused PageRank iteration (spmv_slot_kernel<float,14,PR,HUB> + "
                                "fixup_kernel) on rank 0",
                      "bytes_per_launch": b_iter, "us_per_iteration": t_iter_local * 1e6,
