@@ -94,19 +94,39 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
                                                       n, 0, 32, s));
   const int cand = int(std::min<int64_t>(slots, n));
   std::vector<uint32_t> hc(cand);
+  std::vector<int32_t> hid(cand);
   MBX_CUDA(cudaMemcpyAsync(hc.data(), cnt_sorted, size_t(cand) * 4, cudaMemcpyDeviceToHost, s));
+  MBX_CUDA(cudaMemcpyAsync(hid.data(), ids_sorted, size_t(cand) * 4, cudaMemcpyDeviceToHost, s));
   MBX_CUDA(cudaStreamSynchronize(s));
   // A hub pays off only if it is referenced several times more often than
-  // it is loaded (once per resident CTA per SpMV), and the per-CTA table
+  // it costs to load (once per resident CTA per SpMV), and the per-CTA table
   // load (a serial preamble before any tile) must stay a small fraction
   // (<= 2 %) of that CTA's share of the gathers -- small matrices get small
-  // tables (R-MAT s20: measured 10 % preamble with an uncapped table).
+  // tables (R-MAT s20 in natural order: measured 10 % preamble with an
+  // uncapped table).  The load is counted in 128-byte lines: hubs that share
+  // a line with an earlier hub ride along for free, so the contiguous hub
+  // block of a degree-relabelled matrix (its hubs ARE vertices 0..h-1) costs
+  // 1/32 of a scattered one and small relabelled graphs get full tables.
   const int64_t ctas = int64_t(ctx->sm_count) * tu.ctas_per_sm;
   const uint32_t min_refs = uint32_t(4 * ctas);
-  const int64_t cap = m->nnz / (ctas * 50);
+  const uint32_t min_refs_shared = uint32_t(std::max<int64_t>(ctas / 8, 2));
+  const int64_t cap_lines = m->nnz / (ctas * 50);
+  const int line_shift = m->precision == MBX_F32 ? 5 : 4;  // entries per 128-byte line
+  std::vector<uint8_t> line_seen;
   int h = 0;
-  int64_t covered = 0;
-  while (h < cand && h < cap && hc[h] > min_refs) covered += hc[h++];
+  int64_t covered = 0, lines = 0;
+  while (h < cand) {
+    const int64_t line = int64_t(hid[h]) >> line_shift;
+    if (line_seen.size() <= size_t(line)) line_seen.resize(size_t(line) + 1, 0);
+    const bool fresh = !line_seen[size_t(line)];
+    if (hc[h] <= (fresh ? min_refs : min_refs_shared)) break;
+    if (fresh && lines + 1 > cap_lines) break;
+    if (fresh) {
+      line_seen[size_t(line)] = 1;
+      ++lines;
+    }
+    covered += hc[h++];
+  }
   if (h > 0) {
     MBX_CUDA(cudaMallocAsync(&m->hub_cols, size_t(h) * 4 + 64, s));
     MBX_CUDA(cudaMemcpyAsync(m->hub_cols, ids_sorted, size_t(h) * 4, cudaMemcpyDeviceToDevice, s));
