@@ -457,6 +457,14 @@ def main():
                                               peak)
             extras["spmv_f64"] = spmv_numbers(mb, ctx, stream, scale, np.float64, args.spmv_reps,
                                               peak)
+            # the same SpMVs after the device degree relabelling (preprocessing)
+            for dt, key in ((np.float32, "spmv_f32_relabelled"),
+                            (np.float64, "spmv_f64_relabelled")):
+                extras[key] = spmv_numbers(
+                    mb, ctx, stream, scale, dt, args.spmv_reps, peak,
+                    make=lambda cx, d: mb.DeviceMatrix.rmat(
+                        cx, scale, 16, seed=1, transition=True, dtype=d).relabel_by_degree()[0],
+                    label=f"R-MAT scale {scale} transition, degree-relabelled")
             # BASELINE C3: fp64 power-law, long rows + exactly 10 % empty rows
             extras["c3_powerlaw_f64"] = spmv_numbers(
                 mb, ctx, stream, 0, np.float64, args.spmv_reps, peak,
