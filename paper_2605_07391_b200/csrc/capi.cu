@@ -860,6 +860,7 @@ struct mbx_pagerank_plan_s {
   void* carry_ws = nullptr;
   cudaGraphExec_t graph = nullptr;
   int64_t graph_launches = 0;
+  int64_t* iter_dev = nullptr;  // iterations completed (device-driven loop)
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   bool ran = false;
   // cache key (mbx_pagerank): what the plan was built from
@@ -914,6 +915,25 @@ mbx::PrArgs pr_args(mbx_pagerank_plan* pl, int64_t r, const void* yard) {
   a.iter = int(r);
   a.err_tol = pl->cfg.err_tol;
   return a;
+}
+
+// One body of the device-driven loop: an odd iteration (pi0 -> pi1), an
+// even one (pi1 -> pi0), then the WHILE condition.  Every iteration number,
+// scalar slot and the stop / max_iters guards come from the device.
+void launch_loop_body(mbx_pagerank_plan* pl, cudaGraphConditionalHandle h) {
+  const void* yard = pl->cfg.reference_iters > 0 ? pl->ref[pl->cfg.reference_iters & 1] : nullptr;
+  for (int64_t r = 1; r <= 2; ++r) {
+    mbx::PrArgs a = pr_args(pl, r, yard);
+    a.iter_dev = pl->iter_dev;
+    a.scal_base = pl->scal;
+    a.max_iters = pl->cfg.max_iters;
+    a.prev = nullptr;
+    a.next = nullptr;
+    a.iter = 0;
+    mbx::launch_spmv(pl->ctx, pl->p, pl->t, pl->g, pl->pi[(r - 1) & 1], pl->pi[r & 1],
+                     pl->carry_ws, &a);
+  }
+  mbx::launch_pr_loop_cond(pl->ctx, h, pl->iter_dev, pl->cfg.max_iters, pl->flags);
 }
 
 void launch_power_loop(mbx_pagerank_plan* pl) {
@@ -977,23 +997,48 @@ MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, cons
     pl->carry_ws = dmalloc(ctx, mbx::spmv_workspace_bytes(pl->g, p->precision, true));
     MBX_CUDA(cudaEventCreate(&pl->e0));
     MBX_CUDA(cudaEventCreate(&pl->e1));
-    // Capture the whole fixed-count power loop once as a CUDA graph.
-    if (cfg->max_iters > 0 && cfg->max_iters <= 4096) {
+    pl->iter_dev = static_cast<int64_t*>(dmalloc(ctx, 64));
+    MBX_CUDA(cudaMemsetAsync(pl->iter_dev, 0, 64, ctx->stream));
+    // The power loop as ONE CUDA graph with a device-driven WHILE node: the
+    // body (two iterations + the condition) replays until max_iters or the
+    // stop decision -- an early exit launches nothing more, and any max_iters
+    // fits one small graph.
+    if (cfg->max_iters > 0) {
       MBX_CUDA(cudaStreamSynchronize(ctx->stream));
-      const int64_t before = ctx->launches;
       cudaGraph_t graph;
-      MBX_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      MBX_CUDA(cudaGraphCreate(&graph, 0));
       try {
-        launch_power_loop(pl.get());
+        cudaGraphConditionalHandle h;
+        MBX_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        MBX_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        const int64_t before = ctx->launches;
+        MBX_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal));
+        try {
+          launch_loop_body(pl.get(), h);
+        } catch (...) {
+          cudaGraph_t dummy;
+          cudaStreamEndCapture(ctx->stream, &dummy);
+          throw;
+        }
+        MBX_CUDA(cudaStreamEndCapture(ctx->stream, &body));
+        const int64_t per_body = ctx->launches - before;
+        ctx->launches = before;
+        MBX_CUDA(cudaGraphInstantiate(&pl->graph, graph, 0));
+        // launches of a run to max_iters (an early stop launches fewer)
+        pl->graph_launches = per_body * ((cfg->max_iters + 1) / 2);
       } catch (...) {
-        cudaStreamEndCapture(ctx->stream, &graph);
+        cudaGraphDestroy(graph);
         throw;
       }
-      MBX_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
-      MBX_CUDA(cudaGraphInstantiate(&pl->graph, graph, 0));
       cudaGraphDestroy(graph);
-      pl->graph_launches = ctx->launches - before;
-      ctx->launches = before;
     }
     *out = pl.release();
   });
@@ -1029,6 +1074,7 @@ void plan_prologue(mbx_pagerank_plan* pl, const void* pi0) {
   {
     mbx_context* ctx = pl->ctx;
     MBX_CUDA(cudaMemsetAsync(pl->flags, 0, 8, ctx->stream));
+    if (pl->iter_dev) MBX_CUDA(cudaMemsetAsync(pl->iter_dev, 0, 8, ctx->stream));
     // Yardstick: fixed-count power run on the plain CSR kernel (178-191).
     if (pl->cfg.reference_iters > 0) {
       mbx::launch_pr_init(ctx, pl->p->precision, pl->n, nullptr, pl->ref[0], pl->dangling,
@@ -1117,6 +1163,7 @@ MBX_API int mbx_pagerank_plan_destroy(mbx_pagerank_plan* pl) {
     dfree(ctx, pl->counter);
     dfree(ctx, pl->flags);
     dfree(ctx, pl->carry_ws);
+    dfree(ctx, pl->iter_dev);
     if (pl->e0) cudaEventDestroy(pl->e0);
     if (pl->e1) cudaEventDestroy(pl->e1);
     MBX_CUDA(cudaStreamSynchronize(ctx->stream));

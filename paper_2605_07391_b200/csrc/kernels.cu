@@ -254,16 +254,32 @@ __device__ __forceinline__ void pr_commit(const PrArgs& pr, T base, int64_t row,
                  (pr.dangling[row >> 5] >> (row & 31)) & 1u, out, a);
 }
 
+// iteration bookkeeping of host-unrolled launches (prev/next/iter baked in)
+// and of the device-driven loop (derived from *iter_dev)
+__device__ __forceinline__ bool pr_skip(const PrArgs& pr) {
+  return *pr.stop || (pr.iter_dev && *pr.iter_dev >= pr.max_iters);
+}
+__device__ __forceinline__ const PrScalars* pr_prev(const PrArgs& pr) {
+  return pr.iter_dev ? pr.scal_base + *pr.iter_dev : pr.prev;
+}
+__device__ __forceinline__ PrScalars* pr_next(const PrArgs& pr) {
+  return pr.iter_dev ? pr.scal_base + *pr.iter_dev + 1 : pr.next;
+}
+__device__ __forceinline__ int pr_iter(const PrArgs& pr) {
+  return pr.iter_dev ? int(*pr.iter_dev + 1) : pr.iter;
+}
+
 template <typename T>
 __device__ __forceinline__ T pr_base(const PrArgs& pr) {
   // base = (damping * dangling_mass + 1 - damping) / n, in fp64 then T
-  return static_cast<T>((pr.damping * pr.prev->dangling + (1.0 - pr.damping)) * pr.inv_n);
+  return static_cast<T>((pr.damping * pr_prev(pr)->dangling + (1.0 - pr.damping)) * pr.inv_n);
 }
 
 // Deterministic block reduction of PrAcc (fixed butterfly + fixed warp order)
 // followed by the last-block finalisation into *out.
 __device__ void pr_block_finish(PrAcc a, const PrArgs& pr, double* block_part,
-                                unsigned int* counter, PrScalars* out, bool check_stop) {
+                                unsigned int* counter, PrScalars* out, bool check_stop,
+                                bool advance = false) {
   __shared__ double sm[4][32];
   __shared__ bool is_last;
   // fused exchange: this thread's NVLink stores are performed system-wide
@@ -356,13 +372,16 @@ __device__ void pr_block_finish(PrAcc a, const PrArgs& pr, double* block_part,
     if (check_stop && pr.stop) {
       if (m == 0.0) {
         *pr.stop = 2;  // zero-norm iterate (solvers.hpp:202-205)
-        *pr.stop_iter = pr.iter;
+        *pr.stop_iter = pr_iter(pr);
       } else if (e < pr.err_tol) {
         *pr.stop = 1;  // converged (solvers.hpp:210-213)
-        *pr.stop_iter = pr.iter;
+        *pr.stop_iter = pr_iter(pr);
       }
     }
     *counter = 0;  // ready for the next launch
+    // device-driven loop: this iteration is complete (every block of this
+    // grid has read the old count; the next K2 is stream-ordered after us)
+    if (advance && pr.iter_dev) *pr.iter_dev += 1;
   }
 }
 
@@ -579,7 +598,7 @@ __global__ void __launch_bounds__(1024) spmv_w32_kernel(SpmvParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geometry& g = p.g;
   const int sigma = SIGMA > 0 ? SIGMA : g.sigma;
-  if (PR && *p.pr.stop) return;
+  if (PR && pr_skip(p.pr)) return;
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
   T* hub = reinterpret_cast<T*>(smem_raw);
   const int hub_pad = HUB ? ((g.hub_count + 3) & ~3) : 0;
@@ -610,7 +629,7 @@ __global__ void __launch_bounds__(kThreads) spmv_generic_kernel(SpmvParams<T> p)
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
   const int64_t range = int64_t(blockIdx.x) * g.warps_per_cta + warp;
   if (range >= g.num_ranges) return;
-  if (PR && *p.pr.stop) return;
+  if (PR && pr_skip(p.pr)) return;
   T* buf = reinterpret_cast<T*>(smem_raw) + size_t(warp) * (32 * sigma + 1);
   const uint64_t pol = evict_first_policy();
   const int64_t c0 = range * g.chunks_per_range;
@@ -1045,7 +1064,7 @@ template <typename T, int SIGMA, bool PR, bool HUB, bool PF>
 __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geometry& g = p.g;
-  if (PR && *p.pr.stop) return;
+  if (PR && pr_skip(p.pr)) return;
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
   T* hub = reinterpret_cast<T*>(smem_raw);
   const int hub_pad = HUB ? ((g.hub_count + 3) & ~3) : 0;
@@ -1146,7 +1165,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(const uint32_t* __restrict__
                                                     int64_t num_ranges, int64_t n_rows,
                                                     T* __restrict__ y, PrArgs pr,
                                                     int64_t num_parts) {
-  if (PR && *pr.stop) return;
+  if (PR && pr_skip(pr)) return;
   // one thread per carry entry; the first entry of each run of equal rows
   // folds the run left to right (merbit_spmv.hpp:330-337) -- runs longer
   // than kFixupRun (rows spanning many ranges) are folded by the whole warp
@@ -1214,7 +1233,8 @@ __global__ void __launch_bounds__(256) fixup_kernel(const uint32_t* __restrict__
       acc.mass += rp[2];
       acc.err = fmax(acc.err, rp[3]);
     }
-    pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, pr.check_stop != 0);
+    pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr_next(pr), pr.check_stop != 0,
+                    true);
   }
 }
 
@@ -1551,6 +1571,20 @@ int64_t fixup_blocks(const Geometry& g) {
   const int64_t ne = 2 * g.num_ranges;
   const int64_t n = ne > pr_parts(g) ? ne : pr_parts(g);
   return n > 0 ? (n + 255) / 256 : 1;
+}
+
+// Condition of the device-driven PageRank loop: replay the body while
+// iterations remain and no stop was decided.
+__global__ void pr_loop_cond_kernel(cudaGraphConditionalHandle h, const int64_t* iter_dev,
+                                    int64_t max_iters, const int* stop) {
+  cudaGraphSetConditional(h, (*iter_dev < max_iters && !*stop) ? 1u : 0u);
+}
+
+void launch_pr_loop_cond(mbx_context* ctx, cudaGraphConditionalHandle h, const int64_t* iter_dev,
+                         int64_t max_iters, const int* stop) {
+  pr_loop_cond_kernel<<<1, 1, 0, ctx->stream>>>(h, iter_dev, max_iters, stop);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
 }
 
 size_t spmv_workspace_bytes(const Geometry& g, int precision, bool pagerank) {

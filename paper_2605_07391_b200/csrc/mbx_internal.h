@@ -104,6 +104,13 @@ struct PrArgs {
   static constexpr int kMaxPeers = 7;
   int npeer = 0;
   void* xpeer[kMaxPeers] = {};
+  // Device-driven loop (a CUDA-graph WHILE node replays one body for every
+  // iteration): the iteration number is *iter_dev + 1 (iterations completed
+  // so far, advanced by K3's last block), prev / next are scal_base[r-1] /
+  // scal_base[r], and kernels past max_iters return at once.
+  int64_t* iter_dev = nullptr;
+  PrScalars* scal_base = nullptr;
+  int64_t max_iters = 0;
 };
 
 }  // namespace mbx
@@ -207,6 +214,9 @@ void launch_trace_counts(mbx_context* ctx, const mbx_tile* t,
 void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
                 const PrArgs* pr, double* cta_part, unsigned int* counter);
 int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m);
+// the WHILE node's condition kernel of the device-driven PageRank loop
+void launch_pr_loop_cond(mbx_context* ctx, cudaGraphConditionalHandle h, const int64_t* iter_dev,
+                         int64_t max_iters, const int* stop);
 void launch_pr_init(mbx_context* ctx, int precision, int64_t n,
                     const void* pi0, void* pi, const uint32_t* dangling,
                     PrScalars* out, double* block_part, unsigned int* counter);

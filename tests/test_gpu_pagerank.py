@@ -228,3 +228,41 @@ def test_pagerank_on_iteration_observes_every_iterate(ctx, relabel):
     with pytest.raises(RuntimeError, match="stop here"):
         mb.pagerank(None, cfg, backend=be, on_iteration=boom)
     assert calls == [1, 2, 3]  # the run stops at the raising iterate
+
+
+@pytest.mark.parametrize("iters", [1, 2, 7, 5000])
+def test_device_driven_loop_matches_host_unrolled(ctx, iters):
+    """The CUDA-graph WHILE loop (iteration number, scalar slots and the
+    stop / max_iters guards read on the device) equals the host-unrolled
+    eager loop of the observed path bitwise -- odd and even counts, a single
+    iteration, and a count far beyond what an unrolled graph would hold."""
+    c = mb.SimtConfig.make(32, 14, 128)
+    P = mb.DeviceMatrix.rmat(ctx, 9 if iters > 100 else 11, 16, seed=4, transition=True,
+                             dtype=np.float32)
+    be = type("B", (), {})()
+    be.matrix, be.tile_, be.c = P, mb.generate_tile_for(P, c), c
+    cfg = mb.PageRankConfig(0.85, 1e-30, iters, 0)
+    a = mb.pagerank(None, cfg, backend=be)
+    n_seen = []
+    b = mb.pagerank(None, cfg, backend=be, on_iteration=lambda r, pi, e: n_seen.append(r))
+    assert a.iterations == b.iterations == iters == len(n_seen)
+    assert np.array_equal(a.pi.view(np.uint32), b.pi.view(np.uint32))
+    assert np.array_equal(a.residual_history, b.residual_history)
+
+
+def test_device_driven_loop_early_stop(ctx):
+    """Converged at iteration 1 (a directed ring keeps pi uniform, ERR vs the
+    uniform yardstick is 0): the WHILE loop ends there, pi and the result
+    match the observed (eager) path."""
+    n = 4096
+    ring = O.Csr(n, n, np.arange(n + 1, dtype=np.int64),
+                 np.array([(i - 1) % n for i in range(n)], np.int32), np.ones(n, np.float32))
+    P = mb.DeviceMatrix.from_csr(ctx, ring)
+    c = mb.SimtConfig.make(32, 14, 128)
+    be = type("B", (), {})()
+    be.matrix, be.tile_, be.c = P, mb.generate_tile_for(P, c), c
+    cfg = mb.PageRankConfig(0.85, 1e-6, 210, 0)
+    a = mb.pagerank(None, cfg, backend=be)
+    b = mb.pagerank(None, cfg, backend=be, on_iteration=lambda r, pi, e: None)
+    assert a.status == "converged" and a.iterations == 1 == b.iterations
+    assert np.array_equal(a.pi, b.pi)
