@@ -183,3 +183,27 @@ def test_peer_groups_early_stop_and_start_vector():
         g.quiesce()
     for g in groups:
         g.close()
+
+
+def test_peer_group_world_one_and_limits():
+    """A one-rank peer group (no peers: the barrier meets itself) equals the
+    single-GPU loop bitwise; world > 8 is rejected."""
+    cx = mb.Context(0)
+    P = mb.DeviceMatrix.rmat(cx, 11, 16, seed=8, transition=True, dtype=np.float32)
+    c = mb.SimtConfig.make(32, 14, 128)
+    t = mb.generate_tile_for(P, c)
+    cfg = mb.PageRankConfig(0.85, 1e-30, 9, 0)
+    b = np.array([0, P.n_rows], np.int64)
+    g = PeerShardGroup(cx, P.n_rows, 1, b, 0, P, t, c, cfg)
+    g.connect([g.export()])
+    g.run()
+    res, _ = g.result()
+    be = type("B", (), {})()
+    be.matrix, be.tile_, be.c = P, t, c
+    single = mb.pagerank(None, cfg, backend=be)
+    assert res.iterations == 9
+    assert np.array_equal(g.gather_pi().view(np.uint32), single.pi.view(np.uint32))
+    g.close()
+    with pytest.raises(mb.ConfigError):
+        PeerShardGroup(cx, P.n_rows, 9, np.linspace(0, P.n_rows, 10).astype(np.int64), 0, P, t,
+                       c, cfg)
