@@ -450,8 +450,10 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* m,
  * with its own TILE; pi travels between iterations through one in-place
  * ncclAllGather per iteration over NVLink, the rank's reduction scalars
  * riding in the tail of its chunk.  Replaces the reference's single-process
- * pagerank loop (solvers.hpp:193-215) for the sharded case; reference_iters
- * must be 0 (the yardstick run is single-GPU). */
+ * pagerank loop (solvers.hpp:154-218) for the sharded case, yardstick
+ * included: reference_iters > 0 runs the CSR power iterations (178-191)
+ * through the same exchange and ERR is taken against each rank's rows of
+ * pi*. */
 typedef struct mbx_shard_group_s mbx_shard_group;
 /* ncclGetUniqueId (128 bytes), to be broadcast by the caller's bootstrap. */
 MBX_API int mbx_nccl_unique_id(void* id128);

@@ -333,6 +333,13 @@ struct mbx_shard_group_s {
   mbx::PeerFlags pf{};
   std::vector<void*> opened;   // IPC mappings to close
   int64_t epoch_step = 0;
+  // yardstick run (reference_iters > 0, solvers.hpp:178-191): CSR power
+  // iterations through the same exchange; this rank's rows of pi* stay here
+  void* yloc[2] = {nullptr, nullptr};
+  mbx::PrScalars* yscal = nullptr;
+  // peer barrier slots of one run: 0 entry, 1 + r yardstick iteration r,
+  // main_base + r power iteration r, main_base + max_iters + 1 final
+  int64_t main_base = 2;
 };
 
 namespace {
@@ -366,27 +373,32 @@ void* dm_shared(size_t b) {
 }
 
 // barrier slots of one run: 0 = entry, 1 + r = after iteration r (r >= 0)
-void peer_barrier(mbx_shard_group* G, int slot) {
+void peer_barrier(mbx_shard_group* G, int64_t slot, bool skippable) {
   mbx_context* ctx = G->ctx;
-  mbx::peer_barrier_kernel<<<1, 32, 0, ctx->stream>>>(G->pf, G->run_base, slot,
-                                                      slot > 1 ? G->flags : nullptr, G->perr);
+  mbx::peer_barrier_kernel<<<1, 32, 0, ctx->stream>>>(G->pf, G->run_base, int(slot),
+                                                      skippable ? G->flags : nullptr, G->perr);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
 }
 
-void exchange_and_combine(mbx_shard_group* G, int slot, int iter) {
+// main = false: a yardstick iteration (own scalars, never stops)
+void exchange_and_combine(mbx_shard_group* G, int slot, int iter, bool main = true) {
   mbx_context* ctx = G->ctx;
   unsigned char* base = static_cast<unsigned char*>(G->pi[slot]);
   if (G->peer) {
     // the chunk already went out with the commit: wait for every rank's
-    peer_barrier(G, 1 + iter);
+    if (main)
+      peer_barrier(G, G->main_base + iter, iter > 0);
+    else
+      peer_barrier(G, 1 + iter, false);
   } else if (G->comm) {
     // in-place all-gather: each rank's chunk (pi rows + scalar tail)
     MBX_NCCL(mbx::nccl().AllGather(base + int64_t(G->rank0) * G->chunk_bytes, base, G->chunk_bytes,
                            ncclUint8, G->comm, ctx->stream));
   }
   mbx::combine_kernel<<<1, 32, 0, ctx->stream>>>(base, G->chunk_bytes, G->tail_off, G->world,
-                                                 G->gscal + iter, G->flags, G->flags + 1, iter,
+                                                 (main ? G->gscal : G->yscal) + iter,
+                                                 main ? G->flags : nullptr, G->flags + 1, iter,
                                                  G->cfg.err_tol);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
@@ -402,7 +414,10 @@ void launch_iteration(mbx_shard_group* G, int64_t r) {
     unsigned char* xnew = static_cast<unsigned char*>(G->pi[dst]) + int64_t(s.g) * G->chunk_bytes;
     a.pi_old = pold;
     a.dangling = s.dangling;
-    a.yardstick = nullptr;
+    a.yardstick = G->cfg.reference_iters > 0
+                      ? static_cast<unsigned char*>(G->yloc[G->cfg.reference_iters & 1]) +
+                            int64_t(s.li) * G->lchunk_bytes
+                      : nullptr;
     a.yard_const = G->precision == MBX_F32 ? double(1.0f / float(G->n)) : 1.0 / double(G->n);
     a.damping = G->cfg.damping;
     a.inv_n = 1.0 / double(G->n);
@@ -426,6 +441,38 @@ void launch_iteration(mbx_shard_group* G, int64_t r) {
   exchange_and_combine(G, dst, int(r));
 }
 
+// One yardstick iteration: the plain CSR kernel (spmv_csr_reference, as the
+// single-GPU yardstick) on every local shard, its commit doing the rank
+// update into the local rows of pi* and the exchange copy, then the exchange.
+void launch_yard_iteration(mbx_shard_group* G, int64_t r) {
+  mbx_context* ctx = G->ctx;
+  const int src = int((r - 1) & 1), dst = int(r & 1);
+  for (mbx::Shard& s : G->shards) {
+    mbx::PrArgs a;
+    unsigned char* yold = static_cast<unsigned char*>(G->yloc[src]) + int64_t(s.li) * G->lchunk_bytes;
+    unsigned char* ynew = static_cast<unsigned char*>(G->yloc[dst]) + int64_t(s.li) * G->lchunk_bytes;
+    unsigned char* xnew = static_cast<unsigned char*>(G->pi[dst]) + int64_t(s.g) * G->chunk_bytes;
+    a.pi_old = yold;
+    a.dangling = s.dangling;
+    a.yard_const = 1.0;
+    a.damping = G->cfg.damping;
+    a.inv_n = 1.0 / double(G->n);
+    a.prev = G->yscal + (r - 1);
+    a.next = reinterpret_cast<mbx::PrScalars*>(xnew + G->tail_off);
+    a.xout = G->pi[dst];
+    a.xmap = s.xmap;
+    if (G->peer)
+      for (int k = 0; k < G->world; ++k)
+        if (k != G->rank0) a.xpeer[a.npeer++] = G->xpeer[dst][k];
+    a.stop = G->flags;
+    a.stop_iter = G->flags + 1;
+    a.iter = int(r);
+    a.check_stop = 0;
+    mbx::launch_csr(ctx, &s.view, G->pi[src], ynew, &a, s.block_part, s.counter);
+  }
+  exchange_and_combine(G, dst, int(r), false);
+}
+
 // validation + the fields and buffers every mode shares
 void group_init(mbx_shard_group* G, mbx_context* ctx, int64_t n_global, int world,
                 const int64_t* bounds, int rank0, int nlocal, mbx_matrix* const* mats,
@@ -434,9 +481,6 @@ void group_init(mbx_shard_group* G, mbx_context* ctx, int64_t n_global, int worl
   G->peer = peer;
   if (world < 1 || nlocal < 1 || rank0 < 0 || rank0 + nlocal > world)
     mbx::fail(MBX_CONFIG_ERROR, "shard group: bad world/rank/nlocal");
-  if (cfg->reference_iters != 0)
-    mbx::fail(MBX_UNSUPPORTED, "shard group: the yardstick run (reference_iters > 0) is "
-                               "single-GPU only");
   if (!(cfg->damping >= 0.0 && cfg->damping <= 1.0))
     mbx::fail(MBX_CONFIG_ERROR, "damping must lie in [0, 1]");
   if (!(cfg->err_tol > 0.0)) mbx::fail(MBX_CONFIG_ERROR, "err_tol must be positive");
@@ -472,6 +516,15 @@ void group_init(mbx_shard_group* G, mbx_context* ctx, int64_t n_global, int worl
       MBX_CUDA(cudaMemsetAsync(G->loc[i], 0, G->lchunk_bytes * nlocal, st));
     }
   }
+  if (cfg->reference_iters > 0) {
+    for (int i = 0; i < 2; ++i) {
+      G->yloc[i] = dm(ctx, G->lchunk_bytes * nlocal);
+      MBX_CUDA(cudaMemsetAsync(G->yloc[i], 0, G->lchunk_bytes * nlocal, st));
+    }
+    G->yscal = static_cast<mbx::PrScalars*>(
+        dm(ctx, (cfg->reference_iters + 1) * sizeof(mbx::PrScalars)));
+  }
+  G->main_base = cfg->reference_iters > 0 ? cfg->reference_iters + 3 : 2;
   G->gscal = static_cast<mbx::PrScalars*>(dm(ctx, (cfg->max_iters + 1) * sizeof(mbx::PrScalars)));
   MBX_CUDA(cudaMemsetAsync(G->gscal, 0, (cfg->max_iters + 1) * sizeof(mbx::PrScalars), st));
   G->flags = static_cast<int*>(dm(ctx, 64));
@@ -580,7 +633,8 @@ void group_layout(mbx_shard_group* G, mbx_matrix* const* mats, mbx_tile* const* 
     s.range_part = static_cast<double*>(
         dm(ctx, (std::max(s.geo.num_ranges, mbx::pr_parts(s.geo)) + 1) * 4 * sizeof(double)));
     // K3 blocks, or the pr_init grid (sm_count * 4) when a start vector is given
-    const int64_t nblk = std::max<int64_t>(mbx::fixup_blocks(s.geo) + 1, ctx->sm_count * 4 + 1);
+    const int64_t nblk = std::max<int64_t>({mbx::fixup_blocks(s.geo) + 1, ctx->sm_count * 4 + 1,
+                                            int64_t(mbx::csr_pr_blocks(ctx, &s.view))});
     s.block_part = static_cast<double*>(dm(ctx, nblk * 4 * sizeof(double)));
     s.counter = static_cast<unsigned int*>(dm(ctx, 64));
     MBX_CUDA(cudaMemsetAsync(s.counter, 0, 64, st));
@@ -644,6 +698,8 @@ void group_free(mbx_shard_group* G) {
                     static_cast<void*>(s.counter), s.carry_ws})
       if (p) cudaFreeAsync(p, st);
   }
+  for (void* p : {G->yloc[0], G->yloc[1], static_cast<void*>(G->yscal)})
+    if (p) cudaFreeAsync(p, st);
   for (void* p : {static_cast<void*>(G->gscal), static_cast<void*>(G->flags),
                   static_cast<void*>(G->run_base), static_cast<void*>(G->perr)})
     if (p) cudaFreeAsync(p, st);
@@ -671,6 +727,45 @@ struct GroupDeleter {
   }
 };
 using GroupPtr = std::unique_ptr<mbx_shard_group, GroupDeleter>;
+
+// pi_0 = 1/n on the shard's rows (into `rows_buf`), its non-dangling entries
+// into its chunk of exchange buffer 0 and its scalars into the chunk tail
+void init_shard_uniform(mbx_shard_group* G, const mbx::Shard& s, unsigned char* rows_buf) {
+  mbx_context* ctx = G->ctx;
+  cudaStream_t st = ctx->stream;
+  unsigned char* x0 = static_cast<unsigned char*>(G->pi[0]) + int64_t(s.g) * G->chunk_bytes;
+  auto* tail = reinterpret_cast<mbx::PrScalars*>(x0 + G->tail_off);
+  const int64_t rows = s.r1 - s.r0;
+  auto* cnt = reinterpret_cast<unsigned long long*>(s.counter + 8);
+  MBX_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
+  const unsigned grid = unsigned(ctx->sm_count) * 4;
+  double val;
+  if (G->precision == MBX_F32) {
+    const float v = 1.0f / float(G->n);  // T(1)/static_cast<T>(n) (solvers.hpp:193)
+    val = double(v);
+    mbx::shard_init_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<float*>(rows_buf), rows,
+                                                        v, s.dangling, cnt, s.xmap,
+                                                        static_cast<float*>(G->pi[0]));
+  } else {
+    val = 1.0 / double(G->n);
+    mbx::shard_init_kernel<double><<<grid, 256, 0, st>>>(reinterpret_cast<double*>(rows_buf),
+                                                         rows, val, s.dangling, cnt, s.xmap,
+                                                         static_cast<double*>(G->pi[0]));
+  }
+  mbx::shard_init_tail_kernel<<<1, 1, 0, st>>>(cnt, rows, val, tail);
+  ctx->launches += 2;
+}
+
+// peer groups: this shard's start chunk (values + tail) out to every peer
+void push_start_chunk(mbx_shard_group* G, const mbx::Shard& s) {
+  if (!G->peer) return;
+  const unsigned char* x0 = static_cast<unsigned char*>(G->pi[0]) + int64_t(s.g) * G->chunk_bytes;
+  for (int k = 0; k < G->world; ++k)
+    if (k != G->rank0)
+      MBX_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(G->xpeer[0][k]) +
+                                   int64_t(s.g) * G->chunk_bytes,
+                               x0, G->chunk_bytes, cudaMemcpyDeviceToDevice, G->ctx->stream));
+}
 
 }  // namespace
 
@@ -776,7 +871,8 @@ MBX_API int mbx_shard_group_create_peer(mbx_context* ctx, int64_t n_global, int 
     G->perr = static_cast<int*>(dm(ctx, 64));
     MBX_CUDA(cudaMemsetAsync(G->run_base, 0, 64, ctx->stream));
     MBX_CUDA(cudaMemsetAsync(G->perr, 0, 64, ctx->stream));
-    G->epoch_step = G->cfg.max_iters + 3;  // entry + iterations 0..max + the final barrier
+    // entry, yardstick 0..R, power iterations 0..max, the final barrier
+    G->epoch_step = G->main_base + G->cfg.max_iters + 2;
     local_seen(G.get(), mats, G->seen);
     MBX_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = G.release();
@@ -875,7 +971,22 @@ MBX_API int mbx_shard_group_run(mbx_shard_group* G, const void* pi0_dev) {
       // caller's reads of its rows) is over once all have entered this one
       mbx::bump_epoch_kernel<<<1, 1, 0, st>>>(G->run_base, uint64_t(G->epoch_step));
       ++ctx->launches;
-      peer_barrier(G, 0);
+      peer_barrier(G, 0, false);
+    }
+    // yardstick (reference_iters > 0, solvers.hpp:178-191): CSR power run
+    // from the uniform vector through the same exchange
+    const int64_t R = G->cfg.reference_iters;
+    if (R > 0) {
+      for (mbx::Shard& s : G->shards) {
+        init_shard_uniform(G, s, static_cast<unsigned char*>(G->yloc[0]) +
+                                     int64_t(s.li) * G->lchunk_bytes);
+        push_start_chunk(G, s);
+      }
+      exchange_and_combine(G, 0, 0, false);
+      for (int64_t r = 1; r <= R; ++r) launch_yard_iteration(G, r);
+      // nobody overwrites exchange buffer 0 before every rank's last
+      // yardstick combine has read it
+      if (G->peer) peer_barrier(G, R + 2, false);
     }
     for (mbx::Shard& s : G->shards) {
       unsigned char* x0 = static_cast<unsigned char*>(G->pi[0]) + int64_t(s.g) * G->chunk_bytes;
@@ -899,33 +1010,9 @@ MBX_API int mbx_shard_group_run(mbx_shard_group* G, const void* pi0_dev) {
           ++ctx->launches;
         }
       } else {
-        auto* cnt = reinterpret_cast<unsigned long long*>(s.counter + 8);
-        MBX_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
-        const unsigned grid = unsigned(ctx->sm_count) * 4;
-        double val;
-        if (G->precision == MBX_F32) {
-          const float v = 1.0f / float(G->n);  // T(1)/static_cast<T>(n) (solvers.hpp:193)
-          val = double(v);
-          mbx::shard_init_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<float*>(p0), rows,
-                                                              v, s.dangling, cnt, s.xmap,
-                                                              static_cast<float*>(G->pi[0]));
-        } else {
-          val = 1.0 / double(G->n);
-          mbx::shard_init_kernel<double><<<grid, 256, 0, st>>>(reinterpret_cast<double*>(p0),
-                                                               rows, val, s.dangling, cnt, s.xmap,
-                                                               static_cast<double*>(G->pi[0]));
-        }
-        mbx::shard_init_tail_kernel<<<1, 1, 0, st>>>(cnt, rows, val, tail);
-        ctx->launches += 2;
+        init_shard_uniform(G, s, p0);
       }
-      if (G->peer) {
-        // the start chunk (values + tail) out to every peer, then barrier 1
-        for (int k = 0; k < G->world; ++k)
-          if (k != G->rank0)
-            MBX_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(G->xpeer[0][k]) +
-                                         int64_t(s.g) * G->chunk_bytes,
-                                     x0, G->chunk_bytes, cudaMemcpyDeviceToDevice, st));
-      }
+      push_start_chunk(G, s);
     }
     MBX_CUDA(cudaGetLastError());
     exchange_and_combine(G, 0, 0);
@@ -1037,7 +1124,7 @@ MBX_API int mbx_shard_group_quiesce(mbx_shard_group* G) {
   return sguard([&] {
     if (!G->peer || !G->connected || G->quiesced) return;
     MBX_CUDA(cudaMemsetAsync(G->flags, 0, 8, G->ctx->stream));  // stop must not skip it
-    peer_barrier(G, int(G->epoch_step - 1));
+    peer_barrier(G, G->epoch_step - 1, false);
     G->quiesced = true;
   });
 }

@@ -73,13 +73,33 @@ def test_sharded_convergence_exit(ctx):
     assert grp.gather_pi().tolist() == [0.5, 0.5]
 
 
-def test_reference_iters_rejected_for_shards(ctx):
-    P = mb.DeviceMatrix.rmat(ctx, 10, 16, seed=1, transition=True)
-    c = mb.SimtConfig.make(32, 14, 128)
+@pytest.mark.parametrize("parts", [1, 3])
+def test_shards_with_yardstick_run(ctx, parts):
+    """reference_iters > 0 (the reference's default config runs a 210-step
+    CSR yardstick, solvers.hpp:178-191): the shard group runs it through the
+    same exchange and stops on ERR against it like the single-GPU loop."""
+    P = mb.DeviceMatrix.rmat(ctx, 12, 16, seed=5, transition=True, dtype=np.float64)
+    c = mb.SimtConfig.make(32, 7, 128)
+    cfg = mb.PageRankConfig(0.85, 1e-6, 210, 40)
     t = mb.generate_tile_for(P, c)
-    with pytest.raises(mb.UnsupportedError):
-        ShardGroup(ctx, P.n_rows, 1, [0, P.n_rows], 0, [(P, t)], c, mb.PageRankConfig())
-
+    be = type("B", (), {})()
+    be.matrix, be.tile_, be.c = P, t, c
+    single = mb.pagerank(None, cfg, backend=be)
+    assert single.status == "converged" and 1 < single.iterations < 210
+    ro, _, _ = P.download(want_values=False)
+    b = mb.plan_row_shards(ro, P.n_rows, P.nnz, parts)
+    shards = [(m, mb.generate_tile_for(m, c)) for m in
+              (row_slice(P, int(b[g]), int(b[g + 1])) for g in range(parts))]
+    grp = ShardGroup(ctx, P.n_rows, parts, b, 0, shards, c, cfg)
+    grp.run()
+    res, _ = grp.result()
+    pi = grp.gather_pi()
+    assert res.status == 0 and abs(res.iterations - single.iterations) <= 1
+    if parts == 1:  # the same yardstick and TILE: bitwise
+        assert res.iterations == single.iterations and res.final_err == single.final_err
+        assert np.array_equal(pi, single.pi)
+    else:
+        assert np.abs(pi - single.pi).sum() <= 1e-6
 
 def test_start_vector_path_is_bitwise_equal(ctx):
     import torch

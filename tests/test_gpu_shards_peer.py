@@ -207,3 +207,44 @@ def test_peer_group_world_one_and_limits():
     with pytest.raises(mb.ConfigError):
         PeerShardGroup(cx, P.n_rows, 9, np.linspace(0, P.n_rows, 10).astype(np.int64), 0, P, t,
                        c, cfg)
+
+
+def test_peer_groups_with_yardstick():
+    """The yardstick phase over the fused exchange (its own barrier slots,
+    then a transition barrier before the power loop reuses buffer 0): stop
+    iteration and pi equal the virtual group's."""
+    parts, n_it = 2, 210
+    base = mb.Context(0)
+    c = mb.SimtConfig.make(32, 7, 128)
+    cfg = mb.PageRankConfig(0.85, 1e-6, n_it, 24)
+    P = mb.DeviceMatrix.rmat(base, 11, 16, seed=5, transition=True, dtype=np.float64)
+    ro, _, _ = P.download(want_values=False)
+    b = mb.plan_row_shards(ro, P.n_rows, P.nnz, parts)
+    vs = [(m, mb.generate_tile_for(m, c)) for m in
+          (row_slice(P, int(b[g]), int(b[g + 1])) for g in range(parts))]
+    virt = ShardGroup(base, P.n_rows, parts, b, 0, vs, c, cfg)
+    virt.run()
+    wres, _ = virt.result()
+    want = virt.gather_pi()
+    assert wres.status == 0 and wres.iterations < n_it
+    groups = []
+    for r in range(parts):
+        cx = mb.Context(0)
+        Q = mb.DeviceMatrix.rmat(cx, 11, 16, seed=5, transition=True, dtype=np.float64)
+        L = row_slice(Q, int(b[r]), int(b[r + 1]))
+        groups.append(PeerShardGroup(cx, Q.n_rows, parts, b, r, L, mb.generate_tile_for(L, c),
+                                     c, cfg))
+    blobs = [g.export() for g in groups]
+    for g in groups:
+        g.connect(blobs)
+    for rep in range(2):
+        for g in groups:
+            g.run()
+        for g in groups:
+            res, _ = g.result()
+            assert res.iterations == wres.iterations and res.final_err == wres.final_err
+            assert np.array_equal(g.gather_pi(), want)
+    for g in groups:
+        g.quiesce()
+    for g in groups:
+        g.close()
