@@ -137,3 +137,20 @@ def test_single_rank_nccl_group(ctx):
     single = mb.pagerank(None, mb.PageRankConfig(0.85, 1e-30, 20, 0), backend=be)
     assert res.iterations == 20
     assert np.array_equal(grp.gather_pi().view(np.uint32), single.pi.view(np.uint32))
+
+
+def test_single_rank_nccl_group_with_yardstick(ctx):
+    """The NCCL exchange carries the yardstick phase too (1-rank world)."""
+    from paper_2605_07391_b200.merbit import nccl_unique_id
+    P = mb.DeviceMatrix.rmat(ctx, 11, 16, seed=2, transition=True, dtype=np.float64)
+    c = mb.SimtConfig.make(32, 7, 128)
+    t = mb.generate_tile_for(P, c)
+    cfg = mb.PageRankConfig(0.85, 1e-6, 210, 30)
+    grp = ShardGroup(ctx, P.n_rows, 1, [0, P.n_rows], 0, [(P, t)], c, cfg, nccl_unique_id())
+    grp.run()
+    res, _ = grp.result()
+    be = type("B", (), {})()
+    be.matrix, be.tile_, be.c = P, t, c
+    single = mb.pagerank(None, cfg, backend=be)
+    assert res.iterations == single.iterations and res.final_err == single.final_err
+    assert np.array_equal(grp.gather_pi(), single.pi)
