@@ -263,7 +263,8 @@ __device__ __forceinline__ const PrScalars* pr_prev(const PrArgs& pr) {
   return pr.iter_dev ? pr.scal_base + *pr.iter_dev : pr.prev;
 }
 __device__ __forceinline__ PrScalars* pr_next(const PrArgs& pr) {
-  return pr.iter_dev ? pr.scal_base + *pr.iter_dev + 1 : pr.next;
+  // a baked `next` wins (row shards: the parity's chunk tail)
+  return pr.next ? pr.next : pr.scal_base + *pr.iter_dev + 1;
 }
 __device__ __forceinline__ int pr_iter(const PrArgs& pr) {
   return pr.iter_dev ? int(*pr.iter_dev + 1) : pr.iter;
@@ -1234,7 +1235,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(const uint32_t* __restrict__
       acc.err = fmax(acc.err, rp[3]);
     }
     pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr_next(pr), pr.check_stop != 0,
-                    true);
+                    pr.check_stop != 0);  // row shards: the combine kernel advances
   }
 }
 

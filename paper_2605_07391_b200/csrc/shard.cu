@@ -184,11 +184,19 @@ __global__ void shard_init_tail_kernel(const unsigned long long* count, int64_t 
 
 // Fold the world tails in rank order into the global scalars of iteration
 // `iter` and decide convergence (solvers.hpp:201-213).
+// iter_dev (device-driven loop): the iteration is *iter_dev + 1, `out` is
+// the scalar array's base, and the kernel advances the counter.
 __global__ void combine_kernel(const unsigned char* __restrict__ pi_base, int64_t chunk_bytes,
                                int64_t tail_off, int world, PrScalars* out, int* stop,
-                               int* stop_iter, int iter, double err_tol) {
+                               int* stop_iter, int iter, double err_tol, int64_t* iter_dev,
+                               int64_t max_iters) {
   if (threadIdx.x != 0) return;
   if (stop && *stop) return;
+  if (iter_dev) {
+    if (*iter_dev >= max_iters) return;
+    iter = int(*iter_dev + 1);
+    out += iter;
+  }
   double d = 0.0, r = 0.0, m = 0.0, e = 0.0;
   for (int g = 0; g < world; ++g) {
     const PrScalars* t =
@@ -211,6 +219,12 @@ __global__ void combine_kernel(const unsigned char* __restrict__ pi_base, int64_
       *stop_iter = iter;
     }
   }
+  if (iter_dev) *iter_dev += 1;
+}
+
+__global__ void shard_loop_cond_kernel(cudaGraphConditionalHandle h, const int64_t* iter_dev,
+                                       int64_t max_iters, const int* stop) {
+  cudaGraphSetConditional(h, (*iter_dev < max_iters && !*stop) ? 1u : 0u);
 }
 
 __global__ void slice_rows_kernel(const uint32_t* __restrict__ ro, int64_t r0, int64_t rows,
@@ -239,11 +253,15 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // published it here (acquire).  Skipped once the run has stopped -- every
 // rank reaches the same stop decision at the same iteration.  Bounded: a
 // peer that never arrives sets *err instead of hanging the GPU.
+// iter_dev (device-driven loop): the slot is slot + iteration, and nothing
+// happens past max_iters (every rank skips the same barriers).
 __global__ void peer_barrier_kernel(PeerFlags pf, const uint64_t* __restrict__ base, int slot,
-                                    const int* stop, int* err) {
+                                    const int* stop, int* err, const int64_t* iter_dev,
+                                    int64_t max_iters) {
   if (threadIdx.x != 0) return;
   if (stop && *stop) return;
-  const uint64_t epoch = *base + uint64_t(slot);
+  if (iter_dev && *iter_dev >= max_iters) return;
+  const uint64_t epoch = *base + uint64_t(slot) + (iter_dev ? uint64_t(*iter_dev + 1) : 0ull);
   __threadfence_system();
   for (int k = 0; k < pf.world; ++k)
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pf.f[k] + pf.rank), "l"(epoch)
@@ -340,6 +358,7 @@ struct mbx_shard_group_s {
   // peer barrier slots of one run: 0 entry, 1 + r yardstick iteration r,
   // main_base + r power iteration r, main_base + max_iters + 1 final
   int64_t main_base = 2;
+  int64_t* iter_dev = nullptr;  // device-driven loop (virtual and fused groups)
 };
 
 namespace {
@@ -373,21 +392,28 @@ void* dm_shared(size_t b) {
 }
 
 // barrier slots of one run: 0 = entry, 1 + r = after iteration r (r >= 0)
-void peer_barrier(mbx_shard_group* G, int64_t slot, bool skippable) {
+void peer_barrier(mbx_shard_group* G, int64_t slot, bool skippable,
+                  const int64_t* iter_dev = nullptr) {
   mbx_context* ctx = G->ctx;
   mbx::peer_barrier_kernel<<<1, 32, 0, ctx->stream>>>(G->pf, G->run_base, int(slot),
-                                                      skippable ? G->flags : nullptr, G->perr);
+                                                      skippable ? G->flags : nullptr, G->perr,
+                                                      iter_dev, G->cfg.max_iters);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
 }
 
-// main = false: a yardstick iteration (own scalars, never stops)
-void exchange_and_combine(mbx_shard_group* G, int slot, int iter, bool main = true) {
+// main = false: a yardstick iteration (own scalars, never stops).
+// dev_loop: a power iteration of the device-driven loop (iteration number
+// read from G->iter_dev by the barrier and the combine, which advances it).
+void exchange_and_combine(mbx_shard_group* G, int slot, int iter, bool main = true,
+                          bool dev_loop = false) {
   mbx_context* ctx = G->ctx;
   unsigned char* base = static_cast<unsigned char*>(G->pi[slot]);
   if (G->peer) {
     // the chunk already went out with the commit: wait for every rank's
-    if (main)
+    if (dev_loop)
+      peer_barrier(G, G->main_base, true, G->iter_dev);
+    else if (main)
       peer_barrier(G, G->main_base + iter, iter > 0);
     else
       peer_barrier(G, 1 + iter, false);
@@ -396,15 +422,15 @@ void exchange_and_combine(mbx_shard_group* G, int slot, int iter, bool main = tr
     MBX_NCCL(mbx::nccl().AllGather(base + int64_t(G->rank0) * G->chunk_bytes, base, G->chunk_bytes,
                            ncclUint8, G->comm, ctx->stream));
   }
-  mbx::combine_kernel<<<1, 32, 0, ctx->stream>>>(base, G->chunk_bytes, G->tail_off, G->world,
-                                                 (main ? G->gscal : G->yscal) + iter,
-                                                 main ? G->flags : nullptr, G->flags + 1, iter,
-                                                 G->cfg.err_tol);
+  mbx::combine_kernel<<<1, 32, 0, ctx->stream>>>(
+      base, G->chunk_bytes, G->tail_off, G->world,
+      dev_loop ? G->gscal : (main ? G->gscal : G->yscal) + iter, main ? G->flags : nullptr,
+      G->flags + 1, iter, G->cfg.err_tol, dev_loop ? G->iter_dev : nullptr, G->cfg.max_iters);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
 }
 
-void launch_iteration(mbx_shard_group* G, int64_t r) {
+void launch_iteration(mbx_shard_group* G, int64_t r, bool dev_loop = false) {
   mbx_context* ctx = G->ctx;
   const int src = int((r - 1) & 1), dst = int(r & 1);
   for (mbx::Shard& s : G->shards) {
@@ -436,9 +462,15 @@ void launch_iteration(mbx_shard_group* G, int64_t r) {
     a.iter = int(r);
     a.err_tol = G->cfg.err_tol;
     a.check_stop = 0;
+    if (dev_loop) {  // prev from the device counter, next stays the parity's tail
+      a.iter_dev = G->iter_dev;
+      a.scal_base = G->gscal;
+      a.max_iters = G->cfg.max_iters;
+      a.prev = nullptr;
+    }
     mbx::launch_spmv(ctx, &s.view, s.tile, s.geo, G->pi[src], pnew, s.carry_ws, &a);
   }
-  exchange_and_combine(G, dst, int(r));
+  exchange_and_combine(G, dst, int(r), true, dev_loop);
 }
 
 // One yardstick iteration: the plain CSR kernel (spmv_csr_reference, as the
@@ -649,13 +681,58 @@ void group_layout(mbx_shard_group* G, mbx_matrix* const* mats, mbx_tile* const* 
   MBX_CUDA(cudaStreamSynchronize(st));
 }
 
-// the fixed-count loop as one CUDA graph
+// The power loop as one CUDA graph.  Virtual and fused groups: a
+// device-driven WHILE node (body = an odd and an even iteration + the
+// condition; the combine advances the iteration counter), so an early stop
+// launches nothing more and any max_iters fits.  NCCL groups: the unrolled
+// fixed-count loop (the collective is not placed inside a conditional body).
 void group_capture(mbx_shard_group* G) {
   mbx_context* ctx = G->ctx;
   cudaStream_t st = ctx->stream;
   MBX_CUDA(cudaEventCreate(&G->e0));
   MBX_CUDA(cudaEventCreate(&G->e1));
-  if (G->cfg.max_iters > 0 && G->cfg.max_iters <= 4096) {
+  if (!G->comm && G->cfg.max_iters > 0) {
+    G->iter_dev = static_cast<int64_t*>(dm(ctx, 64));
+    MBX_CUDA(cudaMemsetAsync(G->iter_dev, 0, 64, st));
+    MBX_CUDA(cudaStreamSynchronize(st));
+    cudaGraph_t graph;
+    MBX_CUDA(cudaGraphCreate(&graph, 0));
+    try {
+      cudaGraphConditionalHandle h;
+      MBX_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      MBX_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      const int64_t before = ctx->launches;
+      MBX_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeThreadLocal));
+      try {
+        launch_iteration(G, 1, true);
+        launch_iteration(G, 2, true);
+        mbx::shard_loop_cond_kernel<<<1, 1, 0, st>>>(h, G->iter_dev, G->cfg.max_iters, G->flags);
+        ++ctx->launches;
+        MBX_CUDA(cudaGetLastError());
+      } catch (...) {
+        cudaGraph_t dummy;
+        cudaStreamEndCapture(st, &dummy);
+        throw;
+      }
+      MBX_CUDA(cudaStreamEndCapture(st, &body));
+      const int64_t per_body = ctx->launches - before;
+      ctx->launches = before;
+      MBX_CUDA(cudaGraphInstantiate(&G->graph, graph, 0));
+      G->graph_launches = per_body * ((G->cfg.max_iters + 1) / 2);
+    } catch (...) {
+      cudaGraphDestroy(graph);
+      throw;
+    }
+    cudaGraphDestroy(graph);
+  } else if (G->cfg.max_iters > 0 && G->cfg.max_iters <= 4096) {
     MBX_CUDA(cudaStreamSynchronize(st));
     const int64_t before = ctx->launches;
     cudaGraph_t graph;
@@ -698,7 +775,8 @@ void group_free(mbx_shard_group* G) {
                     static_cast<void*>(s.counter), s.carry_ws})
       if (p) cudaFreeAsync(p, st);
   }
-  for (void* p : {G->yloc[0], G->yloc[1], static_cast<void*>(G->yscal)})
+  for (void* p : {G->yloc[0], G->yloc[1], static_cast<void*>(G->yscal),
+                  static_cast<void*>(G->iter_dev)})
     if (p) cudaFreeAsync(p, st);
   for (void* p : {static_cast<void*>(G->gscal), static_cast<void*>(G->flags),
                   static_cast<void*>(G->run_base), static_cast<void*>(G->perr)})
@@ -1016,6 +1094,7 @@ MBX_API int mbx_shard_group_run(mbx_shard_group* G, const void* pi0_dev) {
     }
     MBX_CUDA(cudaGetLastError());
     exchange_and_combine(G, 0, 0);
+    if (G->iter_dev) MBX_CUDA(cudaMemsetAsync(G->iter_dev, 0, 8, st));
     MBX_CUDA(cudaEventRecord(G->e0, st));
     if (G->graph) {
       MBX_CUDA(cudaGraphLaunch(G->graph, st));

@@ -154,3 +154,22 @@ def test_single_rank_nccl_group_with_yardstick(ctx):
     single = mb.pagerank(None, cfg, backend=be)
     assert res.iterations == single.iterations and res.final_err == single.final_err
     assert np.array_equal(grp.gather_pi(), single.pi)
+
+
+@pytest.mark.parametrize("parts", [1, 2])
+def test_shard_group_device_loop_long_run(ctx, parts):
+    """The shard groups' WHILE-node loop: 5000 iterations (beyond any
+    unrolled graph) equal the single-GPU loop (bitwise with one shard)."""
+    P = mb.DeviceMatrix.rmat(ctx, 8, 16, seed=3, transition=True, dtype=np.float32)
+    c = mb.SimtConfig.make(32, 14, 128)
+    cfg = mb.PageRankConfig(0.85, 1e-30, 5000, 0)
+    pi, res, hist, _ = sharded_pagerank(ctx, P, parts, 5000, c)
+    t = mb.generate_tile_for(P, c)
+    be = type("B", (), {})()
+    be.matrix, be.tile_, be.c = P, t, c
+    single = mb.pagerank(None, cfg, backend=be)
+    assert res.iterations == single.iterations == 5000
+    if parts == 1:
+        assert np.array_equal(pi.view(np.uint32), single.pi.view(np.uint32))
+    else:
+        assert np.abs(pi.astype(np.float64) - single.pi).sum() <= 1e-6
