@@ -11,6 +11,8 @@
 //    into a device TILE (layout in io.cpp).
 #include <cub/cub.cuh>
 
+#include <type_traits>
+
 #include <memory>
 #include <string>
 #include <vector>
@@ -182,6 +184,44 @@ __global__ void relabel_keys_kernel(const uint32_t* __restrict__ ro,
     for (uint32_t k = ro[r] + lid; k < ro[r + 1]; k += 32)
       keys[k] = rr + (unsigned long long)rank[cols[k]];
   }
+}
+
+// new row lengths: row rank[r] of P' is row r of P
+__global__ void relabel_lengths_kernel(const uint32_t* __restrict__ ro, int64_t n,
+                                       const int32_t* __restrict__ rank,
+                                       uint32_t* __restrict__ len) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x)
+    len[rank[r]] = ro[r + 1] - ro[r];
+}
+
+// row r of P goes to row rank[r] of P' with its columns renamed (unsorted;
+// a segmented sort orders them), one warp per row
+template <typename T>
+__global__ void relabel_scatter_kernel(const uint32_t* __restrict__ ro,
+                                       const int32_t* __restrict__ cols,
+                                       const T* __restrict__ vals, int64_t n,
+                                       const int32_t* __restrict__ rank,
+                                       const uint32_t* __restrict__ ro2,
+                                       int32_t* __restrict__ cols2, T* __restrict__ vals2) {
+  const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lid = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < n; r += nw) {
+    const uint32_t b = ro[r], e = ro[r + 1], d = ro2[rank[r]];
+    for (uint32_t k = b + lid; k < e; k += 32) {
+      cols2[d + (k - b)] = rank[cols[k]];
+      vals2[d + (k - b)] = vals[k];
+    }
+  }
+}
+
+// offsets of a row batch relative to its first row
+__global__ void rebase_offsets_kernel(const uint32_t* __restrict__ ro, int64_t r0, int64_t rows,
+                                      int32_t* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= rows;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = int32_t(ro[r0 + i] - ro[r0]);
 }
 
 template <typename F>
@@ -474,36 +514,92 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
     p->ro = static_cast<uint32_t*>(dm((n + 1) * 4 + 64, true));
     MBX_CUDA(cudaMemsetAsync(p->vals, 0, m * vs + 256, s));
     MBX_CUDA(cudaMemsetAsync(p->cols, 0, m * 4 + 256, s));
-    // the sort's input keys are dead after the sort: their buffer takes the
-    // decoded row ids (2 GB less to allocate at s24)
-    auto* keys = static_cast<unsigned long long*>(dm(m * 8 + 8));
-    auto* rows = reinterpret_cast<int64_t*>(keys);
-    if (m) {
-      auto* keys2 = static_cast<unsigned long long*>(dm(m * 8 + 8));
-      mbx::relabel_keys_kernel<<<grid, 256, 0, s>>>(a->ro, a->cols, n, rank, keys);
-      const unsigned long long span = (unsigned long long)n * (unsigned long long)n;
-      int bits = 1;
-      while (bits < 64 && (1ull << bits) < span) ++bits;
-      size_t tb2 = 0;
-      if (a->precision == MBX_F32) {
-        const float* v = static_cast<const float*>(a->vals);
-        MBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, keys, keys2, v,
-                                                 static_cast<float*>(p->vals), m, 0, bits, s));
-        void* t2 = dm(tb2);
-        MBX_CUDA(cub::DeviceRadixSort::SortPairs(t2, tb2, keys, keys2, v,
-                                                 static_cast<float*>(p->vals), m, 0, bits, s));
-      } else {
-        const double* v = static_cast<const double*>(a->vals);
-        MBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, keys, keys2, v,
-                                                 static_cast<double*>(p->vals), m, 0, bits, s));
-        void* t2 = dm(tb2);
-        MBX_CUDA(cub::DeviceRadixSort::SortPairs(t2, tb2, keys, keys2, v,
-                                                 static_cast<double*>(p->vals), m, 0, bits, s));
-      }
-      mbx::split_keys_kernel<<<grid, 256, 0, s>>>(keys2, m, n, rows, p->cols);
+    // P' = Q P Q^T without a global key sort: the new row offsets come from
+    // the permuted row lengths, every row is copied to its new place with
+    // renamed columns, and one segmented sort per row batch restores
+    // ascending columns (8 bytes of scratch per nonzero at fp32 instead of
+    // the ~30 of a 64-bit (row, column) key sort -- the first call in a
+    // process pays for every byte the memory pool grows by)
+    {
+      auto* len = static_cast<uint32_t*>(dm((n + 1) * 4 + 64));
+      MBX_CUDA(cudaMemsetAsync(len, 0, (n + 1) * 4 + 64, s));
+      mbx::relabel_lengths_kernel<<<grid, 256, 0, s>>>(a->ro, n, rank, len);
+      size_t tbs = 0;
+      MBX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tbs, len, p->ro, n + 1, s));
+      void* ts = dm(tbs);
+      MBX_CUDA(cub::DeviceScan::ExclusiveSum(ts, tbs, len, p->ro, n + 1, s));
+      ctx->launches += 2;
     }
-    mbx::row_offsets_kernel<<<mbx::grid_of(n + 1, ctx), 256, 0, s>>>(rows, m, n, p->ro);
-    ctx->launches += 6;
+    if (m) {
+      auto* cols_b = static_cast<int32_t*>(dm(m * 4 + 256));
+      void* vals_b = dm(m * vs + 256);
+      // unsorted rows into the B buffers, sorted by the segmented sort into p
+      if (a->precision == MBX_F32)
+        mbx::relabel_scatter_kernel<float><<<grid, 256, 0, s>>>(
+            a->ro, a->cols, static_cast<const float*>(a->vals), n, rank, p->ro, cols_b,
+            static_cast<float*>(vals_b));
+      else
+        mbx::relabel_scatter_kernel<double><<<grid, 256, 0, s>>>(
+            a->ro, a->cols, static_cast<const double*>(a->vals), n, rank, p->ro, cols_b,
+            static_cast<double*>(vals_b));
+      ++ctx->launches;
+      std::vector<uint32_t> ro_h(n + 1);
+      MBX_CUDA(cudaMemcpyAsync(ro_h.data(), p->ro, (n + 1) * 4, cudaMemcpyDeviceToHost, s));
+      MBX_CUDA(cudaStreamSynchronize(s));
+      // row batches of < 2^30 nonzeros (CUB's item counts are int)
+      constexpr int64_t kBatch = int64_t(1) << 30;
+      auto* offs = static_cast<int32_t*>(dm((n + 1) * 4 + 64));
+      void* tsort = nullptr;
+      size_t tsort_bytes = 0;
+      for (int64_t r0 = 0; r0 < n;) {
+        int64_t r1 = r0 + 1;
+        {  // furthest r1 with ro[r1] - ro[r0] < kBatch (a single longer row stands alone)
+          int64_t lo = r0 + 1, hi = n;
+          while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (int64_t(ro_h[mid]) - int64_t(ro_h[r0]) < kBatch) lo = mid; else hi = mid - 1;
+          }
+          r1 = lo;
+        }
+        const int64_t rows = r1 - r0, base = ro_h[r0], items = int64_t(ro_h[r1]) - base;
+        if (items > 0) {
+          mbx::rebase_offsets_kernel<<<mbx::grid_of(rows + 1, ctx), 256, 0, s>>>(p->ro, r0, rows,
+                                                                                 offs);
+          ++ctx->launches;
+          // ping-pong between the B buffers and p (no internal copies in
+          // the temp storage); a batch that ends in B is copied over
+          auto sort = [&](auto* vb, auto* vp) {
+            using V = std::remove_pointer_t<decltype(vb)>;
+            cub::DoubleBuffer<int32_t> kd(cols_b + base, p->cols + base);
+            cub::DoubleBuffer<V> vd(vb + base, vp + base);
+            size_t need = 0;
+            MBX_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, need, kd, vd, int(items),
+                                                         int(rows), offs, offs + 1, s));
+            if (need > tsort_bytes) {
+              if (tsort) cudaFreeAsync(tsort, s);
+              MBX_CUDA(cudaMallocAsync(&tsort, need, s));
+              tsort_bytes = need;
+            }
+            MBX_CUDA(cub::DeviceSegmentedSort::SortPairs(tsort, need, kd, vd, int(items),
+                                                         int(rows), offs, offs + 1, s));
+            if (kd.Current() != p->cols + base)
+              MBX_CUDA(cudaMemcpyAsync(p->cols + base, kd.Current(), items * 4,
+                                       cudaMemcpyDeviceToDevice, s));
+            if (vd.Current() != vp + base)
+              MBX_CUDA(cudaMemcpyAsync(vp + base, vd.Current(), items * sizeof(V),
+                                       cudaMemcpyDeviceToDevice, s));
+          };
+          if (a->precision == MBX_F32)
+            sort(static_cast<float*>(vals_b), static_cast<float*>(p->vals));
+          else
+            sort(static_cast<double*>(vals_b), static_cast<double*>(p->vals));
+          ++ctx->launches;
+        }
+        r0 = r1;
+      }
+      if (tsort) cudaFreeAsync(tsort, s);
+    }
+    ctx->launches += 3;
     MBX_CUDA(cudaGetLastError());
     if (rank_host && n)
       MBX_CUDA(cudaMemcpyAsync(rank_host, rank, n * 4, cudaMemcpyDeviceToHost, s));
