@@ -804,7 +804,8 @@ class ShardGroup:
     """Row-sharded PageRank: `shards` = [(DeviceMatrix, Tile)] owned by this
     process for ranks rank0 .. rank0+len(shards)-1 of `world`.  nccl_id None:
     all shards local, sharing one buffer (single-GPU check of the sharded
-    path); otherwise one shard per process joined over NCCL."""
+    path); otherwise one shard per process joined over NCCL.  cfg.reference_iters
+    > 0 runs the reference's yardstick through the same exchange first."""
 
     def __init__(self, ctx: Context, n_global: int, world: int, bounds, rank0: int, shards,
                  c: SimtConfig, cfg: PageRankConfig, nccl_id: bytes | None = None):
