@@ -154,6 +154,52 @@ def cpu_reference_pagerank(ro, cols, n, iters_per_step, steps, warmup, nthreads)
     return {"value": done / secs, "seconds": secs, "iterations": done, "preprocess_seconds": pre}
 
 
+def c1_numbers(mb, ctx, stream, peak, with_ref):
+    """BASELINE config 1: R-MAT scale 20 fp32 (values U[0,1)), MERBIT
+    preprocessing (TILE + hub table + slot copy, wall clock incl. syncs) and
+    one SpMV on the device, beside the reference's generate_tile and one
+    spmv_merbit on ThreadPool(nproc) (oracle/_ref) for the same matrix."""
+    import numpy as np
+    import torch
+    A = mb.DeviceMatrix.rmat(ctx, 20, 16, seed=1, dtype=np.float32)
+    c = mb.SimtConfig.make(32, 14, 128)
+    x = torch.rand(A.n_cols, device="cuda", dtype=torch.float32)
+    y = torch.empty(A.n_rows, device="cuda", dtype=torch.float32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    t = mb.generate_tile_for(A, c)
+    A.build_xcache()
+    mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr())  # builds the slot copy
+    torch.cuda.synchronize()
+    first_s = time.perf_counter() - t0
+    ts = time_device(stream, lambda: mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr()), 50)
+    m, n = A.nnz, A.n_rows
+    b = 8 * m + 12 * n + 4
+    out = {"matrix": "R-MAT scale 20 fp32, values U[0,1)", "nnz": m, "n": n,
+           "tile_ms": t.preprocess_seconds * 1e3,
+           "preprocess_plus_first_spmv_ms": first_s * 1e3, "spmv_ms": ts * 1e3,
+           "gflops": 2 * m / ts / 1e9, "frac": b / ts / 1e9 / peak}
+    if with_ref:
+        import oracle as O
+        if O.ref() is not None:
+            ro, cols, vals = A.download()
+            nthreads = os.cpu_count() or 1
+            eng = O.RefEngine(O.Csr(n, A.n_cols, ro, cols, vals), 32, 14, 128, nthreads)
+            xh = x.cpu().numpy()
+            eng.apply(xh)
+            reps = 5
+            t1 = time.perf_counter()
+            for _ in range(reps):
+                eng.apply(xh)
+            ref_spmv = (time.perf_counter() - t1) / reps
+            out.update({"reference_generate_tile_ms": eng.preprocess_seconds * 1e3,
+                        "reference_spmv_ms": ref_spmv * 1e3, "reference_threads": nthreads,
+                        "speedup_spmv": ref_spmv / ts,
+                        "speedup_preprocess": eng.preprocess_seconds / t.preprocess_seconds})
+            eng.close()
+    return out
+
+
 def run_reference(args):
     """--impl reference: the reference CPU implementation on this box's cores."""
     if int(os.environ.get("RANK", "0")) != 0:
@@ -472,6 +518,8 @@ def main():
                     make=lambda cx, d: mb.DeviceMatrix.rmat(
                         cx, scale, 16, seed=1, transition=True, dtype=d).relabel_by_degree()[0],
                     label=f"R-MAT scale {scale} transition, degree-relabelled")
+            extras["c1_rmat_s20_f32"] = c1_numbers(mb, ctx, stream, peak,
+                                                   not args.no_cpu_baseline)
             # BASELINE C3: fp64 power-law, long rows + exactly 10 % empty rows
             extras["c3_powerlaw_f64"] = spmv_numbers(
                 mb, ctx, stream, 0, np.float64, args.spmv_reps, peak,
