@@ -495,7 +495,7 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
     auto* order = static_cast<int32_t*>(dm(n * 4 + 64));
     auto* rank = static_cast<int32_t*>(dm(n * 4 + 64));
     MBX_CUDA(cudaMemsetAsync(cnt, 0, n * 4 + 64, s));
-    if (m) mbx::count_columns_kernel<<<grid, 256, 0, s>>>(a->cols, m, cnt);
+    mbx::launch_count_columns(ctx, a->cols, m, n, cnt);
     mbx::iota32_kernel<<<grid, 256, 0, s>>>(ids, n);
     size_t tb = 0;
     MBX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt, cnt2, ids, order, n, 0,

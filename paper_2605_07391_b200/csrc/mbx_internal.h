@@ -214,6 +214,10 @@ void launch_trace_counts(mbx_context* ctx, const mbx_tile* t,
 void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
                 const PrArgs* pr, double* cta_part, unsigned int* counter);
 int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m);
+// cnt[c] += #{k : cols[k] == c} (cnt zeroed by the caller); hot low columns
+// are counted in shared memory first
+void launch_count_columns(mbx_context* ctx, const int32_t* cols, int64_t nnz, int64_t ncols,
+                          uint32_t* cnt);
 // the WHILE node's condition kernel of the device-driven PageRank loop
 void launch_pr_loop_cond(mbx_context* ctx, cudaGraphConditionalHandle h, const int64_t* iter_dev,
                          int64_t max_iters, const int* stop);
