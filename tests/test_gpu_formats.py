@@ -133,3 +133,49 @@ def test_degree_stats_reference_cases(ctx):
                                                 np.zeros(0, np.int32), np.zeros(0)))
     with pytest.raises(mb.DimensionError):
         empty.degree_stats(7)
+
+
+@pytest.mark.parametrize("case", ["rmat", "empty_rows", "one_dense_row", "single", "no_nnz"])
+def test_relabel_by_degree_structure(ctx, case):
+    """P' = Q P Q^T exactly: rank = vertices by descending column count (ties
+    by id), row rank[r] of P' holds row r of P with columns renamed and sorted
+    ascending, values carried along -- checked against numpy."""
+    rng = np.random.default_rng(11)
+    if case == "rmat":
+        a = O.rmat(11, 8, 2, transposed=True)
+        a = O.Csr(a.n_rows, a.n_cols, a.row_offsets, a.col_indices,
+                  rng.random(a.col_indices.size))
+    elif case == "empty_rows":
+        n = 300
+        lens = rng.integers(0, 6, n)
+        lens[rng.random(n) < 0.4] = 0
+        ro = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]
+                              ).astype(np.int32)
+        a = O.Csr(n, n, ro, cols, rng.random(cols.size))
+    elif case == "one_dense_row":
+        n = 2000
+        ro = np.zeros(n + 1, np.int64)
+        ro[1:] = n  # row 0 holds every column, the rest are empty
+        a = O.Csr(n, n, ro, np.arange(n, dtype=np.int32), rng.random(n))
+    elif case == "single":
+        a = O.Csr(1, 1, np.array([0, 1], np.int64), np.array([0], np.int32), np.array([2.5]))
+    else:
+        a = O.Csr(5, 5, np.zeros(6, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    m = mb.DeviceMatrix.from_csr(ctx, a)
+    q, rank = m.relabel_by_degree()
+    n = a.n_rows
+    cnt = np.bincount(a.col_indices, minlength=n)
+    want_rank = np.empty(n, np.int64)
+    want_rank[np.lexsort((np.arange(n), -cnt))] = np.arange(n)
+    assert np.array_equal(rank, want_rank)
+    ro2, c2, v2 = q.download()
+    lens = np.diff(a.row_offsets)
+    assert np.array_equal(np.diff(ro2)[want_rank], lens)
+    for r in range(n):
+        seg = slice(a.row_offsets[r], a.row_offsets[r + 1])
+        newc = want_rank[a.col_indices[seg]]
+        order = np.argsort(newc, kind="stable")
+        s2 = slice(ro2[want_rank[r]], ro2[want_rank[r] + 1])
+        assert np.array_equal(c2[s2], newc[order])
+        assert np.array_equal(v2[s2], a.values[seg][order])
