@@ -105,16 +105,17 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_peer_groups_across_two_processes(tmp_path):
-    """Two processes, CUDA IPC mappings, gloo only for the bootstrap."""
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_groups_across_processes(tmp_path, world):
+    """Two / three processes, CUDA IPC mappings, gloo only for the bootstrap."""
     iters = 8
     base = mb.Context(0)
-    want, wres, _, b = virtual_pi(base, 11, 2, iters)
+    want, wres, _, b = virtual_pi(base, 11, world, iters)
     np.save(tmp_path / "bounds.npy", b)
     port = _free_port()
     procs = []
-    for r in range(2):
-        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1",
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
                    MASTER_PORT=str(port), PYTHONPATH=ROOT)
         procs.append(subprocess.Popen(
             [sys.executable, os.path.join(ROOT, "tests", "peer_rank.py"), str(tmp_path),
@@ -130,7 +131,7 @@ def test_peer_groups_across_two_processes(tmp_path):
         outs.append(out.decode())
     for p, o in zip(procs, outs):
         assert p.returncode == 0, o
-    for r in range(2):
+    for r in range(world):
         pi = np.load(tmp_path / f"pi{r}.npy")
         assert np.array_equal(pi.view(np.uint32), want.view(np.uint32)), r
         resid = float(np.load(tmp_path / f"resid{r}.npy"))
