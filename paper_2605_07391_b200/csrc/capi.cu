@@ -1002,8 +1002,27 @@ MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, cons
     // The power loop as ONE CUDA graph with a device-driven WHILE node: the
     // body (two iterations + the condition) replays until max_iters or the
     // stop decision -- an early exit launches nothing more, and any max_iters
-    // fits one small graph.
-    if (cfg->max_iters > 0) {
+    // fits one small graph.  MBX_GRAPH_MODE=unrolled captures the fixed-count
+    // loop instead (ncu does not profile kernels inside conditional nodes),
+    // =eager launches every kernel from the host.
+    const mbx::GraphMode gmode = mbx::graph_mode();
+    if (cfg->max_iters > 0 && gmode == mbx::GraphMode::unrolled && cfg->max_iters <= 4096) {
+      MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+      const int64_t before = ctx->launches;
+      cudaGraph_t graph;
+      MBX_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        launch_power_loop(pl.get());
+      } catch (...) {
+        cudaStreamEndCapture(ctx->stream, &graph);
+        throw;
+      }
+      MBX_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+      MBX_CUDA(cudaGraphInstantiate(&pl->graph, graph, 0));
+      cudaGraphDestroy(graph);
+      pl->graph_launches = ctx->launches - before;
+      ctx->launches = before;
+    } else if (cfg->max_iters > 0 && gmode == mbx::GraphMode::device_loop) {
       MBX_CUDA(cudaStreamSynchronize(ctx->stream));
       cudaGraph_t graph;
       MBX_CUDA(cudaGraphCreate(&graph, 0));

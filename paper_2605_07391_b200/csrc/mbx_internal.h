@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "merbit_b200.h"
@@ -214,6 +215,17 @@ void launch_trace_counts(mbx_context* ctx, const mbx_tile* t,
 void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
                 const PrArgs* pr, double* cta_part, unsigned int* counter);
 int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m);
+// How iterative loops are replayed: one graph with a device-driven WHILE node
+// (default), the fixed-count loop captured unrolled, or host launches
+// (MBX_GRAPH_MODE = while | unrolled | eager; profilers do not descend into
+// conditional graph nodes).
+enum class GraphMode { device_loop, unrolled, eager };
+inline GraphMode graph_mode() {
+  const char* e = std::getenv("MBX_GRAPH_MODE");
+  if (e && std::string(e) == "unrolled") return GraphMode::unrolled;
+  if (e && std::string(e) == "eager") return GraphMode::eager;
+  return GraphMode::device_loop;
+}
 // cnt[c] += #{k : cols[k] == c} (cnt zeroed by the caller); hot low columns
 // are counted in shared memory first
 void launch_count_columns(mbx_context* ctx, const int32_t* cols, int64_t nnz, int64_t ncols,

@@ -691,7 +691,9 @@ void group_capture(mbx_shard_group* G) {
   cudaStream_t st = ctx->stream;
   MBX_CUDA(cudaEventCreate(&G->e0));
   MBX_CUDA(cudaEventCreate(&G->e1));
-  if (!G->comm && G->cfg.max_iters > 0) {
+  const mbx::GraphMode gmode = mbx::graph_mode();
+  if (gmode == mbx::GraphMode::eager) return;
+  if (!G->comm && G->cfg.max_iters > 0 && gmode == mbx::GraphMode::device_loop) {
     G->iter_dev = static_cast<int64_t*>(dm(ctx, 64));
     MBX_CUDA(cudaMemsetAsync(G->iter_dev, 0, 64, st));
     MBX_CUDA(cudaStreamSynchronize(st));
