@@ -196,32 +196,70 @@ __global__ void relabel_lengths_kernel(const uint32_t* __restrict__ ro, int64_t 
 }
 
 // row r of P goes to row rank[r] of P' with its columns renamed (unsorted;
-// a segmented sort orders them), one warp per row
+// a segmented sort orders them).  Each thread takes kScatterRun consecutive
+// nonzeros and finds its first row once (binary search), so a hub row of
+// 10^5..10^6 entries is spread over the whole grid instead of one warp.
+constexpr int kScatterRun = 16;
 template <typename T>
 __global__ void relabel_scatter_kernel(const uint32_t* __restrict__ ro,
                                        const int32_t* __restrict__ cols,
-                                       const T* __restrict__ vals, int64_t n,
+                                       const T* __restrict__ vals, int64_t n, int64_t m,
                                        const int32_t* __restrict__ rank,
                                        const uint32_t* __restrict__ ro2,
                                        int32_t* __restrict__ cols2, T* __restrict__ vals2) {
-  const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lid = threadIdx.x & 31;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t r = wid; r < n; r += nw) {
-    const uint32_t b = ro[r], e = ro[r + 1], d = ro2[rank[r]];
-    for (uint32_t k = b + lid; k < e; k += 32) {
-      cols2[d + (k - b)] = rank[cols[k]];
-      vals2[d + (k - b)] = vals[k];
+  const int64_t chunks = (m + kScatterRun - 1) / kScatterRun;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < chunks;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k0 = t * kScatterRun;
+    const int64_t k1 = k0 + kScatterRun < m ? k0 + kScatterRun : m;
+    // last row r with ro[r] <= k0
+    int64_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (int64_t(ro[mid]) <= k0) lo = mid; else hi = mid - 1;
+    }
+    int64_t r = lo;
+    int64_t end = ro[r + 1];
+    int64_t d = int64_t(ro2[rank[r]]) - int64_t(ro[r]);
+    for (int64_t k = k0; k < k1; ++k) {
+      while (k >= end) {  // next non-empty row
+        ++r;
+        end = ro[r + 1];
+        d = int64_t(ro2[rank[r]]) - int64_t(ro[r]);
+      }
+      cols2[k + d] = rank[cols[k]];
+      vals2[k + d] = vals[k];
     }
   }
 }
 
-// offsets of a row batch relative to its first row
+// rows of at least `long_row` entries: (begin, length) pairs, appended
+__global__ void long_rows_kernel(const uint32_t* __restrict__ ro, int64_t n, int64_t long_row,
+                                 long long* __restrict__ out, unsigned int* count, unsigned cap) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t len = int64_t(ro[r + 1]) - ro[r];
+    if (len >= long_row) {
+      const unsigned i = atomicAdd(count, 1u);
+      if (i < cap) {
+        out[2 * i] = ro[r];
+        out[2 * i + 1] = len;
+      }
+    }
+  }
+}
+
+// begin / end offsets of a row batch relative to its first row; rows of at
+// least `long_row` entries get an empty segment (sorted separately)
 __global__ void rebase_offsets_kernel(const uint32_t* __restrict__ ro, int64_t r0, int64_t rows,
-                                      int32_t* __restrict__ out) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= rows;
-       i += int64_t(gridDim.x) * blockDim.x)
-    out[i] = int32_t(ro[r0 + i] - ro[r0]);
+                                      int64_t long_row, int32_t* __restrict__ beg,
+                                      int32_t* __restrict__ end) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = int64_t(ro[r0 + i]) - ro[r0], e = int64_t(ro[r0 + i + 1]) - ro[r0];
+    beg[i] = int32_t(b);
+    end[i] = int32_t(e - b >= long_row ? b : e);
+  }
 }
 
 template <typename F>
@@ -536,24 +574,53 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
       // unsorted rows into the B buffers, sorted by the segmented sort into p
       if (a->precision == MBX_F32)
         mbx::relabel_scatter_kernel<float><<<grid, 256, 0, s>>>(
-            a->ro, a->cols, static_cast<const float*>(a->vals), n, rank, p->ro, cols_b,
+            a->ro, a->cols, static_cast<const float*>(a->vals), n, m, rank, p->ro, cols_b,
             static_cast<float*>(vals_b));
       else
         mbx::relabel_scatter_kernel<double><<<grid, 256, 0, s>>>(
-            a->ro, a->cols, static_cast<const double*>(a->vals), n, rank, p->ro, cols_b,
+            a->ro, a->cols, static_cast<const double*>(a->vals), n, m, rank, p->ro, cols_b,
             static_cast<double*>(vals_b));
       ++ctx->launches;
-      std::vector<uint32_t> ro_h(n + 1);
-      MBX_CUDA(cudaMemcpyAsync(ro_h.data(), p->ro, (n + 1) * 4, cudaMemcpyDeviceToHost, s));
-      MBX_CUDA(cudaStreamSynchronize(s));
-      // row batches of < 2^30 nonzeros (CUB's item counts are int)
+      // row batches of < 2^30 nonzeros (CUB's item counts are int); one
+      // batch needs no host copy of the offsets, only the long-row list
       constexpr int64_t kBatch = int64_t(1) << 30;
+      // rows this long would be sorted by one CTA each (CUB's large-segment
+      // path): they get a device-wide radix sort of their own instead
+      constexpr int64_t kLongRow = 65536;
+      const bool single = m < kBatch;
+      std::vector<uint32_t> ro_h;
+      std::vector<long long> longs;  // (begin, length) pairs
+      if (!single) {
+        ro_h.resize(n + 1);
+        MBX_CUDA(cudaMemcpyAsync(ro_h.data(), p->ro, (n + 1) * 4, cudaMemcpyDeviceToHost, s));
+        MBX_CUDA(cudaStreamSynchronize(s));
+        for (int64_t r = 0; r < n; ++r)
+          if (int64_t(ro_h[r + 1]) - ro_h[r] >= kLongRow) {
+            longs.push_back(ro_h[r]);
+            longs.push_back(int64_t(ro_h[r + 1]) - ro_h[r]);
+          }
+      } else {
+        const unsigned cap = unsigned(m / kLongRow + 1);  // at most m / kLongRow such rows
+        auto* lbuf = static_cast<long long*>(dm(size_t(cap) * 16 + 64));
+        auto* lcnt = static_cast<unsigned int*>(dm(64));
+        MBX_CUDA(cudaMemsetAsync(lcnt, 0, 4, s));
+        mbx::long_rows_kernel<<<grid, 256, 0, s>>>(p->ro, n, kLongRow, lbuf, lcnt, cap);
+        ++ctx->launches;
+        unsigned nl = 0;
+        MBX_CUDA(cudaMemcpyAsync(&nl, lcnt, 4, cudaMemcpyDeviceToHost, s));
+        MBX_CUDA(cudaStreamSynchronize(s));
+        longs.resize(size_t(nl) * 2);
+        if (nl)
+          MBX_CUDA(cudaMemcpyAsync(longs.data(), lbuf, size_t(nl) * 16, cudaMemcpyDeviceToHost, s));
+        MBX_CUDA(cudaStreamSynchronize(s));
+      }
       auto* offs = static_cast<int32_t*>(dm((n + 1) * 4 + 64));
+      auto* offe = static_cast<int32_t*>(dm((n + 1) * 4 + 64));
       void* tsort = nullptr;
       size_t tsort_bytes = 0;
       for (int64_t r0 = 0; r0 < n;) {
-        int64_t r1 = r0 + 1;
-        {  // furthest r1 with ro[r1] - ro[r0] < kBatch (a single longer row stands alone)
+        int64_t r1 = n;
+        if (!single) {  // furthest r1 with ro[r1] - ro[r0] < kBatch (a longer row stands alone)
           int64_t lo = r0 + 1, hi = n;
           while (lo < hi) {
             const int64_t mid = (lo + hi + 1) >> 1;
@@ -561,10 +628,12 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
           }
           r1 = lo;
         }
-        const int64_t rows = r1 - r0, base = ro_h[r0], items = int64_t(ro_h[r1]) - base;
+        const int64_t rows = r1 - r0;
+        const int64_t base = single ? 0 : int64_t(ro_h[r0]);
+        const int64_t items = single ? m : int64_t(ro_h[r1]) - base;
         if (items > 0) {
-          mbx::rebase_offsets_kernel<<<mbx::grid_of(rows + 1, ctx), 256, 0, s>>>(p->ro, r0, rows,
-                                                                                 offs);
+          mbx::rebase_offsets_kernel<<<mbx::grid_of(rows + 1, ctx), 256, 0, s>>>(
+              p->ro, r0, rows, kLongRow, offs, offe);
           ++ctx->launches;
           // ping-pong between the B buffers and p (no internal copies in
           // the temp storage); a batch that ends in B is copied over
@@ -574,20 +643,38 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
             cub::DoubleBuffer<V> vd(vb + base, vp + base);
             size_t need = 0;
             MBX_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, need, kd, vd, int(items),
-                                                         int(rows), offs, offs + 1, s));
+                                                         int(rows), offs, offe, s));
             if (need > tsort_bytes) {
               if (tsort) cudaFreeAsync(tsort, s);
               MBX_CUDA(cudaMallocAsync(&tsort, need, s));
               tsort_bytes = need;
             }
             MBX_CUDA(cub::DeviceSegmentedSort::SortPairs(tsort, need, kd, vd, int(items),
-                                                         int(rows), offs, offs + 1, s));
+                                                         int(rows), offs, offe, s));
             if (kd.Current() != p->cols + base)
               MBX_CUDA(cudaMemcpyAsync(p->cols + base, kd.Current(), items * 4,
                                        cudaMemcpyDeviceToDevice, s));
             if (vd.Current() != vp + base)
               MBX_CUDA(cudaMemcpyAsync(vp + base, vd.Current(), items * sizeof(V),
                                        cudaMemcpyDeviceToDevice, s));
+            // the long rows of this batch: their unsorted copy is still in B
+            int bits = 1;
+            while (bits < 31 && (int64_t(1) << bits) < n) ++bits;
+            for (size_t i = 0; i < longs.size(); i += 2) {
+              const int64_t b = longs[i], len = longs[i + 1];
+              if (b < base || b >= base + items) continue;
+              size_t need2 = 0;
+              MBX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need2, cols_b + b, p->cols + b,
+                                                       vb + b, vp + b, int(len), 0, bits, s));
+              if (need2 > tsort_bytes) {
+                if (tsort) cudaFreeAsync(tsort, s);
+                MBX_CUDA(cudaMallocAsync(&tsort, need2, s));
+                tsort_bytes = need2;
+              }
+              MBX_CUDA(cub::DeviceRadixSort::SortPairs(tsort, need2, cols_b + b, p->cols + b,
+                                                       vb + b, vp + b, int(len), 0, bits, s));
+              ++ctx->launches;
+            }
           };
           if (a->precision == MBX_F32)
             sort(static_cast<float*>(vals_b), static_cast<float*>(p->vals));

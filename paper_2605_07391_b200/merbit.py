@@ -352,15 +352,16 @@ class DeviceMatrix:
                                                   C.byref(d)))
         return DegreeStats(d.mean_degree, bool(d.low_degree), d.max_degree, d.empty_rows)
 
-    def relabel_by_degree(self):
+    def relabel_by_degree(self, want_rank: bool = True):
         """(P', rank): the symmetric degree relabelling P' = Q P Q^T on the
         device (vertex v -> rank[v], by descending column count) -- a locality
-        preprocessing for graphs whose x exceeds L2."""
+        preprocessing for graphs whose x exceeds L2.  rank is None when not
+        wanted (the matrix keeps its vertex map either way)."""
         h = C.c_void_p()
-        rank = np.zeros(max(self.n_rows, 1), np.int32)
-        _check(_lib.lib().mbx_matrix_relabel_by_degree(self.ctx.h, self.h, C.byref(h),
-                                                       rank.ctypes.data))
-        return DeviceMatrix(self.ctx, h), rank[:self.n_rows]
+        rank = np.zeros(max(self.n_rows, 1), np.int32) if want_rank else None
+        _check(_lib.lib().mbx_matrix_relabel_by_degree(
+            self.ctx.h, self.h, C.byref(h), None if rank is None else rank.ctypes.data))
+        return DeviceMatrix(self.ctx, h), (None if rank is None else rank[:self.n_rows])
 
     def slot_info(self):
         """(slots, build seconds) of the lane-major slot copy cached on this

@@ -135,7 +135,8 @@ def test_degree_stats_reference_cases(ctx):
         empty.degree_stats(7)
 
 
-@pytest.mark.parametrize("case", ["rmat", "empty_rows", "one_dense_row", "single", "no_nnz"])
+@pytest.mark.parametrize("case", ["rmat", "empty_rows", "one_dense_row", "long_row", "single",
+                                  "no_nnz"])
 def test_relabel_by_degree_structure(ctx, case):
     """P' = Q P Q^T exactly: rank = vertices by descending column count (ties
     by id), row rank[r] of P' holds row r of P with columns renamed and sorted
@@ -158,6 +159,16 @@ def test_relabel_by_degree_structure(ctx, case):
         ro = np.zeros(n + 1, np.int64)
         ro[1:] = n  # row 0 holds every column, the rest are empty
         a = O.Csr(n, n, ro, np.arange(n, dtype=np.int32), rng.random(n))
+    elif case == "long_row":
+        # a row beyond the segmented sort's long-row cut (65536): sorted on its own
+        n = 70000
+        lens = np.zeros(n, np.int64)
+        lens[0] = n
+        lens[1:200] = rng.integers(1, 40, 199)
+        ro = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        cols = np.concatenate([np.arange(n)] + [np.sort(rng.choice(n, l, replace=False))
+                                                for l in lens[1:200]]).astype(np.int32)
+        a = O.Csr(n, n, ro, cols, rng.random(cols.size))
     elif case == "single":
         a = O.Csr(1, 1, np.array([0, 1], np.int64), np.array([0], np.int32), np.array([2.5]))
     else:
@@ -172,7 +183,7 @@ def test_relabel_by_degree_structure(ctx, case):
     ro2, c2, v2 = q.download()
     lens = np.diff(a.row_offsets)
     assert np.array_equal(np.diff(ro2)[want_rank], lens)
-    for r in range(n):
+    for r in np.nonzero(lens)[0]:
         seg = slice(a.row_offsets[r], a.row_offsets[r + 1])
         newc = want_rank[a.col_indices[seg]]
         order = np.argsort(newc, kind="stable")
