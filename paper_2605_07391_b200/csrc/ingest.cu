@@ -249,16 +249,78 @@ __global__ void long_rows_kernel(const uint32_t* __restrict__ ro, int64_t n, int
   }
 }
 
+// Mid-length rows (R-MAT's degree clusters put ~70 % of the nonzeros in
+// rows of 256..4096 entries) would each take CUB's one-CTA multi-pass
+// large-segment path; they are sorted in shared memory instead: one CTA per
+// row, a bitonic network over the row padded to a power of two.
+constexpr int64_t kMidLo = 128, kMidHi = 8192;  // measured best split at s24 (38.7 ms)
+
+__global__ void mid_rows_kernel(const uint32_t* __restrict__ ro, int64_t n, int64_t lo,
+                                int64_t hi, long long* __restrict__ out,
+                                unsigned int* count) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t len = int64_t(ro[r + 1]) - ro[r];
+    if (len > lo && len <= hi) {
+      const unsigned i = atomicAdd(count, 1u);
+      out[2 * i] = ro[r];
+      out[2 * i + 1] = len;
+    }
+  }
+}
+
+template <typename T>
+__global__ void bitonic_rows_kernel(const int32_t* __restrict__ kin, const T* __restrict__ vin,
+                                    int32_t* __restrict__ kout, T* __restrict__ vout,
+                                    const long long* __restrict__ segs) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int64_t b = segs[2 * blockIdx.x];
+  const int len = int(segs[2 * blockIdx.x + 1]);
+  int pw = 1;
+  while (pw < len) pw <<= 1;
+  T* sv = reinterpret_cast<T*>(sm);
+  int32_t* sk = reinterpret_cast<int32_t*>(sv + pw);
+  for (int i = threadIdx.x; i < pw; i += blockDim.x) {
+    sk[i] = i < len ? kin[b + i] : INT32_MAX;
+    if (i < len) sv[i] = vin[b + i];
+  }
+  __syncthreads();
+  for (int k = 2; k <= pw; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < pw; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const int32_t a = sk[i], c = sk[ixj];
+          if ((a > c) == up) {
+            sk[i] = c;
+            sk[ixj] = a;
+            const T t = sv[i];
+            sv[i] = sv[ixj];
+            sv[ixj] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    kout[b + i] = sk[i];
+    vout[b + i] = sv[i];
+  }
+}
+
 // begin / end offsets of a row batch relative to its first row; rows of at
 // least `long_row` entries get an empty segment (sorted separately)
 __global__ void rebase_offsets_kernel(const uint32_t* __restrict__ ro, int64_t r0, int64_t rows,
-                                      int64_t long_row, int32_t* __restrict__ beg,
-                                      int32_t* __restrict__ end) {
+                                      int64_t long_row, int64_t mid_lo, int64_t mid_hi,
+                                      int32_t* __restrict__ beg, int32_t* __restrict__ end) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t b = int64_t(ro[r0 + i]) - ro[r0], e = int64_t(ro[r0 + i + 1]) - ro[r0];
+    const int64_t len = e - b;
     beg[i] = int32_t(b);
-    end[i] = int32_t(e - b >= long_row ? b : e);
+    end[i] = int32_t(len >= long_row || (len > mid_lo && len <= mid_hi) ? b : e);
   }
 }
 
@@ -614,6 +676,27 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
           MBX_CUDA(cudaMemcpyAsync(longs.data(), lbuf, size_t(nl) * 16, cudaMemcpyDeviceToHost, s));
         MBX_CUDA(cudaStreamSynchronize(s));
       }
+      // mid-length rows: (begin, length) lists for the shared-memory sort,
+      // rows of <= 1024 entries first (the small class)
+      // a mid row has > kMidLo entries, so there are at most m / kMidLo
+      long long* mids = static_cast<long long*>(dm(size_t(m / mbx::kMidLo + 1) * 16 + 64));
+      int64_t nmid = 0, nmid_small = 0;
+      {
+        auto* mcnt = static_cast<unsigned int*>(dm(64));
+        MBX_CUDA(cudaMemsetAsync(mcnt, 0, 8, s));
+        mbx::mid_rows_kernel<<<grid, 256, 0, s>>>(p->ro, n, mbx::kMidLo, 1024, mids, mcnt);
+        unsigned c1 = 0;
+        MBX_CUDA(cudaMemcpyAsync(&c1, mcnt, 4, cudaMemcpyDeviceToHost, s));
+        MBX_CUDA(cudaStreamSynchronize(s));
+        mbx::mid_rows_kernel<<<grid, 256, 0, s>>>(p->ro, n, 1024, mbx::kMidHi, mids + 2 * c1,
+                                                  mcnt + 1);
+        unsigned c2 = 0;
+        MBX_CUDA(cudaMemcpyAsync(&c2, mcnt + 1, 4, cudaMemcpyDeviceToHost, s));
+        MBX_CUDA(cudaStreamSynchronize(s));
+        ctx->launches += 2;
+        nmid_small = c1;
+        nmid = int64_t(c1) + c2;
+      }
       auto* offs = static_cast<int32_t*>(dm((n + 1) * 4 + 64));
       auto* offe = static_cast<int32_t*>(dm((n + 1) * 4 + 64));
       void* tsort = nullptr;
@@ -633,7 +716,7 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
         const int64_t items = single ? m : int64_t(ro_h[r1]) - base;
         if (items > 0) {
           mbx::rebase_offsets_kernel<<<mbx::grid_of(rows + 1, ctx), 256, 0, s>>>(
-              p->ro, r0, rows, kLongRow, offs, offe);
+              p->ro, r0, rows, kLongRow, mbx::kMidLo, mbx::kMidHi, offs, offe);
           ++ctx->launches;
           // ping-pong between the B buffers and p (no internal copies in
           // the temp storage); a batch that ends in B is copied over
@@ -683,6 +766,31 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
           ++ctx->launches;
         }
         r0 = r1;
+      }
+      // the mid-length rows, in shared memory, once every batch's copy-back
+      // is done (their unsorted copy is still in the B buffers); two size
+      // classes so short rows do not reserve a long row's tile
+      auto mid_sort = [&](auto* vb, auto* vp) {
+        using V = std::remove_pointer_t<decltype(vb)>;
+        const size_t es = sizeof(V) + 4;
+        MBX_CUDA(cudaFuncSetAttribute(mbx::bitonic_rows_kernel<V>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(size_t(mbx::kMidHi) * es)));
+        if (nmid_small)
+          mbx::bitonic_rows_kernel<V><<<unsigned(nmid_small), 256, 1024 * es, s>>>(
+              cols_b, vb, p->cols, vp, mids);
+        if (nmid > nmid_small)
+          mbx::bitonic_rows_kernel<V><<<unsigned(nmid - nmid_small), 1024,
+                                        size_t(mbx::kMidHi) * es, s>>>(
+              cols_b, vb, p->cols, vp, mids + 2 * nmid_small);
+        ctx->launches += 2;
+        MBX_CUDA(cudaGetLastError());
+      };
+      if (nmid) {
+        if (a->precision == MBX_F32)
+          mid_sort(static_cast<float*>(vals_b), static_cast<float*>(p->vals));
+        else
+          mid_sort(static_cast<double*>(vals_b), static_cast<double*>(p->vals));
       }
       if (tsort) cudaFreeAsync(tsort, s);
     }

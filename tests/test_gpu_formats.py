@@ -135,8 +135,8 @@ def test_degree_stats_reference_cases(ctx):
         empty.degree_stats(7)
 
 
-@pytest.mark.parametrize("case", ["rmat", "empty_rows", "one_dense_row", "long_row", "single",
-                                  "no_nnz"])
+@pytest.mark.parametrize("case", ["rmat", "empty_rows", "one_dense_row", "long_row", "mid_rows",
+                                  "single", "no_nnz"])
 def test_relabel_by_degree_structure(ctx, case):
     """P' = Q P Q^T exactly: rank = vertices by descending column count (ties
     by id), row rank[r] of P' holds row r of P with columns renamed and sorted
@@ -168,6 +168,17 @@ def test_relabel_by_degree_structure(ctx, case):
         ro = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
         cols = np.concatenate([np.arange(n)] + [np.sort(rng.choice(n, l, replace=False))
                                                 for l in lens[1:200]]).astype(np.int32)
+        a = O.Csr(n, n, ro, cols, rng.random(cols.size))
+    elif case == "mid_rows":
+        # every sort route: CUB small (<= 128), shared-memory bitonic (129..1024
+        # and 1025..8192), CUB large (8193..65535)
+        n = 30000
+        lens = rng.integers(0, 20, n)
+        for i, l in enumerate([128, 129, 257, 1000, 1024, 1025, 3000, 8192, 8193, 16385, 20000]):
+            lens[5 + 37 * i] = l
+        ro = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]
+                              ).astype(np.int32)
         a = O.Csr(n, n, ro, cols, rng.random(cols.size))
     elif case == "single":
         a = O.Csr(1, 1, np.array([0, 1], np.int64), np.array([0], np.int32), np.array([2.5]))
