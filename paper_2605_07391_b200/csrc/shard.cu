@@ -186,11 +186,10 @@ __global__ void shard_init_tail_kernel(const unsigned long long* count, int64_t 
 // `iter` and decide convergence (solvers.hpp:201-213).
 // iter_dev (device-driven loop): the iteration is *iter_dev + 1, `out` is
 // the scalar array's base, and the kernel advances the counter.
-__global__ void combine_kernel(const unsigned char* __restrict__ pi_base, int64_t chunk_bytes,
-                               int64_t tail_off, int world, PrScalars* out, int* stop,
-                               int* stop_iter, int iter, double err_tol, int64_t* iter_dev,
-                               int64_t max_iters) {
-  if (threadIdx.x != 0) return;
+__device__ void combine_body(const unsigned char* __restrict__ pi_base, int64_t chunk_bytes,
+                             int64_t tail_off, int world, PrScalars* out, int* stop,
+                             int* stop_iter, int iter, double err_tol, int64_t* iter_dev,
+                             int64_t max_iters) {
   if (stop && *stop) return;
   if (iter_dev) {
     if (*iter_dev >= max_iters) return;
@@ -221,6 +220,16 @@ __global__ void combine_kernel(const unsigned char* __restrict__ pi_base, int64_
   }
   if (iter_dev) *iter_dev += 1;
 }
+
+__global__ void combine_kernel(const unsigned char* __restrict__ pi_base, int64_t chunk_bytes,
+                               int64_t tail_off, int world, PrScalars* out, int* stop,
+                               int* stop_iter, int iter, double err_tol, int64_t* iter_dev,
+                               int64_t max_iters) {
+  if (threadIdx.x == 0)
+    combine_body(pi_base, chunk_bytes, tail_off, world, out, stop, stop_iter, iter, err_tol,
+                 iter_dev, max_iters);
+}
+
 
 __global__ void shard_loop_cond_kernel(cudaGraphConditionalHandle h, const int64_t* iter_dev,
                                        int64_t max_iters, const int* stop) {
@@ -255,10 +264,9 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // peer that never arrives sets *err instead of hanging the GPU.
 // iter_dev (device-driven loop): the slot is slot + iteration, and nothing
 // happens past max_iters (every rank skips the same barriers).
-__global__ void peer_barrier_kernel(PeerFlags pf, const uint64_t* __restrict__ base, int slot,
-                                    const int* stop, int* err, const int64_t* iter_dev,
-                                    int64_t max_iters) {
-  if (threadIdx.x != 0) return;
+__device__ void peer_barrier_body(const PeerFlags& pf, const uint64_t* __restrict__ base, int slot,
+                                  const int* stop, int* err, const int64_t* iter_dev,
+                                  int64_t max_iters) {
   if (stop && *stop) return;
   if (iter_dev && *iter_dev >= max_iters) return;
   const uint64_t epoch = *base + uint64_t(slot) + (iter_dev ? uint64_t(*iter_dev + 1) : 0ull);
@@ -280,6 +288,25 @@ __global__ void peer_barrier_kernel(PeerFlags pf, const uint64_t* __restrict__ b
       __nanosleep(128);
     }
   }
+}
+
+__global__ void peer_barrier_kernel(PeerFlags pf, const uint64_t* __restrict__ base, int slot,
+                                    const int* stop, int* err, const int64_t* iter_dev,
+                                    int64_t max_iters) {
+  if (threadIdx.x == 0) peer_barrier_body(pf, base, slot, stop, err, iter_dev, max_iters);
+}
+
+// fused groups: the barrier and the fold of the tails in one launch
+__global__ void barrier_combine_kernel(PeerFlags pf, const uint64_t* __restrict__ base, int slot,
+                                       const int* bstop, int* err, const int64_t* biter,
+                                       const unsigned char* __restrict__ pi_base,
+                                       int64_t chunk_bytes, int64_t tail_off, int world,
+                                       PrScalars* out, int* stop, int* stop_iter, int iter,
+                                       double err_tol, int64_t* iter_dev, int64_t max_iters) {
+  if (threadIdx.x != 0) return;
+  peer_barrier_body(pf, base, slot, bstop, err, biter, max_iters);
+  combine_body(pi_base, chunk_bytes, tail_off, world, out, stop, stop_iter, iter, err_tol,
+               iter_dev, max_iters);
 }
 
 __global__ void bump_epoch_kernel(uint64_t* base, uint64_t step) { *base += step; }
@@ -409,23 +436,40 @@ void exchange_and_combine(mbx_shard_group* G, int slot, int iter, bool main = tr
                           bool dev_loop = false) {
   mbx_context* ctx = G->ctx;
   unsigned char* base = static_cast<unsigned char*>(G->pi[slot]);
+  mbx::PrScalars* out = dev_loop ? G->gscal : (main ? G->gscal : G->yscal) + iter;
+  int* stop = main ? G->flags : nullptr;
+  int64_t* idev = dev_loop ? G->iter_dev : nullptr;
   if (G->peer) {
-    // the chunk already went out with the commit: wait for every rank's
-    if (dev_loop)
-      peer_barrier(G, G->main_base, true, G->iter_dev);
-    else if (main)
-      peer_barrier(G, G->main_base + iter, iter > 0);
-    else
-      peer_barrier(G, 1 + iter, false);
-  } else if (G->comm) {
+    // the chunk already went out with the commit: wait for every rank's,
+    // then fold the tails -- one launch
+    int64_t bslot;
+    bool skippable;
+    if (dev_loop) {
+      bslot = G->main_base;
+      skippable = true;
+    } else if (main) {
+      bslot = G->main_base + iter;
+      skippable = iter > 0;
+    } else {
+      bslot = 1 + iter;
+      skippable = false;
+    }
+    mbx::barrier_combine_kernel<<<1, 32, 0, ctx->stream>>>(
+        G->pf, G->run_base, int(bslot), skippable ? G->flags : nullptr, G->perr,
+        dev_loop ? G->iter_dev : nullptr, base, G->chunk_bytes, G->tail_off, G->world, out, stop,
+        G->flags + 1, iter, G->cfg.err_tol, idev, G->cfg.max_iters);
+    ++ctx->launches;
+    MBX_CUDA(cudaGetLastError());
+    return;
+  }
+  if (G->comm) {
     // in-place all-gather: each rank's chunk (pi rows + scalar tail)
     MBX_NCCL(mbx::nccl().AllGather(base + int64_t(G->rank0) * G->chunk_bytes, base, G->chunk_bytes,
                            ncclUint8, G->comm, ctx->stream));
   }
-  mbx::combine_kernel<<<1, 32, 0, ctx->stream>>>(
-      base, G->chunk_bytes, G->tail_off, G->world,
-      dev_loop ? G->gscal : (main ? G->gscal : G->yscal) + iter, main ? G->flags : nullptr,
-      G->flags + 1, iter, G->cfg.err_tol, dev_loop ? G->iter_dev : nullptr, G->cfg.max_iters);
+  mbx::combine_kernel<<<1, 32, 0, ctx->stream>>>(base, G->chunk_bytes, G->tail_off, G->world, out,
+                                                 stop, G->flags + 1, iter, G->cfg.err_tol, idev,
+                                                 G->cfg.max_iters);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
 }
