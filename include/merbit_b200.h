@@ -483,8 +483,9 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global,
  * through the caller's bootstrap (MPI, torch.distributed, ...):
  *   create_peer -> export (MBX_SHARD_BLOB_BYTES) -> all-gather the world's
  *   blobs in rank order -> connect.
- * One shard per group (this rank's rows).  Ranks may share a device (the
- * 2-process test) or a process (peers of the same pid use raw pointers).
+ * One shard per group (this rank's rows), world <= 8, the yardstick
+ * (reference_iters > 0) included.  Ranks may share a device (the 2- and
+ * 3-process tests) or a process (peers of the same pid use raw pointers).
  * run / result / gather_pi / download_local / destroy as above; destroy is
  * collective (a final barrier). */
 #define MBX_SHARD_BLOB_BYTES 512
