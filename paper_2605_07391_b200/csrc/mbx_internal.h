@@ -215,6 +215,22 @@ void launch_trace_counts(mbx_context* ctx, const mbx_tile* t,
 void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
                 const PrArgs* pr, double* cta_part, unsigned int* counter);
 int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m);
+// Makes ctx->device current for the scope of a C-ABI call (the caller's
+// thread may have another device current) and restores the previous one.
+struct DeviceGuard {
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = dev;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+  int prev = 0;
+};
+
 // How iterative loops are replayed: one graph with a device-driven WHILE node
 // (default), the fixed-count loop captured unrolled, or host launches
 // (MBX_GRAPH_MODE = while | unrolled | eager; profilers do not descend into

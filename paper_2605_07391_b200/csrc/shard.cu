@@ -907,6 +907,7 @@ MBX_API int mbx_nccl_unique_id(void* id128) {
 MBX_API int mbx_matrix_row_slice(mbx_context* ctx, const mbx_matrix* m, int64_t r0, int64_t r1,
                                  mbx_matrix** out) {
   return sguard([&] {
+    mbx::DeviceGuard dg(ctx->device);
     if (r0 < 0 || r1 < r0 || r1 > m->n_rows) mbx::fail(MBX_DIMENSION_ERROR, "row slice out of range");
     uint32_t b[2];
     MBX_CUDA(cudaMemcpyAsync(&b[0], m->ro + r0, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -946,6 +947,7 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
                                    const mbx_simt_config* c, const mbx_pagerank_config* cfg,
                                    const void* nccl_id, mbx_shard_group** out) {
   return sguard([&] {
+    mbx::DeviceGuard dg(ctx->device);
     if (!nccl_id && nlocal != world)
       mbx::fail(MBX_CONFIG_ERROR, "shard group: without NCCL every shard must be local");
     GroupPtr G(new mbx_shard_group_s);
@@ -974,6 +976,7 @@ MBX_API int mbx_shard_group_create_peer(mbx_context* ctx, int64_t n_global, int 
                                         mbx_tile* tile, const mbx_simt_config* c,
                                         const mbx_pagerank_config* cfg, mbx_shard_group** out) {
   return sguard([&] {
+    mbx::DeviceGuard dg(ctx->device);
     if (world < 1 || world > 8)
       mbx::fail(MBX_CONFIG_ERROR, "peer shard group: world must be in [1, 8]");
     GroupPtr G(new mbx_shard_group_s);
@@ -1005,6 +1008,7 @@ MBX_API int mbx_shard_group_create_peer(mbx_context* ctx, int64_t n_global, int 
 
 MBX_API int mbx_shard_group_export(mbx_shard_group* G, void* blob) {
   return sguard([&] {
+    mbx::DeviceGuard dg(G->ctx->device);
     if (!G->peer) mbx::fail(MBX_CONFIG_ERROR, "export: not a peer shard group");
     PeerBlob b;
     std::memset(&b, 0, sizeof(b));
@@ -1025,6 +1029,7 @@ MBX_API int mbx_shard_group_export(mbx_shard_group* G, void* blob) {
 
 MBX_API int mbx_shard_group_connect(mbx_shard_group* G, const void* blobs) {
   return sguard([&] {
+    mbx::DeviceGuard dg(G->ctx->device);
     if (!G->peer) mbx::fail(MBX_CONFIG_ERROR, "connect: not a peer shard group");
     if (G->connected) mbx::fail(MBX_CONFIG_ERROR, "connect: already connected");
     mbx_context* ctx = G->ctx;
@@ -1085,6 +1090,7 @@ MBX_API int mbx_shard_group_connect(mbx_shard_group* G, const void* blobs) {
 
 MBX_API int mbx_shard_group_run(mbx_shard_group* G, const void* pi0_dev) {
   return sguard([&] {
+    mbx::DeviceGuard dg(G->ctx->device);
     if (G->peer && !G->connected) mbx::fail(MBX_CONFIG_ERROR, "peer shard group not connected");
     if (G->quiesced) mbx::fail(MBX_CONFIG_ERROR, "peer shard group already quiesced");
     mbx_context* ctx = G->ctx;
@@ -1156,6 +1162,7 @@ MBX_API int mbx_shard_group_run(mbx_shard_group* G, const void* pi0_dev) {
 MBX_API int mbx_shard_group_result(mbx_shard_group* G, mbx_pagerank_result* res,
                                    double* history) {
   return sguard([&] {
+    mbx::DeviceGuard dg(G->ctx->device);
     if (!G->ran) mbx::fail(MBX_ERROR, "shard group has not run");
     cudaStream_t st = G->ctx->stream;
     int flags[2];
@@ -1190,6 +1197,7 @@ MBX_API int mbx_shard_group_result(mbx_shard_group* G, mbx_pagerank_result* res,
 // The full pi (every rank holds all chunks after the final exchange).
 MBX_API int mbx_shard_group_gather_pi(mbx_shard_group* G, void* pi_host) {
   return sguard([&] {
+    mbx::DeviceGuard dg(G->ctx->device);
     cudaStream_t st = G->ctx->stream;
     int flags[2];
     MBX_CUDA(cudaMemcpyAsync(flags, G->flags, 8, cudaMemcpyDeviceToHost, st));
@@ -1224,6 +1232,7 @@ MBX_API int mbx_shard_group_gather_pi(mbx_shard_group* G, void* pi_host) {
 // This process's rows of the final pi (its shards in rank order) to host.
 MBX_API int mbx_shard_group_download_local(mbx_shard_group* G, void* pi_local_host) {
   return sguard([&] {
+    mbx::DeviceGuard dg(G->ctx->device);
     cudaStream_t st = G->ctx->stream;
     int flags[2];
     MBX_CUDA(cudaMemcpyAsync(flags, G->flags, 8, cudaMemcpyDeviceToHost, st));
@@ -1247,6 +1256,7 @@ MBX_API int mbx_shard_group_download_local(mbx_shard_group* G, void* pi_local_ho
 // means no peer can still read or write this rank's buffers.
 MBX_API int mbx_shard_group_quiesce(mbx_shard_group* G) {
   return sguard([&] {
+    mbx::DeviceGuard dg(G->ctx->device);
     if (!G->peer || !G->connected || G->quiesced) return;
     MBX_CUDA(cudaMemsetAsync(G->flags, 0, 8, G->ctx->stream));  // stop must not skip it
     peer_barrier(G, G->epoch_step - 1, false);
@@ -1258,6 +1268,7 @@ MBX_API int mbx_shard_group_quiesce(mbx_shard_group* G) {
 MBX_API int mbx_shard_group_destroy(mbx_shard_group* G) {
   return sguard([&] {
     if (!G) return;
+    mbx::DeviceGuard dg(G->ctx->device);
     if (G->peer && G->connected) {
       const int rc = mbx_shard_group_quiesce(G);
       if (rc) mbx::fail(rc, "quiesce failed");
