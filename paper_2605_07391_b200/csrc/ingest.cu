@@ -581,11 +581,23 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
     cudaStream_t s = ctx->stream;
     const int64_t n = a->n_rows, m = a->nnz;
     const size_t vs = mbx::value_size(a->precision);
-    std::vector<void*> tmp;
+    // scratch is released on every exit; the new matrix's buffers too unless
+    // the call succeeds (a CUDA error part-way must not leak pool memory)
+    struct Scratch {
+      cudaStream_t s;
+      std::vector<void*> tmp, kept;
+      bool done = false;
+      ~Scratch() {
+        for (void* q : tmp) cudaFreeAsync(q, s);
+        if (!done)
+          for (void* q : kept) cudaFreeAsync(q, s);
+      }
+    } scratch{s, {}, {}};
+    std::vector<void*>& tmp = scratch.tmp;
     auto dm = [&](size_t b, bool keep = false) {
       void* p = nullptr;
       MBX_CUDA(cudaMallocAsync(&p, std::max<size_t>(b, 256), s));
-      if (!keep) tmp.push_back(p);
+      (keep ? scratch.kept : tmp).push_back(p);
       return p;
     };
     const unsigned grid = unsigned(ctx->sm_count) * 16;
@@ -807,8 +819,7 @@ MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
       MBX_CUDA(cudaMemcpyAsync(p->vmap, rank, n * 4, cudaMemcpyDeviceToDevice, s));
     }
     MBX_CUDA(cudaStreamSynchronize(s));
-    for (void* q : tmp) cudaFreeAsync(q, s);
-    MBX_CUDA(cudaStreamSynchronize(s));
+    scratch.done = true;
     *out = p.release();
   });
 }
