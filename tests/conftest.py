@@ -30,3 +30,18 @@ def golden():
     here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
     return {name: json.load(open(os.path.join(here, f"{name}.json")))
             for name in ("walkthrough", "fuzz_corpus", "pagerank")}
+
+
+def gpu_shared_between_processes() -> bool:
+    """False when device 0 is in an exclusive compute mode (a second process
+    could not create a context): the multi-process tests then skip."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            mode = pynvml.nvmlDeviceGetComputeMode(pynvml.nvmlDeviceGetHandleByIndex(0))
+        finally:
+            pynvml.nvmlShutdown()
+        return mode == pynvml.NVML_COMPUTEMODE_DEFAULT
+    except Exception:
+        return True

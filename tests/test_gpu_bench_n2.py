@@ -10,11 +10,14 @@ import subprocess
 import sys
 
 import pytest
+from conftest import gpu_shared_between_processes
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+@pytest.mark.skipif(not gpu_shared_between_processes(),
+                    reason="device 0 is in an exclusive compute mode")
 def test_bench_two_ranks_fused_exchange():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

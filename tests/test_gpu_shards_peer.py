@@ -20,6 +20,7 @@ import sys
 
 import numpy as np
 import pytest
+from conftest import gpu_shared_between_processes
 
 import oracle as O
 import paper_2605_07391_b200 as mb
@@ -106,6 +107,8 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.skipif(not gpu_shared_between_processes(),
+                    reason="device 0 is in an exclusive compute mode")
 def test_peer_groups_across_processes(tmp_path, world):
     """Two / three processes, CUDA IPC mappings, gloo only for the bootstrap."""
     iters = 8
