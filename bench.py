@@ -4,18 +4,21 @@
 Workload (BASELINE.json configs[1]): PageRank, 100 fixed iterations
 (reference_iters=0, err_tol=1e-30, so every run does all 100), fp32, on the
 transition matrix of a synthetic R-MAT graph (default scale 24: edge factor
-16, Graph500 a,b,c,d, duplicates merged, natural vertex order), TILE built
-once (preprocessing amortised).  One "step" = one 100-iteration PageRank run.
-At N>1 GPUs (torchrun) the SAME matrix is row-sharded (merge-path balanced)
-with one NCCL all-gather of pi per iteration: strong scaling.  --scale 27
-gives BASELINE config C4.
+16, Graph500 a,b,c,d, duplicates merged; vertices relabelled by degree on the
+device as preprocessing, --vertex-order natural keeps R-MAT's numbering),
+TILE built once (preprocessing amortised).  One "step" = one 100-iteration
+PageRank run.  At N>1 GPUs (torchrun) the SAME matrix is row-sharded
+(cost-weighted cut) and pi is exchanged every iteration, by default with P2P
+stores fused into the commit (--exchange nccl: one ncclAllGather; chosen
+automatically when the GPUs have no peer access): strong scaling.
+--scale 27 gives BASELINE config C4.
 
   value      iterations/s, matrix resident in HBM (CUDA-graph replay), max
              over ranks of the device time
   e2e        same metric with pinned HOST buffers inside the timed region:
              N=1 the one-shot C-ABI call mbx_pagerank (pi0 in, pi out);
              N>1 each rank's pi0 slice H2D + run + its pi slice D2H
-  roofline   the fused PageRank iteration on one GPU (K2 spmv_w32 + K3
+  roofline   the fused PageRank iteration on one GPU (K2 spmv_slot_kernel + K3
              fixup) vs measured HBM copy bandwidth; algorithmic bytes per
              iteration 8m + 16n + 4 (fp32)
   spmv       plain SpMV (K2+K3) on the same matrix (fp32) and on an fp64
@@ -404,6 +407,20 @@ def main():
         del P, P_natural
         P_natural = None
         tile = mb.generate_tile_for(Lm, cfg)
+        if args.exchange == "fused":
+            # the fused exchange stores into the peers' memory: every rank
+            # must reach every other rank's device over P2P (NVLink); on a box
+            # that does not allow it the exchange is the NCCL all-gather
+            ndev = torch.cuda.device_count()
+            ok = all(torch.cuda.can_device_access_peer(local, j)
+                     for j in range(min(world, ndev)) if j != local)
+            t_ok = torch.tensor([1 if ok else 0], dtype=torch.int64)
+            dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+            if int(t_ok[0]) == 0:
+                if rank == 0:
+                    print("bench: no P2P access between the ranks' GPUs; exchange = nccl",
+                          file=sys.stderr)
+                args.exchange = "nccl"
         if args.exchange == "fused":
             # the commit stores pi_new into every peer's buffer over NVLink
             # (CUDA IPC); gloo only carries the setup blobs
