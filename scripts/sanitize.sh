@@ -1,0 +1,19 @@
+#!/usr/bin/env bash
+# compute-sanitizer passes over the hot path (run on a GPU box, from the repo
+# root): memcheck, racecheck (shared memory), synccheck and initcheck of
+# __graft_entry__.smoke() (TILE K1, SpMV K2/K3, fused PageRank graph), then
+# memcheck of the small-matrix SpMV / PageRank / TILE parity tests.
+# Logs go to gpurun_out/sanitize_*.log; the summary line of each is printed.
+set -u
+mkdir -p gpurun_out
+CS="compute-sanitizer --error-exitcode 99 --print-limit 20"
+SMOKE='import __graft_entry__ as g; g.smoke()'
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 900 $CS --tool $tool python -c "$SMOKE" > gpurun_out/sanitize_smoke_$tool.log 2>&1
+  echo "smoke $tool rc=$? :: $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/sanitize_smoke_$tool.log | tail -1)"
+done
+timeout 1500 $CS --tool memcheck python -m pytest -q -x -m gpu -p no:cacheprovider \
+  tests/test_gpu_spmv.py tests/test_gpu_tile.py tests/test_gpu_pagerank.py \
+  -k "walkthrough or fuzz or edge or long_row or many_rows or ring or cycle or dangling or short_rows or empty or odd or dense or device_driven or degree_relabel" \
+  > gpurun_out/sanitize_tests_memcheck.log 2>&1
+echo "tests memcheck rc=$? :: $(grep -E 'passed|failed|ERROR SUMMARY' gpurun_out/sanitize_tests_memcheck.log | tail -2 | tr '\n' ' ')"
