@@ -2,7 +2,8 @@
 # compute-sanitizer passes over the hot path (run on a GPU box, from the repo
 # root): memcheck, racecheck (shared memory), synccheck and initcheck of
 # __graft_entry__.smoke() (TILE K1, SpMV K2/K3, fused PageRank graph), then
-# memcheck of the small-matrix SpMV / PageRank / TILE parity tests.
+# memcheck and synccheck of the small-matrix SpMV / PageRank / TILE (+ BiCGSTAB,
+# comparators: synccheck) parity tests.
 # Logs go to gpurun_out/sanitize_*.log; the summary line of each is printed.
 set -u
 mkdir -p gpurun_out
@@ -17,3 +18,9 @@ timeout 1500 $CS --tool memcheck python -m pytest -q -x -m gpu -p no:cacheprovid
   -k "walkthrough or fuzz or edge or long_row or many_rows or ring or cycle or dangling or short_rows or empty or odd or dense or device_driven or degree_relabel" \
   > gpurun_out/sanitize_tests_memcheck.log 2>&1
 echo "tests memcheck rc=$? :: $(grep -E 'passed|failed|ERROR SUMMARY' gpurun_out/sanitize_tests_memcheck.log | tail -2 | tr '\n' ' ')"
+timeout 1500 $CS --tool synccheck python -m pytest -q -x -m gpu -p no:cacheprovider \
+  tests/test_gpu_spmv.py tests/test_gpu_tile.py tests/test_gpu_pagerank.py tests/test_gpu_bicgstab.py \
+  tests/test_gpu_comparators.py \
+  -k "walkthrough or fuzz or edge or long_row or many_rows or ring or cycle or dangling or short_rows or empty or odd or dense or device_driven or degree_relabel or stencil or laplacian or singular or trivial or corpus" \
+  > gpurun_out/sanitize_tests_synccheck.log 2>&1
+echo "tests synccheck rc=$? :: $(grep -E 'passed|failed|ERROR SUMMARY' gpurun_out/sanitize_tests_synccheck.log | tail -2 | tr '\n' ' ')"
