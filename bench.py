@@ -136,6 +136,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_reference_pagerank(ro, cols, n, iters_per_step, steps, warmup, nthreads):
     """The reference's pagerank<float> with MerbitBackend on ThreadPool(nthreads)
     (oracle/_ref = the unmodified reference compiled from its sources)."""
@@ -230,12 +241,32 @@ def run_reference(args):
                    "scale": args.scale, "nnz": p.nnz, "n": p.n_rows, "omega": 32, "sigma": 14,
                    "block_size": 128, "threads": nthreads},
         "cpu_baseline": {"value": v, "unit": "iters/s", "cores": nthreads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"{args.steps} x {iters} PageRank iterations of the reference "
                                    f"MerbitBackend<float> on ThreadPool({nthreads})"},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_preprocess_seconds": r["preprocess_seconds"],
         "input_generation_seconds": gen}))
     return 0
+
+
+def single_gpu_rate(mb, stream, P, cfg, steps, iters=100):
+    """PageRank iterations/s of P on this one GPU (TILE + hub table + slot
+    copy, then `steps` timed runs of `iters` iterations after one warm-up);
+    the derived copies are released afterwards so P can be sharded next."""
+    t = mb.generate_tile_for(P, cfg)
+    xc_s = P.build_xcache()
+    plan = mb.PageRankPlan(P, t, cfg, mb.PageRankConfig(0.85, 1e-30, iters, 0))
+    pre_ms = (t.preprocess_seconds + xc_s + P.slot_info()[1]) * 1e3
+    plan.run()
+    ts = time_device(stream, plan.run, steps)
+    res, _ = plan.result()
+    plan.close()
+    del t
+    P.release_caches()
+    return {"n_gpus": 1, "iters_per_s": iters / ts, "us_per_iteration": ts * 1e6 / iters,
+            "steps": steps, "iterations_per_step": iters, "preprocess_ms": pre_ms,
+            "mass": res.mass}
 
 
 def time_device(stream, fn, reps):
@@ -251,7 +282,36 @@ def time_device(stream, fn, reps):
     return e0.elapsed_time(e1) * 1e-3 / reps
 
 
-def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak, make=None, label=None):
+def reference_spmv(mb, A, sigma, sample):
+    """The reference's generate_tile + spmv_merbit<T> (MerbitBackend on
+    ThreadPool(nproc), oracle/_ref) on the host copy of A: one warm-up and
+    three timed applies.  None when oracle/_ref is absent."""
+    import numpy as np
+
+    import oracle as O
+    if O.ref() is None:
+        return None
+    ro, cols, vals = A.download()
+    nthreads = os.cpu_count() or 1
+    eng = O.RefEngine(O.Csr(A.n_rows, A.n_cols, ro, cols, vals), 32, sigma, 128, nthreads)
+    x = O.hash_uniform(7, A.n_cols, -1.0, 1.0, vals.dtype)
+    eng.apply(x)
+    reps = 3
+    t1 = time.perf_counter()
+    for _ in range(reps):
+        eng.apply(x)
+    ts = (time.perf_counter() - t1) / reps
+    out = {"sample": sample, "nnz": A.nnz, "n": A.n_rows, "threads": nthreads,
+           "cpu_model": cpu_model(), "kind": "reference",
+           "generate_tile_ms": eng.preprocess_seconds * 1e3, "spmv_ms": ts * 1e3,
+           "gflops": 2 * A.nnz / ts / 1e9}
+    eng.close()
+    del ro, cols, vals
+    return out
+
+
+def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak, make=None, label=None,
+                 reference=None):
     """Plain SpMV (K2+K3) on an R-MAT matrix (or make(ctx, dtype)) of the
     given precision."""
     import numpy as np
@@ -293,6 +353,21 @@ def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak, make=None, label=Non
     out["comparators"] = base
     if "ms" in base.get("coo_atomic", {}):
         out["speedup_vs_coo"] = base["coo_atomic"]["ms"] * 1e-3 / ts  # BenchRecord.speedup
+    if reference is not None:
+        # the reference's CPU path on this box (a bounded sample when the full
+        # matrix would not fit the host / time budget): reported, not a target
+        try:
+            if reference == "same":
+                ref = reference_spmv(mb, A, c.sigma, "the same matrix")
+            else:
+                S = reference[0](ctx, dtype)
+                ref = reference_spmv(mb, S, c.sigma, reference[1])
+                del S
+            if ref is not None:
+                ref["gpu_speedup_gflops"] = (2 * m / ts / 1e9) / ref["gflops"]
+            out["reference_cpu"] = ref
+        except Exception as e:
+            out["reference_cpu"] = {"unavailable": str(e)[:160]}
     if label:
         tr = mb.trace_counts(t)
         out.update({"matrix": label, "n": n, "fast_tiles": tr.fast_tiles,
@@ -308,12 +383,15 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--scale", type=int, default=None,
+                    help="R-MAT scale (default: 24 = C2 at N = 1, 27 = C4 at N > 1)")
     ap.add_argument("--iters", type=int, default=100, help="PageRank iterations per step")
     ap.add_argument("--block-size", type=int, default=128)
     ap.add_argument("--ref-iters-per-step", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip the spmv f32/f64 extras")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the extras (N = 1: SpMV f32/f64, C1, C3, C5, C4 on one GPU; "
+                         "N > 1: the one-GPU anchor, the NCCL exchange, C2 sharded)")
     ap.add_argument("--spmv-reps", type=int, default=30)
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
                     help="N > 1: fused = the commit stores into the peers' buffers (P2P, "
@@ -334,7 +412,7 @@ def main():
     import paper_2605_07391_b200 as mb
     from paper_2605_07391_b200 import _lib
     from paper_2605_07391_b200.merbit import (PeerShardGroup, ShardGroup, nccl_unique_id,
-                                              pagerank_row_weight, row_slice)
+                                              prepare_rank_shard)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -342,8 +420,12 @@ def main():
     if os.environ.get("MBX_BENCH_ONE_DEVICE") == "1":
         local = 0  # plumbing check of N > 1 on a one-GPU box (fused exchange only)
     if world > 1:
-        # gloo only bootstraps (NCCL id broadcast, barriers, max-over-ranks);
-        # the pi exchange is the library's own NCCL all-gather
+        # gloo only bootstraps (IPC blobs, NCCL id broadcast, barriers,
+        # max-over-ranks); the pi exchange is the library's fused P2P stores
+        # or its own NCCL all-gather.  NCCL's init log stays on so the
+        # communicator's rank count is visible in the run's output.
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     stream = torch.cuda.Stream()
@@ -364,7 +446,53 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t[0])
 
-    scale = args.scale
+    extras = {}
+
+    def peer_ok():
+        """The fused exchange stores into the peers' memory: every rank must
+        reach every other rank's device over P2P (NVLink), and CUDA IPC
+        handles only open on one node (every rank local)."""
+        ndev = torch.cuda.device_count()
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        ok = local_world == world and all(torch.cuda.can_device_access_peer(local, j)
+                                          for j in range(min(world, ndev)) if j != local)
+        t_ok = torch.tensor([1 if ok else 0], dtype=torch.int64)
+        dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+        return int(t_ok[0]) == 1
+
+    def make_shard_runner(exchange, n_global, bounds, Lm, tile, prc):
+        if exchange == "fused":
+            # the commit stores pi_new into every peer's buffer over NVLink
+            # (CUDA IPC); gloo only carries the setup blobs
+            g = PeerShardGroup(ctx, n_global, world, bounds, rank, Lm, tile, cfg, prc)
+            blobs = [None] * world
+            dist.all_gather_object(blobs, g.export())
+            g.connect(blobs)
+            return g
+        ids = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        return ShardGroup(ctx, n_global, world, bounds, rank, [(Lm, tile)], cfg, prc, ids[0])
+
+    def time_shard_runner(g, warmup, steps, iters):
+        """iterations/s of a shard group: device time, max over ranks."""
+        for _ in range(warmup):
+            g.run()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            g.run()
+        e1.record(stream)
+        barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        res, _ = g.result()
+        assert res.iterations == iters, res.iterations
+        return {"iters_per_s": iters * steps / (ms * 1e-3), "ms_per_step": ms / steps,
+                "us_per_iteration": ms * 1e3 / (iters * steps), "steps": steps,
+                "mass": res.mass}
+
+    scale = args.scale if args.scale is not None else (24 if world == 1 else 27)
     t0 = time.perf_counter()
     P = mb.DeviceMatrix.rmat(ctx, scale, 16, seed=1, transition=True, dtype=np.float32)
     gen_s = time.perf_counter() - t0
@@ -399,42 +527,25 @@ def main():
         run = runner.run
         pre_ms = (relabel_s + tile.preprocess_seconds + xc_s + P.slot_info()[1]) * 1e3
     else:
-        ro_host, _, _ = P.download(want_values=False)
-        row_w = pagerank_row_weight(n, 4)
         hub_cov = None  # the shard group builds its own hub tables
-        bounds = mb.plan_row_shards(ro_host, n, m, world, row_w)
-        Lm = row_slice(P, int(bounds[rank]), int(bounds[rank + 1]))
+        if rank == 0 and not args.no_extras:
+            # the one-GPU anchor of THIS matrix, timed on rank 0 before the
+            # cut (the other ranks wait): the strong-scaling reference
+            extras["n1_anchor"] = single_gpu_rate(mb, stream, P, cfg, 3)
+        barrier()
+        bounds, Lm, tile, row_w = prepare_rank_shard(P, world, rank, cfg)
         del P, P_natural
         P_natural = None
-        tile = mb.generate_tile_for(Lm, cfg)
-        if args.exchange == "fused":
-            # the fused exchange stores into the peers' memory: every rank
-            # must reach every other rank's device over P2P (NVLink); on a box
-            # that does not allow it the exchange is the NCCL all-gather
-            ndev = torch.cuda.device_count()
-            ok = all(torch.cuda.can_device_access_peer(local, j)
-                     for j in range(min(world, ndev)) if j != local)
-            t_ok = torch.tensor([1 if ok else 0], dtype=torch.int64)
-            dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
-            if int(t_ok[0]) == 0:
-                if rank == 0:
-                    print("bench: no P2P access between the ranks' GPUs; exchange = nccl",
-                          file=sys.stderr)
-                args.exchange = "nccl"
-        if args.exchange == "fused":
-            # the commit stores pi_new into every peer's buffer over NVLink
-            # (CUDA IPC); gloo only carries the setup blobs
-            runner = PeerShardGroup(ctx, n, world, bounds, rank, Lm, tile, cfg, prc)
-            blobs = [None] * world
-            dist.all_gather_object(blobs, runner.export())
-            runner.connect(blobs)
-        else:
-            ids = [nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(ids, src=0)
-            runner = ShardGroup(ctx, n, world, bounds, rank, [(Lm, tile)], cfg, prc, ids[0])
+        if args.exchange == "fused" and not peer_ok():
+            if rank == 0:
+                print("bench: no P2P access between the ranks' GPUs; exchange = nccl",
+                      file=sys.stderr)
+            args.exchange = "nccl"
+        runner = make_shard_runner(args.exchange, n, bounds, Lm, tile, prc)
         local_rows, local_nnz = int(bounds[rank + 1] - bounds[rank]), Lm.nnz
         run = runner.run
         pre_ms = (relabel_s + tile.preprocess_seconds) * 1e3
+        barrier()  # every rank's preprocessing is done before the first run
 
     for _ in range(args.warmup):
         run()
@@ -443,17 +554,20 @@ def main():
     sampler.start()
     time.sleep(0.2)
     launches0 = ctx.launch_count
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    # one event per step boundary (recording does not synchronise): the
+    # total over the K steps is the value, the per-step median goes beside it
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier()
-    ev0.record(stream)
-    for _ in range(args.steps):
+    evs[0].record(stream)
+    for k in range(args.steps):
         run()
-    ev1.record(stream)
+        evs[k + 1].record(stream)
     barrier()
     clocks = sampler.stop()
     launches = ctx.launch_count - launches0
-    ms_local = ev0.elapsed_time(ev1)
+    ms_local = evs[0].elapsed_time(evs[-1])
+    step_ms = sorted(evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps))
+    step_ms_median = max_over_ranks(step_ms[len(step_ms) // 2])
     ms_total = max_over_ranks(ms_local)
     res, hist = runner.result(want_history=True)
     assert res.iterations == args.iters, res.iterations
@@ -500,15 +614,62 @@ def main():
         h2d = d2h = 4 * (r1 - r0)
     e2e_call()
     barrier()
+    e2e_steps = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        e2e_call()
+        t1 = time.perf_counter()
+        e2e_call()  # synchronous: ends with pi on the host
+        e2e_steps.append(time.perf_counter() - t1)
     barrier()
     e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
     e2e_val = args.iters / e2e_s
+    e2e_steps.sort()
+    e2e_median_s = max_over_ranks(e2e_steps[len(e2e_steps) // 2])
     mass = float(pi_out.double().sum()) if world == 1 else res.mass
+    # the device-resident loop once more right after the e2e window: the two
+    # windows see the same clocks / power state only if these agree
+    recheck = {}
+    if args.steps >= 2:
+        barrier()
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(2):
+            run()
+        r1.record(stream)
+        barrier()
+        rms = max_over_ranks(r0.elapsed_time(r1)) / 2
+        recheck = {"iters_per_s": args.iters / (rms * 1e-3), "ms_per_step": rms, "steps": 2}
 
-    extras = {}
+    if world > 1 and not args.no_extras:
+        if args.exchange == "fused":
+            # north_star's exchange, timed beside the fused one on the same
+            # shards: one in-place ncclAllGather of the compacted pi per
+            # iteration (NVLink / NVSwitch, NVLS when NCCL enables it)
+            if os.environ.get("MBX_BENCH_ONE_DEVICE") == "1":
+                extras["nccl_allgather_exchange"] = {
+                    "unavailable": "the ranks share one device; NCCL needs one GPU per rank"}
+            else:
+                g2 = make_shard_runner("nccl", n, bounds, Lm, tile, prc)
+                extras["nccl_allgather_exchange"] = time_shard_runner(g2, 2, args.steps,
+                                                                      args.iters)
+                g2.close()
+        if scale != 24:
+            # BASELINE C2's matrix (scale 24) sharded the same way: the
+            # strong-scaling counterpart of the N = 1 line
+            Q = mb.DeviceMatrix.rmat(ctx, 24, 16, seed=1, transition=True, dtype=np.float32)
+            if args.vertex_order == "degree":
+                Q, _ = Q.relabel_by_degree(want_rank=False)
+            nq = Q.n_rows
+            qb, QL, qt, _ = prepare_rank_shard(Q, world, rank, cfg)
+            del Q
+            gq = make_shard_runner(args.exchange, nq, qb, QL, qt, prc)
+            d = time_shard_runner(gq, 2, args.steps, args.iters)
+            d["exchange"] = args.exchange
+            extras["c2_s24_sharded"] = d
+            gq.close()
+            del QL, qt
+
     cpu = None
     if rank == 0 and world == 1:
         if args.vertex_order == "degree" and P_natural is not None and not args.no_extras:
@@ -541,24 +702,42 @@ def main():
             extras["c3_powerlaw_f64"] = spmv_numbers(
                 mb, ctx, stream, 0, np.float64, args.spmv_reps, peak,
                 make=lambda cx, dt: mb.DeviceMatrix.powerlaw(cx, 22, seed=3, dtype=dt),
-                label="power-law 2^22 rows, 10% empty, rows up to 2^20 nnz")
+                label="power-law 2^22 rows, 10% empty, rows up to 2^20 nnz",
+                reference=None if args.no_cpu_baseline else "same")
             # BASELINE C5: 27-point stencil, 64M rows (uniform sparsity)
             for dt, key in ((np.float32, "c5_stencil_f32"), (np.float64, "c5_stencil_f64")):
                 extras[key] = spmv_numbers(
                     mb, ctx, stream, 0, dt, max(5, args.spmv_reps // 3), peak,
                     make=lambda cx, d: mb.DeviceMatrix.stencil27(cx, 400, d),
-                    label="27-point stencil 400^3 (64M rows)")
+                    label="27-point stencil 400^3 (64M rows)",
+                    reference=None if args.no_cpu_baseline else (
+                        lambda cx, d: mb.DeviceMatrix.stencil27(cx, 160, d),
+                        "27-point stencil 160^3 (4.1M rows, 109M nonzeros): a bounded sample "
+                        "of C5 (the full 1.7 G-nonzero matrix takes ~20 GB of host memory)"))
+            # BASELINE C4's matrix (scale 27, 2.1 G nonzeros) on this one GPU:
+            # the anchor of the 2/4/8-GPU runs (bench.py --gpus N defaults to it)
+            Q = mb.DeviceMatrix.rmat(ctx, 27, 16, seed=1, transition=True, dtype=np.float32)
+            if args.vertex_order == "degree":
+                Q, _ = Q.relabel_by_degree(want_rank=False)
+            d = single_gpu_rate(mb, stream, Q, cfg, 2, args.iters)
+            d.update({"scale": 27, "n": Q.n_rows, "nnz": Q.nnz,
+                      "frac": (8 * Q.nnz + 16 * Q.n_rows + 4) / (d["us_per_iteration"] * 1e-6)
+                      / 1e9 / peak})
+            extras["c4_s27_n1"] = d
+            del Q
+            torch.cuda.synchronize()
         if not args.no_cpu_baseline:
             import oracle as O
             if O.ref() is not None:
                 ro, cols, _ = P_natural.download(want_values=False)  # R-MAT's own numbering
                 nthreads = os.cpu_count() or 1
-                r = cpu_reference_pagerank(ro, cols, n, 2, 3, 1, nthreads)
+                r = cpu_reference_pagerank(ro, cols, n, 2, 5, 1, nthreads)
                 cpu = {"value": r["value"], "unit": "iters/s", "cores": nthreads,
-                       "kind": "reference",
-                       "sample": f"3 x 2 PageRank iterations (after 1 warm-up) of the reference "
-                                 f"MerbitBackend<float> on ThreadPool({nthreads}), same scale-"
-                                 f"{scale} transition matrix; its generate_tile took "
+                       "kind": "reference", "cpu_model": cpu_model(),
+                       "sample": f"5 x 2 = {r['iterations']} PageRank iterations (after one "
+                                 f"2-iteration warm-up) of the reference MerbitBackend<float> on "
+                                 f"ThreadPool({nthreads}), same scale-{scale} transition matrix "
+                                 f"(natural order); its generate_tile took "
                                  f"{r['preprocess_seconds']:.2f} s"}
     line = {
         "metric": METRIC, "value": iters_per_s, "unit": "iters/s", "n_gpus": world,
@@ -585,7 +764,12 @@ def main():
                      "bytes_per_launch": b_iter, "us_per_iteration": t_iter_local * 1e6,
                      "gather_bound": gather_bound},
         "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "mass": mass},
+                "d2h_bytes_per_step": d2h, "mass": mass,
+                "median_step_ms": e2e_median_s * 1e3,
+                "median_iters_per_s": args.iters / e2e_median_s},
+        "median_step_ms": step_ms_median,
+        "median_iters_per_s": args.iters / (step_ms_median * 1e-3),
+        "recheck_after_e2e": recheck,
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": cpu,

@@ -250,6 +250,10 @@ MBX_API int mbx_matrix_build_xcache(mbx_context* ctx, mbx_matrix* m,
                                     int max_hubs, double* seconds);
 MBX_API int mbx_matrix_xcache_info(const mbx_matrix* m, int* hubs,
                                    double* coverage);
+/* Frees the matrix's derived device copies -- the K2 slot copy, the x hub
+ * cache and the COO comparator's row array -- keeping only the CSR.  Plans
+ * over the matrix rebuild what they need before their next run. */
+MBX_API int mbx_matrix_release_caches(mbx_matrix* m);
 /* Device pointers of the hub-encoded column array and the hub column list
  * (NULL when no cache is built). */
 MBX_API int mbx_matrix_xcache_ptrs(const mbx_matrix* m,

@@ -289,6 +289,14 @@ mbx_matrix* upload_common(mbx_context* ctx, int precision, int64_t n_rows, int64
 
 }  // namespace
 
+namespace mbx {
+// the C-ABI's config / TILE validation, shared with solvers.cu
+void validate_config(const mbx_simt_config* c) { check_config(c); }
+void validate_tile(const mbx_matrix* m, const mbx_tile* t, const mbx_simt_config* c) {
+  check_tile_matches(m, t, c);
+}
+}  // namespace mbx
+
 // ============================================================================
 // C ABI
 // ============================================================================
@@ -640,6 +648,26 @@ MBX_API int mbx_matrix_xcache_ptrs(const mbx_matrix* m, const int32_t** cols_hub
   });
 }
 
+MBX_API int mbx_matrix_release_caches(mbx_matrix* m) {
+  return guarded([&] {
+    mbx_context* ctx = m->ctx;
+    Device dg(ctx->device);
+    mbx::free_slots(ctx, m);
+    if (m->cols_hub || m->hub_cols) {
+      dfree(ctx, m->cols_hub);
+      dfree(ctx, m->hub_cols);
+      m->cols_hub = m->hub_cols = nullptr;
+      m->hub_avail = 0;
+      m->hub_coverage = 0.0;
+      ++m->version;
+      ++m->gen;
+    }
+    dfree(ctx, m->coo_rows);
+    m->coo_rows = nullptr;
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 MBX_API int mbx_matrix_destroy(mbx_matrix* m) {
   return guarded([&] {
     if (!m) return;
@@ -865,6 +893,7 @@ struct mbx_pagerank_plan_s {
   bool ran = false;
   // cache key (mbx_pagerank): what the plan was built from
   uint64_t p_version = 0, t_serial = 0, tuning_epoch = 0;
+  uint64_t p_gen = 0;  // the matrix's buffer generation the graph captured
   mbx_pagerank_config cfg_in{};
 };
 
@@ -947,6 +976,92 @@ void launch_power_loop(mbx_pagerank_plan* pl) {
 
 }  // namespace
 
+namespace {
+
+// Capture the power loop of `pl` (geometry already made): records the
+// matrix's buffer generation the graph was captured against.
+void capture_plan(mbx_pagerank_plan* pl) {
+  mbx_context* ctx = pl->ctx;
+  if (pl->graph) {
+    cudaGraphExecDestroy(pl->graph);
+    pl->graph = nullptr;
+  }
+  pl->p_gen = pl->p->gen;
+  // The power loop as ONE CUDA graph with a device-driven WHILE node: the
+  // body (two iterations + the condition) replays until max_iters or the
+  // stop decision -- an early exit launches nothing more, and any max_iters
+  // fits one small graph.  MBX_GRAPH_MODE=unrolled captures the fixed-count
+  // loop instead (ncu does not profile kernels inside conditional nodes),
+  // =eager launches every kernel from the host.
+  const mbx::GraphMode gmode = mbx::graph_mode();
+  if (pl->cfg.max_iters > 0 && gmode == mbx::GraphMode::unrolled && pl->cfg.max_iters <= 4096) {
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int64_t before = ctx->launches;
+    cudaGraph_t graph;
+    MBX_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      launch_power_loop(pl);
+    } catch (...) {
+      cudaStreamEndCapture(ctx->stream, &graph);
+      throw;
+    }
+    MBX_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+    MBX_CUDA(cudaGraphInstantiate(&pl->graph, graph, 0));
+    cudaGraphDestroy(graph);
+    pl->graph_launches = ctx->launches - before;
+    ctx->launches = before;
+  } else if (pl->cfg.max_iters > 0 && gmode == mbx::GraphMode::device_loop) {
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaGraph_t graph;
+    MBX_CUDA(cudaGraphCreate(&graph, 0));
+    try {
+      cudaGraphConditionalHandle h;
+      MBX_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      MBX_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      const int64_t before = ctx->launches;
+      MBX_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeThreadLocal));
+      try {
+        launch_loop_body(pl, h);
+      } catch (...) {
+        cudaGraph_t dummy;
+        cudaStreamEndCapture(ctx->stream, &dummy);
+        throw;
+      }
+      MBX_CUDA(cudaStreamEndCapture(ctx->stream, &body));
+      const int64_t per_body = ctx->launches - before;
+      ctx->launches = before;
+      MBX_CUDA(cudaGraphInstantiate(&pl->graph, graph, 0));
+      // launches of a run to max_iters (an early stop launches fewer)
+      pl->graph_launches = per_body * ((pl->cfg.max_iters + 1) / 2);
+    } catch (...) {
+      cudaGraphDestroy(graph);
+      throw;
+    }
+    cudaGraphDestroy(graph);
+  }
+}
+
+// The matrix freed or rebuilt a buffer the plan's graph / geometry points at
+// (slot copy rebuilt for another TILE or hub setting, x hub cache rebuilt):
+// make the geometry again (rebuilding the slot copy for this TILE) and
+// re-capture before the next replay.
+void refresh_plan(mbx_pagerank_plan* pl) {
+  if (pl->p->gen == pl->p_gen) return;
+  MBX_CUDA(cudaStreamSynchronize(pl->ctx->stream));
+  pl->g = mbx::make_geometry(pl->ctx, pl->p, pl->t, pl->c.block_size);
+  capture_plan(pl);
+}
+
+}  // namespace
+
 extern "C" {
 
 MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, const mbx_tile* t,
@@ -999,66 +1114,7 @@ MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, cons
     MBX_CUDA(cudaEventCreate(&pl->e1));
     pl->iter_dev = static_cast<int64_t*>(dmalloc(ctx, 64));
     MBX_CUDA(cudaMemsetAsync(pl->iter_dev, 0, 64, ctx->stream));
-    // The power loop as ONE CUDA graph with a device-driven WHILE node: the
-    // body (two iterations + the condition) replays until max_iters or the
-    // stop decision -- an early exit launches nothing more, and any max_iters
-    // fits one small graph.  MBX_GRAPH_MODE=unrolled captures the fixed-count
-    // loop instead (ncu does not profile kernels inside conditional nodes),
-    // =eager launches every kernel from the host.
-    const mbx::GraphMode gmode = mbx::graph_mode();
-    if (cfg->max_iters > 0 && gmode == mbx::GraphMode::unrolled && cfg->max_iters <= 4096) {
-      MBX_CUDA(cudaStreamSynchronize(ctx->stream));
-      const int64_t before = ctx->launches;
-      cudaGraph_t graph;
-      MBX_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-      try {
-        launch_power_loop(pl.get());
-      } catch (...) {
-        cudaStreamEndCapture(ctx->stream, &graph);
-        throw;
-      }
-      MBX_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
-      MBX_CUDA(cudaGraphInstantiate(&pl->graph, graph, 0));
-      cudaGraphDestroy(graph);
-      pl->graph_launches = ctx->launches - before;
-      ctx->launches = before;
-    } else if (cfg->max_iters > 0 && gmode == mbx::GraphMode::device_loop) {
-      MBX_CUDA(cudaStreamSynchronize(ctx->stream));
-      cudaGraph_t graph;
-      MBX_CUDA(cudaGraphCreate(&graph, 0));
-      try {
-        cudaGraphConditionalHandle h;
-        MBX_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
-        cudaGraphNodeParams cp = {};
-        cp.type = cudaGraphNodeTypeConditional;
-        cp.conditional.handle = h;
-        cp.conditional.type = cudaGraphCondTypeWhile;
-        cp.conditional.size = 1;
-        cudaGraphNode_t node;
-        MBX_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
-        cudaGraph_t body = cp.conditional.phGraph_out[0];
-        const int64_t before = ctx->launches;
-        MBX_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
-                                               cudaStreamCaptureModeThreadLocal));
-        try {
-          launch_loop_body(pl.get(), h);
-        } catch (...) {
-          cudaGraph_t dummy;
-          cudaStreamEndCapture(ctx->stream, &dummy);
-          throw;
-        }
-        MBX_CUDA(cudaStreamEndCapture(ctx->stream, &body));
-        const int64_t per_body = ctx->launches - before;
-        ctx->launches = before;
-        MBX_CUDA(cudaGraphInstantiate(&pl->graph, graph, 0));
-        // launches of a run to max_iters (an early stop launches fewer)
-        pl->graph_launches = per_body * ((cfg->max_iters + 1) / 2);
-      } catch (...) {
-        cudaGraphDestroy(graph);
-        throw;
-      }
-      cudaGraphDestroy(graph);
-    }
+    capture_plan(pl.get());
     *out = pl.release();
   });
 }
@@ -1074,6 +1130,7 @@ MBX_API int mbx_pagerank_plan_run(mbx_pagerank_plan* pl, const void* pi0) {
   return guarded([&] {
     mbx_context* ctx = pl->ctx;
     Device dg(ctx->device);
+    refresh_plan(pl);
     plan_prologue(pl, pi0);
     MBX_CUDA(cudaEventRecord(pl->e0, ctx->stream));
     if (pl->graph) {

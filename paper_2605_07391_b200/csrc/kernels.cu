@@ -21,6 +21,7 @@
 // table); every row of y is ASSIGNED exactly once (interior rows by the warp
 // that closes them, boundary rows by K3), so no zero-fill, no atomics, and
 // bitwise run-to-run determinism.
+#include <atomic>
 #include <cfloat>
 #include <cmath>
 
@@ -68,6 +69,21 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t po
 }
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// Opt a kernel in to the device's full dynamic shared memory once per
+// (kernel variant, device): a per-instantiation bitmask of devices, updated
+// atomically (cudaFuncSetAttribute is idempotent, so two threads racing on
+// the same device both set it and both see the bit).
+template <typename K>
+void allow_max_smem(K kern, int device, int variant) {
+  static std::atomic<uint64_t> done[2];
+  const uint64_t bit = device < 64 ? (uint64_t(1) << device) : 0;
+  if (bit && (done[variant].load(std::memory_order_acquire) & bit)) return;
+  int optin = 0;
+  MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  MBX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  done[variant].fetch_or(bit, std::memory_order_acq_rel);
+}
 
 template <typename T>
 struct VecOf {
@@ -1141,13 +1157,7 @@ template <typename T, int SIGMA, bool PR, bool HUB>
 void launch_slot(mbx_context* ctx, const SlotParams<T>& p, size_t smem) {
   auto kern = p.g.prefetch ? spmv_slot_kernel<T, SIGMA, PR, HUB, true>
                            : spmv_slot_kernel<T, SIGMA, PR, HUB, false>;
-  static int configured[2] = {-1, -1};
-  if (configured[p.g.prefetch ? 1 : 0] != ctx->device) {
-    int optin = 0;
-    MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-    MBX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    configured[p.g.prefetch ? 1 : 0] = ctx->device;
-  }
+  allow_max_smem(kern, ctx->device, p.g.prefetch ? 1 : 0);
   const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
   const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));
   kern<<<grid, p.g.warps_per_cta * 32, smem, ctx->stream>>>(p);
@@ -1449,13 +1459,7 @@ template <typename T, int SIGMA, bool PR, bool HUB>
 void launch_w32(mbx_context* ctx, const SpmvParams<T>& p, size_t smem) {
   auto kern = p.g.prefetch ? spmv_w32_kernel<T, SIGMA, PR, HUB, true>
                            : spmv_w32_kernel<T, SIGMA, PR, HUB, false>;
-  static int configured[2] = {-1, -1};
-  if (configured[p.g.prefetch ? 1 : 0] != ctx->device) {
-    int optin = 0;
-    MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-    MBX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    configured[p.g.prefetch ? 1 : 0] = ctx->device;
-  }
+  allow_max_smem(kern, ctx->device, p.g.prefetch ? 1 : 0);
   const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
   const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));
   kern<<<grid, p.g.warps_per_cta * 32, smem, ctx->stream>>>(p);
@@ -1596,6 +1600,7 @@ size_t spmv_workspace_bytes(const Geometry& g, int precision, bool pagerank) {
 }
 
 void free_slots(mbx_context* ctx, const mbx_matrix* m) {
+  if (m->slots.vals || m->slots.cols) ++m->gen;
   if (m->slots.vals) cudaFreeAsync(m->slots.vals, ctx->stream);
   if (m->slots.cols) cudaFreeAsync(m->slots.cols, ctx->stream);
   m->slots = mbx_matrix::SlotCache{};

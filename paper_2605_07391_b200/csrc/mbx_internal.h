@@ -150,6 +150,10 @@ struct mbx_matrix_s {
   int hub_avail = 0;
   double hub_coverage = 0.0;  // fraction of nonzeros that reference a hub
   uint64_t version = 0;       // bumped whenever cols_hub is rebuilt
+  // bumped whenever a device buffer a captured PageRank plan may reference
+  // (slot copy, cols_hub, hub_cols) is freed or rebuilt: plans compare it
+  // before every replay and re-capture on a change
+  mutable uint64_t gen = 0;
   // Lane-major slot copy of (values, [hub-encoded] columns) for one TILE:
   // slot (chunk c, step i, lane l) holds the element lane l consumes at step
   // i (zero for Down steps); built once per (TILE, column encoding) and
@@ -215,6 +219,9 @@ void launch_trace_counts(mbx_context* ctx, const mbx_tile* t,
 void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
                 const PrArgs* pr, double* cta_part, unsigned int* counter);
 int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m);
+// capi.cu's validation of a SimtConfig and of a TILE against (matrix, config)
+void validate_config(const mbx_simt_config* c);
+void validate_tile(const mbx_matrix* m, const mbx_tile* t, const mbx_simt_config* c);
 // Makes ctx->device current for the scope of a C-ABI call (the caller's
 // thread may have another device current) and restores the previous one.
 struct DeviceGuard {

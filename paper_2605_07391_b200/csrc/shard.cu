@@ -950,6 +950,8 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
     mbx::DeviceGuard dg(ctx->device);
     if (!nccl_id && nlocal != world)
       mbx::fail(MBX_CONFIG_ERROR, "shard group: without NCCL every shard must be local");
+    if (nccl_id && nlocal != 1)
+      mbx::fail(MBX_CONFIG_ERROR, "shard group: with NCCL each process holds exactly one shard");
     GroupPtr G(new mbx_shard_group_s);
     group_init(G.get(), ctx, n_global, world, bounds, rank0, nlocal, mats, c, cfg, false);
     cudaStream_t st = ctx->stream;

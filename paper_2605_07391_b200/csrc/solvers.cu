@@ -371,11 +371,10 @@ MBX_API int mbx_bicgstab(mbx_context* ctx, const mbx_matrix* a, const mbx_tile* 
   return bguard([&] {
     using mbx::fail;
     if (a->n_rows != a->n_cols) fail(MBX_DIMENSION_ERROR, "bicgstab needs a square system");
-    if (t->info.omega != c->omega || t->info.sigma != c->sigma ||
-        t->info.n_rows != a->n_rows || t->info.nnz != a->nnz)
-      fail(MBX_CONFIG_ERROR, "bicgstab: TILE does not match the matrix / config");
+    mbx::validate_config(c);
+    mbx::validate_tile(a, t, c);
     if (cfg->max_iters < 0) fail(MBX_CONFIG_ERROR, "bicgstab: max_iters must be >= 0");
-    MBX_CUDA(cudaSetDevice(ctx->device));
+    mbx::DeviceGuard dg(ctx->device);  // the caller's current device is restored
     cudaStream_t s = ctx->stream;
     const int64_t n = a->n_rows;
     const size_t vs = mbx::value_size(a->precision);

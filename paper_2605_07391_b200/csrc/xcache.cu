@@ -97,6 +97,7 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   m->hub_avail = 0;
   m->hub_coverage = 0.0;
   ++m->version;  // invalidates slot copies built over the old encoding
+  ++m->gen;      // and the graphs captured over the old buffers
   const Tuning& tu = ctx->tuning;
   int slots = max_hub_slots(ctx, tu.warps_per_cta, tu.ctas_per_sm,
                             m->precision == MBX_F32 ? 14 : 7, m->precision);

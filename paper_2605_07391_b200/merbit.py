@@ -326,6 +326,18 @@ class DeviceMatrix:
         _check(_lib.lib().mbx_matrix_download(self.h, _ptr(ro), _ptr(cols), _ptr(vals)))
         return ro, cols[:self.nnz], (vals[:self.nnz] if want_values else None)
 
+    def row_offsets(self):
+        """Only the row offsets (int64[n_rows + 1]) on the host: no column or
+        value bytes cross the bus (row-shard planning at scale 27 would
+        otherwise copy 8.5 GB of columns per rank)."""
+        ro = np.zeros(self.n_rows + 1, np.int64)
+        _check(_lib.lib().mbx_matrix_download(self.h, _ptr(ro), None, None))
+        return ro
+
+    def release_caches(self):
+        """Free the slot copy, x hub cache and COO rows (CSR kept)."""
+        _check(_lib.lib().mbx_matrix_release_caches(self.h))
+
     def build_xcache(self, max_hubs: int = -1) -> float:
         """Rank columns by reference count and stage the hottest x entries in
         shared memory during SpMV (results bitwise unchanged).  Returns seconds."""
@@ -799,6 +811,19 @@ def row_slice(m: DeviceMatrix, r0: int, r1: int) -> DeviceMatrix:
     h = C.c_void_p()
     _check(_lib.lib().mbx_matrix_row_slice(m.ctx.h, m.h, r0, r1, C.byref(h)))
     return DeviceMatrix(m.ctx, h)
+
+
+def prepare_rank_shard(P: DeviceMatrix, world: int, rank: int, c: SimtConfig,
+                       row_weight: float | None = None):
+    """One rank's preprocessing of the row-sharded PageRank (bench.py N > 1,
+    the path tests/test_gpu_bench_path.py gates): the cost-weighted cut of P's
+    rows (only the row offsets come to the host), this rank's row slice and
+    its TILE.  Returns (bounds, local matrix, local TILE, row weight)."""
+    n = P.n_rows
+    w = pagerank_row_weight(n, np.dtype(P.dtype).itemsize) if row_weight is None else row_weight
+    bounds = plan_row_shards(P.row_offsets(), n, P.nnz, world, w)
+    L = row_slice(P, int(bounds[rank]), int(bounds[rank + 1]))
+    return bounds, L, generate_tile_for(L, c), w
 
 
 class ShardGroup:

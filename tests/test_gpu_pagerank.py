@@ -266,3 +266,42 @@ def test_device_driven_loop_early_stop(ctx):
     b = mb.pagerank(None, cfg, backend=be, on_iteration=lambda r, pi, e: None)
     assert a.status == "converged" and a.iterations == 1 == b.iterations
     assert np.array_equal(a.pi, b.pi)
+
+
+
+def test_plan_recaptures_after_matrix_buffers_change(ctx):
+    """A captured PageRank plan holds raw pointers to the matrix's slot copy
+    and x hub cache.  Rebuilding either -- an SpMV with another TILE rebuilds
+    the slot copy; build_xcache frees and rebuilds the hub encoding -- bumps
+    the matrix's buffer generation, and the plan (here the one mbx_pagerank
+    keeps on the context, and a PageRankPlan) re-captures before its next
+    replay: results stay bitwise equal to the first run."""
+    import torch
+    c = mb.SimtConfig.make(32, 14, 128)
+    c2 = mb.SimtConfig.make(32, 14, 64)
+    P = mb.DeviceMatrix.rmat(ctx, 13, 16, seed=5, transition=True, dtype=np.float32)
+    n = P.n_rows
+    be = type("B", (), {})()
+    be.matrix, be.tile_, be.c = P, mb.generate_tile_for(P, c), c
+    t2 = mb.generate_tile_for(P, c2)
+    cfg = mb.PageRankConfig(0.85, 1e-30, 20, 0)
+    a = mb.pagerank(None, cfg, backend=be)  # plan cached on the context
+    x = O.hash_uniform(3, n, 0.0, 1.0, np.float32)
+    y2 = mb.spmv_merbit(P, t2, c2, x, mb.DualBuffer(n, np.float32))  # slot copy for t2
+    b = mb.pagerank(None, cfg, backend=be)  # cached plan, slot copy rebuilt for t1
+    assert np.array_equal(a.pi.view(np.uint32), b.pi.view(np.uint32))
+    # the plan object: run, rebuild the hub cache + slots, run again
+    plan = mb.PageRankPlan(P, be.tile_, c, cfg)
+    xd = torch.empty(n, dtype=torch.float32, device="cuda")
+    yd = torch.empty(n, dtype=torch.float32, device="cuda")
+    plan.run()
+    r1, h1 = plan.result(want_history=True)
+    P.build_xcache()
+    mb.spmv_device(P, t2, c2, xd.data_ptr(), yd.data_ptr())
+    torch.cuda.synchronize()
+    plan.run()
+    r2, h2 = plan.result(want_history=True)
+    assert np.array_equal(h1, h2) and r1.l1_residual == r2.l1_residual
+    y2b = mb.spmv_merbit(P, t2, c2, x, mb.DualBuffer(n, np.float32))
+    assert np.array_equal(y2.view(np.uint32), y2b.view(np.uint32))
+    plan.close()
