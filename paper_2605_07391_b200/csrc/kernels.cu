@@ -71,18 +71,19 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t po
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 // Opt a kernel in to the device's full dynamic shared memory once per
-// (kernel variant, device): a per-instantiation bitmask of devices, updated
-// atomically (cudaFuncSetAttribute is idempotent, so two threads racing on
-// the same device both set it and both see the bit).
+// (kernel, device).  `done` is the calling launcher's own bitmask of devices
+// (one per kernel instantiation -- kernels of one signature share a pointer
+// TYPE, so the memo cannot live in a template over that type), updated
+// atomically: cudaFuncSetAttribute is idempotent, so two threads racing on
+// the same device both set it and both see the bit.
 template <typename K>
-void allow_max_smem(K kern, int device, int variant) {
-  static std::atomic<uint64_t> done[2];
+void allow_max_smem(K kern, int device, std::atomic<uint64_t>& done) {
   const uint64_t bit = device < 64 ? (uint64_t(1) << device) : 0;
-  if (bit && (done[variant].load(std::memory_order_acquire) & bit)) return;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return;
   int optin = 0;
   MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   MBX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  done[variant].fetch_or(bit, std::memory_order_acq_rel);
+  done.fetch_or(bit, std::memory_order_acq_rel);
 }
 
 template <typename T>
@@ -1157,7 +1158,8 @@ template <typename T, int SIGMA, bool PR, bool HUB>
 void launch_slot(mbx_context* ctx, const SlotParams<T>& p, size_t smem) {
   auto kern = p.g.prefetch ? spmv_slot_kernel<T, SIGMA, PR, HUB, true>
                            : spmv_slot_kernel<T, SIGMA, PR, HUB, false>;
-  allow_max_smem(kern, ctx->device, p.g.prefetch ? 1 : 0);
+  static std::atomic<uint64_t> done[2];  // per (T, SIGMA, PR, HUB), prefetch variant
+  allow_max_smem(kern, ctx->device, done[p.g.prefetch ? 1 : 0]);
   const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
   const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));
   kern<<<grid, p.g.warps_per_cta * 32, smem, ctx->stream>>>(p);
@@ -1459,7 +1461,8 @@ template <typename T, int SIGMA, bool PR, bool HUB>
 void launch_w32(mbx_context* ctx, const SpmvParams<T>& p, size_t smem) {
   auto kern = p.g.prefetch ? spmv_w32_kernel<T, SIGMA, PR, HUB, true>
                            : spmv_w32_kernel<T, SIGMA, PR, HUB, false>;
-  allow_max_smem(kern, ctx->device, p.g.prefetch ? 1 : 0);
+  static std::atomic<uint64_t> done[2];  // per (T, SIGMA, PR, HUB), prefetch variant
+  allow_max_smem(kern, ctx->device, done[p.g.prefetch ? 1 : 0]);
   const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
   const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));
   kern<<<grid, p.g.warps_per_cta * 32, smem, ctx->stream>>>(p);
