@@ -1742,6 +1742,22 @@ void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
   MBX_CUDA(cudaGetLastError());
 }
 
+// Loads the PageRank start / yardstick kernels of `precision` now.  With
+// CUDA's lazy module loading the FIRST launch of a kernel loads its module,
+// which waits for the kernels already running in the context; a caller that
+// has a spinning peer barrier in flight (several ranks of a fused shard
+// group in one process) would block there until the barrier gives up.
+void preload_pr_kernels(int precision) {
+  cudaFuncAttributes a;
+  if (precision == MBX_F32) {
+    MBX_CUDA(cudaFuncGetAttributes(&a, pr_init_kernel<float>));
+    MBX_CUDA(cudaFuncGetAttributes(&a, csr_kernel<float, true>));
+  } else {
+    MBX_CUDA(cudaFuncGetAttributes(&a, pr_init_kernel<double>));
+    MBX_CUDA(cudaFuncGetAttributes(&a, csr_kernel<double, true>));
+  }
+}
+
 void launch_pr_init(mbx_context* ctx, int precision, int64_t n, const void* pi0, void* pi,
                     const uint32_t* dangling, PrScalars* out, double* block_part,
                     unsigned int* counter) {

@@ -219,6 +219,7 @@ void launch_trace_counts(mbx_context* ctx, const mbx_tile* t,
 void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
                 const PrArgs* pr, double* cta_part, unsigned int* counter);
 int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m);
+void preload_pr_kernels(int precision);
 // capi.cu's validation of a SimtConfig and of a TILE against (matrix, config)
 void validate_config(const mbx_simt_config* c);
 void validate_tile(const mbx_matrix* m, const mbx_tile* t, const mbx_simt_config* c);

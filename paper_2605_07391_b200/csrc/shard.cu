@@ -880,6 +880,28 @@ void init_shard_uniform(mbx_shard_group* G, const mbx::Shard& s, unsigned char* 
   ctx->launches += 2;
 }
 
+// Load every kernel a run launches outside the captured graph before the
+// first run: under lazy module loading a first launch waits for the running
+// kernels of the context, and with several ranks of a fused group in one
+// process that includes a peer barrier spinning until the next rank's run is
+// issued -- from this very thread.
+void preload_run_kernels(mbx_shard_group* G) {
+  cudaFuncAttributes a;
+  MBX_CUDA(cudaFuncGetAttributes(&a, mbx::peer_barrier_kernel));
+  MBX_CUDA(cudaFuncGetAttributes(&a, mbx::barrier_combine_kernel));
+  MBX_CUDA(cudaFuncGetAttributes(&a, mbx::combine_kernel));
+  MBX_CUDA(cudaFuncGetAttributes(&a, mbx::bump_epoch_kernel));
+  MBX_CUDA(cudaFuncGetAttributes(&a, mbx::shard_init_tail_kernel));
+  if (G->precision == MBX_F32) {
+    MBX_CUDA(cudaFuncGetAttributes(&a, mbx::shard_init_kernel<float>));
+    MBX_CUDA(cudaFuncGetAttributes(&a, mbx::scatter_exchange_kernel<float>));
+  } else {
+    MBX_CUDA(cudaFuncGetAttributes(&a, mbx::shard_init_kernel<double>));
+    MBX_CUDA(cudaFuncGetAttributes(&a, mbx::scatter_exchange_kernel<double>));
+  }
+  mbx::preload_pr_kernels(G->precision);
+}
+
 // peer groups: this shard's start chunk (values + tail) out to every peer
 void push_start_chunk(mbx_shard_group* G, const mbx::Shard& s) {
   if (!G->peer) return;
@@ -1086,6 +1108,7 @@ MBX_API int mbx_shard_group_connect(mbx_shard_group* G, const void* blobs) {
     group_layout(G, mats, tiles, gseen, G->chunk_bytes);
     cudaFreeAsync(gseen, st);
     group_capture(G);
+    preload_run_kernels(G);
     G->connected = true;
   });
 }

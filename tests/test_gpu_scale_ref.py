@@ -121,7 +121,9 @@ def test_c5_full_size_random_x(cx, dtype):
     tdt = torch.float32 if dtype == np.float32 else torch.float64
     xd = torch.from_numpy(x).to("cuda")
     yd = torch.empty(A.n_rows, dtype=tdt, device="cuda")
+    torch.cuda.synchronize()  # x is on the device before the library's stream reads it
     mb.spmv_device(A, t, c, xd.data_ptr(), yd.data_ptr())
+    cx.synchronize()  # and y is complete before torch's stream copies it out
     y = yd.cpu().numpy().astype(np.float64)
     del A, t, xd, yd
     torch.cuda.synchronize()
