@@ -77,6 +77,7 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   }
   // lane-major slot copy for this TILE (built once, outside any capture)
   g.slots = ensure_slots(const_cast<mbx_context*>(ctx), m, t, g) ? 1 : 0;
+
   if (!g.slots && g.hub_count > 0) {
     // the staged kernel needs more shared memory per warp than the slot one
     const bool slot_budget = ctx->tuning.layout == 1 && g.sigma == default_sigma(m->precision);
@@ -879,6 +880,7 @@ struct mbx_pagerank_plan_s {
   void* pi[2] = {nullptr, nullptr};
   void* ref[2] = {nullptr, nullptr};
   uint32_t* dangling = nullptr;
+  int64_t dang_from = -1;  // dangling rows = [dang_from, n) when a suffix
   mbx::PrScalars* scal = nullptr;      // [max_iters + 1]
   mbx::PrScalars* ref_scal = nullptr;  // [reference_iters + 1]
   double* range_part = nullptr;
@@ -930,6 +932,7 @@ mbx::PrArgs pr_args(mbx_pagerank_plan* pl, int64_t r, const void* yard) {
   mbx::PrArgs a;
   a.pi_old = pl->pi[(r - 1) & 1];
   a.dangling = pl->dangling;
+  a.dang_from = pl->dang_from;
   a.yardstick = yard;
   a.yard_const = pl->p->precision == MBX_F32 ? double(1.0f / float(pl->n)) : 1.0 / double(pl->n);
   a.damping = pl->cfg.damping;
@@ -1096,6 +1099,7 @@ MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, cons
       for (int i = 0; i < 2; ++i) pl->ref[i] = dmalloc(ctx, pl->n * pl->vs + 256);
     pl->dangling = static_cast<uint32_t*>(dmalloc(ctx, ((pl->n + 31) / 32) * 4 + 64));
     mbx::launch_dangling_mask(ctx, p, pl->dangling);
+    pl->dang_from = mbx::dangling_suffix_start(ctx, pl->dangling, pl->n);
     pl->scal = static_cast<mbx::PrScalars*>(dmalloc(ctx, (cfg->max_iters + 1) * sizeof(mbx::PrScalars)));
     pl->ref_scal = static_cast<mbx::PrScalars*>(
         dmalloc(ctx, (cfg->reference_iters + 1) * sizeof(mbx::PrScalars)));
@@ -1159,6 +1163,7 @@ void plan_prologue(mbx_pagerank_plan* pl, const void* pi0) {
         mbx::PrArgs a;
         a.pi_old = pl->ref[(r - 1) & 1];
         a.dangling = pl->dangling;
+        a.dang_from = pl->dang_from;
         a.yard_const = 1.0;
         a.damping = pl->cfg.damping;
         a.inv_n = 1.0 / double(pl->n);

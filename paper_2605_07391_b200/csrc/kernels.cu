@@ -24,8 +24,18 @@
 #include <atomic>
 #include <cfloat>
 #include <cmath>
+#include <vector>
 
 #include "mbx_internal.h"
+
+// rows per lane whose loads one memory round trip carries in the PageRank
+// commit of row-heavy (> kSlotRowBuf rows) and nonzero-free tiles
+#ifndef MBX_DIRECT_UNROLL
+#define MBX_DIRECT_UNROLL 2
+#endif
+#ifndef MBX_EMPTY_UNROLL
+#define MBX_EMPTY_UNROLL 2
+#endif
 
 namespace mbx {
 namespace {
@@ -264,11 +274,16 @@ __device__ __forceinline__ void pr_commit_v(const PrArgs& pr, T base, int64_t ro
   }
 }
 
+__device__ __forceinline__ bool pr_dang(const PrArgs& pr, int64_t row) {
+  return pr.dang_from >= 0 ? row >= pr.dang_from
+                           : ((__ldg(pr.dangling + (row >> 5)) >> (row & 31)) & 1u) != 0u;
+}
+
 template <typename T>
 __device__ __forceinline__ void pr_commit(const PrArgs& pr, T base, int64_t row,
                                           T w, T* __restrict__ out, PrAcc& a) {
-  pr_commit_v<T>(pr, base, row, w, reinterpret_cast<const T*>(pr.pi_old)[row],
-                 (pr.dangling[row >> 5] >> (row & 31)) & 1u, out, a);
+  pr_commit_v<T>(pr, base, row, w, reinterpret_cast<const T*>(pr.pi_old)[row], pr_dang(pr, row),
+                 out, a);
 }
 
 // iteration bookkeeping of host-unrolled launches (prev/next/iter baked in)
@@ -886,6 +901,74 @@ __device__ __forceinline__ void store_acc(double* wa, int lid, const PrAcc& a) {
   wa[96 + lid] = a.err;
 }
 
+// ---- TMA bulk staging of the next tile's column slots + descriptors ----
+// (mode 2 of the slot kernel): one lane per warp arms the warp's mbarrier
+// with the byte count and issues two cp.async.bulk copies global -> shared;
+// the lanes wait on the barrier's phase, read their operands with LDS, and
+// the buffer is re-armed for the following tile.  The column stream then
+// pays its DRAM latency behind the previous tile's gathers and commit.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(m)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t phase) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(m)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+// lane 0 only: stage chunk c's column slots (TS int32) and its 32
+// descriptors into the warp's buffers (the generic-proxy reads of the
+// previous contents are ordered before the async-proxy writes)
+__device__ __forceinline__ void stage_chunk(uint64_t* m, int32_t* colbuf, uint32_t* descbuf,
+                                            const int32_t* scols, const uint32_t* lane_desc,
+                                            int64_t c, int ts, uint64_t pol) {
+  const uint32_t cbytes = uint32_t(ts) * 4u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)),
+               "r"(cbytes + 128u)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(colbuf)),
+      "l"(scols + c * ts), "r"(cbytes), "r"(smem_u32(m)), "l"(pol)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], 128, [%2], %3;" ::"r"(smem_u32(descbuf)),
+      "l"(lane_desc + c * 32), "r"(smem_u32(m)), "l"(pol)
+      : "memory");
+}
+template <int SIGMA, int G>
+__device__ __forceinline__ void lds_slot_cols(const int32_t* colbuf, int lid, int (&c)[SIGMA]) {
+  if constexpr (G == 2) {
+#pragma unroll
+    for (int g = 0; g < SIGMA / 2; ++g) {
+      const int2 v = *reinterpret_cast<const int2*>(colbuf + g * 64 + 2 * lid);
+      c[2 * g] = v.x;
+      c[2 * g + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < SIGMA; ++i) c[i] = colbuf[i * 32 + lid];
+  }
+}
+
+// per-warp staging area of mode 2 (after the row buffers and accumulators)
+template <int SIGMA>
+struct StageBytes {
+  static constexpr size_t value = size_t(32 * SIGMA) * 4 + 128 + 16;
+};
+
 template <typename T, bool PR>
 __device__ __forceinline__ void commit_row(const SlotParams<T>& p, T base, int64_t row, T w,
                                            PrAcc& acc) {
@@ -895,10 +978,16 @@ __device__ __forceinline__ void commit_row(const SlotParams<T>& p, T base, int64
     p.y[row] = w;
 }
 
-template <typename T, int SIGMA, bool PR, bool HUB, bool PF>
+template <typename T, int SIGMA, bool PR, bool HUB, int MODE>
 __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub, T* rowbuf,
                                            int64_t range, int lid, uint64_t pol, T base,
-                                           double* wacc) {
+                                           double* wacc, unsigned char* stg, uint32_t& phase,
+                                           int64_t next_range) {
+  constexpr bool PF = MODE == 1;
+  constexpr bool TMA = MODE == 2;
+  int32_t* colbuf = reinterpret_cast<int32_t*>(stg);
+  uint32_t* descbuf = reinterpret_cast<uint32_t*>(stg + size_t(32 * SIGMA) * 4);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(stg + size_t(32 * SIGMA) * 4 + 128);
   constexpr int G = 8 / int(sizeof(T));
   constexpr int TS = 32 * SIGMA;
   const Geometry& g = p.g;
@@ -929,6 +1018,27 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
     const int nrows = static_cast<int>(y1 - y0);
     const T* vb = p.svals + c * TS;
     const int32_t* cb = p.scols + c * TS;
+    if (TMA) {
+      mbar_wait(mbar, phase);  // chunk c's columns + descriptors have landed
+      phase ^= 1u;
+    }
+    // the next chunk this warp walks: c + 1, or the first of its next range
+    const int64_t cnext = ci + 1 < nc ? c + 1
+                          : next_range >= 0 ? next_range * g.chunks_per_range : int64_t(-1);
+    // TMA: every lane has its operands in registers -> re-arm the buffer
+    auto restage = [&]() {
+      if (TMA) {
+        __syncwarp();
+        if (lid == 0 && cnext >= 0)
+          stage_chunk(mbar, colbuf, descbuf, p.scols, p.lane_desc, cnext, TS, pol);
+      }
+    };
+    auto get_cols = [&](int (&col)[SIGMA]) {
+      if (TMA)
+        lds_slot_cols<SIGMA, G>(colbuf, lid, col);
+      else
+        load_slot_cols<SIGMA, G>(cb, lid, col, pol);
+    };
     if (PF && lid == 0 && ci + 1 < nc) {
       // one bulk L2 prefetch per stream for the next tile: its column and
       // value slots then arrive at L2 latency instead of DRAM latency
@@ -942,7 +1052,8 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
       // (fast_tile_reduce, merbit_spmv.hpp:58-77) -- the butterfly's lane 0
       // adds exactly the halving tree's operand pairs
       int col[SIGMA];
-      load_slot_cols<SIGMA, G>(cb, lid, col, pol);
+      get_cols(col);
+      restage();
       uint32_t live = 0;
 #pragma unroll
       for (int i = 0; i < SIGMA; ++i) live |= (32 * i + lid < cnt ? 1u : 0u) << i;
@@ -960,24 +1071,51 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
     if (cnt == 0) {
       // no nonzero: the first closure ends the carried row, the rest are
       // empty rows (merbit_spmv.hpp:217-224)
-      PrAcc acc;
-      if (PR) acc = load_acc(wacc, lid);
+      restage();
+      if (PR) {
+        if (nrows > 0) {
+          if (head_open) head_val = carry;
+          constexpr int kU = MBX_EMPTY_UNROLL;
+          const T* pold = reinterpret_cast<const T*>(p.pr.pi_old);
+          PrAcc acc = load_acc(wacc, lid);
+          for (int k0 = lid; k0 < nrows; k0 += 32 * kU) {
+            T po[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const int k = k0 + 32 * u;
+              po[u] = k < nrows ? __ldg(pold + int64_t(y0) + k) : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const int k = k0 + 32 * u;
+              if (k < nrows && !(k == 0 && head_open)) {
+                const int64_t row = int64_t(y0) + k;
+                pr_commit_v<T>(p.pr, base, row, k == 0 ? carry : T(0), po[u], pr_dang(p.pr, row),
+                               p.y, acc);
+              }
+            }
+          }
+          store_acc(wacc, lid, acc);
+          head_open = false;
+        }
+        carry = T(0);
+        continue;
+      }
       for (int k = lid; k < nrows; k += 32) {
         const T w = k == 0 ? carry : T(0);
         if (k == 0 && head_open) {
           head_val = w;
           continue;
         }
-        commit_row<T, PR>(p, base, int64_t(y0) + k, w, acc);
+        p.y[int64_t(y0) + k] = w;
       }
-      if (PR) store_acc(wacc, lid, acc);
       carry = T(0);
       if (nrows > 0) head_open = false;
       continue;
     }
     const int64_t j = c * 32 + lid;
     const bool valid = j < g.lane_num;
-    const uint32_t d = valid ? ld_stream_u32(p.lane_desc + j, pol) : 0u;
+    const uint32_t d = !valid ? 0u : TMA ? descbuf[lid] : ld_stream_u32(p.lane_desc + j, pol);
     const int steps = valid ? static_cast<int>(imin64(SIGMA, total - j * SIGMA)) : 0;
     const uint32_t live = steps >= 32 ? kFull : ((1u << steps) - 1u);
     const uint32_t dmask = (d >> (2 * ob)) & live;
@@ -990,10 +1128,12 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
       const T* po = reinterpret_cast<const T*>(p.pr.pi_old) + y0;
       if (lid < nrows) cp_async(pobuf + lid, po + lid);
       if (lid + 32 < nrows) cp_async(pobuf + lid + 32, po + lid + 32);
-      if (lid < 3) cp_async(dwbuf + lid, p.pr.dangling + (y0 >> 5) + lid);  // padded array
+      if (p.pr.dang_from < 0 && lid < 3)
+        cp_async(dwbuf + lid, p.pr.dangling + (y0 >> 5) + lid);  // padded array
     }
     int col[SIGMA];
-    load_slot_cols<SIGMA, G>(cb, lid, col, pol);
+    get_cols(col);
+    restage();
     T xv[SIGMA], v[SIGMA];
     gather_slots<T, SIGMA, HUB>(p.x, hub, col, rmask, xv);
     load_slot_vals<T, SIGMA>(vb, lid, v, pol);
@@ -1040,8 +1180,10 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
         }
         const int64_t row = int64_t(y0) + k;
         if (PR) {
-          const uint32_t dw = dwbuf[(uint32_t(row) >> 5) - (y0 >> 5)];
-          pr_commit_v<T>(p.pr, base, row, w, pobuf[k], (dw >> (row & 31)) & 1u, p.y, acc);
+          const bool dg = p.pr.dang_from >= 0
+                              ? row >= p.pr.dang_from
+                              : ((dwbuf[(uint32_t(row) >> 5) - (y0 >> 5)] >> (row & 31)) & 1u);
+          pr_commit_v<T>(p.pr, base, row, w, pobuf[k], dg, p.y, acc);
         } else {
           p.y[row] = w;
         }
@@ -1057,11 +1199,31 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
       if (had_down && !(opens && head_open)) p.y[int64_t(y0) + r0] = headv;
       __syncwarp();
       if (PR) {
+        // the PageRank update over the tile's rows, coalesced, kU rows per
+        // lane in flight per memory round trip
+        constexpr int kU = MBX_DIRECT_UNROLL;
+        const T* pold = reinterpret_cast<const T*>(p.pr.pi_old);
         PrAcc acc = load_acc(wacc, lid);
-        for (int k = lid; k < nrows; k += 32) {
-          if (k == 0 && head_open) continue;
-          const int64_t row = int64_t(y0) + k;
-          pr_commit<T>(p.pr, base, row, p.y[row], p.y, acc);
+        for (int k0 = lid; k0 < nrows; k0 += 32 * kU) {
+          T w[kU], po[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int k = k0 + 32 * u;
+            w[u] = T(0);
+            po[u] = T(0);
+            if (k < nrows && !(k == 0 && head_open)) {
+              w[u] = p.y[int64_t(y0) + k];
+              po[u] = __ldg(pold + int64_t(y0) + k);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int k = k0 + 32 * u;
+            if (k < nrows && !(k == 0 && head_open)) {
+              const int64_t row = int64_t(y0) + k;
+              pr_commit_v<T>(p.pr, base, row, w[u], po[u], pr_dang(p.pr, row), p.y, acc);
+            }
+          }
         }
         store_acc(wacc, lid, acc);
         __syncwarp();
@@ -1078,7 +1240,7 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
   }
 }
 
-template <typename T, int SIGMA, bool PR, bool HUB, bool PF>
+template <typename T, int SIGMA, bool PR, bool HUB, int MODE>
 __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geometry& g = p.g;
@@ -1098,9 +1260,24 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   T base = T(0);
   if (PR) base = pr_base<T>(p.pr);
   const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t range = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp; range < g.num_ranges;
-       range += wstride)
-    slot_range<T, SIGMA, PR, HUB, PF>(p, hub, rowbuf, range, lid, pol, base, wacc);
+  const int64_t first = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
+  // mode 2: the warp's staging area (columns, descriptors, mbarrier)
+  unsigned char* stg = reinterpret_cast<unsigned char*>(wacc - size_t(warp) * 128 +
+                                                        size_t(blockDim.x >> 5) * 128) +
+                       size_t(warp) * StageBytes<SIGMA>::value;
+  uint32_t phase = 0;
+  if (MODE == 2 && lid == 0) {
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(stg + size_t(32 * SIGMA) * 4 + 128);
+    mbar_init(mbar);
+    if (first < g.num_ranges)
+      stage_chunk(mbar, reinterpret_cast<int32_t*>(stg),
+                  reinterpret_cast<uint32_t*>(stg + size_t(32 * SIGMA) * 4), p.scols, p.lane_desc,
+                  first * g.chunks_per_range, 32 * SIGMA, pol);
+  }
+  for (int64_t range = first; range < g.num_ranges; range += wstride)
+    slot_range<T, SIGMA, PR, HUB, MODE>(p, hub, rowbuf, range, lid, pol, base, wacc, stg, phase,
+                                        range + wstride < g.num_ranges ? range + wstride : -1);
+
   __syncwarp();
   if (PR && p.pr.npeer) __threadfence_system();  // NVLink stores performed (fused exchange)
   if (PR) write_warp_part(load_acc(wacc, lid), p.pr.range_part, lid);
@@ -1156,10 +1333,11 @@ __global__ void build_slots_kernel(const T* __restrict__ vals, const int32_t* __
 
 template <typename T, int SIGMA, bool PR, bool HUB>
 void launch_slot(mbx_context* ctx, const SlotParams<T>& p, size_t smem) {
-  auto kern = p.g.prefetch ? spmv_slot_kernel<T, SIGMA, PR, HUB, true>
-                           : spmv_slot_kernel<T, SIGMA, PR, HUB, false>;
-  static std::atomic<uint64_t> done[2];  // per (T, SIGMA, PR, HUB), prefetch variant
-  allow_max_smem(kern, ctx->device, done[p.g.prefetch ? 1 : 0]);
+  auto kern = p.g.prefetch == 2   ? spmv_slot_kernel<T, SIGMA, PR, HUB, 2>
+              : p.g.prefetch == 1 ? spmv_slot_kernel<T, SIGMA, PR, HUB, 1>
+                                  : spmv_slot_kernel<T, SIGMA, PR, HUB, 0>;
+  static std::atomic<uint64_t> done[3];  // per (T, SIGMA, PR, HUB), staging mode
+  allow_max_smem(kern, ctx->device, done[p.g.prefetch == 2 ? 2 : p.g.prefetch ? 1 : 0]);
   const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
   const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));
   kern<<<grid, p.g.warps_per_cta * 32, smem, ctx->stream>>>(p);
@@ -1539,11 +1717,15 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
 
 }  // namespace
 
+size_t stage_bytes(int sigma) { return size_t(32 * sigma) * 4 + 128 + 16; }
+
 size_t spmv_smem_bytes(const Geometry& g, int precision) {
   const size_t vs = value_size(precision);
   const size_t hub = g.hub_count > 0 ? size_t((g.hub_count + 3) & ~3) : 0;
   if (g.slots)  // hub | per warp: rows, pi_old rows, dangling words | parked accumulators
-    return hub * vs + size_t(g.warps_per_cta) * (2 * kSlotRowBuf * vs + 16 + 128 * sizeof(double));
+                // | (mode 2) staged column slots + descriptors + mbarrier
+    return hub * vs + size_t(g.warps_per_cta) * (2 * kSlotRowBuf * vs + 16 + 128 * sizeof(double) +
+                                                 (g.prefetch == 2 ? stage_bytes(g.sigma) : 0));
   return (hub + size_t(g.warps_per_cta) * (32 * g.sigma + 1)) * vs;
 }
 
@@ -1562,9 +1744,11 @@ int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, in
   if (per_cta > optin) per_cta = optin;
   const int64_t vs = int64_t(value_size(precision));
   const bool slot_layout = ctx->tuning.layout == 1 && sigma == default_sigma(precision);
-  const int64_t bufs = slot_layout
-                           ? int64_t(warps_per_cta) * (2 * kSlotRowBuf * vs + 16 + 128 * 8)
-                           : int64_t(warps_per_cta) * (32 * sigma + 1) * vs;
+  const int64_t bufs =
+      slot_layout ? int64_t(warps_per_cta) *
+                        (2 * kSlotRowBuf * vs + 16 + 128 * 8 +
+                         (ctx->tuning.prefetch == 2 ? int64_t(stage_bytes(sigma)) : 0))
+                  : int64_t(warps_per_cta) * (32 * sigma + 1) * vs;
   const int64_t slots = (per_cta - bufs) / vs - 4;
   return slots > 0 ? int(slots & ~int64_t(3)) : 0;
 }
@@ -1740,6 +1924,21 @@ void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
   }
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
+}
+
+int64_t dangling_suffix_start(mbx_context* ctx, const uint32_t* mask_dev, int64_t n) {
+  const int64_t words = (n + 31) / 32;
+  if (n <= 0) return 0;
+  std::vector<uint32_t> m(words);
+  MBX_CUDA(cudaMemcpyAsync(m.data(), mask_dev, words * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+  int64_t f = n;  // walk down from the top while rows are dangling
+  while (f > 0 && ((m[(f - 1) >> 5] >> ((f - 1) & 31)) & 1u)) --f;
+  for (int64_t w = 0; w < (f >> 5); ++w)  // nothing dangling below f
+    if (m[w]) return -1;
+  for (int64_t r = f & ~int64_t(31); r < f; ++r)
+    if ((m[r >> 5] >> (r & 31)) & 1u) return -1;
+  return f;
 }
 
 // Loads the PageRank start / yardstick kernels of `precision` now.  With

@@ -79,6 +79,10 @@ struct PrScalars {
 struct PrArgs {
   const void* pi_old = nullptr;        // x of this iteration
   const uint32_t* dangling = nullptr;  // bit r set <=> vertex r dangling
+  // >= 0: the dangling vertices are exactly the rows >= dang_from (a degree
+  // relabelled matrix puts its empty columns last), so the commit compares
+  // instead of fetching bitmask words
+  int64_t dang_from = -1;
   const void* yardstick = nullptr;     // pi*; NULL => constant yard_const
   double yard_const = 0.0;
   double damping = 0.85;
@@ -220,6 +224,9 @@ void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
                 const PrArgs* pr, double* cta_part, unsigned int* counter);
 int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m);
 void preload_pr_kernels(int precision);
+// First row of the dangling set when it is a suffix [f, n) of the rows
+// (f = n when empty), else -1: one host pass over the bitmask (preprocessing).
+int64_t dangling_suffix_start(mbx_context* ctx, const uint32_t* mask_dev, int64_t n);
 // capi.cu's validation of a SimtConfig and of a TILE against (matrix, config)
 void validate_config(const mbx_simt_config* c);
 void validate_tile(const mbx_matrix* m, const mbx_tile* t, const mbx_simt_config* c);

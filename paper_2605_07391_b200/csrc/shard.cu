@@ -334,6 +334,7 @@ struct Shard {
   Geometry geo;
   int32_t* cols_remap = nullptr;
   uint32_t* dangling = nullptr;
+  int64_t dang_from = -1;  // local dangling rows = [dang_from, rows) when a suffix
   double* range_part = nullptr;
   double* block_part = nullptr;
   unsigned int* counter = nullptr;
@@ -484,6 +485,7 @@ void launch_iteration(mbx_shard_group* G, int64_t r, bool dev_loop = false) {
     unsigned char* xnew = static_cast<unsigned char*>(G->pi[dst]) + int64_t(s.g) * G->chunk_bytes;
     a.pi_old = pold;
     a.dangling = s.dangling;
+    a.dang_from = s.dang_from;
     a.yardstick = G->cfg.reference_iters > 0
                       ? static_cast<unsigned char*>(G->yloc[G->cfg.reference_iters & 1]) +
                             int64_t(s.li) * G->lchunk_bytes
@@ -530,6 +532,7 @@ void launch_yard_iteration(mbx_shard_group* G, int64_t r) {
     unsigned char* xnew = static_cast<unsigned char*>(G->pi[dst]) + int64_t(s.g) * G->chunk_bytes;
     a.pi_old = yold;
     a.dangling = s.dangling;
+    a.dang_from = s.dang_from;
     a.yard_const = 1.0;
     a.damping = G->cfg.damping;
     a.inv_n = 1.0 / double(G->n);
@@ -705,6 +708,7 @@ void group_layout(mbx_shard_group* G, mbx_matrix* const* mats, mbx_tile* const* 
     s.dangling = static_cast<uint32_t*>(dm(ctx, ((rows + 31) / 32) * 4 + 64));
     mbx::local_dangling_kernel<<<unsigned((rows + 31) / 32 / 256 + 1), 256, 0, st>>>(
         seen, s.r0, rows, s.dangling);
+    s.dang_from = mbx::dangling_suffix_start(ctx, s.dangling, rows);
     s.geo = mbx::make_geometry(ctx, &s.view, s.tile, c->block_size);
     s.range_part = static_cast<double*>(
         dm(ctx, (std::max(s.geo.num_ranges, mbx::pr_parts(s.geo)) + 1) * 4 * sizeof(double)));

@@ -180,3 +180,4 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
 }
 
 }  // namespace mbx
+
