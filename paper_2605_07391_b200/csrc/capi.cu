@@ -60,6 +60,7 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   g.num_chunks = (g.lane_num + 31) / 32;
   g.warps_per_cta = ctx->tuning.warps_per_cta;
   g.grid = ctx->sm_count * ctx->tuning.ctas_per_sm;
+  g.sms = ctx->sm_count;
   // b/32 tiles per warp range (the reference's block of b/omega tiles), but
   // at least ~8 ranges per resident warp so small matrices do not leave the
   // persistent grid with a long tail
@@ -883,7 +884,7 @@ struct mbx_pagerank_plan_s {
   int64_t dang_from = -1;  // dangling rows = [dang_from, n) when a suffix
   mbx::PrScalars* scal = nullptr;      // [max_iters + 1]
   mbx::PrScalars* ref_scal = nullptr;  // [reference_iters + 1]
-  double* range_part = nullptr;
+  uint32_t* carry_mask = nullptr;  // K2 -> K3: the range boundary rows
   double* block_part = nullptr;
   unsigned int* counter = nullptr;
   int* flags = nullptr;  // [0] stop, [1] stop_iter
@@ -939,7 +940,7 @@ mbx::PrArgs pr_args(mbx_pagerank_plan* pl, int64_t r, const void* yard) {
   a.inv_n = 1.0 / double(pl->n);
   a.prev = pl->scal + (r - 1);
   a.next = pl->scal + r;
-  a.range_part = pl->range_part;
+  a.carry_mask = pl->carry_mask;
   a.block_part = pl->block_part;
   a.done_counter = pl->counter;
   a.stop = pl->flags;
@@ -1104,9 +1105,11 @@ MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, cons
     pl->ref_scal = static_cast<mbx::PrScalars*>(
         dmalloc(ctx, (cfg->reference_iters + 1) * sizeof(mbx::PrScalars)));
     MBX_CUDA(cudaMemsetAsync(pl->scal, 0, (cfg->max_iters + 1) * sizeof(mbx::PrScalars), ctx->stream));
-    pl->range_part = static_cast<double*>(
-        dmalloc(ctx, (std::max(pl->g.num_ranges, mbx::pr_parts(pl->g)) + 1) * 4 * sizeof(double)));
-    const int64_t k3_blocks = mbx::fixup_blocks(pl->g) + 1;
+    const size_t mask_bytes = size_t((pl->n + 31) / 32) * 4 + 64;
+    pl->carry_mask = static_cast<uint32_t*>(dmalloc(ctx, mask_bytes));
+    MBX_CUDA(cudaMemsetAsync(pl->carry_mask, 0, mask_bytes, ctx->stream));
+    const int64_t k3_blocks =
+        std::max(mbx::fixup_blocks(pl->g, true), mbx::fixup_blocks(pl->g, false)) + 1;
     const int64_t nb = std::max<int64_t>({k3_blocks, int64_t(mbx::csr_pr_blocks(ctx, p)),
                                           int64_t(ctx->sm_count) * 4 + 1});
     pl->block_part = static_cast<double*>(dmalloc(ctx, nb * 4 * sizeof(double)));
@@ -1239,7 +1242,7 @@ MBX_API int mbx_pagerank_plan_destroy(mbx_pagerank_plan* pl) {
     dfree(ctx, pl->dangling);
     dfree(ctx, pl->scal);
     dfree(ctx, pl->ref_scal);
-    dfree(ctx, pl->range_part);
+    dfree(ctx, pl->carry_mask);
     dfree(ctx, pl->block_part);
     dfree(ctx, pl->counter);
     dfree(ctx, pl->flags);

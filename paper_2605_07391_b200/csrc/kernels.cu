@@ -24,18 +24,11 @@
 #include <atomic>
 #include <cfloat>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "mbx_internal.h"
 
-// rows per lane whose loads one memory round trip carries in the PageRank
-// commit of row-heavy (> kSlotRowBuf rows) and nonzero-free tiles
-#ifndef MBX_DIRECT_UNROLL
-#define MBX_DIRECT_UNROLL 2
-#endif
-#ifndef MBX_EMPTY_UNROLL
-#define MBX_EMPTY_UNROLL 2
-#endif
 
 namespace mbx {
 namespace {
@@ -242,22 +235,33 @@ struct PrAcc {
 // max|pi - s| and the division happens once in pr_block_finish: division by
 // a positive constant is monotone, so max(fl(|d|/s)) == fl(max|d| / s) and
 // ERR stays bitwise equal to rank_error's formula.
+// c * w + base with the product rounded first, as rank_update computes it
+// (solvers.hpp:110-112; no contraction into an FMA)
 template <typename T>
-__device__ __forceinline__ void pr_commit_v(const PrArgs& pr, T base, int64_t row, T w, T po,
-                                            bool dang, T* __restrict__ out, PrAcc& a) {
-  // c * w + base with the product rounded first, as rank_update computes it
-  // (solvers.hpp:110-112; no contraction into an FMA)
-  const T pn = mul_rn(static_cast<T>(pr.damping), w) + base;
+__device__ __forceinline__ T pr_value(const PrArgs& pr, T base, T w) {
+  return mul_rn(static_cast<T>(pr.damping), w) + base;
+}
+
+// pi_new[row] = pn, plus (row shards) the exchange copy of a non-dangling
+// vertex in this rank's buffer and, fused exchange, in every peer's
+template <typename T>
+__device__ __forceinline__ void pr_store(const PrArgs& pr, int64_t row, T pn,
+                                         T* __restrict__ out) {
   out[row] = pn;
-  if (pr.xout) {  // row shards: the exchange copy of a non-dangling vertex
+  if (pr.xout) {
     const int32_t q = pr.xmap[row];
     if (q >= 0) {
       static_cast<T*>(pr.xout)[q] = pn;
       for (int k = 0; k < pr.npeer; ++k) static_cast<T*>(pr.xpeer[k])[q] = pn;  // NVLink
     }
   }
-  // |pn - po| is formed in T (the reference's own precision for pi) and
-  // accumulated in fp64
+}
+
+// One committed row's share of the fused reductions.  |pn - po| is formed
+// in T (the reference's own precision for pi) and accumulated in fp64.
+template <typename T>
+__device__ __forceinline__ void pr_accum(const PrArgs& pr, int64_t row, T pn, T po, bool dang,
+                                         PrAcc& a) {
   a.resid += static_cast<double>(fabs(pn - po));
   if (dang) a.dang += static_cast<double>(pn);
   a.mass += fabs(static_cast<double>(pn));
@@ -274,6 +278,14 @@ __device__ __forceinline__ void pr_commit_v(const PrArgs& pr, T base, int64_t ro
   }
 }
 
+template <typename T>
+__device__ __forceinline__ void pr_commit_v(const PrArgs& pr, T base, int64_t row, T w, T po,
+                                            bool dang, T* __restrict__ out, PrAcc& a) {
+  const T pn = pr_value(pr, base, w);
+  pr_store(pr, row, pn, out);
+  pr_accum(pr, row, pn, po, dang, a);
+}
+
 __device__ __forceinline__ bool pr_dang(const PrArgs& pr, int64_t row) {
   return pr.dang_from >= 0 ? row >= pr.dang_from
                            : ((__ldg(pr.dangling + (row >> 5)) >> (row & 31)) & 1u) != 0u;
@@ -284,6 +296,14 @@ __device__ __forceinline__ void pr_commit(const PrArgs& pr, T base, int64_t row,
                                           T w, T* __restrict__ out, PrAcc& a) {
   pr_commit_v<T>(pr, base, row, w, reinterpret_cast<const T*>(pr.pi_old)[row], pr_dang(pr, row),
                  out, a);
+}
+
+// K2, PageRank: the range's head and tail rows go through the carry table;
+// K3 commits them and its row reduction must skip them
+__device__ __forceinline__ void mark_carry_rows(const PrArgs& pr, uint32_t head_row,
+                                                uint32_t tail_row, int64_t n_rows) {
+  if (int64_t(head_row) < n_rows) atomicOr(pr.carry_mask + (head_row >> 5), 1u << (head_row & 31));
+  if (int64_t(tail_row) < n_rows) atomicOr(pr.carry_mask + (tail_row >> 5), 1u << (tail_row & 31));
 }
 
 // iteration bookkeeping of host-unrolled launches (prev/next/iter baked in)
@@ -494,8 +514,7 @@ __device__ __forceinline__ T lane_walk_and_scan(T* buf, int cnt, int sigma, uint
 // One warp range: `chunks_per_range` consecutive tiles (chunk == tile here).
 template <typename T, int SIGMA, bool PR, bool HUB, bool PF>
 __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, T* buf,
-                                          int64_t range, int lid, uint64_t pol, T base,
-                                          PrAcc& acc) {
+                                          int64_t range, int lid, uint64_t pol, T base) {
   const Geometry& g = p.g;
   const int sigma = SIGMA > 0 ? SIGMA : g.sigma;
   const int64_t c0 = range * g.chunks_per_range;
@@ -548,20 +567,7 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
       carry += warp_sum(s);
       continue;
     }
-    // PR: the tile's first 32 rows of pi_old and their dangling bits are
-    // loaded before the lane walk (after staging, off the register peak), so
-    // the commit does not wait on another memory round trip
-    T po_pre = T(0);
-    uint32_t dw_pre = 0u;
-    auto preload = [&]() {
-      if (PR && lid < nrows) {
-        const int64_t r = int64_t(y0) + lid;
-        po_pre = __ldg(reinterpret_cast<const T*>(p.pr.pi_old) + r);
-        dw_pre = __ldg(p.pr.dangling + (r >> 5));
-      }
-    };
     if (cnt == 0) {
-      preload();
       // no nonzero: every step closes a row (merbit_spmv.hpp:217-224); the
       // first closes the carried row, the rest are empty rows.
       for (int k = lid; k < nrows; k += 32) buf[k] = k == 0 ? carry : T(0);
@@ -573,7 +579,6 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
       const uint32_t d = valid ? ld_stream_u32(p.lane_desc + j, pol) : 0u;
       const int steps = valid ? static_cast<int>(imin64(sigma, total - j * sigma)) : 0;
       stage_products<T, false, MAXV, HUB>(p.vals, p.cols, p.x, hub, x0, x1, buf, lid, pol);
-      preload();
       __syncwarp();
       carry = lane_walk_and_scan<T, SIGMA>(buf, cnt, sigma, d, steps, ob, lid, carry,
                                            static_cast<int>(d & omask),
@@ -588,14 +593,10 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
         continue;
       }
       const int64_t row = int64_t(y0) + k;
-      if (PR) {
-        if (k < 32)
-          pr_commit_v<T>(p.pr, base, row, w, po_pre, (dw_pre >> (row & 31)) & 1u, p.y, acc);
-        else
-          pr_commit<T>(p.pr, base, row, w, p.y, acc);
-      } else {
+      if (PR)
+        pr_store<T>(p.pr, row, pr_value(p.pr, base, w), p.y);
+      else
         p.y[row] = w;
-      }
     }
     if (nrows > 0) head_open = false;
     __syncwarp();
@@ -605,22 +606,7 @@ __device__ __forceinline__ void w32_range(const SpmvParams<T>& p, const T* hub, 
     p.carry_val[2 * range] = head_open ? T(0) : head_val;
     p.carry_row[2 * range + 1] = tail_row;
     p.carry_val[2 * range + 1] = carry;
-  }
-}
-
-// Warp partials of the fused PageRank reductions: one slot per warp of the
-// persistent grid (fixed range->warp map, so the sums are deterministic).
-__device__ __forceinline__ void write_warp_part(PrAcc acc, double* parts, int lid) {
-  acc.resid = warp_sum(acc.resid);
-  acc.dang = warp_sum(acc.dang);
-  acc.mass = warp_sum(acc.mass);
-  acc.err = warp_max(acc.err);
-  if (lid == 0) {
-    double* rp = parts + 4 * (int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5));
-    rp[0] = acc.resid;
-    rp[1] = acc.dang;
-    rp[2] = acc.mass;
-    rp[3] = acc.err;
+    if (PR) mark_carry_rows(p.pr, head_row, tail_row, g.n_rows);
   }
 }
 
@@ -641,12 +627,10 @@ __global__ void __launch_bounds__(1024) spmv_w32_kernel(SpmvParams<T> p) {
   T base = T(0);
   if (PR) base = pr_base<T>(p.pr);
   const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
-  PrAcc acc;
   for (int64_t range = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp; range < g.num_ranges;
        range += wstride)
-    w32_range<T, SIGMA, PR, HUB, PF>(p, hub, buf, range, lid, pol, base, acc);
+    w32_range<T, SIGMA, PR, HUB, PF>(p, hub, buf, range, lid, pol, base);
   if (PR && p.pr.npeer) __threadfence_system();  // NVLink stores performed (fused exchange)
-  if (PR) write_warp_part(acc, p.pr.range_part, lid);
 }
 
 // ---------------------------------------------------------------------------
@@ -674,7 +658,6 @@ __global__ void __launch_bounds__(kThreads) spmv_generic_kernel(SpmvParams<T> p)
   T carry = T(0), head_val = T(0);
   bool head_open = true;
   T base = T(0);
-  PrAcc acc;
   if (PR) base = pr_base<T>(p.pr);
   uint32_t head_row = 0, y1 = 0;
 
@@ -716,7 +699,7 @@ __global__ void __launch_bounds__(kThreads) spmv_generic_kernel(SpmvParams<T> p)
       }
       const int64_t row = yy0 + k;
       if (PR)
-        pr_commit<T>(p.pr, base, row, w, p.y, acc);
+        pr_store<T>(p.pr, row, pr_value(p.pr, base, w), p.y);
       else
         p.y[row] = w;
     }
@@ -728,21 +711,9 @@ __global__ void __launch_bounds__(kThreads) spmv_generic_kernel(SpmvParams<T> p)
     p.carry_val[2 * range] = head_open ? T(0) : head_val;
     p.carry_row[2 * range + 1] = y1;
     p.carry_val[2 * range + 1] = carry;
+    if (PR) mark_carry_rows(p.pr, head_row, y1, g.n_rows);
   }
-  if (PR) {
-    if (p.pr.npeer) __threadfence_system();  // NVLink stores performed (fused exchange)
-    acc.resid = warp_sum(acc.resid);
-    acc.dang = warp_sum(acc.dang);
-    acc.mass = warp_sum(acc.mass);
-    acc.err = warp_max(acc.err);
-    if (lid == 0) {
-      double* rp = p.pr.range_part + 4 * range;
-      rp[0] = acc.resid;
-      rp[1] = acc.dang;
-      rp[2] = acc.mass;
-      rp[3] = acc.err;
-    }
-  }
+  if (PR && p.pr.npeer) __threadfence_system();  // NVLink stores performed (fused exchange)
 }
 
 // ---------------------------------------------------------------------------
@@ -860,46 +831,6 @@ __device__ __forceinline__ T seg_scan(T sum, T head, bool had_down, int lid, T c
   return __shfl_sync(kFull, S_, 31);
 }
 
-// Asynchronous global->shared copies (LDGSTS): the commit's pi_old rows and
-// dangling words are fetched at the start of a tile without holding
-// registers through the gather phase.
-__device__ __forceinline__ void cp_async(void* smem, const float* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                   static_cast<unsigned>(__cvta_generic_to_shared(smem))),
-               "l"(g));
-}
-__device__ __forceinline__ void cp_async(void* smem, const double* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                   static_cast<unsigned>(__cvta_generic_to_shared(smem))),
-               "l"(g));
-}
-__device__ __forceinline__ void cp_async(void* smem, const uint32_t* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                   static_cast<unsigned>(__cvta_generic_to_shared(smem))),
-               "l"(g));
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-// Per-lane PageRank accumulators parked in shared memory between commits
-// ([field][lane] per warp, conflict-free): keeps the 8 fp64 registers out of
-// the gather phase, where the 64-register budget of a 1024-thread CTA is
-// spent on the lane's sigma operands.
-__device__ __forceinline__ PrAcc load_acc(const double* wa, int lid) {
-  PrAcc a;
-  a.resid = wa[lid];
-  a.dang = wa[32 + lid];
-  a.mass = wa[64 + lid];
-  a.err = wa[96 + lid];
-  return a;
-}
-__device__ __forceinline__ void store_acc(double* wa, int lid, const PrAcc& a) {
-  wa[lid] = a.resid;
-  wa[32 + lid] = a.dang;
-  wa[64 + lid] = a.mass;
-  wa[96 + lid] = a.err;
-}
 
 // ---- TMA bulk staging of the next tile's column slots + descriptors ----
 // (mode 2 of the slot kernel): one lane per warp arms the warp's mbarrier
@@ -969,19 +900,10 @@ struct StageBytes {
   static constexpr size_t value = size_t(32 * SIGMA) * 4 + 128 + 16;
 };
 
-template <typename T, bool PR>
-__device__ __forceinline__ void commit_row(const SlotParams<T>& p, T base, int64_t row, T w,
-                                           PrAcc& acc) {
-  if (PR)
-    pr_commit<T>(p.pr, base, row, w, p.y, acc);
-  else
-    p.y[row] = w;
-}
-
 template <typename T, int SIGMA, bool PR, bool HUB, int MODE>
 __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub, T* rowbuf,
                                            int64_t range, int lid, uint64_t pol, T base,
-                                           double* wacc, unsigned char* stg, uint32_t& phase,
+                                           unsigned char* stg, uint32_t& phase,
                                            int64_t next_range) {
   constexpr bool PF = MODE == 1;
   constexpr bool TMA = MODE == 2;
@@ -1075,27 +997,11 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
       if (PR) {
         if (nrows > 0) {
           if (head_open) head_val = carry;
-          constexpr int kU = MBX_EMPTY_UNROLL;
-          const T* pold = reinterpret_cast<const T*>(p.pr.pi_old);
-          PrAcc acc = load_acc(wacc, lid);
-          for (int k0 = lid; k0 < nrows; k0 += 32 * kU) {
-            T po[kU];
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-              const int k = k0 + 32 * u;
-              po[u] = k < nrows ? __ldg(pold + int64_t(y0) + k) : T(0);
-            }
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-              const int k = k0 + 32 * u;
-              if (k < nrows && !(k == 0 && head_open)) {
-                const int64_t row = int64_t(y0) + k;
-                pr_commit_v<T>(p.pr, base, row, k == 0 ? carry : T(0), po[u], pr_dang(p.pr, row),
-                               p.y, acc);
-              }
-            }
+          const T pb = pr_value(p.pr, base, T(0));  // an empty row: c * 0 + base
+          for (int kk = lid; kk < nrows; kk += 32) {
+            if (kk == 0 && head_open) continue;
+            pr_store<T>(p.pr, int64_t(y0) + kk, kk == 0 ? pr_value(p.pr, base, carry) : pb, p.y);
           }
-          store_acc(wacc, lid, acc);
           head_open = false;
         }
         carry = T(0);
@@ -1122,15 +1028,6 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
     const uint32_t rmask = ~(d >> (2 * ob)) & live;
     const int r0 = static_cast<int>((d >> ob) & omask);
     const bool direct = nrows > kSlotRowBuf;  // warp-uniform
-    T* pobuf = rowbuf + kSlotRowBuf;                            // pi_old of the rows
-    uint32_t* dwbuf = reinterpret_cast<uint32_t*>(pobuf + kSlotRowBuf);  // dangling words
-    if (PR && !direct) {
-      const T* po = reinterpret_cast<const T*>(p.pr.pi_old) + y0;
-      if (lid < nrows) cp_async(pobuf + lid, po + lid);
-      if (lid + 32 < nrows) cp_async(pobuf + lid + 32, po + lid + 32);
-      if (p.pr.dang_from < 0 && lid < 3)
-        cp_async(dwbuf + lid, p.pr.dangling + (y0 >> 5) + lid);  // padded array
-    }
     int col[SIGMA];
     get_cols(col);
     restage();
@@ -1141,18 +1038,18 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
     // predicated selects (no divergent branches per step): a Down step
     // closes a row -- the lane's first closure is its head, later ones are
     // rows opened and closed inside the lane -- and a Right step adds its
-    // product; rows beyond the commit buffer go straight to y (raw sums,
-    // PageRank update below)
+    // product; rows beyond the commit buffer go straight to y (PageRank:
+    // already rank-updated)
     T sum = T(0), head = T(0);
     bool had_down = false;
-    auto walk = [&](T* sink) {
+    auto walk = [&](T* sink, bool upd) {
       int r = r0;
 #pragma unroll
       for (int i = 0; i < SIGMA; ++i) {
         const bool dn = (dmask >> i) & 1u;
         const bool rt = (rmask >> i) & 1u;
         const T prod = mul_rn(v[i], xv[i]);
-        if (dn && had_down) sink[r] = sum;
+        if (dn && had_down) sink[r] = upd ? pr_value(p.pr, base, sum) : sum;
         head = (dn && !had_down) ? sum : head;
         had_down = had_down || dn;
         sum = dn ? T(0) : (rt ? sum + prod : sum);
@@ -1160,17 +1057,14 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
       }
     };
     if (!direct)
-      walk(rowbuf);
+      walk(rowbuf, false);
     else
-      walk(p.y + y0);
+      walk(p.y + y0, PR);
     T headv;
     carry = seg_scan<T>(sum, head, had_down, lid, carry, headv);
     if (!direct) {
       if (had_down) rowbuf[r0] = headv;
-      if (PR) cp_async_wait_all();
       __syncwarp();
-      PrAcc acc;
-      if (PR) acc = load_acc(wacc, lid);
       // coalesced commit of the tile's rows (Alg. 6 load_mem)
       for (int k = lid; k < nrows; k += 32) {
         const T w = rowbuf[k];
@@ -1179,54 +1073,24 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
           continue;
         }
         const int64_t row = int64_t(y0) + k;
-        if (PR) {
-          const bool dg = p.pr.dang_from >= 0
-                              ? row >= p.pr.dang_from
-                              : ((dwbuf[(uint32_t(row) >> 5) - (y0 >> 5)] >> (row & 31)) & 1u);
-          pr_commit_v<T>(p.pr, base, row, w, pobuf[k], dg, p.y, acc);
-        } else {
+        if (PR)
+          pr_store<T>(p.pr, row, pr_value(p.pr, base, w), p.y);
+        else
           p.y[row] = w;
-        }
       }
-      if (PR) store_acc(wacc, lid, acc);
       __syncwarp();
     } else {
-      // more rows than the row buffer: raw sums went straight to y; the
-      // PageRank update then runs over the tile's rows, coalesced
+      // more rows than the row buffer: the sums went straight to y
       const bool opens = had_down && r0 == 0;  // this lane closes the tile's row 0
       const unsigned who = __ballot_sync(kFull, opens);
       const T hv = __shfl_sync(kFull, headv, who ? __ffs(who) - 1 : 0);
-      if (had_down && !(opens && head_open)) p.y[int64_t(y0) + r0] = headv;
-      __syncwarp();
-      if (PR) {
-        // the PageRank update over the tile's rows, coalesced, kU rows per
-        // lane in flight per memory round trip
-        constexpr int kU = MBX_DIRECT_UNROLL;
-        const T* pold = reinterpret_cast<const T*>(p.pr.pi_old);
-        PrAcc acc = load_acc(wacc, lid);
-        for (int k0 = lid; k0 < nrows; k0 += 32 * kU) {
-          T w[kU], po[kU];
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int k = k0 + 32 * u;
-            w[u] = T(0);
-            po[u] = T(0);
-            if (k < nrows && !(k == 0 && head_open)) {
-              w[u] = p.y[int64_t(y0) + k];
-              po[u] = __ldg(pold + int64_t(y0) + k);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int k = k0 + 32 * u;
-            if (k < nrows && !(k == 0 && head_open)) {
-              const int64_t row = int64_t(y0) + k;
-              pr_commit_v<T>(p.pr, base, row, w[u], po[u], pr_dang(p.pr, row), p.y, acc);
-            }
-          }
-        }
-        store_acc(wacc, lid, acc);
+      if (had_down && !(opens && head_open))
+        p.y[int64_t(y0) + r0] = PR ? pr_value(p.pr, base, headv) : headv;
+      if (PR && p.pr.xout) {
+        // row shards: the exchange copies of the tile's rows, coalesced
         __syncwarp();
+        for (int k = lid; k < nrows; k += 32)
+          if (!(k == 0 && head_open)) pr_store<T>(p.pr, int64_t(y0) + k, p.y[int64_t(y0) + k], p.y);
       }
       if (head_open && who) head_val = hv;
     }
@@ -1237,6 +1101,7 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
     p.carry_val[2 * range] = head_open ? T(0) : head_val;
     p.carry_row[2 * range + 1] = tail_row;
     p.carry_val[2 * range + 1] = carry;
+    if (PR) mark_carry_rows(p.pr, head_row, tail_row, g.n_rows);
   }
 }
 
@@ -1248,13 +1113,10 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
   T* hub = reinterpret_cast<T*>(smem_raw);
   const int hub_pad = HUB ? ((g.hub_count + 3) & ~3) : 0;
-  // per warp: row buffer (64 T), pi_old rows (64 T), dangling words (4 u32)
-  constexpr size_t kWarpBytes = 2 * kSlotRowBuf * sizeof(T) + 16;
+  // per warp: the row buffer (kSlotRowBuf T); mode 2: then the staging areas
+  constexpr size_t kWarpBytes = kSlotRowBuf * sizeof(T);
   unsigned char* wbase = reinterpret_cast<unsigned char*>(hub + hub_pad);
   T* rowbuf = reinterpret_cast<T*>(wbase + size_t(warp) * kWarpBytes);
-  double* wacc = reinterpret_cast<double*>(wbase + size_t(blockDim.x >> 5) * kWarpBytes) +
-                 size_t(warp) * 128;
-  if (PR) store_acc(wacc, lid, PrAcc());
   if (HUB) stage_hubs<T>(hub, p.x, p.hub_cols, g.hub_count);
   const uint64_t pol = evict_first_policy();
   T base = T(0);
@@ -1262,8 +1124,7 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
   const int64_t first = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
   // mode 2: the warp's staging area (columns, descriptors, mbarrier)
-  unsigned char* stg = reinterpret_cast<unsigned char*>(wacc - size_t(warp) * 128 +
-                                                        size_t(blockDim.x >> 5) * 128) +
+  unsigned char* stg = wbase + size_t(blockDim.x >> 5) * kWarpBytes +
                        size_t(warp) * StageBytes<SIGMA>::value;
   uint32_t phase = 0;
   if (MODE == 2 && lid == 0) {
@@ -1275,12 +1136,9 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
                   first * g.chunks_per_range, 32 * SIGMA, pol);
   }
   for (int64_t range = first; range < g.num_ranges; range += wstride)
-    slot_range<T, SIGMA, PR, HUB, MODE>(p, hub, rowbuf, range, lid, pol, base, wacc, stg, phase,
+    slot_range<T, SIGMA, PR, HUB, MODE>(p, hub, rowbuf, range, lid, pol, base, stg, phase,
                                         range + wstride < g.num_ranges ? range + wstride : -1);
-
-  __syncwarp();
   if (PR && p.pr.npeer) __threadfence_system();  // NVLink stores performed (fused exchange)
-  if (PR) write_warp_part(load_acc(wacc, lid), p.pr.range_part, lid);
 }
 
 // One thread per (chunk, lane): writes that lane's sigma slots.
@@ -1349,24 +1207,18 @@ void launch_slot(mbx_context* ctx, const SlotParams<T>& p, size_t smem) {
 // the reference's fold order) and ASSIGNED; the terminal row n is dropped.
 // ---------------------------------------------------------------------------
 constexpr int kFixupRun = 32;  // carries one thread folds before the warp takes over
+constexpr int kK3BlocksPerSM = 3;  // PageRank K3: persistent grid, blocks of 256 per SM
 
+// One carry entry e (the thread's): the first entry of each run of equal
+// rows folds the run left to right (merbit_spmv.hpp:330-337) -- runs longer
+// than kFixupRun (rows spanning many ranges) are folded by the whole warp in
+// a fixed lane-strided order + butterfly.  Called by all 32 lanes.
 template <typename T, bool PR>
-__global__ void __launch_bounds__(256) fixup_kernel(const uint32_t* __restrict__ crow,
-                                                    const T* __restrict__ cval,
-                                                    int64_t num_ranges, int64_t n_rows,
-                                                    T* __restrict__ y, PrArgs pr,
-                                                    int64_t num_parts) {
-  if (PR && pr_skip(pr)) return;
-  // one thread per carry entry; the first entry of each run of equal rows
-  // folds the run left to right (merbit_spmv.hpp:330-337) -- runs longer
-  // than kFixupRun (rows spanning many ranges) are folded by the whole warp
-  // in a fixed lane-strided order + butterfly
-  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void fold_carry(const uint32_t* __restrict__ crow,
+                                           const T* __restrict__ cval, int64_t ne, int64_t e,
+                                           int64_t n_rows, T* __restrict__ y, const PrArgs& pr,
+                                           T base, PrAcc& acc) {
   const int lid = threadIdx.x & 31;
-  const int64_t ne = 2 * num_ranges;
-  PrAcc acc;
-  T base = T(0);
-  if (PR) base = pr_base<T>(pr);
   uint32_t r = 0;
   bool start = false, lng = false;
   T sum = T(0);
@@ -1416,14 +1268,64 @@ __global__ void __launch_bounds__(256) fixup_kernel(const uint32_t* __restrict__
     else
       y[r] = sum;
   }
+}
+
+// K3.  Plain SpMV: one thread per carry entry.  PageRank: a persistent grid
+// (kK3BlocksPerSM per SM) strides over the carry entries, then streams the
+// reductions of every other row, then the last block finalises the scalars.
+template <typename T, bool PR>
+__global__ void __launch_bounds__(256, PR ? kK3BlocksPerSM : 1)
+    fixup_kernel(const uint32_t* __restrict__ crow, const T* __restrict__ cval,
+                 int64_t num_ranges, int64_t n_rows, T* __restrict__ y, PrArgs pr) {
+  if (PR && pr_skip(pr)) return;
+  const int64_t ne = 2 * num_ranges;
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  PrAcc acc;
+  T base = T(0);
+  if (PR) base = pr_base<T>(pr);
+  if (!PR) {
+    fold_carry<T, PR>(crow, cval, ne, tid, n_rows, y, pr, base, acc);
+    return;
+  }
+  const int64_t nt = int64_t(gridDim.x) * blockDim.x;
+  // warp-uniform trip count (the fold uses warp collectives)
+  for (int64_t e0 = tid - (threadIdx.x & 31); e0 < ne; e0 += nt)
+    fold_carry<T, PR>(crow, cval, ne, e0 + (threadIdx.x & 31), n_rows, y, pr, base, acc);
   if (PR) {
-    if (e < num_parts) {
-      const double* rp = pr.range_part + 4 * e;
-      acc.resid += rp[0];
-      acc.dang += rp[1];
-      acc.mass += rp[2];
-      acc.err = fmax(acc.err, rp[3]);
+    // the reductions over every row K2 committed (all but the carry rows,
+    // whose share the fold above took): pi_new (just written, L2-resident)
+    // and pi_old streamed once -- K2 itself only stores pi_new.
+    // each thread takes 16 (fp32) / 8 (fp64) consecutive rows per step: four
+    // 16-byte loads of pi_new, four of pi_old, one carry-mask word
+    constexpr int kV = 16 / int(sizeof(T));  // rows per 16-byte vector
+    constexpr int kR = 4 * kV;               // rows per thread and step
+    using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    const T* pold = reinterpret_cast<const T*>(pr.pi_old);
+    const int64_t full = n_rows / kR;  // whole groups; the tail row by row
+    for (int64_t gi = tid; gi < full; gi += nt) {
+      const int64_t r0 = gi * kR;
+      V a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = *reinterpret_cast<const V*>(y + r0 + u * kV);
+        b[u] = __ldg(reinterpret_cast<const V*>(pold + r0 + u * kV));
+      }
+      const uint32_t mw = __ldg(pr.carry_mask + (r0 >> 5)) >> (r0 & 31);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const T* pa = reinterpret_cast<const T*>(&a[u]);
+        const T* pb = reinterpret_cast<const T*>(&b[u]);
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          const int q = u * kV + v;
+          const int64_t row = r0 + q;
+          if (!((mw >> q) & 1u)) pr_accum<T>(pr, row, pa[v], pb[v], pr_dang(pr, row), acc);
+        }
+      }
     }
+    for (int64_t row = full * kR + tid; row < n_rows; row += nt)
+      if (!((__ldg(pr.carry_mask + (row >> 5)) >> (row & 31)) & 1u))
+        pr_accum<T>(pr, row, y[row], __ldg(pold + row), pr_dang(pr, row), acc);
     pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr_next(pr), pr.check_stop != 0,
                     pr.check_stop != 0);  // row shards: the combine kernel advances
   }
@@ -1708,9 +1610,9 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
   }
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
-  const unsigned fgrid = static_cast<unsigned>(fixup_blocks(g));
+  const unsigned fgrid = static_cast<unsigned>(fixup_blocks(g, PR));
   fixup_kernel<T, PR><<<fgrid, 256, 0, ctx->stream>>>(p.carry_row, p.carry_val, g.num_ranges,
-                                                     g.n_rows, p.y, p.pr, pr_parts(g));
+                                                     g.n_rows, p.y, p.pr);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
 }
@@ -1722,9 +1624,9 @@ size_t stage_bytes(int sigma) { return size_t(32 * sigma) * 4 + 128 + 16; }
 size_t spmv_smem_bytes(const Geometry& g, int precision) {
   const size_t vs = value_size(precision);
   const size_t hub = g.hub_count > 0 ? size_t((g.hub_count + 3) & ~3) : 0;
-  if (g.slots)  // hub | per warp: rows, pi_old rows, dangling words | parked accumulators
-                // | (mode 2) staged column slots + descriptors + mbarrier
-    return hub * vs + size_t(g.warps_per_cta) * (2 * kSlotRowBuf * vs + 16 + 128 * sizeof(double) +
+  if (g.slots)  // hub | per warp: row buffer | (mode 2) per warp: staged column
+                // slots + descriptors + mbarrier
+    return hub * vs + size_t(g.warps_per_cta) * (kSlotRowBuf * vs +
                                                  (g.prefetch == 2 ? stage_bytes(g.sigma) : 0));
   return (hub + size_t(g.warps_per_cta) * (32 * g.sigma + 1)) * vs;
 }
@@ -1746,23 +1648,19 @@ int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, in
   const bool slot_layout = ctx->tuning.layout == 1 && sigma == default_sigma(precision);
   const int64_t bufs =
       slot_layout ? int64_t(warps_per_cta) *
-                        (2 * kSlotRowBuf * vs + 16 + 128 * 8 +
+                        (kSlotRowBuf * vs +
                          (ctx->tuning.prefetch == 2 ? int64_t(stage_bytes(sigma)) : 0))
                   : int64_t(warps_per_cta) * (32 * sigma + 1) * vs;
   const int64_t slots = (per_cta - bufs) / vs - 4;
   return slots > 0 ? int(slots & ~int64_t(3)) : 0;
 }
 
-int64_t pr_parts(const Geometry& g) {
-  if (g.omega != 32) return g.num_ranges;  // spmv_generic_kernel: one per range
-  const int64_t need = (g.num_ranges + g.warps_per_cta - 1) / g.warps_per_cta;
-  return imin64(g.grid, need) * g.warps_per_cta;  // persistent: one per warp
-}
 
-int64_t fixup_blocks(const Geometry& g) {
-  const int64_t ne = 2 * g.num_ranges;
-  const int64_t n = ne > pr_parts(g) ? ne : pr_parts(g);
-  return n > 0 ? (n + 255) / 256 : 1;
+int64_t fixup_blocks(const Geometry& g, bool pagerank) {
+  // plain SpMV: one thread per carry entry; PageRank: one resident wave
+  const int64_t carry = (2 * g.num_ranges + 255) / 256;
+  const int64_t b = pagerank ? int64_t(g.sms) * kK3BlocksPerSM : carry;
+  return b > 0 ? b : 1;
 }
 
 // Condition of the device-driven PageRank loop: replay the body while

@@ -39,6 +39,7 @@ struct Geometry {
   int warps_per_cta = 8;
   // persistent launch: grid = sm_count * ctas_per_sm, warps stride over ranges
   int grid = 0;
+  int sms = 148;  // multiprocessors of the device
   // x hub cache: the first hub_count entries of the column-frequency order
   // are staged in shared memory; encoded columns (sign bit) address them.
   int hub_count = 0;
@@ -83,13 +84,16 @@ struct PrArgs {
   // relabelled matrix puts its empty columns last), so the commit compares
   // instead of fetching bitmask words
   int64_t dang_from = -1;
+  // bit r set <=> row r is a range boundary row whose final value K3's carry
+  // fold writes; K2 sets the bits (every iteration, same rows), K3's
+  // streaming reduction skips them (the fold accounts for them)
+  uint32_t* carry_mask = nullptr;
   const void* yardstick = nullptr;     // pi*; NULL => constant yard_const
   double yard_const = 0.0;
   double damping = 0.85;
   double inv_n = 0.0;
   const PrScalars* prev = nullptr;  // scalars of pi_old (dangling mass)
   PrScalars* next = nullptr;        // scalars of pi_new (written by K3)
-  double* range_part = nullptr;     // 4 doubles per K2 part (K2 -> K3), see pr_parts
   double* block_part = nullptr;     // 4 doubles per K3 block
   unsigned int* done_counter = nullptr;
   int* stop = nullptr;         // set once converged / failed
@@ -215,9 +219,9 @@ void launch_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
 size_t spmv_workspace_bytes(const Geometry& g, int precision, bool pagerank);
 // PageRank partial sums K2 hands to K3: one per warp of the persistent
 // omega-32 kernels, one per range otherwise.
-int64_t pr_parts(const Geometry& g);
 // K3 blocks of one SpMV / PageRank iteration (block_part slots it needs).
-int64_t fixup_blocks(const Geometry& g);
+// K3 grid (plain SpMV / PageRank); PageRank buffers size by the larger
+int64_t fixup_blocks(const Geometry& g, bool pagerank);
 void launch_trace_counts(mbx_context* ctx, const mbx_tile* t,
                          unsigned long long* counters_dev);
 void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,

@@ -335,7 +335,7 @@ struct Shard {
   int32_t* cols_remap = nullptr;
   uint32_t* dangling = nullptr;
   int64_t dang_from = -1;  // local dangling rows = [dang_from, rows) when a suffix
-  double* range_part = nullptr;
+  uint32_t* carry_mask = nullptr;  // K2 -> K3: the range boundary rows
   double* block_part = nullptr;
   unsigned int* counter = nullptr;
   void* carry_ws = nullptr;
@@ -500,7 +500,7 @@ void launch_iteration(mbx_shard_group* G, int64_t r, bool dev_loop = false) {
     if (G->peer)
       for (int k = 0; k < G->world; ++k)
         if (k != G->rank0) a.xpeer[a.npeer++] = G->xpeer[dst][k];
-    a.range_part = s.range_part;
+    a.carry_mask = s.carry_mask;
     a.block_part = s.block_part;
     a.done_counter = s.counter;
     a.stop = G->flags;
@@ -710,10 +710,10 @@ void group_layout(mbx_shard_group* G, mbx_matrix* const* mats, mbx_tile* const* 
         seen, s.r0, rows, s.dangling);
     s.dang_from = mbx::dangling_suffix_start(ctx, s.dangling, rows);
     s.geo = mbx::make_geometry(ctx, &s.view, s.tile, c->block_size);
-    s.range_part = static_cast<double*>(
-        dm(ctx, (std::max(s.geo.num_ranges, mbx::pr_parts(s.geo)) + 1) * 4 * sizeof(double)));
+    s.carry_mask = static_cast<uint32_t*>(dm(ctx, ((rows + 31) / 32) * 4 + 64));
+    MBX_CUDA(cudaMemsetAsync(s.carry_mask, 0, ((rows + 31) / 32) * 4 + 64, st));
     // K3 blocks, or the pr_init grid (sm_count * 4) when a start vector is given
-    const int64_t nblk = std::max<int64_t>({mbx::fixup_blocks(s.geo) + 1, ctx->sm_count * 4 + 1,
+    const int64_t nblk = std::max<int64_t>({mbx::fixup_blocks(s.geo, true) + 1, mbx::fixup_blocks(s.geo, false) + 1, ctx->sm_count * 4 + 1,
                                             int64_t(mbx::csr_pr_blocks(ctx, &s.view))});
     s.block_part = static_cast<double*>(dm(ctx, nblk * 4 * sizeof(double)));
     s.counter = static_cast<unsigned int*>(dm(ctx, 64));
@@ -821,7 +821,7 @@ void group_free(mbx_shard_group* G) {
     for (void* p : {static_cast<void*>(s.cols_remap), static_cast<void*>(s.dangling),
                     static_cast<void*>(s.xmap),
                     static_cast<void*>(s.view.cols_hub), static_cast<void*>(s.view.hub_cols),
-                    static_cast<void*>(s.range_part), static_cast<void*>(s.block_part),
+                    static_cast<void*>(s.carry_mask), static_cast<void*>(s.block_part),
                     static_cast<void*>(s.counter), s.carry_ws})
       if (p) cudaFreeAsync(p, st);
   }
