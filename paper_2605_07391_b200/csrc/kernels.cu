@@ -1207,7 +1207,9 @@ void launch_slot(mbx_context* ctx, const SlotParams<T>& p, size_t smem) {
 // the reference's fold order) and ASSIGNED; the terminal row n is dropped.
 // ---------------------------------------------------------------------------
 constexpr int kFixupRun = 32;  // carries one thread folds before the warp takes over
-constexpr int kK3BlocksPerSM = 3;  // PageRank K3: persistent grid, blocks of 256 per SM
+// PageRank K3: a persistent grid of blocks of 256 (measured: 3 per SM beats
+// 4 and 6, whose lower register budgets cost more than the extra warps gain)
+constexpr int kK3BlocksPerSM = 3;
 
 // One carry entry e (the thread's): the first entry of each run of equal
 // rows folds the run left to right (merbit_spmv.hpp:330-337) -- runs longer
