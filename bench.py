@@ -193,6 +193,7 @@ def c1_numbers(mb, ctx, stream, peak, with_ref):
            "tile_ms": t.preprocess_seconds * 1e3,
            "preprocess_plus_first_spmv_ms": first_s * 1e3, "spmv_ms": ts * 1e3,
            "gflops": 2 * m / ts / 1e9, "frac": b / ts / 1e9 / peak}
+    out.update(comparator_numbers(A, c, x, y, stream, ts, 50))
     if with_ref:
         import oracle as O
         if O.ref() is not None:
@@ -310,6 +311,39 @@ def reference_spmv(mb, A, sigma, sample):
     return out
 
 
+COMPARATORS = ("coo_atomic", "csr_vector", "merge_runtime", "merge_cub", "cusparse_coo_alg1",
+               "cusparse_coo_alg2", "cusparse_csr_alg1", "cusparse_csr_alg2")
+
+
+def comparator_numbers(A, c, x, y, stream, ts, reps):
+    """The paper's comparators on the same device and inputs:
+    each one's time and MERBIT's speedup over it; speedup_vs_cusparse_coo is
+    the paper's headline ratio (cuSPARSE COO) against
+    cuSPARSE's faster COO algorithm, speedup_vs_coo the reference's
+    CooReferenceBackend on the GPU (BenchRecord.speedup)."""
+    from paper_2605_07391_b200.merbit import spmv_baseline_device
+    base = {}
+    for kind in COMPARATORS:
+        try:
+            fn = (lambda k=kind: spmv_baseline_device(A, k, x.data_ptr(), y.data_ptr(), c.sigma))
+            fn()
+            tb = time_device(stream, fn, reps)
+            base[kind] = {"ms": tb * 1e3, "gflops": 2 * A.nnz / tb / 1e9,
+                          "merbit_speedup": tb / ts}
+        except Exception as e:  # e.g. 32-bit offsets at > 2^31 nonzeros
+            base[kind] = {"unavailable": str(e)[:120]}
+    out = {"comparators": base}
+    if "ms" in base.get("coo_atomic", {}):
+        out["speedup_vs_coo"] = base["coo_atomic"]["ms"] * 1e-3 / ts  # BenchRecord.speedup
+    coo = [base[k]["ms"] for k in ("cusparse_coo_alg1", "cusparse_coo_alg2") if "ms" in base[k]]
+    if coo:
+        out["speedup_vs_cusparse_coo"] = min(coo) * 1e-3 / ts
+    csr = [base[k]["ms"] for k in ("cusparse_csr_alg1", "cusparse_csr_alg2") if "ms" in base[k]]
+    if csr:
+        out["speedup_vs_cusparse_csr"] = min(csr) * 1e-3 / ts
+    return out
+
+
 def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak, make=None, label=None,
                  reference=None):
     """Plain SpMV (K2+K3) on an R-MAT matrix (or make(ctx, dtype)) of the
@@ -338,21 +372,7 @@ def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak, make=None, label=Non
            "preprocess_slots_ms": slot_s * 1e3,
            "preprocess_over_spmv": (t.preprocess_seconds + xc_s + slot_s) / ts,
            "xcache_hubs": A.xcache_info()[0], "xcache_coverage": A.xcache_info()[1]}
-    # the paper's comparators on the same device and inputs
-    from paper_2605_07391_b200.merbit import spmv_baseline_device
-    base = {}
-    for kind in ("coo_atomic", "csr_vector", "merge_runtime", "merge_cub"):
-        try:
-            fn = (lambda k=kind: spmv_baseline_device(A, k, x.data_ptr(), y.data_ptr(), c.sigma))
-            fn()
-            tb = time_device(stream, fn, max(3, reps // 3))
-            base[kind] = {"ms": tb * 1e3, "gflops": 2 * A.nnz / tb / 1e9,
-                          "merbit_speedup": tb / ts}
-        except Exception as e:  # e.g. merge_cub's int32 offsets at > 2^31 nonzeros
-            base[kind] = {"unavailable": str(e)[:120]}
-    out["comparators"] = base
-    if "ms" in base.get("coo_atomic", {}):
-        out["speedup_vs_coo"] = base["coo_atomic"]["ms"] * 1e-3 / ts  # BenchRecord.speedup
+    out.update(comparator_numbers(A, c, x, y, stream, ts, max(3, reps // 3)))
     if reference is not None:
         # the reference's CPU path on this box (a bounded sample when the full
         # matrix would not fit the host / time budget): reported, not a target

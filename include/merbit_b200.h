@@ -182,8 +182,10 @@ MBX_API int mbx_context_synchronize(mbx_context* ctx);
  * SM (persistent grid), hub-cache cap (-1 auto, 0 off).  Defaults 32/1/-1. */
 MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta,
                                    int ctas_per_sm, int max_hubs);
-/* Shared-memory budget per SM for K2 (bytes; the rest is L1) and L2
- * prefetch of the next tile's streams (0/1).  Defaults 131072 / 0. */
+/* Shared-memory budget per SM for K2 (bytes; the rest is L1) and how K2
+ * stages the next tile: 0 nothing, 1 L2 prefetch of its streams, 2 TMA bulk
+ * copy of its column slots + descriptors into shared memory (slot layout),
+ * -1 auto (2 for fp64, 0 for fp32).  Defaults 131072 / -1. */
 MBX_API int mbx_context_set_tuning_ex(mbx_context* ctx, int smem_per_sm,
                                       int prefetch);
 /* K2 data layout: 1 (default) = lane-major slot copy of the matrix, built
@@ -307,12 +309,15 @@ MBX_API int mbx_spmv_csr_device(mbx_context* ctx, const mbx_matrix* m,
 /* The paper's baselines on the same device: kind 0
  * csr_vector (warp per row), 1 coo_atomic (CooReferenceBackend, backend.hpp:
  * 67-84), 2 merge_runtime (spmv_merge_runtime, merge_spmv.hpp:21-82, with
- * this sigma), 3 merge_cub (cub::DeviceSpmv::CsrMV, library). */
+ * this sigma), 3 merge_cub (cub::DeviceSpmv::CsrMV, library), 4..7 cuSPARSE
+ * cusparseSpMV COO ALG1, COO ALG2, CSR ALG1, CSR ALG2 (the paper's baseline,
+ * PAPER.md:32; libcusparse resolved with dlopen, MBX_UNSUPPORTED when absent;
+ * 32-bit indices: nnz < 2^31). */
 MBX_API int mbx_spmv_baseline_device(mbx_context* ctx, const mbx_matrix* m, int kind,
                                      int sigma, const void* x_dev, void* y_dev);
 
 /* Mean device time of one multiply (CUDA events; x uploaded once, warm-up
- * untimed): kind -1 = MERBIT (K2+K3 with t), 0..3 = the comparators above. */
+ * untimed): kind -1 = MERBIT (K2+K3 with t), 0..7 = the comparators above. */
 MBX_API int mbx_bench_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
                            const mbx_simt_config* c, int kind, int iters, int warmup,
                            const void* x_host, double* mean_seconds);

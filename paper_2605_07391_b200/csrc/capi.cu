@@ -68,7 +68,7 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   const int64_t fit = std::max<int64_t>(1, g.num_chunks / (8 * warps));
   g.chunks_per_range = int(std::max<int64_t>(1, std::min<int64_t>({31, block_size / 32, fit})));
   g.num_ranges = (g.num_chunks + g.chunks_per_range - 1) / g.chunks_per_range;
-  g.prefetch = ctx->tuning.prefetch;
+  g.prefetch = resolve_prefetch(ctx->tuning.prefetch, m->precision);
   g.hub_count = 0;
   if (m->cols_hub && m->hub_avail > 0 && g.omega == 32 && ctx->tuning.max_hubs != 0 &&
       (ctx->tuning.max_hubs < 0 || ctx->tuning.max_hubs >= m->hub_avail)) {
@@ -446,6 +446,7 @@ MBX_API int mbx_context_destroy(mbx_context* ctx) {
     if (!ctx) return;
     Device dg(ctx->device);
     drop_pr_cache(ctx);
+    mbx::free_sparse_handle(ctx);
     if (ctx->scratch) cudaFreeAsync(ctx->scratch, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
@@ -664,6 +665,7 @@ MBX_API int mbx_matrix_release_caches(mbx_matrix* m) {
       ++m->version;
       ++m->gen;
     }
+    mbx::free_sparse_state(ctx, m);
     dfree(ctx, m->coo_rows);
     m->coo_rows = nullptr;
     MBX_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -682,6 +684,7 @@ MBX_API int mbx_matrix_destroy(mbx_matrix* m) {
     dfree(ctx, m->cols_hub);
     dfree(ctx, m->hub_cols);
     mbx::free_slots(ctx, m);
+    mbx::free_sparse_state(ctx, m);
     dfree(ctx, m->coo_rows);
     dfree(ctx, m->vmap);
     MBX_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -15,12 +15,23 @@
 //                          folded in ascending lane order (long runs by a warp)
 //   kind 3  merge_cub      cub::DeviceSpmv::CsrMV (Merrill & Garland
 //                          merge-path SpMV), library code, int32 offsets
+//   kind 4-7 cuSPARSE      cusparseSpMV: COO ALG1, COO ALG2, CSR ALG1, CSR
+//                          ALG2 -- the paper's own baseline (PAPER.md:32,
+//                          494-496: speedups are quoted against cuSPARSE COO).
+//                          libcusparse is resolved with dlopen at first use so
+//                          the library itself links nothing but the runtime;
+//                          the descriptors and the work buffer (and the ALG2
+//                          preprocessing) are built once per matrix and kind.
 //
 // No preprocessing is cached by kinds 0, 2, 3; kind 1 expands the row
 // indices once per matrix (the COO row array).
 #define CUB_IGNORE_DEPRECATED_API 1
 #include <cub/cub.cuh>
 
+#include <cusparse.h>
+#include <dlfcn.h>
+
+#include <mutex>
 #include <string>
 
 #include "mbx_internal.h"
@@ -206,6 +217,160 @@ void launch_baseline_t(mbx_context* ctx, const mbx_matrix* m, int kind, int sigm
   MBX_CUDA(cudaGetLastError());
 }
 
+
+// ---- cuSPARSE (dlopen) ------------------------------------------------------
+struct SparseApi {
+  decltype(&cusparseCreate) create = nullptr;
+  decltype(&cusparseDestroy) destroy = nullptr;
+  decltype(&cusparseSetStream) set_stream = nullptr;
+  decltype(&cusparseCreateCoo) create_coo = nullptr;
+  decltype(&cusparseCreateCsr) create_csr = nullptr;
+  decltype(&cusparseDestroySpMat) destroy_spmat = nullptr;
+  decltype(&cusparseCreateDnVec) create_dnvec = nullptr;
+  decltype(&cusparseDestroyDnVec) destroy_dnvec = nullptr;
+  decltype(&cusparseDnVecSetValues) dnvec_set = nullptr;
+  decltype(&cusparseSpMV_bufferSize) buffer_size = nullptr;
+  decltype(&cusparseSpMV) spmv = nullptr;
+  decltype(&cusparseSpMV_preprocess) preprocess = nullptr;  // optional
+  std::string error;
+};
+
+const SparseApi& sparse_api() {
+  static SparseApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = nullptr;
+    for (const char* name : {"libcusparse.so.12", "/usr/local/cuda/lib64/libcusparse.so.12",
+                             "libcusparse.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+      if (h) break;
+    }
+    if (!h) {
+      api.error = "cuSPARSE comparator: libcusparse.so.12 not found";
+      return;
+    }
+    auto sym = [&](auto& fn, const char* name, bool required = true) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      if (!fn && required && api.error.empty())
+        api.error = std::string("cuSPARSE comparator: missing ") + name;
+    };
+    sym(api.create, "cusparseCreate");
+    sym(api.destroy, "cusparseDestroy");
+    sym(api.set_stream, "cusparseSetStream");
+    sym(api.create_coo, "cusparseCreateCoo");
+    sym(api.create_csr, "cusparseCreateCsr");
+    sym(api.destroy_spmat, "cusparseDestroySpMat");
+    sym(api.create_dnvec, "cusparseCreateDnVec");
+    sym(api.destroy_dnvec, "cusparseDestroyDnVec");
+    sym(api.dnvec_set, "cusparseDnVecSetValues");
+    sym(api.buffer_size, "cusparseSpMV_bufferSize");
+    sym(api.spmv, "cusparseSpMV");
+    sym(api.preprocess, "cusparseSpMV_preprocess", false);
+  });
+  if (!api.error.empty()) fail(MBX_UNSUPPORTED, api.error);
+  return api;
+}
+
+#define MBX_SPARSE(call)                                                              \
+  do {                                                                                \
+    const cusparseStatus_t st_ = (call);                                              \
+    if (st_ != CUSPARSE_STATUS_SUCCESS)                                               \
+      fail(MBX_CUDA_ERROR, "cuSPARSE status " + std::to_string(int(st_)) + " in " #call); \
+  } while (0)
+
+}  // namespace
+
+struct SparseState {
+  cusparseSpMatDescr_t mat = nullptr;
+  cusparseDnVecDescr_t vx = nullptr, vy = nullptr;
+  void* buffer = nullptr;
+};
+
+void free_sparse_state(mbx_context* ctx, const mbx_matrix* m) {
+  for (SparseState*& s : m->sparse) {
+    if (!s) continue;
+    const SparseApi& api = sparse_api();
+    if (s->mat) api.destroy_spmat(s->mat);
+    if (s->vx) api.destroy_dnvec(s->vx);
+    if (s->vy) api.destroy_dnvec(s->vy);
+    if (s->buffer) cudaFreeAsync(s->buffer, ctx->stream);
+    delete s;
+    s = nullptr;
+  }
+}
+
+void free_sparse_handle(mbx_context* ctx) {
+  if (ctx->cusparse) {
+    sparse_api().destroy(static_cast<cusparseHandle_t>(ctx->cusparse));
+    ctx->cusparse = nullptr;
+  }
+}
+
+namespace {
+
+// kinds 4..7: cusparseSpMV with COO ALG1 / COO ALG2 / CSR ALG1 / CSR ALG2
+void launch_cusparse(mbx_context* ctx, const mbx_matrix* m, int kind, const void* x, void* y) {
+  const SparseApi& api = sparse_api();
+  if (m->nnz >= (int64_t(1) << 31))
+    fail(MBX_CAPACITY_ERROR, "cuSPARSE comparator: 32-bit indices need nnz < 2^31");
+  cudaStream_t s = ctx->stream;
+  if (m->n_rows == 0) return;
+  if (m->nnz == 0) {  // cuSPARSE rejects empty matrices: y = 0
+    MBX_CUDA(cudaMemsetAsync(y, 0, m->n_rows * value_size(m->precision), s));
+    return;
+  }
+  if (!ctx->cusparse) {
+    cusparseHandle_t h;
+    MBX_SPARSE(api.create(&h));
+    ctx->cusparse = h;
+  }
+  cusparseHandle_t h = static_cast<cusparseHandle_t>(ctx->cusparse);
+  MBX_SPARSE(api.set_stream(h, s));
+  const bool coo = kind == 4 || kind == 5;
+  const cusparseSpMVAlg_t alg = kind == 4   ? CUSPARSE_SPMV_COO_ALG1
+                                : kind == 5 ? CUSPARSE_SPMV_COO_ALG2
+                                : kind == 6 ? CUSPARSE_SPMV_CSR_ALG1
+                                            : CUSPARSE_SPMV_CSR_ALG2;
+  const cudaDataType dt = m->precision == MBX_F32 ? CUDA_R_32F : CUDA_R_64F;
+  const double one64 = 1.0, zero64 = 0.0;
+  const float one32 = 1.0f, zero32 = 0.0f;
+  const void* alpha = m->precision == MBX_F32 ? static_cast<const void*>(&one32) : &one64;
+  const void* beta = m->precision == MBX_F32 ? static_cast<const void*>(&zero32) : &zero64;
+  SparseState*& st = m->sparse[kind - 4];
+  if (!st) {
+    if (coo && !m->coo_rows) {
+      MBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&m->coo_rows), m->nnz * 4 + 256, s));
+      if (m->n_rows > 0) {
+        expand_rows_kernel<<<unsigned(ctx->sm_count) * 16, 256, 0, s>>>(m->ro, m->n_rows,
+                                                                        m->coo_rows);
+        ++ctx->launches;
+      }
+    }
+    auto ns = std::make_unique<SparseState>();
+    if (coo)
+      MBX_SPARSE(api.create_coo(&ns->mat, m->n_rows, m->n_cols, m->nnz, m->coo_rows, m->cols,
+                                m->vals, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, dt));
+    else
+      MBX_SPARSE(api.create_csr(&ns->mat, m->n_rows, m->n_cols, m->nnz, m->ro, m->cols, m->vals,
+                                CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO,
+                                dt));
+    MBX_SPARSE(api.create_dnvec(&ns->vx, m->n_cols, const_cast<void*>(x), dt));
+    MBX_SPARSE(api.create_dnvec(&ns->vy, m->n_rows, y, dt));
+    size_t bytes = 0;
+    MBX_SPARSE(api.buffer_size(h, CUSPARSE_OPERATION_NON_TRANSPOSE, alpha, ns->mat, ns->vx, beta,
+                               ns->vy, dt, alg, &bytes));
+    MBX_CUDA(cudaMallocAsync(&ns->buffer, bytes > 0 ? bytes : 256, s));
+    if (api.preprocess)
+      MBX_SPARSE(api.preprocess(h, CUSPARSE_OPERATION_NON_TRANSPOSE, alpha, ns->mat, ns->vx, beta,
+                                ns->vy, dt, alg, ns->buffer));
+    st = ns.release();
+  }
+  MBX_SPARSE(api.dnvec_set(st->vx, const_cast<void*>(x)));
+  MBX_SPARSE(api.dnvec_set(st->vy, y));
+  MBX_SPARSE(api.spmv(h, CUSPARSE_OPERATION_NON_TRANSPOSE, alpha, st->mat, st->vx, beta, st->vy,
+                      dt, alg, st->buffer));
+}
+
 template <typename F>
 int cguard(F&& f) {
   try {
@@ -228,10 +393,14 @@ extern "C" {
 MBX_API int mbx_spmv_baseline_device(mbx_context* ctx, const mbx_matrix* m, int kind, int sigma,
                                      const void* x, void* y) {
   return mbx::cguard([&] {
-    MBX_CUDA(cudaSetDevice(ctx->device));
+    mbx::DeviceGuard dg(ctx->device);
     if (kind == 0) {
       const int rc = mbx_spmv_csr_device(ctx, m, x, y);
       if (rc) mbx::fail(rc, mbx_last_error());
+      return;
+    }
+    if (kind >= 4 && kind <= 7) {
+      mbx::launch_cusparse(ctx, m, kind, x, y);
       return;
     }
     if (sigma < 1) mbx::fail(MBX_CONFIG_ERROR, "sigma must be >= 1");
@@ -245,14 +414,14 @@ MBX_API int mbx_spmv_baseline_device(mbx_context* ctx, const mbx_matrix* m, int 
 }
 
 // Device-resident timing of one multiply kind on this matrix (CUDA events on
-// the context stream): kind -1 = MERBIT (K2+K3 with the given TILE), 0..3 the
+// the context stream): kind -1 = MERBIT (K2+K3 with the given TILE), 0..7 the
 // comparators above.  x is uploaded once; warm-up launches are untimed.
 MBX_API int mbx_bench_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
                            const mbx_simt_config* c, int kind, int iters, int warmup,
                            const void* x_host, double* mean_seconds) {
   return mbx::cguard([&] {
     if (iters < 1) mbx::fail(MBX_CONFIG_ERROR, "--iters must be at least 1");
-    MBX_CUDA(cudaSetDevice(ctx->device));
+    mbx::DeviceGuard dg(ctx->device);
     cudaStream_t s = ctx->stream;
     const size_t vs = mbx::value_size(m->precision);
     void *x = nullptr, *y = nullptr;

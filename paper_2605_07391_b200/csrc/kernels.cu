@@ -1541,10 +1541,10 @@ inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148LL * 64) {
 
 template <typename T, int SIGMA, bool PR, bool HUB>
 void launch_w32(mbx_context* ctx, const SpmvParams<T>& p, size_t smem) {
-  auto kern = p.g.prefetch ? spmv_w32_kernel<T, SIGMA, PR, HUB, true>
-                           : spmv_w32_kernel<T, SIGMA, PR, HUB, false>;
+  auto kern = p.g.prefetch == 1 ? spmv_w32_kernel<T, SIGMA, PR, HUB, true>
+                                : spmv_w32_kernel<T, SIGMA, PR, HUB, false>;
   static std::atomic<uint64_t> done[2];  // per (T, SIGMA, PR, HUB), prefetch variant
-  allow_max_smem(kern, ctx->device, done[p.g.prefetch ? 1 : 0]);
+  allow_max_smem(kern, ctx->device, done[p.g.prefetch == 1 ? 1 : 0]);
   const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
   const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));
   kern<<<grid, p.g.warps_per_cta * 32, smem, ctx->stream>>>(p);
@@ -1621,6 +1621,10 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
 
 }  // namespace
 
+int resolve_prefetch(int tuning, int precision) {
+  return tuning >= 0 ? tuning : (precision == MBX_F64 ? 2 : 0);
+}
+
 size_t stage_bytes(int sigma) { return size_t(32 * sigma) * 4 + 128 + 16; }
 
 size_t spmv_smem_bytes(const Geometry& g, int precision) {
@@ -1651,7 +1655,9 @@ int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, in
   const int64_t bufs =
       slot_layout ? int64_t(warps_per_cta) *
                         (kSlotRowBuf * vs +
-                         (ctx->tuning.prefetch == 2 ? int64_t(stage_bytes(sigma)) : 0))
+                         (resolve_prefetch(ctx->tuning.prefetch, precision) == 2
+                              ? int64_t(stage_bytes(sigma))
+                              : 0))
                   : int64_t(warps_per_cta) * (32 * sigma + 1) * vs;
   const int64_t slots = (per_cta - bufs) / vs - 4;
   return slots > 0 ? int(slots & ~int64_t(3)) : 0;

@@ -58,8 +58,11 @@ struct Tuning {
   // every in-flight miss: a hub table that squeezes L1 below ~80 KB starves
   // memory-level parallelism (measured, profiles/).
   int smem_per_sm = 128 * 1024;
-  int prefetch = 0;  // L2 prefetch of the next tile's value/column lines
-                     // (measured: costs request-port slots, off by default)
+  // K2 staging of the next tile: 0 none, 1 L2 prefetch of its value/column
+  // lines (measured: costs request-port slots), 2 TMA bulk copy of its column
+  // slots + descriptors into shared memory (slot layout; measured: fp64 -9 %,
+  // fp32 +8 % at R-MAT s24), -1 auto = 2 for fp64, 0 for fp32
+  int prefetch = -1;
   // K2 data layout: 1 = lane-major slots (default, omega 32 with the
   // default sigma), 0 = CSR order staged through shared memory
   int layout = 1;
@@ -141,7 +144,12 @@ struct mbx_context_s {
   // power-loop graph) for the next call on the same matrix, TILE and
   // configs; dropped when either is destroyed or by mbx_context_release_cache
   struct mbx_pagerank_plan_s* pr_cache = nullptr;
+  void* cusparse = nullptr;  // cusparseHandle_t of the cuSPARSE comparators (lazy)
 };
+
+namespace mbx {
+struct SparseState;  // comparators.cu
+}  // namespace mbx
 
 struct mbx_matrix_s {
   mbx_context* ctx = nullptr;
@@ -177,6 +185,9 @@ struct mbx_matrix_s {
   };
   mutable SlotCache slots;
   mutable int32_t* coo_rows = nullptr;  // COO row array of the coo_atomic comparator
+  // cuSPARSE comparator state (comparators.cu): descriptors + work buffer
+  // per algorithm, built on first use
+  mutable mbx::SparseState* sparse[4] = {nullptr, nullptr, nullptr, nullptr};
   // Set on a matrix made by mbx_matrix_relabel_by_degree: vertex v of the
   // original graph is vertex vmap[v] here.  Host-facing PageRank I/O
   // (pi0 in, pi / yardstick out) stays in the ORIGINAL vertex order.
@@ -209,6 +220,8 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs);
 bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, const Geometry& g);
 void free_slots(mbx_context* ctx, const mbx_matrix* m);
 int default_sigma(int precision);
+// Tuning::prefetch with -1 (auto) resolved for a precision
+int resolve_prefetch(int tuning, int precision);
 
 // ---- kernels (kernels.cu) ----
 void launch_generate_tile(mbx_context* ctx, const uint32_t* ro, int64_t n_rows,
@@ -231,6 +244,9 @@ void preload_pr_kernels(int precision);
 // First row of the dangling set when it is a suffix [f, n) of the rows
 // (f = n when empty), else -1: one host pass over the bitmask (preprocessing).
 int64_t dangling_suffix_start(mbx_context* ctx, const uint32_t* mask_dev, int64_t n);
+// comparators.cu: release the cuSPARSE state of a matrix / a context
+void free_sparse_state(mbx_context* ctx, const mbx_matrix* m);
+void free_sparse_handle(mbx_context* ctx);
 // capi.cu's validation of a SimtConfig and of a TILE against (matrix, config)
 void validate_config(const mbx_simt_config* c);
 void validate_tile(const mbx_matrix* m, const mbx_tile* t, const mbx_simt_config* c);

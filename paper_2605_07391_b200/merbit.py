@@ -210,12 +210,13 @@ class Context:
     def set_tuning(self, warps_per_cta: int = 32, ctas_per_sm: int = 1, max_hubs: int = -1,
                    smem_per_sm: int | None = None, prefetch: int | None = None):
         """K2 launch shape (persistent grid), x hub-cache cap (-1 auto, 0 off),
-        shared-memory budget per SM and L2 prefetch of the next tile."""
+        shared-memory budget per SM and the next tile's staging (0 none,
+        1 L2 prefetch, 2 TMA bulk copy into shared memory, -1 auto)."""
         _check(_lib.lib().mbx_context_set_tuning(self.h, warps_per_cta, ctas_per_sm, max_hubs))
         if smem_per_sm is not None or prefetch is not None:
             _check(_lib.lib().mbx_context_set_tuning_ex(
                 self.h, 131072 if smem_per_sm is None else smem_per_sm,
-                0 if prefetch is None else prefetch))
+                -1 if prefetch is None else prefetch))
 
     def set_layout(self, layout: int):
         """K2 data layout: 1 lane-major slots (default), 0 staged CSR order."""
@@ -547,12 +548,15 @@ def spmv_device(m: DeviceMatrix, t: Tile, c: SimtConfig, x_ptr: int, y_ptr: int)
     _check(_lib.lib().mbx_spmv_device(m.ctx.h, m.h, t.h, C.byref(cc), x_ptr, y_ptr))
 
 
-BASELINE_KINDS = {"csr_vector": 0, "coo_atomic": 1, "merge_runtime": 2, "merge_cub": 3}
+BASELINE_KINDS = {"csr_vector": 0, "coo_atomic": 1, "merge_runtime": 2, "merge_cub": 3,
+                  "cusparse_coo_alg1": 4, "cusparse_coo_alg2": 5, "cusparse_csr_alg1": 6,
+                  "cusparse_csr_alg2": 7}
 
 
 def spmv_baseline_device(m: DeviceMatrix, kind: str, x_ptr: int, y_ptr: int, sigma: int = 0):
     """The paper's comparators on the GPU (csr_vector, coo_atomic,
-    merge_runtime with `sigma`, merge_cub); device pointers in and out."""
+    merge_runtime with `sigma`, merge_cub, cuSPARSE COO/CSR ALG1/ALG2);
+    device pointers in and out."""
     if sigma <= 0:
         sigma = 14 if m.dtype == np.float32 else 7
     _check(_lib.lib().mbx_spmv_baseline_device(m.ctx.h, m.h, BASELINE_KINDS[kind], sigma,

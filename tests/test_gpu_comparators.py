@@ -1,6 +1,7 @@
 """GPU comparators: the paper's baselines on the same
 device -- csr_vector, coo_atomic (CooReferenceBackend), merge_runtime (the
-reference's spmv_merge_runtime, merge_spmv.hpp:21-82) and merge_cub -- each
+reference's spmv_merge_runtime, merge_spmv.hpp:21-82), merge_cub and the
+paper's own baseline, cuSPARSE SpMV (COO / CSR, ALG1 / ALG2) -- each
 within the reference's ToleranceBound; merge_runtime bitwise equal to the
 reference's own implementation where no carry run exceeds one warp."""
 import numpy as np
@@ -13,7 +14,8 @@ from paper_2605_07391_b200.merbit import spmv_baseline_device
 from helpers import first_violation, tolerance_bound
 
 pytestmark = pytest.mark.gpu
-KINDS = ["csr_vector", "coo_atomic", "merge_runtime", "merge_cub"]
+KINDS = ["csr_vector", "coo_atomic", "merge_runtime", "merge_cub", "cusparse_coo_alg1",
+         "cusparse_coo_alg2", "cusparse_csr_alg1", "cusparse_csr_alg2"]
 
 
 def run(ctx, a, kind, x, sigma=0):
