@@ -70,7 +70,7 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   g.num_ranges = (g.num_chunks + g.chunks_per_range - 1) / g.chunks_per_range;
   g.prefetch = resolve_prefetch(ctx->tuning.prefetch, m->precision);
   g.hub_count = 0;
-  if (m->cols_hub && m->hub_avail > 0 && g.omega == 32 && ctx->tuning.max_hubs != 0 &&
+  if (m->hub_cols && m->hub_avail > 0 && g.omega == 32 && ctx->tuning.max_hubs != 0 &&
       (ctx->tuning.max_hubs < 0 || ctx->tuning.max_hubs >= m->hub_avail)) {
     const int slots = max_hub_slots(ctx, g.warps_per_cta, ctx->tuning.ctas_per_sm, g.sigma,
                                     m->precision);
@@ -84,6 +84,7 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
     const bool slot_budget = ctx->tuning.layout == 1 && g.sigma == default_sigma(m->precision);
     if (slot_budget) g.hub_count = 0;
   }
+  if (!g.slots && g.hub_count > 0) ensure_cols_hub(const_cast<mbx_context*>(ctx), m);
   return g;
 }
 

@@ -1142,8 +1142,19 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
 }
 
 // One thread per (chunk, lane): writes that lane's sigma slots.
+// hub encoding of a column: prefix > 0 -- the hubs are columns 0..prefix-1
+// (degree-relabelled), slot c; else slot_of lookup (nullptr: no hubs)
+__device__ __forceinline__ int32_t hub_encode(const int32_t* __restrict__ slot_of, int prefix,
+                                              int32_t c) {
+  if (prefix > 0) return c < prefix ? int32_t(0x80000000u | uint32_t(c)) : c;
+  if (!slot_of) return c;
+  const int32_t s = __ldg(slot_of + c);
+  return s >= 0 ? int32_t(0x80000000u | uint32_t(s)) : c;
+}
+
 template <typename T>
 __global__ void build_slots_kernel(const T* __restrict__ vals, const int32_t* __restrict__ cols,
+                                   const int32_t* __restrict__ slot_of, int prefix,
                                    const uint32_t* __restrict__ tile_x,
                                    const uint32_t* __restrict__ tile_y,
                                    const uint32_t* __restrict__ lane_desc, int64_t lane_num,
@@ -1163,7 +1174,7 @@ __global__ void build_slots_kernel(const T* __restrict__ vals, const int32_t* __
         const int64_t pos = sb + int64_t(i / G) * 32 * G + (i % G);
         const bool ok = e < x1;
         svals[pos] = ok ? vals[e] : T(0);
-        scols[pos] = ok ? cols[e] : 0;
+        scols[pos] = ok ? hub_encode(slot_of, prefix, cols[e]) : 0;
       }
     } else {
       uint32_t d = 0;
@@ -1178,7 +1189,7 @@ __global__ void build_slots_kernel(const T* __restrict__ vals, const int32_t* __
         const int64_t pos = sb + int64_t(i / G) * 32 * G + (i % G);
         if (i < steps && !((fl >> i) & 1u)) {
           svals[pos] = vals[x];
-          scols[pos] = cols[x];
+          scols[pos] = hub_encode(slot_of, prefix, cols[x]);
           ++x;
         } else {
           svals[pos] = T(0);
@@ -1366,9 +1377,9 @@ __global__ void gen_tile_kernel(const uint32_t* __restrict__ ro, int64_t n, int6
   const int64_t total = m + n;
   int64_t x = 0, y = 0;
   const int64_t diag = j * sigma;
-  if (valid) d_merge_search(ro, n, m, diag, x, y);
   int64_t tsx, tsy;
   int leader = 0;
+  if (valid) d_merge_search(ro, n, m, diag, x, y);
   if (small_omega) {
     leader = lid & ~(omega - 1);
     tsx = __shfl_sync(kFull, x, leader);
@@ -1719,20 +1730,24 @@ bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, cons
   MBX_CUDA(cudaMallocAsync(&sc.vals, count * vs + 256, ctx->stream));
   MBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc.cols), count * 4 + 256, ctx->stream));
   MBX_CUDA(cudaEventRecord(e0, ctx->stream));  // build time, not the allocation
-  const int32_t* src_cols = hub ? m->cols_hub : m->cols;
+  // the hub encoding is applied while the slots are written (no encoded
+  // copy of the CSR columns is kept)
+  const int prefix = hub && m->hub_prefix ? m->hub_avail : 0;
+  int32_t* slot_of = hub && !prefix ? hub_slot_map(ctx, m) : nullptr;
   const unsigned grid = grid_for(g.num_chunks * 32, 256, int64_t(ctx->sm_count) * 16);
   const int64_t total = g.nnz + g.n_rows;
   if (m->precision == MBX_F32)
     build_slots_kernel<float><<<grid, 256, 0, ctx->stream>>>(
-        static_cast<const float*>(m->vals), src_cols, t->tile_x, t->tile_y, t->lane_desc,
+        static_cast<const float*>(m->vals), m->cols, slot_of, prefix, t->tile_x, t->tile_y, t->lane_desc,
         g.lane_num, g.num_chunks, total, g.sigma, g.ob, static_cast<float*>(sc.vals), sc.cols);
   else
     build_slots_kernel<double><<<grid, 256, 0, ctx->stream>>>(
-        static_cast<const double*>(m->vals), src_cols, t->tile_x, t->tile_y, t->lane_desc,
+        static_cast<const double*>(m->vals), m->cols, slot_of, prefix, t->tile_x, t->tile_y, t->lane_desc,
         g.lane_num, g.num_chunks, total, g.sigma, g.ob, static_cast<double*>(sc.vals), sc.cols);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
   MBX_CUDA(cudaEventRecord(e1, ctx->stream));
+  if (slot_of) cudaFreeAsync(slot_of, ctx->stream);
   MBX_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
   MBX_CUDA(cudaEventElapsedTime(&ms, e0, e1));

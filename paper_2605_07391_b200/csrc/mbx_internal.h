@@ -159,11 +159,13 @@ struct mbx_matrix_s {
   int32_t* cols = nullptr;     // int32[nnz] (+ pad)
   uint32_t* ro = nullptr;      // u32[n_rows+1]
   // x hub cache (mbx_matrix_build_xcache): hub_cols lists the most
-  // referenced columns in descending frequency; cols_hub is cols with every
-  // reference to hub slot s < hub_avail rewritten as (INT32_MIN | s).
+  // referenced columns in descending frequency; cols_hub (built only when a
+  // staged / generic K2 needs it) is cols with every reference to hub slot
+  // s < hub_avail rewritten as (INT32_MIN | s).
   int32_t* cols_hub = nullptr;
   int32_t* hub_cols = nullptr;
   int hub_avail = 0;
+  int hub_prefix = 0;         // 1: hub_cols is 0..hub_avail-1 (degree-relabelled)
   double hub_coverage = 0.0;  // fraction of nonzeros that reference a hub
   uint64_t version = 0;       // bumped whenever cols_hub is rebuilt
   // bumped whenever a device buffer a captured PageRank plan may reference
@@ -215,6 +217,10 @@ size_t spmv_smem_bytes(const Geometry& g, int precision);
 int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, int sigma,
                   int precision);
 void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs);
+// slot_of[c] = hub slot of column c or -1 (n_cols int32; the caller frees)
+int32_t* hub_slot_map(mbx_context* ctx, const mbx_matrix* m);
+// build m->cols_hub (hub-encoded CSR columns) if missing: staged / generic K2
+void ensure_cols_hub(mbx_context* ctx, const mbx_matrix* m);
 // slots.cu: make m->slots match (t, hub encoding of g); false if the slot
 // layout does not apply (then K2 uses the staged CSR order)
 bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, const Geometry& g);

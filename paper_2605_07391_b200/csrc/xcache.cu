@@ -4,10 +4,11 @@
 // the SpMV kernel on power-law inputs (ncu: l1tex2xbar request port ~81%,
 // hottest L2 slices ~95% while DRAM sits at ~27%).  The most referenced
 // columns ("hubs") are therefore staged once per CTA in shared memory by K2.
-// This pass ranks columns by reference count (stable: ties keep ascending
-// column order), keeps those referenced more often than the number of CTAs
-// that will each load them, and writes a second column array where every
-// hub reference becomes (INT32_MIN | slot).  The TILE is untouched and the
+// This pass ranks columns by their reference count in a sample of the
+// nonzeros (stable: ties keep ascending column order) and keeps those
+// referenced more often than the number of CTAs that will each load them;
+// the slot copy K2 walks then encodes every hub reference as
+// (INT32_MIN | slot).  The TILE is untouched and the
 // SpMV result is bitwise identical with or without the cache (the same
 // x value is read, the summation order does not change).
 #include <cub/cub.cuh>
@@ -84,6 +85,45 @@ void launch_count_columns(mbx_context* ctx, const int32_t* cols, int64_t nnz, in
   MBX_CUDA(cudaGetLastError());
 }
 
+namespace {
+
+// Column reference counts over a sample of the nonzeros: every S-th run of
+// 32 consecutive nonzeros (one warp-coalesced load each), so the selection
+// costs at most ~2^22 scattered increments whatever the matrix size.  The
+// counts only rank candidate hubs: a hub's value in shared memory is the same
+// x entry, so results do not depend on which columns are chosen.
+constexpr int64_t kSampleRuns = int64_t(1) << 17;  // 32 nonzeros each (4 M samples)
+
+__global__ void count_sample_kernel(const int32_t* __restrict__ cols, int64_t nnz,
+                                    int64_t stride_runs, uint32_t* __restrict__ cnt) {
+  const int lid = threadIdx.x & 31;
+  const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t runs = (nnz + 31) / 32;
+  for (int64_t r = w * stride_runs; r < runs; r += nw * stride_runs) {
+    const int64_t k = r * 32 + lid;
+    if (k < nnz) atomicAdd(cnt + __ldg(cols + k), 1u);
+  }
+}
+
+// candidates: columns whose sampled count exceeds `t`
+__global__ void flag_above_kernel(const uint32_t* __restrict__ cnt, int64_t n, uint32_t t,
+                                  uint8_t* __restrict__ flag) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    flag[i] = cnt[i] > t;
+}
+
+__global__ void gather_counts_kernel(const uint32_t* __restrict__ cnt,
+                                     const int32_t* __restrict__ ids, int64_t k,
+                                     uint32_t* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < k;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = cnt[ids[i]];
+}
+
+}  // namespace
+
 void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   cudaStream_t s = ctx->stream;
   if (m->cols_hub) {
@@ -95,6 +135,7 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
     m->hub_cols = nullptr;
   }
   m->hub_avail = 0;
+  m->hub_prefix = 0;
   m->hub_coverage = 0.0;
   ++m->version;  // invalidates slot copies built over the old encoding
   ++m->gen;      // and the graphs captured over the old buffers
@@ -104,30 +145,7 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   if (max_hubs >= 0) slots = std::min(slots, max_hubs);
   if (slots <= 0 || m->nnz == 0 || m->n_cols == 0) return;
   const int64_t n = m->n_cols;
-  const unsigned grid = unsigned(ctx->sm_count) * 8;
-  uint32_t *cnt = nullptr, *cnt_sorted = nullptr;
-  int32_t *ids = nullptr, *ids_sorted = nullptr;
-  MBX_CUDA(cudaMallocAsync(&cnt, n * 4, s));
-  MBX_CUDA(cudaMallocAsync(&cnt_sorted, n * 4, s));
-  MBX_CUDA(cudaMallocAsync(&ids, n * 4, s));
-  MBX_CUDA(cudaMallocAsync(&ids_sorted, n * 4, s));
-  MBX_CUDA(cudaMemsetAsync(cnt, 0, n * 4, s));
-  count_cols_kernel<<<unsigned(ctx->sm_count) * 2, 512, 0, s>>>(m->cols, m->nnz, n, cnt);
-  iota_kernel<<<grid, 256, 0, s>>>(ids, n);
-  ctx->launches += 2;
-  size_t tb = 0;
-  MBX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt, cnt_sorted, ids,
-                                                      ids_sorted, n, 0, 32, s));
-  void* temp = nullptr;
-  MBX_CUDA(cudaMallocAsync(&temp, tb, s));
-  MBX_CUDA(cub::DeviceRadixSort::SortPairsDescending(temp, tb, cnt, cnt_sorted, ids, ids_sorted,
-                                                      n, 0, 32, s));
-  const int cand = int(std::min<int64_t>(slots, n));
-  std::vector<uint32_t> hc(cand);
-  std::vector<int32_t> hid(cand);
-  MBX_CUDA(cudaMemcpyAsync(hc.data(), cnt_sorted, size_t(cand) * 4, cudaMemcpyDeviceToHost, s));
-  MBX_CUDA(cudaMemcpyAsync(hid.data(), ids_sorted, size_t(cand) * 4, cudaMemcpyDeviceToHost, s));
-  MBX_CUDA(cudaStreamSynchronize(s));
+  const int64_t runs = (m->nnz + 31) / 32;
   // A hub pays off only if it is referenced several times more often than
   // it costs to load (once per resident CTA per SpMV), and the per-CTA table
   // load (a serial preamble before any tile) must stay a small fraction
@@ -140,6 +158,113 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   const int64_t ctas = int64_t(ctx->sm_count) * tu.ctas_per_sm;
   const uint32_t min_refs = uint32_t(4 * ctas);
   const uint32_t min_refs_shared = uint32_t(std::max<int64_t>(ctas / 8, 2));
+  // sample stride: at most ~kSampleRuns runs, but never so sparse that a
+  // column at the hub threshold expects fewer than 16 sampled references
+  // (a stencil's 27-reference columns must not pass by sampling luck)
+  const int64_t S = std::max<int64_t>(
+      1, std::min<int64_t>((runs + kSampleRuns - 1) / kSampleRuns, int64_t(min_refs) / 16));
+  uint32_t* cnt = nullptr;
+  MBX_CUDA(cudaMallocAsync(&cnt, n * 4 + 64, s));
+  MBX_CUDA(cudaMemsetAsync(cnt, 0, n * 4, s));
+  count_sample_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(m->cols, m->nnz, S, cnt);
+  ++ctx->launches;
+  // no column can reach even the shared-line threshold (a stencil: at most
+  // 27 references per column): no table, nothing more to do
+  uint32_t* dmax = nullptr;
+  size_t tb = 0;
+  MBX_CUDA(cub::DeviceReduce::Max(nullptr, tb, cnt, dmax, n, s));
+  void* temp = nullptr;
+  MBX_CUDA(cudaMallocAsync(&temp, tb + 64, s));
+  MBX_CUDA(cudaMallocAsync(&dmax, 64, s));
+  MBX_CUDA(cub::DeviceReduce::Max(temp, tb, cnt, dmax, n, s));
+  uint32_t cmax = 0;
+  MBX_CUDA(cudaMemcpyAsync(&cmax, dmax, 4, cudaMemcpyDeviceToHost, s));
+  MBX_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(temp, s);
+  cudaFreeAsync(dmax, s);
+  auto done = [&] {
+    cudaFreeAsync(cnt, s);
+    MBX_CUDA(cudaStreamSynchronize(s));
+  };
+  if (int64_t(cmax) * S <= int64_t(min_refs)) return done();
+  m->hub_prefix = 0;
+  if (m->vmap) {
+    // degree-relabelled: columns are already ranked by count (vertex v has
+    // the v-th largest column count), so the candidates are the prefix in
+    // order -- no selection, no sort, and the slot copy encodes a hub as
+    // c < h without a lookup.  The sampled counts are noisy but the true ones
+    // descend: their suffix maximum is the ranking used.
+    const int cand = int(std::min<int64_t>(slots, n));
+    std::vector<uint32_t> raw(cand), hc(cand);
+    MBX_CUDA(cudaMemcpyAsync(raw.data(), cnt, size_t(cand) * 4, cudaMemcpyDeviceToHost, s));
+    MBX_CUDA(cudaStreamSynchronize(s));
+    if (cand > 0) hc[cand - 1] = raw[cand - 1];
+    for (int i = cand - 2; i >= 0; --i) hc[i] = std::max(raw[i], hc[i + 1]);
+    const int64_t cap_lines = m->nnz / (ctas * 50);
+    const int line_shift = m->precision == MBX_F32 ? 5 : 4;
+    int h = 0;
+    int64_t covered = 0;
+    while (h < cand) {
+      const bool fresh = (h & ((1 << line_shift) - 1)) == 0;
+      if (int64_t(hc[h]) * S <= int64_t(fresh ? min_refs : min_refs_shared)) break;
+      if (fresh && (int64_t(h) >> line_shift) + 1 > cap_lines) break;
+      covered += int64_t(raw[h++]) * S;
+    }
+    if (h > 0) {
+      MBX_CUDA(cudaMallocAsync(&m->hub_cols, size_t(h) * 4 + 64, s));
+      iota_kernel<<<(h + 255) / 256, 256, 0, s>>>(m->hub_cols, h);
+      ++ctx->launches;
+      m->hub_avail = h;
+      m->hub_prefix = 1;
+      m->hub_coverage = std::min(1.0, double(covered) / double(m->nnz));
+    }
+    return done();
+  }
+  // candidates: every column whose (scaled) sampled count passes the lower
+  // threshold, ranked by count descending (stable: ties in column order)
+  const uint32_t t = uint32_t(min_refs_shared / S);
+  uint8_t* flag = nullptr;
+  int32_t *cid = nullptr, *cid_sorted = nullptr;
+  uint32_t *ccnt = nullptr, *ccnt_sorted = nullptr;
+  int64_t* dk = nullptr;
+  MBX_CUDA(cudaMallocAsync(&flag, n + 64, s));
+  MBX_CUDA(cudaMallocAsync(&dk, 64, s));
+  const unsigned grid = unsigned(ctx->sm_count) * 8;
+  flag_above_kernel<<<grid, 256, 0, s>>>(cnt, n, t, flag);
+  ++ctx->launches;
+  MBX_CUDA(cudaMallocAsync(&cid, n * 4 + 64, s));
+  cub::CountingInputIterator<int32_t> it(0);
+  tb = 0;
+  MBX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flag, cid, dk, n, s));
+  MBX_CUDA(cudaMallocAsync(&temp, tb + 64, s));
+  MBX_CUDA(cub::DeviceSelect::Flagged(temp, tb, it, flag, cid, dk, n, s));
+  int64_t K = 0;
+  MBX_CUDA(cudaMemcpyAsync(&K, dk, 8, cudaMemcpyDeviceToHost, s));
+  MBX_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(temp, s);
+  cudaFreeAsync(flag, s);
+  cudaFreeAsync(dk, s);
+  if (K == 0) {
+    cudaFreeAsync(cid, s);
+    return done();
+  }
+  MBX_CUDA(cudaMallocAsync(&ccnt, K * 4 + 64, s));
+  MBX_CUDA(cudaMallocAsync(&ccnt_sorted, K * 4 + 64, s));
+  MBX_CUDA(cudaMallocAsync(&cid_sorted, K * 4 + 64, s));
+  gather_counts_kernel<<<grid, 256, 0, s>>>(cnt, cid, K, ccnt);
+  ++ctx->launches;
+  tb = 0;
+  MBX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, ccnt, ccnt_sorted, cid,
+                                                      cid_sorted, int(K), 0, 32, s));
+  MBX_CUDA(cudaMallocAsync(&temp, tb + 64, s));
+  MBX_CUDA(cub::DeviceRadixSort::SortPairsDescending(temp, tb, ccnt, ccnt_sorted, cid,
+                                                      cid_sorted, int(K), 0, 32, s));
+  const int cand = int(std::min<int64_t>(slots, K));
+  std::vector<uint32_t> hc(cand);
+  std::vector<int32_t> hid(cand);
+  MBX_CUDA(cudaMemcpyAsync(hc.data(), ccnt_sorted, size_t(cand) * 4, cudaMemcpyDeviceToHost, s));
+  MBX_CUDA(cudaMemcpyAsync(hid.data(), cid_sorted, size_t(cand) * 4, cudaMemcpyDeviceToHost, s));
+  MBX_CUDA(cudaStreamSynchronize(s));
   const int64_t cap_lines = m->nnz / (ctas * 50);
   const int line_shift = m->precision == MBX_F32 ? 5 : 4;  // entries per 128-byte line
   std::vector<uint8_t> line_seen;
@@ -149,34 +274,55 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
     const int64_t line = int64_t(hid[h]) >> line_shift;
     if (line_seen.size() <= size_t(line)) line_seen.resize(size_t(line) + 1, 0);
     const bool fresh = !line_seen[size_t(line)];
-    if (hc[h] <= (fresh ? min_refs : min_refs_shared)) break;
+    if (int64_t(hc[h]) * S <= int64_t(fresh ? min_refs : min_refs_shared)) break;
     if (fresh && lines + 1 > cap_lines) break;
     if (fresh) {
       line_seen[size_t(line)] = 1;
       ++lines;
     }
-    covered += hc[h++];
+    covered += int64_t(hc[h++]) * S;
   }
   if (h > 0) {
     MBX_CUDA(cudaMallocAsync(&m->hub_cols, size_t(h) * 4 + 64, s));
-    MBX_CUDA(cudaMemcpyAsync(m->hub_cols, ids_sorted, size_t(h) * 4, cudaMemcpyDeviceToDevice, s));
-    int32_t* slot_of = reinterpret_cast<int32_t*>(cnt);  // reuse
-    fill_kernel<<<grid, 256, 0, s>>>(slot_of, n, -1);
-    slot_map_kernel<<<(h + 255) / 256, 256, 0, s>>>(m->hub_cols, h, slot_of);
-    MBX_CUDA(cudaMallocAsync(&m->cols_hub, m->nnz * 4 + 256, s));
-    MBX_CUDA(cudaMemsetAsync(m->cols_hub, 0, m->nnz * 4 + 256, s));
-    encode_kernel<<<grid, 256, 0, s>>>(m->cols, m->nnz, slot_of, m->cols_hub);
-    ctx->launches += 3;
-    MBX_CUDA(cudaGetLastError());
+    MBX_CUDA(cudaMemcpyAsync(m->hub_cols, cid_sorted, size_t(h) * 4, cudaMemcpyDeviceToDevice, s));
     m->hub_avail = h;
-    m->hub_coverage = double(covered) / double(m->nnz);
+    // estimated from the sample when S > 1
+    m->hub_coverage = std::min(1.0, double(covered) / double(m->nnz));
   }
   cudaFreeAsync(temp, s);
-  cudaFreeAsync(cnt, s);
-  cudaFreeAsync(cnt_sorted, s);
-  cudaFreeAsync(ids, s);
-  cudaFreeAsync(ids_sorted, s);
-  MBX_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(ccnt, s);
+  cudaFreeAsync(ccnt_sorted, s);
+  cudaFreeAsync(cid, s);
+  cudaFreeAsync(cid_sorted, s);
+  done();
+}
+
+// slot_of[c] = hub slot of column c, or -1 (n_cols int32, caller frees)
+int32_t* hub_slot_map(mbx_context* ctx, const mbx_matrix* m) {
+  cudaStream_t s = ctx->stream;
+  int32_t* slot_of = nullptr;
+  MBX_CUDA(cudaMallocAsync(&slot_of, m->n_cols * 4 + 64, s));
+  fill_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(slot_of, m->n_cols, -1);
+  slot_map_kernel<<<(m->hub_avail + 255) / 256, 256, 0, s>>>(m->hub_cols, m->hub_avail, slot_of);
+  ctx->launches += 2;
+  MBX_CUDA(cudaGetLastError());
+  return slot_of;
+}
+
+// The hub-encoded column array of the staged (layout 0) and generic K2
+// paths: every reference to a hub becomes (INT32_MIN | slot).  The default
+// slot-layout K2 encodes its slot copy directly and never needs it.
+void ensure_cols_hub(mbx_context* ctx, const mbx_matrix* m_) {
+  mbx_matrix* m = const_cast<mbx_matrix*>(m_);
+  if (m->cols_hub || m->hub_avail <= 0) return;
+  cudaStream_t s = ctx->stream;
+  int32_t* slot_of = hub_slot_map(ctx, m);
+  MBX_CUDA(cudaMallocAsync(&m->cols_hub, m->nnz * 4 + 256, s));
+  MBX_CUDA(cudaMemsetAsync(m->cols_hub, 0, m->nnz * 4 + 256, s));
+  encode_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(m->cols, m->nnz, slot_of, m->cols_hub);
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+  cudaFreeAsync(slot_of, s);
 }
 
 }  // namespace mbx
