@@ -24,6 +24,7 @@
 #include <atomic>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -89,6 +90,42 @@ void allow_max_smem(K kern, int device, std::atomic<uint64_t>& done) {
   done.fetch_or(bit, std::memory_order_acq_rel);
 }
 
+// Programmatic dependent launch (PDL): K2 and K3 are launched so that the
+// next one is scheduled while the previous one drains (its launch latency and
+// CTA rasterisation overlap the tail); each waits for its predecessor's
+// completion and memory before reading anything it produced, and lets its
+// own dependent launch right away (whose CTAs then wait the same way).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// cudaLaunchKernelEx with the PDL attribute (MBX_PDL=0 disables it)
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MBX_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// (used for the plain SpMV: inside the PageRank graphs, whose kernel
+// boundaries are already cheap, it measured 1 % slower)
+template <typename... KArgs, typename... Args>
+void launch_pdl(bool on, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = on && pdl_enabled() ? 1 : 0;
+  MBX_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 template <typename T>
 struct VecOf {
   static constexpr int N = 16 / sizeof(T);
@@ -111,7 +148,20 @@ __device__ __forceinline__ double warp_max(double v) {
 // round trips before the CTA's first tile).
 template <typename T>
 __device__ __forceinline__ void stage_hubs(T* hub, const T* __restrict__ x,
-                                           const int32_t* __restrict__ hub_cols, int hc) {
+                                           const int32_t* __restrict__ hub_cols, int hc,
+                                           const T* __restrict__ hub_x) {
+  if (hub_x) {
+    // the hub values are contiguous (a degree-relabelled x, whose hubs are
+    // its first entries, or the per-multiply hub gather): 16-byte copies,
+    // 1/32 of the requests of a scattered table
+    constexpr int V = 16 / int(sizeof(T));
+    const int nv = hc / V;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x)
+      reinterpret_cast<float4*>(hub)[i] = __ldg(reinterpret_cast<const float4*>(hub_x) + i);
+    for (int i = nv * V + threadIdx.x; i < hc; i += blockDim.x) hub[i] = __ldg(hub_x + i);
+    __syncthreads();
+    return;
+  }
   constexpr int U = 8;
   for (int i0 = threadIdx.x; i0 < hc; i0 += blockDim.x * U) {
     int idx[U];
@@ -451,6 +501,7 @@ struct SpmvParams {
   const uint32_t* tile_y;
   const uint32_t* lane_desc;
   const int32_t* hub_cols;
+  const T* hub_x;  // contiguous hub values (nullptr: gather x[hub_cols])
   uint32_t* carry_row;
   T* carry_val;
   Geometry g;
@@ -622,7 +673,7 @@ __global__ void __launch_bounds__(1024) spmv_w32_kernel(SpmvParams<T> p) {
   T* hub = reinterpret_cast<T*>(smem_raw);
   const int hub_pad = HUB ? ((g.hub_count + 3) & ~3) : 0;
   T* buf = hub + hub_pad + size_t(warp) * (32 * sigma + 1);
-  if (HUB) stage_hubs<T>(hub, p.x, p.hub_cols, g.hub_count);
+  if (HUB) stage_hubs<T>(hub, p.x, p.hub_cols, g.hub_count, p.hub_x);
   const uint64_t pol = evict_first_policy();
   T base = T(0);
   if (PR) base = pr_base<T>(p.pr);
@@ -778,6 +829,7 @@ struct SlotParams {
   const uint32_t* tile_y;
   const uint32_t* lane_desc;
   const int32_t* hub_cols;
+  const T* hub_x;  // contiguous hub values (nullptr: gather x[hub_cols])
   uint32_t* carry_row;
   T* carry_val;
   Geometry g;
@@ -1109,6 +1161,8 @@ template <typename T, int SIGMA, bool PR, bool HUB, int MODE>
 __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geometry& g = p.g;
+  pdl_wait();     // the previous kernel's x / scalars are complete
+  pdl_trigger();  // K3 may be scheduled (its CTAs wait for this grid)
   if (PR && pr_skip(p.pr)) return;
   const int warp = threadIdx.x >> 5, lid = threadIdx.x & 31;
   T* hub = reinterpret_cast<T*>(smem_raw);
@@ -1117,7 +1171,7 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   constexpr size_t kWarpBytes = kSlotRowBuf * sizeof(T);
   unsigned char* wbase = reinterpret_cast<unsigned char*>(hub + hub_pad);
   T* rowbuf = reinterpret_cast<T*>(wbase + size_t(warp) * kWarpBytes);
-  if (HUB) stage_hubs<T>(hub, p.x, p.hub_cols, g.hub_count);
+  if (HUB) stage_hubs<T>(hub, p.x, p.hub_cols, g.hub_count, p.hub_x);
   const uint64_t pol = evict_first_policy();
   T base = T(0);
   if (PR) base = pr_base<T>(p.pr);
@@ -1209,7 +1263,7 @@ void launch_slot(mbx_context* ctx, const SlotParams<T>& p, size_t smem) {
   allow_max_smem(kern, ctx->device, done[p.g.prefetch == 2 ? 2 : p.g.prefetch ? 1 : 0]);
   const int64_t need = (p.g.num_ranges + p.g.warps_per_cta - 1) / p.g.warps_per_cta;
   const unsigned grid = static_cast<unsigned>(imin64(p.g.grid, need));
-  kern<<<grid, p.g.warps_per_cta * 32, smem, ctx->stream>>>(p);
+  launch_pdl(!PR, kern, grid, unsigned(p.g.warps_per_cta * 32), smem, ctx->stream, p);
 }
 
 // ---------------------------------------------------------------------------
@@ -1290,6 +1344,8 @@ template <typename T, bool PR>
 __global__ void __launch_bounds__(256, PR ? kK3BlocksPerSM : 1)
     fixup_kernel(const uint32_t* __restrict__ crow, const T* __restrict__ cval,
                  int64_t num_ranges, int64_t n_rows, T* __restrict__ y, PrArgs pr) {
+  pdl_wait();     // K2's carries, rows and marks are complete
+  pdl_trigger();
   if (PR && pr_skip(pr)) return;
   const int64_t ne = 2 * num_ranges;
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1561,6 +1617,15 @@ void launch_w32(mbx_context* ctx, const SpmvParams<T>& p, size_t smem) {
   kern<<<grid, p.g.warps_per_cta * 32, smem, ctx->stream>>>(p);
 }
 
+// The hub values of this multiply, contiguous: hub_x[i] = x[hub_cols[i]]
+// (once per multiply; every CTA then stages them with coalesced copies)
+template <typename T>
+__global__ void hub_gather_kernel(const T* __restrict__ x, const int32_t* __restrict__ hub_cols,
+                                  int hc, T* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < hc; i += gridDim.x * blockDim.x)
+    out[i] = __ldg(x + __ldg(hub_cols + i));
+}
+
 template <typename T, bool PR>
 void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
                    const Geometry& g, const void* x, void* y, void* ws, const PrArgs* pr) {
@@ -1580,6 +1645,19 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
   const size_t row_bytes = ((ne * 4 + 255) / 256) * 256;
   p.carry_val = reinterpret_cast<T*>(static_cast<char*>(ws) + row_bytes);
   if (pr) p.pr = *pr;
+  p.hub_x = nullptr;
+  if (g.hub_count > 0) {
+    if (m->hub_prefix) {
+      p.hub_x = p.x;  // the hubs are x's first entries
+    } else {
+      T* hx = reinterpret_cast<T*>(static_cast<char*>(ws) + row_bytes +
+                                   ((ne * sizeof(T) + 255) / 256) * 256);
+      hub_gather_kernel<T><<<unsigned((g.hub_count + 255) / 256), 256, 0, ctx->stream>>>(
+          p.x, m->hub_cols, g.hub_count, hx);
+      ++ctx->launches;
+      p.hub_x = hx;
+    }
+  }
   if (g.slots) {
     SlotParams<T> q;
     q.svals = static_cast<const T*>(m->slots.vals);
@@ -1590,6 +1668,7 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
     q.tile_y = p.tile_y;
     q.lane_desc = p.lane_desc;
     q.hub_cols = p.hub_cols;
+    q.hub_x = p.hub_x;
     q.carry_row = p.carry_row;
     q.carry_val = p.carry_val;
     q.g = g;
@@ -1624,8 +1703,8 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
   const unsigned fgrid = static_cast<unsigned>(fixup_blocks(g, PR));
-  fixup_kernel<T, PR><<<fgrid, 256, 0, ctx->stream>>>(p.carry_row, p.carry_val, g.num_ranges,
-                                                     g.n_rows, p.y, p.pr);
+  launch_pdl(!PR, fixup_kernel<T, PR>, fgrid, 256u, 0, ctx->stream, p.carry_row,
+             static_cast<const T*>(p.carry_val), g.num_ranges, g.n_rows, p.y, p.pr);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
 }
@@ -1697,8 +1776,11 @@ void launch_pr_loop_cond(mbx_context* ctx, cudaGraphConditionalHandle h, const i
 }
 
 size_t spmv_workspace_bytes(const Geometry& g, int precision, bool pagerank) {
+  // carry rows | carry values | the multiply's contiguous hub values
   const int64_t ne = 2 * g.num_ranges;
-  size_t b = ((ne * 4 + 255) / 256) * 256 + ((ne * value_size(precision) + 255) / 256) * 256;
+  const size_t vs = value_size(precision);
+  size_t b = ((ne * 4 + 255) / 256) * 256 + ((ne * vs + 255) / 256) * 256;
+  b += ((size_t(g.hub_count) * vs + 255) / 256) * 256;
   (void)pagerank;
   return b + 256;
 }

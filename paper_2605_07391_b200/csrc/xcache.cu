@@ -265,21 +265,19 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   MBX_CUDA(cudaMemcpyAsync(hc.data(), ccnt_sorted, size_t(cand) * 4, cudaMemcpyDeviceToHost, s));
   MBX_CUDA(cudaMemcpyAsync(hid.data(), cid_sorted, size_t(cand) * 4, cudaMemcpyDeviceToHost, s));
   MBX_CUDA(cudaStreamSynchronize(s));
+  // Each multiply gathers the hub values into a contiguous block once
+  // (hub_gather_kernel) and every CTA copies that block with coalesced
+  // loads: a hub costs ~1/32 of a request per CTA, so the table fills up to
+  // the shared-memory budget with every column referenced more than
+  // min_refs_shared times, under the same 2 %-of-a-CTA's-gathers line cap
+  // as a relabelled prefix.
   const int64_t cap_lines = m->nnz / (ctas * 50);
   const int line_shift = m->precision == MBX_F32 ? 5 : 4;  // entries per 128-byte line
-  std::vector<uint8_t> line_seen;
   int h = 0;
-  int64_t covered = 0, lines = 0;
+  int64_t covered = 0;
   while (h < cand) {
-    const int64_t line = int64_t(hid[h]) >> line_shift;
-    if (line_seen.size() <= size_t(line)) line_seen.resize(size_t(line) + 1, 0);
-    const bool fresh = !line_seen[size_t(line)];
-    if (int64_t(hc[h]) * S <= int64_t(fresh ? min_refs : min_refs_shared)) break;
-    if (fresh && lines + 1 > cap_lines) break;
-    if (fresh) {
-      line_seen[size_t(line)] = 1;
-      ++lines;
-    }
+    if (int64_t(hc[h]) * S <= int64_t(min_refs_shared)) break;
+    if ((h & ((1 << line_shift) - 1)) == 0 && (int64_t(h) >> line_shift) + 1 > cap_lines) break;
     covered += int64_t(hc[h++]) * S;
   }
   if (h > 0) {
