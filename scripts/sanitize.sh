@@ -7,11 +7,16 @@
 # Logs go to gpurun_out/sanitize_*.log; the summary line of each is printed.
 set -u
 mkdir -p gpurun_out
-CS="compute-sanitizer --error-exitcode 99 --print-limit 20"
+# 32 mbarriers per K2 CTA in the fp64 TMA staging mode: synccheck's default
+# tracking table overflows ("overflow of tracked cuda::barrier structures")
+CS="compute-sanitizer --error-exitcode 99 --print-limit 20 --num-cuda-barriers 64"
 SMOKE='import __graft_entry__ as g; g.smoke()'
 # synccheck runs the PageRank loop as an unrolled graph: inside a conditional
 # (WHILE) graph node it reports barrier divergence and aborts the same kernels
-# that are clean in eager and unrolled replays (a tool limitation, like ncu's)
+# that are clean in eager and unrolled replays -- a tool limitation, like
+# ncu's: scripts/debug/synccheck_while_repro.cu reproduces it with a textbook
+# block reduction (clean eagerly, "divergent thread(s) in warp" at its
+# __syncthreads as the body of a WHILE node; profiles/r2_sanitizers.md)
 for tool in memcheck racecheck synccheck initcheck; do
   mode=while; [ $tool = synccheck ] && mode=unrolled
   MBX_GRAPH_MODE=$mode timeout 900 $CS --tool $tool python -c "$SMOKE" > gpurun_out/sanitize_smoke_$tool.log 2>&1

@@ -23,8 +23,9 @@ def run(ctx, a, kind, x, sigma=0):
     tdt = torch.float64 if a.values.dtype == np.float64 else torch.float32
     xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
     yd = torch.full((max(a.n_rows, 1),), float("nan"), dtype=tdt, device="cuda")
+    torch.cuda.synchronize()  # torch's stream is done with x and y
     spmv_baseline_device(m, kind, xd.data_ptr(), yd.data_ptr(), sigma)
-    torch.cuda.synchronize()
+    ctx.synchronize()  # the library's stream is done with y
     return yd.cpu().numpy()[:a.n_rows]
 
 

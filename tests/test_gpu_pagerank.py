@@ -297,8 +297,9 @@ def test_plan_recaptures_after_matrix_buffers_change(ctx):
     plan.run()
     r1, h1 = plan.result(want_history=True)
     P.build_xcache()
-    mb.spmv_device(P, t2, c2, xd.data_ptr(), yd.data_ptr())
     torch.cuda.synchronize()
+    mb.spmv_device(P, t2, c2, xd.data_ptr(), yd.data_ptr())
+    ctx.synchronize()
     plan.run()
     r2, h2 = plan.result(want_history=True)
     assert np.array_equal(h1, h2) and r1.l1_residual == r2.l1_residual

@@ -100,7 +100,9 @@ def test_c5_stencil_64m_rows_exact_row_sums(ctx, dtype):
     n = A.n_rows
     x = torch.ones(n, dtype=tdt, device="cuda")
     y = torch.empty(n, dtype=tdt, device="cuda")
+    torch.cuda.synchronize()  # x is written before the library's stream reads it
     mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr())
+    ctx.synchronize()  # and y is complete before torch's stream reads it
     i = torch.arange(n, device="cuda", dtype=torch.int64)
     cnt = torch.ones(n, device="cuda", dtype=torch.int64)
     for v in ((i // (g * g)), (i // g) % g, i % g):
@@ -109,7 +111,9 @@ def test_c5_stencil_64m_rows_exact_row_sums(ctx, dtype):
     assert torch.equal(y, want)
     if dtype == np.float64:
         xc = i.to(torch.float64)
+        torch.cuda.synchronize()
         mb.spmv_device(A, t, c, xc.data_ptr(), y.data_ptr())
+        ctx.synchronize()
         # sum over in-grid neighbours of their index, by separability
         def axis_sum(v, stride):  # sum of (v + d) * stride over valid d, and count
             s = torch.zeros_like(v, dtype=torch.float64)
