@@ -1572,6 +1572,43 @@ __global__ void __launch_bounds__(256) csr_kernel(const uint32_t* __restrict__ r
   if (PR) pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, false);
 }
 
+template <typename T>
+__device__ __forceinline__ T add_rn(T a, T b);
+template <>
+__device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+
+// The PageRank yardstick (solvers.hpp:178-191): the reference runs it over
+// its CSR backend, whose spmv_csr_reference sums each row left to right in T
+// (reference.hpp:28-37).  One thread per row reproduces that order and
+// rounding exactly (products rounded, then added; no FMA contraction), so
+// pi* -- and with it ERR and the stop iteration -- equal the reference's.
+template <typename T>
+__global__ void __launch_bounds__(256) csr_rowserial_pr_kernel(
+    const uint32_t* __restrict__ ro, const int32_t* __restrict__ cols,
+    const T* __restrict__ vals, const T* __restrict__ x, T* __restrict__ y, int64_t n_rows,
+    PrArgs pr) {
+  PrAcc acc;
+  const T base = pr_base<T>(pr);
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    T s = T(0);
+    const uint32_t k1 = __ldg(ro + r + 1);
+    uint32_t k = __ldg(ro + r);
+    for (; k + 4 <= k1; k += 4) {  // loads run ahead of the dependent adds
+      T p[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) p[u] = mul_rn(__ldg(vals + k + u), __ldg(x + __ldg(cols + k + u)));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s = add_rn(s, p[u]);
+    }
+    for (; k < k1; ++k) s = add_rn(s, mul_rn(__ldg(vals + k), __ldg(x + __ldg(cols + k))));
+    pr_commit<T>(pr, base, r, s, y, acc);
+  }
+  pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, false);
+}
+
 // pi_0 (copy or uniform) and its dangling mass.
 template <typename T>
 __global__ void pr_init_kernel(const T* __restrict__ pi0, T* __restrict__ pi, int64_t n,
@@ -1935,7 +1972,16 @@ void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
     a.block_part = cta_part;
     a.done_counter = counter;
   }
-  if (m->precision == MBX_F32) {
+  if (pr) {  // the yardstick: row-serial sums in T, the reference's order
+    if (m->precision == MBX_F32)
+      csr_rowserial_pr_kernel<float><<<grid, 256, 0, ctx->stream>>>(
+          m->ro, m->cols, static_cast<const float*>(m->vals), static_cast<const float*>(x),
+          static_cast<float*>(y), m->n_rows, a);
+    else
+      csr_rowserial_pr_kernel<double><<<grid, 256, 0, ctx->stream>>>(
+          m->ro, m->cols, static_cast<const double*>(m->vals), static_cast<const double*>(x),
+          static_cast<double*>(y), m->n_rows, a);
+  } else if (m->precision == MBX_F32) {
     if (pr)
       csr_kernel<float, true><<<grid, 256, 0, ctx->stream>>>(
           m->ro, m->cols, static_cast<const float*>(m->vals), static_cast<const float*>(x),
@@ -1982,10 +2028,10 @@ void preload_pr_kernels(int precision) {
   cudaFuncAttributes a;
   if (precision == MBX_F32) {
     MBX_CUDA(cudaFuncGetAttributes(&a, pr_init_kernel<float>));
-    MBX_CUDA(cudaFuncGetAttributes(&a, csr_kernel<float, true>));
+    MBX_CUDA(cudaFuncGetAttributes(&a, csr_rowserial_pr_kernel<float>));
   } else {
     MBX_CUDA(cudaFuncGetAttributes(&a, pr_init_kernel<double>));
-    MBX_CUDA(cudaFuncGetAttributes(&a, csr_kernel<double, true>));
+    MBX_CUDA(cudaFuncGetAttributes(&a, csr_rowserial_pr_kernel<double>));
   }
 }
 
