@@ -549,7 +549,18 @@ def main():
         local_rows, local_nnz = n, m
         run = runner.run
         pre_ms = (relabel_s + tile.preprocess_seconds + xc_s + P.slot_info()[1]) * 1e3
+        # the CSR values / columns are not read by the loop: keep only the
+        # slot copy (rebuilt into CSR on demand)
+        resident_full = P.resident_bytes()
+        P.compact(tile)
+        footprint = {"csr_bytes": m * 8 + 4 * (n + 1),
+                     "resident_bytes_before_compact": resident_full,
+                     "resident_bytes": P.resident_bytes(),
+                     "tile_bytes": 4 * (2 * (tile.tile_num + 1) + tile.lane_num)}
+        footprint["resident_over_csr"] = footprint["resident_bytes"] / footprint["csr_bytes"]
+        footprint["resident_bytes_per_nnz"] = footprint["resident_bytes"] / m
     else:
+        footprint = None
         hub_cov = None  # the shard group builds its own hub tables
         if rank == 0 and not args.no_extras:
             # the one-GPU anchor of THIS matrix, timed on rank 0 before the
@@ -797,6 +808,7 @@ def main():
         "clocks": clocks,
         "cpu_baseline": cpu,
         "preprocess_ms": pre_ms,
+        "hbm_footprint": footprint,
         "relabel_ms": relabel_s * 1e3,
         "relabel_ms_repeat": relabel_warm_s * 1e3,
         "l1_residual_last": res.l1_residual,

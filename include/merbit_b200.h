@@ -252,6 +252,17 @@ MBX_API int mbx_matrix_build_xcache(mbx_context* ctx, mbx_matrix* m,
                                     int max_hubs, double* seconds);
 MBX_API int mbx_matrix_xcache_info(const mbx_matrix* m, int* hubs,
                                    double* coverage);
+/* Compact form: once the K2 slot copy for TILE t exists (an SpMV or a
+ * PageRank plan with t built it), free the CSR values and columns -- the slot
+ * copy holds every (value, column) -- keeping a private copy of t's arrays.
+ * Any later call that reads the CSR (download, relabel, row slices, the
+ * yardstick, comparators, another TILE's slot copy, plan creation) rebuilds
+ * it from the slot copy first.  Resident bytes drop from CSR + slots to
+ * about the slot copy alone. */
+MBX_API int mbx_matrix_compact(mbx_matrix* m, const mbx_tile* t);
+/* Device bytes the matrix holds now: CSR arrays, row offsets, slot copy, hub
+ * cache, vertex map, comparator state, a compact form's TILE copy. */
+MBX_API int mbx_matrix_resident_bytes(const mbx_matrix* m, int64_t* bytes);
 /* Frees the matrix's derived device copies -- the K2 slot copy, the x hub
  * cache and the COO comparator's row array -- keeping only the CSR.  Plans
  * over the matrix rebuild what they need before their next run. */

@@ -84,6 +84,7 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
     const bool slot_budget = ctx->tuning.layout == 1 && g.sigma == default_sigma(m->precision);
     if (slot_budget) g.hub_count = 0;
   }
+  if (!g.slots) ensure_csr(const_cast<mbx_context*>(ctx), m);  // staged / generic K2 read CSR
   if (!g.slots && g.hub_count > 0) ensure_cols_hub(const_cast<mbx_context*>(ctx), m);
   return g;
 }
@@ -555,6 +556,7 @@ MBX_API int mbx_matrix_download(const mbx_matrix* m, int64_t* ro, int32_t* cols,
   return guarded([&] {
     mbx_context* ctx = m->ctx;
     Device dg(ctx->device);
+    mbx::ensure_csr(ctx, m);  // a compacted matrix rebuilds its CSR
     if (ro) {
       std::vector<uint32_t> r(m->n_rows + 1);
       MBX_CUDA(cudaMemcpyAsync(r.data(), m->ro, (m->n_rows + 1) * 4, cudaMemcpyDeviceToHost,
@@ -574,6 +576,10 @@ MBX_API int mbx_matrix_download(const mbx_matrix* m, int64_t* ro, int32_t* cols,
 MBX_API int mbx_matrix_device_ptrs(const mbx_matrix* m, const void** values,
                                    const int32_t** cols, const uint32_t** ro) {
   return guarded([&] {
+    {
+      Device dg(m->ctx->device);
+      mbx::ensure_csr(m->ctx, m);
+    }
     if (values) *values = m->vals;
     if (cols) *cols = m->cols;
     if (ro) *ro = m->ro;
@@ -622,6 +628,7 @@ MBX_API int mbx_matrix_build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hub
                                     double* seconds) {
   return guarded([&] {
     Device dg(ctx->device);
+    mbx::ensure_csr(ctx, m);
     cudaEvent_t e0, e1;
     MBX_CUDA(cudaEventCreate(&e0));
     MBX_CUDA(cudaEventCreate(&e1));
@@ -652,10 +659,37 @@ MBX_API int mbx_matrix_xcache_ptrs(const mbx_matrix* m, const int32_t** cols_hub
   });
 }
 
+MBX_API int mbx_matrix_compact(mbx_matrix* m, const mbx_tile* t) {
+  return guarded([&] {
+    mbx_context* ctx = m->ctx;
+    Device dg(ctx->device);
+    if (t->ctx != ctx) fail(MBX_CONFIG_ERROR, "compact: TILE of another context");
+    mbx::compact_matrix(ctx, m, t);
+  });
+}
+
+MBX_API int mbx_matrix_resident_bytes(const mbx_matrix* m, int64_t* bytes) {
+  return guarded([&] {
+    const int64_t vs = int64_t(mbx::value_size(m->precision));
+    int64_t b = (m->n_rows + 1) * 4;
+    if (m->vals) b += m->nnz * vs;
+    if (m->cols) b += m->nnz * 4;
+    if (m->cols_hub) b += m->nnz * 4;
+    if (m->hub_cols) b += int64_t(m->hub_avail) * 4;
+    if (m->slots.vals) b += m->slots.count * (vs + 4);
+    if (m->coo_rows) b += m->nnz * 4;
+    if (m->vmap) b += m->n_rows * 4;
+    if (m->compact)
+      b += (2 * (m->compact->info.tile_num + 1) + m->compact->info.lane_num) * 4;
+    *bytes = b;
+  });
+}
+
 MBX_API int mbx_matrix_release_caches(mbx_matrix* m) {
   return guarded([&] {
     mbx_context* ctx = m->ctx;
     Device dg(ctx->device);
+    mbx::ensure_csr(ctx, m);  // the slot copy is a compacted matrix's only data
     mbx::free_slots(ctx, m);
     if (m->cols_hub || m->hub_cols) {
       dfree(ctx, m->cols_hub);
@@ -685,6 +719,7 @@ MBX_API int mbx_matrix_destroy(mbx_matrix* m) {
     dfree(ctx, m->cols_hub);
     dfree(ctx, m->hub_cols);
     mbx::free_slots(ctx, m);
+    mbx::free_compact_tile(ctx, m);
     mbx::free_sparse_state(ctx, m);
     dfree(ctx, m->coo_rows);
     dfree(ctx, m->vmap);
@@ -864,6 +899,7 @@ MBX_API int mbx_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
 MBX_API int mbx_spmv_csr_device(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y) {
   return guarded([&] {
     Device dg(ctx->device);
+    mbx::ensure_csr(ctx, m);
     mbx::launch_csr(ctx, m, x, y, nullptr, nullptr, nullptr);
   });
 }
@@ -1085,6 +1121,7 @@ MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, cons
     check_config(c);
     check_tile_matches(p, t, c);
     Device dg(ctx->device);
+    mbx::ensure_csr(ctx, p);  // the dangling mask reads the columns
     auto pl = std::make_unique<mbx_pagerank_plan>();
     pl->ctx = ctx;
     pl->p = p;

@@ -394,6 +394,7 @@ MBX_API int mbx_spmv_baseline_device(mbx_context* ctx, const mbx_matrix* m, int 
                                      const void* x, void* y) {
   return mbx::cguard([&] {
     mbx::DeviceGuard dg(ctx->device);
+    mbx::ensure_csr(ctx, m);
     if (kind == 0) {
       const int rc = mbx_spmv_csr_device(ctx, m, x, y);
       if (rc) mbx::fail(rc, mbx_last_error());

@@ -360,7 +360,7 @@ MBX_API int mbx_matrix_from_coo(mbx_context* ctx, int precision, const mbx_coo* 
       fail(MBX_CAPACITY_ERROR, "n_cols must be < 2^31 (int32 device column indices)");
     if (coo->nnz > 0 && (!coo->rows || !coo->cols || !coo->vals))
       fail(MBX_DIMENSION_ERROR, "null COO arrays");
-    MBX_CUDA(cudaSetDevice(ctx->device));
+    mbx::DeviceGuard dg(ctx->device);  // the caller's device is restored
     cudaStream_t s = ctx->stream;
     const int64_t n = coo->nnz, nr = coo->n_rows, nc = coo->n_cols;
     auto dm = [&](size_t b) {
@@ -477,12 +477,13 @@ MBX_API int mbx_matrix_from_coo(mbx_context* ctx, int precision, const mbx_coo* 
 MBX_API int mbx_matrix_build_transition(mbx_context* ctx, const mbx_matrix* a,
                                         mbx_matrix** out) {
   return mbx::iguard([&] {
+    mbx::DeviceGuard dg0(ctx->device);
+    mbx::ensure_csr(ctx, a);
     using mbx::fail;
     if (a->n_rows != a->n_cols)
       fail(MBX_DIMENSION_ERROR, "transition matrix needs a square adjacency (" +
                                     std::to_string(a->n_rows) + "x" + std::to_string(a->n_cols) +
                                     ")");
-    MBX_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     const int64_t n = a->n_rows, m = a->nnz;
     const size_t vs = mbx::value_size(a->precision);
@@ -551,8 +552,9 @@ MBX_API int mbx_matrix_build_transition(mbx_context* ctx, const mbx_matrix* a,
 MBX_API int mbx_matrix_degree_stats(mbx_context* ctx, const mbx_matrix* m, int sigma_threshold,
                                     mbx_degree_stats* out) {
   return mbx::iguard([&] {
+    mbx::DeviceGuard dg0(ctx->device);
+    mbx::ensure_csr(ctx, m);
     if (m->n_rows <= 0) mbx::fail(MBX_DIMENSION_ERROR, "degree stats of a matrix with no rows");
-    MBX_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     unsigned long long* d = nullptr;
     MBX_CUDA(cudaMallocAsync(&d, 16, s));
@@ -575,9 +577,10 @@ MBX_API int mbx_matrix_degree_stats(mbx_context* ctx, const mbx_matrix* m, int s
 MBX_API int mbx_matrix_relabel_by_degree(mbx_context* ctx, const mbx_matrix* a,
                                          mbx_matrix** out, int32_t* rank_host) {
   return mbx::iguard([&] {
+    mbx::DeviceGuard dg0(ctx->device);
+    mbx::ensure_csr(ctx, a);
     using mbx::fail;
     if (a->n_rows != a->n_cols) fail(MBX_DIMENSION_ERROR, "relabelling needs a square matrix");
-    MBX_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     const int64_t n = a->n_rows, m = a->nnz;
     const size_t vs = mbx::value_size(a->precision);

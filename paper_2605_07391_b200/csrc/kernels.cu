@@ -1254,6 +1254,57 @@ __global__ void build_slots_kernel(const T* __restrict__ vals, const int32_t* __
   }
 }
 
+// Inverse of build_slots_kernel: the CSR values / columns back from the
+// slot copy (hub references decoded through hub_cols).  A compacted matrix
+// (mbx_matrix_compact) keeps only the slot copy and rebuilds its CSR with
+// this on first use.
+template <typename T>
+__global__ void unslot_kernel(const T* __restrict__ svals, const int32_t* __restrict__ scols,
+                              const int32_t* __restrict__ hub_cols,
+                              const uint32_t* __restrict__ tile_x,
+                              const uint32_t* __restrict__ tile_y,
+                              const uint32_t* __restrict__ lane_desc, int64_t lane_num,
+                              int64_t num_chunks, int64_t total, int sigma, int ob,
+                              T* __restrict__ vals, int32_t* __restrict__ cols) {
+  constexpr int G = 8 / int(sizeof(T));
+  const uint32_t omask = (1u << ob) - 1u;
+  auto decode = [&](int32_t c) { return c < 0 ? __ldg(hub_cols + (c & 0x7FFFFFFF)) : c; };
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < num_chunks * 32;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = j >> 5;
+    const int l = static_cast<int>(j & 31);
+    const int64_t x0 = tile_x[c], x1 = tile_x[c + 1];
+    const int64_t sb = c * 32 * sigma + int64_t(l) * G;
+    if (tile_y[c] & kLongRowMask) {
+      for (int i = 0; i < sigma; ++i) {
+        const int64_t e = x0 + int64_t(i) * 32 + l;
+        const int64_t pos = sb + int64_t(i / G) * 32 * G + (i % G);
+        if (e < x1) {
+          vals[e] = svals[pos];
+          cols[e] = decode(scols[pos]);
+        }
+      }
+    } else {
+      uint32_t d = 0;
+      int steps = 0;
+      if (j < lane_num) {
+        d = lane_desc[j];
+        steps = static_cast<int>(imin64(sigma, total - j * sigma));
+      }
+      int64_t x = x0 + (d & omask);
+      const uint32_t fl = d >> (2 * ob);
+      for (int i = 0; i < steps; ++i) {
+        if (!((fl >> i) & 1u)) {
+          const int64_t pos = sb + int64_t(i / G) * 32 * G + (i % G);
+          vals[x] = svals[pos];
+          cols[x] = decode(scols[pos]);
+          ++x;
+        }
+      }
+    }
+  }
+}
+
 template <typename T, int SIGMA, bool PR, bool HUB>
 void launch_slot(mbx_context* ctx, const SlotParams<T>& p, size_t smem) {
   auto kern = p.g.prefetch == 2   ? spmv_slot_kernel<T, SIGMA, PR, HUB, 2>
@@ -1869,6 +1920,7 @@ bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, cons
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   MBX_CUDA(cudaStreamIsCapturing(ctx->stream, &cap));
   if (cap != cudaStreamCaptureStatusNone) return false;  // never build inside a capture
+  ensure_csr(ctx, m);  // a compacted matrix rebuilds its CSR from the old slots first
   free_slots(ctx, m);
   const int64_t count = g.num_chunks * 32 * g.sigma;
   const size_t vs = value_size(m->precision);
@@ -1907,6 +1959,81 @@ bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, cons
   sc.count = count;
   sc.seconds = ms * 1e-3;
   return true;
+}
+
+void compact_matrix(mbx_context* ctx, mbx_matrix* m, const mbx_tile* t) {
+  mbx_matrix::SlotCache& sc = m->slots;
+  if (!sc.vals || sc.tile_serial != t->serial)
+    fail(MBX_CONFIG_ERROR, "compact: the matrix holds no slot copy for this TILE (run an SpMV "
+                           "or create a PageRank plan with it first)");
+  if (!m->vals) return;  // already compact
+  cudaStream_t s = ctx->stream;
+  // a private copy of the TILE the slot copy follows (the caller may destroy
+  // its TILE handle); then the CSR values and columns go
+  const int64_t tn = t->info.tile_num, ln = t->info.lane_num;
+  auto* tc = new mbx_matrix::CompactTile;
+  tc->info = t->info;
+  tc->ob = t->offset_bits;
+  MBX_CUDA(cudaMallocAsync(&tc->tile_x, (tn + 1) * 4 + 256, s));
+  MBX_CUDA(cudaMallocAsync(&tc->tile_y, (tn + 1) * 4 + 256, s));
+  MBX_CUDA(cudaMallocAsync(&tc->lane_desc, ln * 4 + 256, s));
+  MBX_CUDA(cudaMemcpyAsync(tc->tile_x, t->tile_x, (tn + 1) * 4, cudaMemcpyDeviceToDevice, s));
+  MBX_CUDA(cudaMemcpyAsync(tc->tile_y, t->tile_y, (tn + 1) * 4, cudaMemcpyDeviceToDevice, s));
+  MBX_CUDA(cudaMemcpyAsync(tc->lane_desc, t->lane_desc, ln * 4, cudaMemcpyDeviceToDevice, s));
+  if (m->cols_hub) {  // derived from the CSR columns: rebuilt on demand
+    cudaFreeAsync(m->cols_hub, s);
+    m->cols_hub = nullptr;
+  }
+  cudaFreeAsync(m->vals, s);
+  cudaFreeAsync(m->cols, s);
+  m->vals = nullptr;
+  m->cols = nullptr;
+  m->compact = tc;
+  ++m->gen;  // graphs captured over a non-slot path would read the freed CSR
+  MBX_CUDA(cudaStreamSynchronize(s));
+}
+
+void ensure_csr(mbx_context* ctx, const mbx_matrix* m_) {
+  mbx_matrix* m = const_cast<mbx_matrix*>(m_);
+  if (m->vals || !m->compact) return;
+  mbx_matrix::CompactTile* tc = m->compact;
+  cudaStream_t s = ctx->stream;
+  const size_t vs = value_size(m->precision);
+  void* vals = nullptr;
+  int32_t* cols = nullptr;
+  MBX_CUDA(cudaMallocAsync(&vals, m->nnz * vs + 256, s));
+  MBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cols), m->nnz * 4 + 256, s));
+  const int64_t chunks = (tc->info.lane_num + 31) / 32;
+  const int64_t total = m->nnz + m->n_rows;
+  const unsigned grid = grid_for(chunks * 32, 256, int64_t(ctx->sm_count) * 16);
+  if (chunks > 0) {
+    if (m->precision == MBX_F32)
+      unslot_kernel<float><<<grid, 256, 0, s>>>(
+          static_cast<const float*>(m->slots.vals), m->slots.cols, m->hub_cols, tc->tile_x,
+          tc->tile_y, tc->lane_desc, tc->info.lane_num, chunks, total, tc->info.sigma, tc->ob,
+          static_cast<float*>(vals), cols);
+    else
+      unslot_kernel<double><<<grid, 256, 0, s>>>(
+          static_cast<const double*>(m->slots.vals), m->slots.cols, m->hub_cols, tc->tile_x,
+          tc->tile_y, tc->lane_desc, tc->info.lane_num, chunks, total, tc->info.sigma, tc->ob,
+          static_cast<double*>(vals), cols);
+    ++ctx->launches;
+    MBX_CUDA(cudaGetLastError());
+  }
+  m->vals = vals;
+  m->cols = cols;
+  free_compact_tile(ctx, m);
+  MBX_CUDA(cudaStreamSynchronize(s));
+}
+
+void free_compact_tile(mbx_context* ctx, const mbx_matrix* m_) {
+  mbx_matrix* m = const_cast<mbx_matrix*>(m_);
+  if (!m->compact) return;
+  cudaFreeAsync(m->compact->tile_x, ctx->stream);
+  cudaFreeAsync(m->compact->tile_y, ctx->stream);
+  cudaFreeAsync(m->compact->lane_desc, ctx->stream);
+  delete m->compact;
+  m->compact = nullptr;
 }
 
 void launch_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, const Geometry& g,
@@ -1965,6 +2092,7 @@ int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m) {
 void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
                 const PrArgs* pr, double* cta_part, unsigned int* counter) {
   if (m->n_rows == 0) return;
+  ensure_csr(ctx, m);
   const unsigned grid = static_cast<unsigned>(csr_pr_blocks(ctx, m));
   PrArgs a;
   if (pr) {

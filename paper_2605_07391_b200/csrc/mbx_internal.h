@@ -190,6 +190,16 @@ struct mbx_matrix_s {
   // cuSPARSE comparator state (comparators.cu): descriptors + work buffer
   // per algorithm, built on first use
   mutable mbx::SparseState* sparse[4] = {nullptr, nullptr, nullptr, nullptr};
+  // mbx_matrix_compact: the CSR values / columns were freed; the slot copy
+  // and this private copy of its TILE rebuild them on first use (ensure_csr)
+  struct CompactTile {
+    mbx_tile_info info{};
+    int ob = 0;
+    uint32_t* tile_x = nullptr;
+    uint32_t* tile_y = nullptr;
+    uint32_t* lane_desc = nullptr;
+  };
+  CompactTile* compact = nullptr;
   // Set on a matrix made by mbx_matrix_relabel_by_degree: vertex v of the
   // original graph is vertex vmap[v] here.  Host-facing PageRank I/O
   // (pi0 in, pi / yardstick out) stays in the ORIGINAL vertex order.
@@ -225,6 +235,11 @@ void ensure_cols_hub(mbx_context* ctx, const mbx_matrix* m);
 // layout does not apply (then K2 uses the staged CSR order)
 bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, const Geometry& g);
 void free_slots(mbx_context* ctx, const mbx_matrix* m);
+// compacted matrices (mbx_matrix_compact): drop the CSR values / columns,
+// rebuild them from the slot copy on first use
+void compact_matrix(mbx_context* ctx, mbx_matrix* m, const mbx_tile* t);
+void ensure_csr(mbx_context* ctx, const mbx_matrix* m);
+void free_compact_tile(mbx_context* ctx, const mbx_matrix* m);
 int default_sigma(int precision);
 // Tuning::prefetch with -1 (auto) resolved for a precision
 int resolve_prefetch(int tuning, int precision);

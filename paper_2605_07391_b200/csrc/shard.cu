@@ -934,6 +934,7 @@ MBX_API int mbx_matrix_row_slice(mbx_context* ctx, const mbx_matrix* m, int64_t 
                                  mbx_matrix** out) {
   return sguard([&] {
     mbx::DeviceGuard dg(ctx->device);
+    mbx::ensure_csr(ctx, m);
     if (r0 < 0 || r1 < r0 || r1 > m->n_rows) mbx::fail(MBX_DIMENSION_ERROR, "row slice out of range");
     uint32_t b[2];
     MBX_CUDA(cudaMemcpyAsync(&b[0], m->ro + r0, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -974,6 +975,7 @@ MBX_API int mbx_shard_group_create(mbx_context* ctx, int64_t n_global, int world
                                    const void* nccl_id, mbx_shard_group** out) {
   return sguard([&] {
     mbx::DeviceGuard dg(ctx->device);
+    for (int i = 0; i < nlocal; ++i) mbx::ensure_csr(ctx, mats[i]);
     if (!nccl_id && nlocal != world)
       mbx::fail(MBX_CONFIG_ERROR, "shard group: without NCCL every shard must be local");
     if (nccl_id && nlocal != 1)
@@ -1005,6 +1007,7 @@ MBX_API int mbx_shard_group_create_peer(mbx_context* ctx, int64_t n_global, int 
                                         const mbx_pagerank_config* cfg, mbx_shard_group** out) {
   return sguard([&] {
     mbx::DeviceGuard dg(ctx->device);
+    mbx::ensure_csr(ctx, local);
     if (world < 1 || world > 8)
       mbx::fail(MBX_CONFIG_ERROR, "peer shard group: world must be in [1, 8]");
     GroupPtr G(new mbx_shard_group_s);

@@ -335,6 +335,16 @@ class DeviceMatrix:
         _check(_lib.lib().mbx_matrix_download(self.h, _ptr(ro), None, None))
         return ro
 
+    def compact(self, tile: "Tile"):
+        """Free the CSR values / columns once the slot copy for `tile`
+        exists; they are rebuilt from it when a later call needs them."""
+        _check(_lib.lib().mbx_matrix_compact(self.h, tile.h))
+
+    def resident_bytes(self) -> int:
+        b = C.c_int64()
+        _check(_lib.lib().mbx_matrix_resident_bytes(self.h, C.byref(b)))
+        return b.value
+
     def release_caches(self):
         """Free the slot copy, x hub cache and COO rows (CSR kept)."""
         _check(_lib.lib().mbx_matrix_release_caches(self.h))
