@@ -681,6 +681,7 @@ MBX_API int mbx_matrix_resident_bytes(const mbx_matrix* m, int64_t* bytes) {
     if (m->vmap) b += m->n_rows * 4;
     if (m->compact)
       b += (2 * (m->compact->info.tile_num + 1) + m->compact->info.lane_num) * 4;
+    if (m->dmask) b += ((m->n_cols + 31) / 32) * 4;
     *bytes = b;
   });
 }
@@ -720,6 +721,7 @@ MBX_API int mbx_matrix_destroy(mbx_matrix* m) {
     dfree(ctx, m->hub_cols);
     mbx::free_slots(ctx, m);
     mbx::free_compact_tile(ctx, m);
+    dfree(ctx, m->dmask);
     mbx::free_sparse_state(ctx, m);
     dfree(ctx, m->coo_rows);
     dfree(ctx, m->vmap);
@@ -1121,7 +1123,6 @@ MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, cons
     check_config(c);
     check_tile_matches(p, t, c);
     Device dg(ctx->device);
-    mbx::ensure_csr(ctx, p);  // the dangling mask reads the columns
     auto pl = std::make_unique<mbx_pagerank_plan>();
     pl->ctx = ctx;
     pl->p = p;

@@ -2182,9 +2182,18 @@ void launch_pr_init(mbx_context* ctx, int precision, int64_t n, const void* pi0,
   MBX_CUDA(cudaGetLastError());
 }
 
-void launch_dangling_mask(mbx_context* ctx, const mbx_matrix* m, uint32_t* mask) {
+void launch_dangling_mask(mbx_context* ctx, const mbx_matrix* m_, uint32_t* mask) {
+  mbx_matrix* m = const_cast<mbx_matrix*>(m_);
   const int64_t words = (m->n_cols + 31) / 32;
-  MBX_CUDA(cudaMemsetAsync(mask, 0, size_t(words > 0 ? words : 1) * 4, ctx->stream));
+  const size_t bytes = size_t(words > 0 ? words : 1) * 4;
+  // the empty columns depend on the pattern alone: computed once per matrix
+  // (a compacted matrix then needs no CSR for later PageRank plans)
+  if (m->dmask) {
+    MBX_CUDA(cudaMemcpyAsync(mask, m->dmask, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    return;
+  }
+  ensure_csr(ctx, m);
+  MBX_CUDA(cudaMemsetAsync(mask, 0, bytes, ctx->stream));
   if (m->nnz > 0) {
     seen_columns_kernel<<<grid_for(m->nnz, 256), 256, 0, ctx->stream>>>(m->cols, m->nnz, mask);
     ++ctx->launches;
@@ -2195,6 +2204,8 @@ void launch_dangling_mask(mbx_context* ctx, const mbx_matrix* m, uint32_t* mask)
     ++ctx->launches;
   }
   MBX_CUDA(cudaGetLastError());
+  MBX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&m->dmask), bytes + 64, ctx->stream));
+  MBX_CUDA(cudaMemcpyAsync(m->dmask, mask, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
 }
 
 template <typename T>

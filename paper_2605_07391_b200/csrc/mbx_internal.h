@@ -200,6 +200,8 @@ struct mbx_matrix_s {
     uint32_t* lane_desc = nullptr;
   };
   CompactTile* compact = nullptr;
+  // dangling-column bitmask (empty columns), cached by the first PageRank plan
+  mutable uint32_t* dmask = nullptr;
   // Set on a matrix made by mbx_matrix_relabel_by_degree: vertex v of the
   // original graph is vertex vmap[v] here.  Host-facing PageRank I/O
   // (pi0 in, pi / yardstick out) stays in the ORIGINAL vertex order.
