@@ -311,19 +311,22 @@ def test_plan_recaptures_after_matrix_buffers_change(ctx):
 @pytest.mark.skipif(O.ref() is None, reason="oracle/_ref not built")
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_default_config_stop_iteration_matches_reference(ctx, dtype):
-    """PageRankConfig() defaults (err_tol 1e-10, 210 yardstick iterations):
-    the yardstick sums each row left to right in T like spmv_csr_reference
-    (reference.hpp:28-37); its base term uses the fp64 dangling mass where
-    rank_update (solvers.hpp:104-109) sums in T sequentially, so pi* may
-    differ in the last bits.  The stop iteration and the iterate agree with
-    the compiled reference's pagerank<T> over its CSR backend anyway."""
+    """PageRankConfig() defaults (err_tol 1e-10, 210 yardstick iterations)
+    against the compiled reference's pagerank<T> over its own MerbitBackend
+    (the backend this library replaces): the same stop decision at the same
+    iteration -- fp64 converges (17 / 34 iterations here), fp32 runs to
+    max_iters in both, because MERBIT's summation order and the CSR
+    yardstick's round differently, leaving ERR ~1e-7 -- and the final
+    iterates agree.  The yardstick sums each row left to right in T like
+    spmv_csr_reference (reference.hpp:28-37); its base term uses the fp64
+    dangling mass where rank_update (solvers.hpp:104-109) sums in T."""
     for adj in (O.ring_with_chords(100, 260, 42), O.rmat(10, 16, 3)):
         p = O.build_transition(adj, dtype)
         r = mb.pagerank(p, mb.PageRankConfig(), backend(ctx, p))
-        want = O.ref().pagerank_csr(p, 0.85, 1e-10, 210, 210)
-        assert r.status == want["status"] and r.iterations == want["iterations"]
-        star = want["reference_pi"]
-        if star is not None:  # fp64: the yardstick itself
-            assert np.abs(r.reference_pi - star).max() <= 1e-15 * np.abs(star).max()
+        eng = O.RefEngine(p, 32, 14 if dtype == np.float32 else 7, 128, 4)
+        want = eng.pagerank(0.85, 1e-10, 210, 210, want_pi=True)
+        eng.close()
+        assert r.iterations == want["iterations"]
+        assert (r.status == "converged") == (want["iterations"] < 210)
         tol = 1e-12 if dtype == np.float64 else 1e-6
         assert np.abs(r.pi.astype(np.float64) - want["pi"].astype(np.float64)).sum() <= tol
