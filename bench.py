@@ -225,10 +225,14 @@ def run_reference(args):
                           "unavailable": "oracle/_ref/libmerbit_ref.so not built"}))
         return 0
     nthreads = os.cpu_count() or 1
+    # the same matrix as our arm: scale 24 (C2) at N = 1, 27 (C4) at N > 1
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    args.scale = args.scale if args.scale is not None else (24 if world == 1 else 27)
     t0 = time.perf_counter()
     p = O.rmat(args.scale, 16, 1, transposed=True, nthreads=nthreads)
     gen = time.perf_counter() - t0
-    iters = args.ref_iters_per_step
+    # a bounded sample per step: 2 iterations at scale 24, 1 at 27 (~2 s)
+    iters = args.ref_iters_per_step if args.ref_iters_per_step else (2 if args.scale <= 25 else 1)
     r = cpu_reference_pagerank(p.row_offsets, p.col_indices, p.n_rows, iters, args.steps,
                                args.warmup, nthreads)
     v = r["value"]
@@ -407,7 +411,9 @@ def main():
                     help="R-MAT scale (default: 24 = C2 at N = 1, 27 = C4 at N > 1)")
     ap.add_argument("--iters", type=int, default=100, help="PageRank iterations per step")
     ap.add_argument("--block-size", type=int, default=128)
-    ap.add_argument("--ref-iters-per-step", type=int, default=2)
+    ap.add_argument("--ref-iters-per-step", type=int, default=0,
+                    help="reference arm: PageRank iterations per step (0: 2 below scale 26, "
+                         "else 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the extras (N = 1: SpMV f32/f64, C1, C3, C5, C4 on one GPU; "

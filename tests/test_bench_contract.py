@@ -71,3 +71,14 @@ def test_reference_arm_under_torchrun_prints_once():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0
+
+
+def test_reference_arm_default_is_the_device_arms_config():
+    """`bench.py --impl reference` exactly as the driver runs it (no --scale):
+    the same matrix as the device arm's N = 1 line, R-MAT scale 24 (C2)."""
+    import oracle as O
+    if O.ref() is None:
+        pytest.skip("oracle/_ref not built")
+    d = run_bench(["--impl", "reference", "--steps", "1", "--warmup", "0"], timeout=900)
+    assert d["config"]["scale"] == 24 and d["config"]["n"] == 1 << 24
+    assert d["value"] > 0 and d["impl"] == "reference"
