@@ -185,7 +185,8 @@ MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta,
 /* Shared-memory budget per SM for K2 (bytes; the rest is L1) and how K2
  * stages the next tile: 0 nothing, 1 L2 prefetch of its streams, 2 TMA bulk
  * copy of its column slots + descriptors into shared memory (slot layout),
- * -1 auto (2 for fp64, 0 for fp32).  Defaults 131072 / -1. */
+ * -1 auto (2 for fp64, 0 for fp32).  smem_per_sm -1: 160 KB for fp32, 128 KB
+ * for fp64.  Defaults -1 / -1. */
 MBX_API int mbx_context_set_tuning_ex(mbx_context* ctx, int smem_per_sm,
                                       int prefetch);
 /* K2 data layout: 1 (default) = lane-major slot copy of the matrix, built

@@ -1853,8 +1853,10 @@ int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, in
                                   ctx->device));
   MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const int64_t reserve = 1024;  // per-CTA system reservation
-  if (ctx->tuning.smem_per_sm > 0 && ctx->tuning.smem_per_sm < per_sm)
-    per_sm = ctx->tuning.smem_per_sm;
+  const int budget = ctx->tuning.smem_per_sm > 0 ? ctx->tuning.smem_per_sm
+                     : precision == MBX_F32       ? 160 * 1024
+                                                  : 128 * 1024;
+  if (budget < per_sm) per_sm = budget;
   int64_t per_cta = per_sm / ctas_per_sm - reserve;
   if (per_cta > optin) per_cta = optin;
   const int64_t vs = int64_t(value_size(precision));

@@ -57,7 +57,10 @@ struct Tuning {
   // Shared memory K2 may take per SM.  The rest stays L1, which also stages
   // every in-flight miss: a hub table that squeezes L1 below ~80 KB starves
   // memory-level parallelism (measured, profiles/).
-  int smem_per_sm = 128 * 1024;
+  // -1 (default): 160 KB for fp32, 128 KB for fp64 (measured at R-MAT s24:
+  // fp32 PageRank 830 -> 790 us / iteration with 38.6 K instead of 30.5 K hubs;
+  // fp64 slower above 128 KB, its TMA staging areas already take 33 KB)
+  int smem_per_sm = -1;
   // K2 staging of the next tile: 0 none, 1 L2 prefetch of its value/column
   // lines (measured: costs request-port slots), 2 TMA bulk copy of its column
   // slots + descriptors into shared memory (slot layout; measured: fp64 -9 %,

@@ -215,7 +215,7 @@ class Context:
         _check(_lib.lib().mbx_context_set_tuning(self.h, warps_per_cta, ctas_per_sm, max_hubs))
         if smem_per_sm is not None or prefetch is not None:
             _check(_lib.lib().mbx_context_set_tuning_ex(
-                self.h, 131072 if smem_per_sm is None else smem_per_sm,
+                self.h, -1 if smem_per_sm is None else smem_per_sm,
                 -1 if prefetch is None else prefetch))
 
     def set_layout(self, layout: int):

@@ -27,8 +27,8 @@ ctx.set_stream(s.cuda_stream)
 if os.environ.get("SMEM") or os.environ.get("MODE"):
     # K2 shared-memory budget per SM and staging mode (0 LDG, 1 L2 prefetch,
     # 2 TMA bulk staging of the next tile's columns + descriptors)
-    ctx.set_tuning(32, 1, -1, smem_per_sm=int(os.environ.get("SMEM", 131072)),
-                   prefetch=int(os.environ.get("MODE", 0)))
+    ctx.set_tuning(32, 1, -1, smem_per_sm=int(os.environ.get("SMEM", -1)),
+                   prefetch=int(os.environ.get("MODE", -1)))
 P = mb.DeviceMatrix.rmat(ctx, scale, 16, seed=1, transition=True, dtype=np.float32)
 if not natural:
     P, _ = P.relabel_by_degree(want_rank=False)

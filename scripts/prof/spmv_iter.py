@@ -20,8 +20,8 @@ s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 ctx.set_stream(s.cuda_stream)
 if os.environ.get("SMEM") or os.environ.get("MODE"):
-    ctx.set_tuning(32, 1, -1, smem_per_sm=int(os.environ.get("SMEM", 131072)),
-                   prefetch=int(os.environ.get("MODE", 0)))
+    ctx.set_tuning(32, 1, -1, smem_per_sm=int(os.environ.get("SMEM", -1)),
+                   prefetch=int(os.environ.get("MODE", -1)))
 A = mb.DeviceMatrix.rmat(ctx, scale, 16, seed=1, transition=bool(trans), dtype=dt)
 if relabel:
     A, _ = A.relabel_by_degree(want_rank=False)
