@@ -313,6 +313,19 @@ MBX_API int mbx_spmv_device(mbx_context* ctx, const mbx_matrix* m,
  * kernel's own predicate). */
 MBX_API int mbx_spmv_trace_counts(mbx_context* ctx, const mbx_tile* t,
                                   mbx_spmv_trace* trace);
+/* SpmvTrace::deposits (merbit_spmv.hpp:21-28, 339-349): the (row, partial
+ * sum) contributions the MERBIT decomposition forms for y = A x -- per lane,
+ * one at each Down step and one for the row it leaves open; per lane of a
+ * long-row tile, its lane-strided subtotal.  Per-row totals reproduce y up to
+ * regrouping (the conservation property tests/test_kernel.cpp:136-158
+ * checks).  rows_host / amounts_host NULL: *count = the capacity that always
+ * suffices.  Otherwise at most `capacity` pairs are written (unordered) and
+ * *count is the total; rows in the caller's vertex order (the terminal row
+ * n_rows may appear, as in the reference). */
+MBX_API int mbx_spmv_deposits(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                              const mbx_simt_config* c, const void* x_host,
+                              int64_t* rows_host, void* amounts_host, int64_t capacity,
+                              int64_t* count);
 /* Plain row-parallel CSR SpMV on the device (the yardstick kernel of
  * pagerank, solvers.hpp:178-191, and a non-MERBIT comparator). */
 MBX_API int mbx_spmv_csr_device(mbx_context* ctx, const mbx_matrix* m,

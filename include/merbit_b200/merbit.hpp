@@ -285,15 +285,22 @@ class DualBuffer {
   int parity_ = 0;
 };
 
-struct SpmvTrace {  // merbit_spmv.hpp:21-28 (no deposit log on the device)
+// merbit_spmv.hpp:21-28: routing counters and, with collect_deposits, the
+// (row, partial) contributions of the decomposition (mbx_spmv_deposits;
+// unordered, rows in the caller's vertex order)
+template <typename T = double>
+struct SpmvTraceT {
+  bool collect_deposits = false;
   std::int64_t fast_tiles = 0, normal_tiles = 0, skipped_tiles = 0;
+  std::vector<std::pair<index_t, T>> deposits;
 };
+using SpmvTrace = SpmvTraceT<double>;
 
 // spmv_merbit (merbit_spmv.hpp:136-352): out.active() = A x on the GPU,
 // companion zeroed, parity flipped.
-template <typename T>
+template <typename T, typename TT = double>
 void spmv_merbit(const DeviceCsr<T>& a, const DeviceTile& t, const SimtConfig& c,
-                 std::span<const T> x, DualBuffer<T>& out, SpmvTrace* trace = nullptr) {
+                 std::span<const T> x, DualBuffer<T>& out, SpmvTraceT<TT>* trace = nullptr) {
   if (static_cast<index_t>(x.size()) != a.n_cols())
     throw dimension_error("spmv: x has " + std::to_string(x.size()) + " entries, matrix has " +
                           std::to_string(a.n_cols()) + " columns");
@@ -310,6 +317,18 @@ void spmv_merbit(const DeviceCsr<T>& a, const DeviceTile& t, const SimtConfig& c
     trace->fast_tiles += tr.fast_tiles;
     trace->normal_tiles += tr.normal_tiles;
     trace->skipped_tiles += tr.skipped_tiles;
+    if (trace->collect_deposits) {
+      std::int64_t cap = 0, got = 0;
+      check(mbx_spmv_deposits(a.context().get(), a.get(), t.get(), &cc, nullptr, nullptr,
+                              nullptr, 0, &cap));
+      std::vector<std::int64_t> rows(static_cast<std::size_t>(cap > 0 ? cap : 1));
+      std::vector<T> amounts(rows.size());
+      check(mbx_spmv_deposits(a.context().get(), a.get(), t.get(), &cc, x.data(), rows.data(),
+                              amounts.data(), cap, &got));
+      for (std::int64_t k = 0; k < got && k < cap; ++k)
+        trace->deposits.emplace_back(static_cast<index_t>(rows[static_cast<std::size_t>(k)]),
+                                     static_cast<TT>(amounts[static_cast<std::size_t>(k)]));
+    }
   }
 }
 

@@ -136,6 +136,8 @@ SIGNATURES = {
     "mbx_matrix_destroy": ([VP], C.c_int),
     "mbx_matrix_release_caches": ([VP], C.c_int),
     "mbx_matrix_compact": ([VP, VP], C.c_int),
+    "mbx_spmv_deposits": ([VP, VP, VP, C.POINTER(mbx_simt_config), VP, VP, VP, C.c_int64,
+                           C.POINTER(C.c_int64)], C.c_int),
     "mbx_matrix_resident_bytes": ([VP, C.POINTER(C.c_int64)], C.c_int),
     "mbx_generate_tile": ([VP, VP, C.c_int64, C.c_int64, C.POINTER(mbx_simt_config),
                            C.POINTER(VP)], C.c_int),

@@ -898,6 +898,65 @@ MBX_API int mbx_spmv(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
   });
 }
 
+MBX_API int mbx_spmv_deposits(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
+                              const mbx_simt_config* c, const void* x_host, int64_t* rows_host,
+                              void* amounts_host, int64_t capacity, int64_t* count) {
+  return guarded([&] {
+    check_config(c);
+    check_tile_matches(m, t, c);
+    Device dg(ctx->device);
+    const size_t vs = mbx::value_size(m->precision);
+    const int64_t lanes = t->info.lane_num;
+    // a lane deposits at most once per step plus its trailing partial
+    const int64_t bound = lanes * (int64_t(t->info.sigma) + 1);
+    if (!rows_host || !amounts_host) {  // capacity query
+      *count = bound;
+      return;
+    }
+    void* x = dmalloc(ctx, m->n_cols * vs + 256);
+    void* tmp = m->vmap ? dmalloc(ctx, m->n_cols * vs + 256) : nullptr;
+    if (m->n_cols)
+      MBX_CUDA(cudaMemcpyAsync(m->vmap ? tmp : x, x_host, m->n_cols * vs, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    if (m->vmap) mbx::launch_vertex_map(ctx, m->precision, m->n_cols, m->vmap, tmp, x, true);
+    const int64_t cap = std::min(capacity, bound);
+    auto* counter = static_cast<unsigned long long*>(dmalloc(ctx, 64));
+    int64_t* rows = static_cast<int64_t*>(dmalloc(ctx, cap * 8 + 256));
+    void* amounts = dmalloc(ctx, cap * vs + 256);
+    MBX_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
+    mbx::launch_deposits(ctx, m, t, x, counter, cap, rows, amounts);
+    unsigned long long n = 0;
+    MBX_CUDA(cudaMemcpyAsync(&n, counter, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int64_t got = std::min<int64_t>(int64_t(n), cap);
+    if (got) {
+      MBX_CUDA(cudaMemcpyAsync(rows_host, rows, got * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      MBX_CUDA(cudaMemcpyAsync(amounts_host, amounts, got * vs, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    }
+    std::vector<int32_t> vmap;
+    if (m->vmap && got) {  // rows back to the caller's vertex numbering
+      vmap.resize(size_t(m->n_rows));
+      MBX_CUDA(cudaMemcpyAsync(vmap.data(), m->vmap, m->n_rows * 4, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    }
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (!vmap.empty()) {
+      std::vector<int64_t> orig(size_t(m->n_rows));
+      for (int64_t v = 0; v < m->n_rows; ++v) orig[size_t(vmap[size_t(v)])] = v;
+      for (int64_t k = 0; k < got; ++k)
+        if (rows_host[k] < m->n_rows) rows_host[k] = orig[size_t(rows_host[k])];
+    }
+    *count = int64_t(n);
+    dfree(ctx, x);
+    dfree(ctx, tmp);
+    dfree(ctx, counter);
+    dfree(ctx, rows);
+    dfree(ctx, amounts);
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 MBX_API int mbx_spmv_csr_device(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y) {
   return guarded([&] {
     Device dg(ctx->device);

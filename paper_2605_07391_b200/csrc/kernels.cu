@@ -1660,6 +1660,88 @@ __global__ void __launch_bounds__(256) csr_rowserial_pr_kernel(
   pr_block_finish(acc, pr, pr.block_part, pr.done_counter, pr.next, false);
 }
 
+// SpmvTrace deposit log (merbit_spmv.hpp:21-28, 339-349): every partial row
+// sum the MERBIT decomposition forms, one thread per lane -- a normal lane
+// deposits at each Down step the partial of the row it closes and, after its
+// last step, the partial of the row it leaves open (the segmented sum and the
+// carries only regroup these); a lane of a marked (long-row) tile deposits
+// its lane-strided subtotal (fast_tile_reduce).  Every staged product lands
+// in exactly one deposit, so per-row totals reproduce y up to regrouping.
+template <typename T>
+__global__ void deposit_kernel(const T* __restrict__ vals, const int32_t* __restrict__ cols,
+                               const T* __restrict__ x, const uint32_t* __restrict__ tile_x,
+                               const uint32_t* __restrict__ tile_y,
+                               const uint32_t* __restrict__ lane_desc, int64_t lane_num,
+                               int64_t total, int omega, int sigma, int ob,
+                               unsigned long long* counter, int64_t capacity,
+                               int64_t* __restrict__ rows, T* __restrict__ amounts) {
+  const uint32_t omask = (1u << ob) - 1u;
+  auto deposit = [&](int64_t row, T v) {
+    const unsigned long long k = atomicAdd(counter, 1ull);
+    if (int64_t(k) < capacity) {
+      rows[k] = row;
+      amounts[k] = v;
+    }
+  };
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < lane_num;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t tile = j / omega;
+    const int l = int(j % omega);
+    const uint32_t ty = tile_y[tile];
+    const int64_t x0 = tile_x[tile], y0 = ty & ~kLongRowMask;
+    if (ty & kLongRowMask) {
+      const int64_t x1 = tile_x[tile + 1];
+      if (x0 + l >= x1) continue;
+      T s = T(0);
+      for (int64_t e = x0 + l; e < x1; e += omega) s = add_rn(s, mul_rn(vals[e], x[cols[e]]));
+      deposit(y0, s);
+      continue;
+    }
+    const uint32_t d = lane_desc[j];
+    const int steps = int(imin64(sigma, total - j * sigma));
+    int64_t xx = x0 + (d & omask), yy = y0 + ((d >> ob) & omask);
+    const uint32_t fl = d >> (2 * ob);
+    T sum = T(0);
+    for (int k = 0; k < steps; ++k) {
+      if ((fl >> k) & 1u) {
+        deposit(yy, sum);
+        sum = T(0);
+        ++yy;
+      } else {
+        sum = add_rn(sum, mul_rn(vals[xx], x[cols[xx]]));
+        ++xx;
+      }
+    }
+    if (steps > 0) deposit(yy, sum);
+  }
+}
+
+}  // namespace
+
+void launch_deposits(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, const void* x,
+                     unsigned long long* counter, int64_t capacity, int64_t* rows,
+                     void* amounts) {
+  ensure_csr(ctx, m);
+  const int64_t lanes = t->info.lane_num;
+  if (lanes == 0) return;
+  const unsigned grid = unsigned(imin64((lanes + 255) / 256, int64_t(ctx->sm_count) * 16));
+  const int64_t total = m->nnz + m->n_rows;
+  if (m->precision == MBX_F32)
+    deposit_kernel<float><<<grid, 256, 0, ctx->stream>>>(
+        static_cast<const float*>(m->vals), m->cols, static_cast<const float*>(x), t->tile_x,
+        t->tile_y, t->lane_desc, lanes, total, t->info.omega, t->info.sigma, t->offset_bits,
+        counter, capacity, rows, static_cast<float*>(amounts));
+  else
+    deposit_kernel<double><<<grid, 256, 0, ctx->stream>>>(
+        static_cast<const double*>(m->vals), m->cols, static_cast<const double*>(x), t->tile_x,
+        t->tile_y, t->lane_desc, lanes, total, t->info.omega, t->info.sigma, t->offset_bits,
+        counter, capacity, rows, static_cast<double*>(amounts));
+  ++ctx->launches;
+  MBX_CUDA(cudaGetLastError());
+}
+
+namespace {
+
 // pi_0 (copy or uniform) and its dangling mass.
 template <typename T>
 __global__ void pr_init_kernel(const T* __restrict__ pi0, T* __restrict__ pi, int64_t n,

@@ -267,6 +267,11 @@ void launch_csr(mbx_context* ctx, const mbx_matrix* m, const void* x, void* y,
                 const PrArgs* pr, double* cta_part, unsigned int* counter);
 int csr_pr_blocks(mbx_context* ctx, const mbx_matrix* m);
 void preload_pr_kernels(int precision);
+// SpmvTrace deposits of y = A x (x on the device): (row, partial) pairs via
+// an atomic counter; at most `capacity` are written, *counter counts all
+void launch_deposits(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, const void* x,
+                     unsigned long long* counter, int64_t capacity, int64_t* rows,
+                     void* amounts);
 // First row of the dangling set when it is a suffix [f, n) of the rows
 // (f = n when empty), else -1: one host pass over the bitmask (preprocessing).
 int64_t dangling_suffix_start(mbx_context* ctx, const uint32_t* mask_dev, int64_t n);

@@ -491,7 +491,10 @@ def generate_tile_for(m: DeviceMatrix, c: SimtConfig) -> Tile:
 # ---------------------------------------------------------------------------
 @dataclass
 class SpmvTrace:
-    """merbit_spmv.hpp:21-28 (deposit logging is not supported on the device)."""
+    """merbit_spmv.hpp:21-28: tile-routing counters and, with
+    collect_deposits, every (row, partial sum) contribution of the MERBIT
+    decomposition (mbx_spmv_deposits; unordered, rows in the caller's
+    vertex order)."""
     collect_deposits: bool = False
     fast_tiles: int = 0
     normal_tiles: int = 0
@@ -529,8 +532,6 @@ class DualBuffer:
 def spmv_merbit(m: DeviceMatrix, t: Tile, c: SimtConfig, x, out: DualBuffer,
                 trace: SpmvTrace | None = None):
     """y = A x into out.active(); companion zeroed; parity flipped."""
-    if trace is not None and trace.collect_deposits:
-        raise UnsupportedError("per-row deposit logging is not available on the device path")
     xv = np.ascontiguousarray(x, m.dtype)
     if xv.size != m.n_cols:
         raise DimensionError(f"spmv: x has {xv.size} entries, matrix has {m.n_cols} columns")
@@ -550,6 +551,19 @@ def spmv_merbit(m: DeviceMatrix, t: Tile, c: SimtConfig, x, out: DualBuffer,
         trace.fast_tiles += tr.fast_tiles
         trace.normal_tiles += tr.normal_tiles
         trace.skipped_tiles += tr.skipped_tiles
+        if trace.collect_deposits:
+            L = _lib.lib()
+            cap = C.c_int64()
+            _check(L.mbx_spmv_deposits(m.ctx.h, m.h, t.h, C.byref(cc), None, None, None, 0,
+                                       C.byref(cap)))
+            rows = np.zeros(max(cap.value, 1), np.int64)
+            amounts = np.zeros(max(cap.value, 1), m.dtype)
+            got = C.c_int64()
+            _check(L.mbx_spmv_deposits(m.ctx.h, m.h, t.h, C.byref(cc),
+                                       _ptr(xv) if xv.size else None, _ptr(rows),
+                                       _ptr(amounts), cap.value, C.byref(got)))
+            k = min(got.value, cap.value)
+            trace.deposits.extend(zip(rows[:k].tolist(), amounts[:k].tolist()))
     return out.last_output()
 
 

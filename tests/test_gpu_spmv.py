@@ -304,3 +304,46 @@ def test_compact_matrix_round_trip(ctx, dtype, relabel):
     S = row_slice(A, 0, half)
     rs, cs, vs_ = S.download()
     assert np.array_equal(cs, cols[:ro[half]]) and np.array_equal(vs_, vals[:ro[half]])
+
+
+@pytest.mark.parametrize("cfg", [(4, 4, 16), (32, 7, 64), (32, 14, 128)])
+def test_trace_deposits_conserve_every_product(ctx, cfg):
+    """tests/test_kernel.cpp:136-158 on the device: with collect_deposits the
+    trace holds every (row, partial) contribution the decomposition forms;
+    per-row totals reproduce y within the reference's ToleranceBound, rows in
+    [0, n_rows] (the terminal row may appear), every shape of the corpus --
+    and the same for a degree-relabelled matrix (rows in the original
+    vertex order)."""
+    w, s, b = cfg
+    for shape in O.SHAPES:
+        a = O.random_matrix(shape, 505)
+        x = O.seed_test_vector(a.n_cols, -1, 1, 31)
+        m = mb.DeviceMatrix.from_csr(ctx, a)
+        c = mb.SimtConfig.make(w, s, b)
+        t = mb.generate_tile(a.row_offsets, a.n_rows, a.nnz, c, ctx)
+        tr = mb.SpmvTrace(collect_deposits=True)
+        mb.spmv_merbit(m, t, c, x, mb.DualBuffer(a.n_rows, np.float64), tr)
+        totals = np.zeros(a.n_rows)
+        for row, amount in tr.deposits:
+            assert 0 <= row <= a.n_rows
+            if row < a.n_rows:
+                totals[row] += amount
+        want = O.spmv_csr_f64(a, x)
+        assert first_violation(tolerance_bound(a, x, np.float64), want, totals) == -1, shape
+        assert tr.normal_tiles + tr.fast_tiles + tr.skipped_tiles == t.tile_num
+    P = mb.DeviceMatrix.rmat(ctx, 10, 16, seed=3, dtype=np.float64, lo=-1.0, hi=1.0)
+    ro, cols, vals = P.download()
+    Q, _ = P.relabel_by_degree(want_rank=False)
+    c = mb.SimtConfig.make(32, 7, 128)
+    tq = mb.generate_tile_for(Q, c)
+    x = O.seed_test_vector(P.n_cols, -1, 1, 7)
+    tr = mb.SpmvTrace(collect_deposits=True)
+    y = mb.spmv_merbit(Q, tq, c, x, mb.DualBuffer(P.n_rows, np.float64), tr)
+    totals = np.zeros(P.n_rows)
+    for row, amount in tr.deposits:
+        if row < P.n_rows:
+            totals[row] += amount
+    a = O.Csr(P.n_rows, P.n_cols, ro, cols, vals)
+    want, mag = O.spmv_csr_f64(a, x, want_abs=True)
+    assert (np.abs(totals - want) <= 1e-12 * np.where(mag > 0, mag, 1)).all()
+    assert (np.abs(y - want) <= 1e-12 * np.where(mag > 0, mag, 1)).all()
