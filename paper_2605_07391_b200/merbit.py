@@ -158,10 +158,11 @@ PAGERANK_ROW_WEIGHT = 3.4
 
 def pagerank_row_weight(n_vertices: int, value_bytes: int = 4) -> float:
     """Row weight for plan_row_shards.  Once pi no longer sits in L2 (s27:
-    512 MB) each gathered nonzero costs more relative to a row's commit; the
-    measured best cut there is ~2.5 (slowest of 8 shards 1.37 ms vs 1.43 ms at
-    3.4), at s24 (64 MB of pi) 3.4 (0.159 ms vs 0.257 ms at the merge-path 1.0)."""
-    return PAGERANK_ROW_WEIGHT if n_vertices * value_bytes <= (96 << 20) else 2.5
+    512 MB) each gathered nonzero costs more relative to a row's commit; with
+    round 2's store-only commit the measured best cut there is ~1.5 (slowest
+    of 8 shards 1.519 ms vs 1.574 at 2.5 and 1.587 at 3.0,
+    profiles/r2_shard_projection.json); at s24 (64 MB of pi) 3.4."""
+    return PAGERANK_ROW_WEIGHT if n_vertices * value_bytes <= (96 << 20) else 1.5
 
 
 def plan_row_shards(row_offsets, n_rows: int, nnz: int, parts: int,
