@@ -1195,60 +1195,103 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
   if (PR && p.pr.npeer) __threadfence_system();  // NVLink stores performed (fused exchange)
 }
 
-// One thread per (chunk, lane): writes that lane's sigma slots.
 // hub encoding of a column: prefix > 0 -- the hubs are columns 0..prefix-1
-// (degree-relabelled), slot c; else slot_of lookup (nullptr: no hubs)
-__device__ __forceinline__ int32_t hub_encode(const int32_t* __restrict__ slot_of, int prefix,
+// (degree-relabelled), slot c; else the hub word map (nullptr: no hubs)
+__device__ __forceinline__ int32_t hub_encode(const uint2* __restrict__ map, int prefix,
                                               int32_t c) {
   if (prefix > 0) return c < prefix ? int32_t(0x80000000u | uint32_t(c)) : c;
-  if (!slot_of) return c;
-  const int32_t s = __ldg(slot_of + c);
-  return s >= 0 ? int32_t(0x80000000u | uint32_t(s)) : c;
+  return map ? hub_word_encode(map, c) : c;
 }
 
-template <typename T>
-__global__ void build_slots_kernel(const T* __restrict__ vals, const int32_t* __restrict__ cols,
-                                   const int32_t* __restrict__ slot_of, int prefix,
-                                   const uint32_t* __restrict__ tile_x,
-                                   const uint32_t* __restrict__ tile_y,
-                                   const uint32_t* __restrict__ lane_desc, int64_t lane_num,
-                                   int64_t num_chunks, int64_t total, int sigma, int ob,
-                                   T* __restrict__ svals, int32_t* __restrict__ scols) {
+// One warp per chunk: the chunk's CSR run (at most 32*SIGMA nonzeros) is
+// read coalesced into shared memory and hub-encoded there, then every lane
+// picks its SIGMA slots out of it (a long-row chunk element-interleaved, a
+// normal one along its lane descriptor) and the warp writes them with 8-byte
+// stores, 256 contiguous bytes per instruction.
+template <typename T, int SIGMA>
+__global__ void __launch_bounds__(256) build_slots_kernel(
+    const T* __restrict__ vals, const int32_t* __restrict__ cols, const uint2* __restrict__ map,
+    int prefix, const uint32_t* __restrict__ tile_x, const uint32_t* __restrict__ tile_y,
+    const uint32_t* __restrict__ lane_desc, int64_t lane_num, int64_t num_chunks, int64_t total,
+    int ob, T* __restrict__ svals, int32_t* __restrict__ scols) {
   constexpr int G = 8 / int(sizeof(T));
+  constexpr int E = 32 * SIGMA;
+  static_assert(SIGMA % G == 0, "slot groups");
+  __shared__ T sv[8][E];
+  __shared__ int32_t sc[8][E];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const uint32_t omask = (1u << ob) - 1u;
-  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < num_chunks * 32;
-       j += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t c = j >> 5;
-    const int l = static_cast<int>(j & 31);
-    const int64_t x0 = tile_x[c], x1 = tile_x[c + 1];
-    const int64_t sb = c * 32 * sigma + int64_t(l) * G;
+  const int64_t nw = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t c = int64_t(blockIdx.x) * (blockDim.x >> 5) + w; c < num_chunks; c += nw) {
+    const int64_t x0 = tile_x[c];
+    const int n = int(imin64(int64_t(tile_x[c + 1]) - x0, E));
+    {  // every load of the run in flight at once
+      T lv[SIGMA];
+      int32_t lc[SIGMA];
+#pragma unroll
+      for (int i = 0; i < SIGMA; ++i) {
+        const int k = i * 32 + l;
+        lv[i] = k < n ? __ldcs(vals + x0 + k) : T(0);
+        lc[i] = k < n ? __ldcs(cols + x0 + k) : 0;
+      }
+#pragma unroll
+      for (int i = 0; i < SIGMA; ++i) {
+        const int k = i * 32 + l;
+        if (k < n) {
+          sv[w][k] = lv[i];
+          sc[w][k] = hub_encode(map, prefix, lc[i]);
+        }
+      }
+    }
+    __syncwarp();
+    T v[SIGMA];
+    int32_t q[SIGMA];
     if (tile_y[c] & kLongRowMask) {
-      for (int i = 0; i < sigma; ++i) {
-        const int64_t e = x0 + int64_t(i) * 32 + l;
-        const int64_t pos = sb + int64_t(i / G) * 32 * G + (i % G);
-        const bool ok = e < x1;
-        svals[pos] = ok ? vals[e] : T(0);
-        scols[pos] = ok ? hub_encode(slot_of, prefix, cols[e]) : 0;
+#pragma unroll
+      for (int i = 0; i < SIGMA; ++i) {
+        const int k = i * 32 + l;
+        v[i] = k < n ? sv[w][k] : T(0);
+        q[i] = k < n ? sc[w][k] : 0;
       }
     } else {
+      const int64_t j = c * 32 + l;
       uint32_t d = 0;
       int steps = 0;
       if (j < lane_num) {
         d = lane_desc[j];
-        steps = static_cast<int>(imin64(sigma, total - j * sigma));
+        steps = static_cast<int>(imin64(SIGMA, total - j * SIGMA));
       }
-      int64_t x = x0 + (d & omask);
+      int k = int(d & omask);
       const uint32_t fl = d >> (2 * ob);
-      for (int i = 0; i < sigma; ++i) {
-        const int64_t pos = sb + int64_t(i / G) * 32 * G + (i % G);
+#pragma unroll
+      for (int i = 0; i < SIGMA; ++i) {
+        v[i] = T(0);
+        q[i] = 0;
         if (i < steps && !((fl >> i) & 1u)) {
-          svals[pos] = vals[x];
-          scols[pos] = hub_encode(slot_of, prefix, cols[x]);
-          ++x;
-        } else {
-          svals[pos] = T(0);
-          scols[pos] = 0;
+          if (k < n) {
+            v[i] = sv[w][k];
+            q[i] = sc[w][k];
+          } else {  // not reached for a well-formed TILE; stay exact anyway
+            v[i] = vals[x0 + k];
+            q[i] = hub_encode(map, prefix, cols[x0 + k]);
+          }
+          ++k;
         }
+      }
+    }
+    __syncwarp();
+    const int64_t sb = c * E + int64_t(l) * G;
+    if constexpr (G == 2) {
+#pragma unroll
+      for (int g = 0; g < SIGMA / 2; ++g) {
+        *reinterpret_cast<float2*>(svals + sb + g * 64) = make_float2(v[2 * g], v[2 * g + 1]);
+        *reinterpret_cast<int2*>(scols + sb + g * 64) = make_int2(q[2 * g], q[2 * g + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < SIGMA; ++i) {
+        svals[sb + i * 32] = v[i];
+        scols[sb + i * 32] = q[i];
       }
     }
   }
@@ -1548,6 +1591,80 @@ __global__ void gen_tile_kernel(const uint32_t* __restrict__ ro, int64_t n, int6
       tile_x[j / omega] = uint32_t(tsx);
       tile_y[j / omega] = uint32_t(tsy) | (any_down ? 0u : kLongRowMask);
     }
+  }
+}
+
+// K1 for omega dividing 32 (the default 32): one CTA per 256 lanes, no
+// per-lane search.  The merge path moves down exactly at diagonal
+// e_r = ro[r+1] + r (the step after row r's last nonzero), so a lane's step
+// flags are the row ends that fall in its sigma diagonals, and its start
+// row is the CTA's start row plus the row ends before it.  The CTA's start
+// rows come from one global merge-path search per CTA boundary
+// (gen_tile_bounds_kernel, all in parallel); the CTA then reads its rows'
+// offsets once, coalesced, scatters each row end into its lane's flag word
+// (shared-memory atomicOr), and a block scan of the flag popcounts gives
+// every lane's (x, y).  The per-lane binary search of gen_tile_kernel cost
+// ~log2(n) dependent loads per lane.  Output byte-identical.
+__global__ void gen_tile_bounds_kernel(const uint32_t* __restrict__ ro, int64_t n, int64_t m,
+                                       int sigma, int64_t blocks, int64_t* __restrict__ bnd) {
+  const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b > blocks) return;
+  int64_t x, y;
+  d_merge_search(ro, n, m, imin64(b * 256 * sigma, m + n), x, y);
+  bnd[b] = y;
+}
+
+__global__ void __launch_bounds__(256) gen_tile_scan_kernel(
+    const uint32_t* __restrict__ ro, int64_t n, int64_t m, int omega, int sigma, int ob,
+    int64_t lane_num, const int64_t* __restrict__ bnd, uint32_t* __restrict__ tile_x,
+    uint32_t* __restrict__ tile_y, uint32_t* __restrict__ lane_desc) {
+  __shared__ uint32_t fl[256];
+  __shared__ int wsum[8];
+  const int tid = threadIdx.x, lid = tid & 31, wid = tid >> 5;
+  const int64_t j0 = int64_t(blockIdx.x) * 256;
+  const int64_t d0 = j0 * sigma;
+  const int64_t total = m + n;
+  const int64_t span = imin64(int64_t(256) * sigma, total - d0);  // this CTA's diagonals
+  const int64_t y0 = bnd[blockIdx.x];
+  const int64_t r1 = imin64(bnd[blockIdx.x + 1], n - 1);  // last row that can end inside
+  fl[tid] = 0u;
+  __syncthreads();
+  for (int64_t r = y0 + tid; r <= r1; r += 256) {
+    const int64_t p = int64_t(__ldg(ro + r + 1)) + r - d0;  // e_r - d0 >= 0
+    if (p < span) {
+      const int q = int(p);  // < 256 * sigma
+      const int l = q / sigma;
+      atomicOr(&fl[l], 1u << (q - l * sigma));
+    }
+  }
+  __syncthreads();
+  const uint32_t flags = fl[tid];
+  // exclusive scan of the row ends per lane
+  const int c = __popc(flags);
+  int inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(kFull, inc, o);
+    if (lid >= o) inc += v;
+  }
+  if (lid == 31) wsum[wid] = inc;
+  __syncthreads();
+  int before = inc - c;
+  for (int w = 0; w < wid; ++w) before += wsum[w];
+  const int64_t j = j0 + tid;
+  const bool valid = j < lane_num;
+  const int64_t y = y0 + before;
+  const int64_t x = j * sigma - y;
+  const int leader = lid & ~(omega - 1);
+  const int64_t tsx = __shfl_sync(kFull, x, leader);
+  const int64_t tsy = __shfl_sync(kFull, y, leader);
+  if (valid) lane_desc[j] = (flags << (2 * ob)) | (uint32_t(y - tsy) << ob) | uint32_t(x - tsx);
+  const unsigned ballot = __ballot_sync(kFull, valid && flags != 0u);
+  const unsigned gmask = omega >= 32 ? kFull : ((1u << omega) - 1u);
+  const bool any_down = ((ballot >> leader) & gmask) != 0u;
+  if (valid && lid == leader) {
+    tile_x[j / omega] = uint32_t(tsx);
+    tile_y[j / omega] = uint32_t(tsy) | (any_down ? 0u : kLongRowMask);
   }
 }
 
@@ -2017,21 +2134,21 @@ bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, cons
   // the hub encoding is applied while the slots are written (no encoded
   // copy of the CSR columns is kept)
   const int prefix = hub && m->hub_prefix ? m->hub_avail : 0;
-  int32_t* slot_of = hub && !prefix ? hub_slot_map(ctx, m) : nullptr;
-  const unsigned grid = grid_for(g.num_chunks * 32, 256, int64_t(ctx->sm_count) * 16);
+  uint2* map = hub && !prefix ? hub_word_map(ctx, m) : nullptr;
+  const unsigned grid = grid_for((g.num_chunks + 7) / 8, 1, int64_t(ctx->sm_count) * 8);
   const int64_t total = g.nnz + g.n_rows;
   if (m->precision == MBX_F32)
-    build_slots_kernel<float><<<grid, 256, 0, ctx->stream>>>(
-        static_cast<const float*>(m->vals), m->cols, slot_of, prefix, t->tile_x, t->tile_y, t->lane_desc,
-        g.lane_num, g.num_chunks, total, g.sigma, g.ob, static_cast<float*>(sc.vals), sc.cols);
+    build_slots_kernel<float, 14><<<grid, 256, 0, ctx->stream>>>(
+        static_cast<const float*>(m->vals), m->cols, map, prefix, t->tile_x, t->tile_y,
+        t->lane_desc, g.lane_num, g.num_chunks, total, g.ob, static_cast<float*>(sc.vals), sc.cols);
   else
-    build_slots_kernel<double><<<grid, 256, 0, ctx->stream>>>(
-        static_cast<const double*>(m->vals), m->cols, slot_of, prefix, t->tile_x, t->tile_y, t->lane_desc,
-        g.lane_num, g.num_chunks, total, g.sigma, g.ob, static_cast<double*>(sc.vals), sc.cols);
+    build_slots_kernel<double, 7><<<grid, 256, 0, ctx->stream>>>(
+        static_cast<const double*>(m->vals), m->cols, map, prefix, t->tile_x, t->tile_y,
+        t->lane_desc, g.lane_num, g.num_chunks, total, g.ob, static_cast<double*>(sc.vals), sc.cols);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
   MBX_CUDA(cudaEventRecord(e1, ctx->stream));
-  if (slot_of) cudaFreeAsync(slot_of, ctx->stream);
+  if (map) cudaFreeAsync(map, ctx->stream);
   MBX_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
   MBX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
@@ -2141,9 +2258,20 @@ void launch_generate_tile(mbx_context* ctx, const uint32_t* ro, int64_t n_rows, 
   const bool small = c.omega <= 32 && (32 % c.omega) == 0;
   if (lanes > 0) {
     const int64_t blocks = (lanes + 255) / 256;
-    gen_tile_kernel<<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(
-        ro, n_rows, nnz, c.omega, c.sigma, c.offset_bits, lanes, t->tile_x, t->tile_y,
-        t->lane_desc, small ? 1 : 0);
+    if (small) {
+      int64_t* bnd = nullptr;
+      MBX_CUDA(cudaMallocAsync(&bnd, size_t(blocks + 1) * 8 + 64, ctx->stream));
+      gen_tile_bounds_kernel<<<static_cast<unsigned>((blocks + 256) / 256), 256, 0,
+                               ctx->stream>>>(ro, n_rows, nnz, c.sigma, blocks, bnd);
+      gen_tile_scan_kernel<<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(
+          ro, n_rows, nnz, c.omega, c.sigma, c.offset_bits, lanes, bnd, t->tile_x, t->tile_y,
+          t->lane_desc);
+      ++ctx->launches;
+      cudaFreeAsync(bnd, ctx->stream);
+    } else
+      gen_tile_kernel<<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(
+          ro, n_rows, nnz, c.omega, c.sigma, c.offset_bits, lanes, t->tile_x, t->tile_y,
+          t->lane_desc, small ? 1 : 0);
     ++ctx->launches;
     MBX_CUDA(cudaGetLastError());
     if (!small) {

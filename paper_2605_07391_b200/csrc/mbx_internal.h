@@ -40,8 +40,8 @@ struct Geometry {
   // persistent launch: grid = sm_count * ctas_per_sm, warps stride over ranges
   int grid = 0;
   int sms = 148;  // multiprocessors of the device
-  // x hub cache: the first hub_count entries of the column-frequency order
-  // are staged in shared memory; encoded columns (sign bit) address them.
+  // x hub cache: the hub_count (0 or hub_avail) hub values are staged in
+  // shared memory; encoded columns (sign bit) address them.
   int hub_count = 0;
   int prefetch = 0;
   // 1: K2 walks the lane-major slot copy of the matrix (slots.cu) instead of
@@ -162,7 +162,7 @@ struct mbx_matrix_s {
   int32_t* cols = nullptr;     // int32[nnz] (+ pad)
   uint32_t* ro = nullptr;      // u32[n_rows+1]
   // x hub cache (mbx_matrix_build_xcache): hub_cols lists the most
-  // referenced columns in descending frequency; cols_hub (built only when a
+  // referenced columns in ascending column order (slot = rank); cols_hub (built only when a
   // staged / generic K2 needs it) is cols with every reference to hub slot
   // s < hub_avail rewritten as (INT32_MIN | s).
   int32_t* cols_hub = nullptr;
@@ -233,7 +233,17 @@ int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, in
                   int precision);
 void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs);
 // slot_of[c] = hub slot of column c or -1 (n_cols int32; the caller frees)
-int32_t* hub_slot_map(mbx_context* ctx, const mbx_matrix* m);
+// hub lookup words (hub_cols ascending): .x = hub bits of columns 32w..32w+31,
+// .y = slot of the first of them
+uint2* hub_word_map(mbx_context* ctx, const mbx_matrix* m);
+#ifdef __CUDACC__
+// column c -> (INT32_MIN | slot) for a hub, c otherwise
+__device__ __forceinline__ int32_t hub_word_encode(const uint2* __restrict__ map, int32_t c) {
+  const uint2 e = __ldg(map + (c >> 5));
+  const uint32_t b = 1u << (c & 31);
+  return (e.x & b) ? int32_t(0x80000000u | (e.y + uint32_t(__popc(e.x & (b - 1u))))) : c;
+}
+#endif
 // build m->cols_hub (hub-encoded CSR columns) if missing: staged / generic K2
 void ensure_cols_hub(mbx_context* ctx, const mbx_matrix* m);
 // slots.cu: make m->slots match (t, hub encoding of g); false if the slot

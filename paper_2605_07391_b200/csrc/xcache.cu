@@ -60,19 +60,22 @@ __global__ void fill_kernel(int32_t* v, int64_t n, int32_t val) {
     v[i] = val;
 }
 
-__global__ void slot_map_kernel(const int32_t* __restrict__ hub_cols, int h, int32_t* slot_of) {
+// word map of the (ascending) hub list: map[w].x = the hubs among columns
+// 32w..32w+31 as bits, map[w].y = slot of the first of them
+__global__ void hub_word_kernel(const int32_t* __restrict__ hub_cols, int h, uint2* map) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < h) slot_of[hub_cols[i]] = i;
+  if (i >= h) return;
+  const int32_t c = hub_cols[i];
+  const int32_t w = c >> 5;
+  atomicOr(&map[w].x, 1u << (c & 31));
+  if (i == 0 || (hub_cols[i - 1] >> 5) != w) map[w].y = uint32_t(i);
 }
 
 __global__ void encode_kernel(const int32_t* __restrict__ cols, int64_t nnz,
-                              const int32_t* __restrict__ slot_of, int32_t* __restrict__ out) {
+                              const uint2* __restrict__ map, int32_t* __restrict__ out) {
   for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < nnz;
-       k += int64_t(gridDim.x) * blockDim.x) {
-    const int32_t c = cols[k];
-    const int32_t s = slot_of[c];
-    out[k] = s >= 0 ? int32_t(0x80000000u | uint32_t(s)) : c;
-  }
+       k += int64_t(gridDim.x) * blockDim.x)
+    out[k] = hub_word_encode(map, cols[k]);
 }
 
 }  // namespace
@@ -281,8 +284,15 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
     covered += int64_t(hc[h++]) * S;
   }
   if (h > 0) {
+    // slots in ascending column order: a column's slot is then its rank
+    // among the hub columns, which hub_word_map encodes in n/32 words
     MBX_CUDA(cudaMallocAsync(&m->hub_cols, size_t(h) * 4 + 64, s));
-    MBX_CUDA(cudaMemcpyAsync(m->hub_cols, cid_sorted, size_t(h) * 4, cudaMemcpyDeviceToDevice, s));
+    size_t tk = 0;
+    MBX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tk, cid_sorted, m->hub_cols, h, 0, 32, s));
+    void* tsort = nullptr;
+    MBX_CUDA(cudaMallocAsync(&tsort, tk + 64, s));
+    MBX_CUDA(cub::DeviceRadixSort::SortKeys(tsort, tk, cid_sorted, m->hub_cols, h, 0, 32, s));
+    cudaFreeAsync(tsort, s);
     m->hub_avail = h;
     // estimated from the sample when S > 1
     m->hub_coverage = std::min(1.0, double(covered) / double(m->nnz));
@@ -295,16 +305,19 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   done();
 }
 
-// slot_of[c] = hub slot of column c, or -1 (n_cols int32, caller frees)
-int32_t* hub_slot_map(mbx_context* ctx, const mbx_matrix* m) {
+// The hub lookup of the encoders (caller frees): n_cols/32 + 1 words, 8 bytes
+// each (4 MB at R-MAT scale 24), so the per-nonzero test hits L2 instead of
+// an n_cols-entry slot table.
+uint2* hub_word_map(mbx_context* ctx, const mbx_matrix* m) {
   cudaStream_t s = ctx->stream;
-  int32_t* slot_of = nullptr;
-  MBX_CUDA(cudaMallocAsync(&slot_of, m->n_cols * 4 + 64, s));
-  fill_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(slot_of, m->n_cols, -1);
-  slot_map_kernel<<<(m->hub_avail + 255) / 256, 256, 0, s>>>(m->hub_cols, m->hub_avail, slot_of);
-  ctx->launches += 2;
+  uint2* map = nullptr;
+  const size_t words = size_t(m->n_cols / 32 + 1);
+  MBX_CUDA(cudaMallocAsync(&map, words * 8 + 64, s));
+  MBX_CUDA(cudaMemsetAsync(map, 0, words * 8, s));
+  hub_word_kernel<<<(m->hub_avail + 255) / 256, 256, 0, s>>>(m->hub_cols, m->hub_avail, map);
+  ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
-  return slot_of;
+  return map;
 }
 
 // The hub-encoded column array of the staged (layout 0) and generic K2
@@ -314,13 +327,13 @@ void ensure_cols_hub(mbx_context* ctx, const mbx_matrix* m_) {
   mbx_matrix* m = const_cast<mbx_matrix*>(m_);
   if (m->cols_hub || m->hub_avail <= 0) return;
   cudaStream_t s = ctx->stream;
-  int32_t* slot_of = hub_slot_map(ctx, m);
+  uint2* map = hub_word_map(ctx, m);
   MBX_CUDA(cudaMallocAsync(&m->cols_hub, m->nnz * 4 + 256, s));
   MBX_CUDA(cudaMemsetAsync(m->cols_hub, 0, m->nnz * 4 + 256, s));
-  encode_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(m->cols, m->nnz, slot_of, m->cols_hub);
+  encode_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(m->cols, m->nnz, map, m->cols_hub);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
-  cudaFreeAsync(slot_of, s);
+  cudaFreeAsync(map, s);
 }
 
 }  // namespace mbx
