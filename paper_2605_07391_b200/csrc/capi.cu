@@ -990,6 +990,8 @@ struct mbx_pagerank_plan_s {
   unsigned int* counter = nullptr;
   int* flags = nullptr;  // [0] stop, [1] stop_iter
   void* carry_ws = nullptr;
+  size_t carry_ws_bytes = 0;  // its size: a re-made geometry may need more
+  int64_t block_part_n = 0;   // block_part slots (4 doubles each)
   cudaGraphExec_t graph = nullptr;
   int64_t graph_launches = 0;
   int64_t* iter_dev = nullptr;  // iterations completed (device-driven loop)
@@ -1083,6 +1085,13 @@ void launch_power_loop(mbx_pagerank_plan* pl) {
 
 namespace {
 
+// block_part slots a plan's K3 / yardstick / pi_0 grids need
+int64_t plan_block_slots(mbx_context* ctx, const mbx_matrix* p, const mbx::Geometry& g) {
+  const int64_t k3_blocks = std::max(mbx::fixup_blocks(g, true), mbx::fixup_blocks(g, false)) + 1;
+  return std::max<int64_t>({k3_blocks, int64_t(mbx::csr_pr_blocks(ctx, p)),
+                            int64_t(ctx->sm_count) * 4 + 1});
+}
+
 // Capture the power loop of `pl` (geometry already made): records the
 // matrix's buffer generation the graph was captured against.
 void capture_plan(mbx_pagerank_plan* pl) {
@@ -1160,8 +1169,23 @@ void capture_plan(mbx_pagerank_plan* pl) {
 // re-capture before the next replay.
 void refresh_plan(mbx_pagerank_plan* pl) {
   if (pl->p->gen == pl->p_gen) return;
-  MBX_CUDA(cudaStreamSynchronize(pl->ctx->stream));
-  pl->g = mbx::make_geometry(pl->ctx, pl->p, pl->t, pl->c.block_size);
+  mbx_context* ctx = pl->ctx;
+  MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+  pl->g = mbx::make_geometry(ctx, pl->p, pl->t, pl->c.block_size);
+  // the new geometry's workspace (e.g. a hub table that did not exist at
+  // capture: the gathered hub values live after the carries) must fit
+  const size_t ws = mbx::spmv_workspace_bytes(pl->g, pl->p->precision, true);
+  if (ws > pl->carry_ws_bytes) {
+    dfree(ctx, pl->carry_ws);
+    pl->carry_ws = dmalloc(ctx, ws);
+    pl->carry_ws_bytes = ws;
+  }
+  const int64_t nb = plan_block_slots(ctx, pl->p, pl->g);
+  if (nb > pl->block_part_n) {
+    dfree(ctx, pl->block_part);
+    pl->block_part = static_cast<double*>(dmalloc(ctx, nb * 4 * sizeof(double)));
+    pl->block_part_n = nb;
+  }
   capture_plan(pl);
 }
 
@@ -1209,15 +1233,14 @@ MBX_API int mbx_pagerank_plan_create(mbx_context* ctx, const mbx_matrix* p, cons
     const size_t mask_bytes = size_t((pl->n + 31) / 32) * 4 + 64;
     pl->carry_mask = static_cast<uint32_t*>(dmalloc(ctx, mask_bytes));
     MBX_CUDA(cudaMemsetAsync(pl->carry_mask, 0, mask_bytes, ctx->stream));
-    const int64_t k3_blocks =
-        std::max(mbx::fixup_blocks(pl->g, true), mbx::fixup_blocks(pl->g, false)) + 1;
-    const int64_t nb = std::max<int64_t>({k3_blocks, int64_t(mbx::csr_pr_blocks(ctx, p)),
-                                          int64_t(ctx->sm_count) * 4 + 1});
+    const int64_t nb = plan_block_slots(ctx, p, pl->g);
     pl->block_part = static_cast<double*>(dmalloc(ctx, nb * 4 * sizeof(double)));
+    pl->block_part_n = nb;
     pl->counter = static_cast<unsigned int*>(dmalloc(ctx, 64));
     pl->flags = static_cast<int*>(dmalloc(ctx, 64));
     MBX_CUDA(cudaMemsetAsync(pl->counter, 0, 64, ctx->stream));
-    pl->carry_ws = dmalloc(ctx, mbx::spmv_workspace_bytes(pl->g, p->precision, true));
+    pl->carry_ws_bytes = mbx::spmv_workspace_bytes(pl->g, p->precision, true);
+    pl->carry_ws = dmalloc(ctx, pl->carry_ws_bytes);
     MBX_CUDA(cudaEventCreate(&pl->e0));
     MBX_CUDA(cudaEventCreate(&pl->e1));
     pl->iter_dev = static_cast<int64_t*>(dmalloc(ctx, 64));

@@ -1594,7 +1594,7 @@ __global__ void gen_tile_kernel(const uint32_t* __restrict__ ro, int64_t n, int6
   }
 }
 
-// K1 for omega dividing 32 (the default 32): one CTA per 256 lanes, no
+// K1 for omega dividing 32 (the default 32): one CTA per 1024 lanes, no
 // per-lane search.  The merge path moves down exactly at diagonal
 // e_r = ro[r+1] + r (the step after row r's last nonzero), so a lane's step
 // flags are the row ends that fall in its sigma diagonals, and its start
@@ -1605,12 +1605,14 @@ __global__ void gen_tile_kernel(const uint32_t* __restrict__ ro, int64_t n, int6
 // (shared-memory atomicOr), and a block scan of the flag popcounts gives
 // every lane's (x, y).  The per-lane binary search of gen_tile_kernel cost
 // ~log2(n) dependent loads per lane.  Output byte-identical.
+constexpr int kK1Lanes = 1024;  // lanes per CTA (4 per thread)
+
 __global__ void gen_tile_bounds_kernel(const uint32_t* __restrict__ ro, int64_t n, int64_t m,
                                        int sigma, int64_t blocks, int64_t* __restrict__ bnd) {
   const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b > blocks) return;
   int64_t x, y;
-  d_merge_search(ro, n, m, imin64(b * 256 * sigma, m + n), x, y);
+  d_merge_search(ro, n, m, imin64(b * kK1Lanes * sigma, m + n), x, y);
   bnd[b] = y;
 }
 
@@ -1618,29 +1620,32 @@ __global__ void __launch_bounds__(256) gen_tile_scan_kernel(
     const uint32_t* __restrict__ ro, int64_t n, int64_t m, int omega, int sigma, int ob,
     int64_t lane_num, const int64_t* __restrict__ bnd, uint32_t* __restrict__ tile_x,
     uint32_t* __restrict__ tile_y, uint32_t* __restrict__ lane_desc) {
-  __shared__ uint32_t fl[256];
+  __shared__ uint32_t fl[kK1Lanes];
+  __shared__ int pre[kK1Lanes + 1];  // row ends before each lane (CTA-relative)
   __shared__ int wsum[8];
   const int tid = threadIdx.x, lid = tid & 31, wid = tid >> 5;
-  const int64_t j0 = int64_t(blockIdx.x) * 256;
+  const int64_t j0 = int64_t(blockIdx.x) * kK1Lanes;
   const int64_t d0 = j0 * sigma;
   const int64_t total = m + n;
-  const int64_t span = imin64(int64_t(256) * sigma, total - d0);  // this CTA's diagonals
+  const int64_t span = imin64(int64_t(kK1Lanes) * sigma, total - d0);  // this CTA's diagonals
   const int64_t y0 = bnd[blockIdx.x];
   const int64_t r1 = imin64(bnd[blockIdx.x + 1], n - 1);  // last row that can end inside
-  fl[tid] = 0u;
+  reinterpret_cast<uint4*>(fl)[tid] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
+#pragma unroll 4
   for (int64_t r = y0 + tid; r <= r1; r += 256) {
     const int64_t p = int64_t(__ldg(ro + r + 1)) + r - d0;  // e_r - d0 >= 0
     if (p < span) {
-      const int q = int(p);  // < 256 * sigma
+      const int q = int(p);  // < kK1Lanes * sigma
       const int l = q / sigma;
       atomicOr(&fl[l], 1u << (q - l * sigma));
     }
   }
   __syncthreads();
-  const uint32_t flags = fl[tid];
-  // exclusive scan of the row ends per lane
-  const int c = __popc(flags);
+  const uint4 f4 = reinterpret_cast<const uint4*>(fl)[tid];
+  const uint32_t f[4] = {f4.x, f4.y, f4.z, f4.w};
+  const int c0 = __popc(f[0]), c1 = __popc(f[1]), c2 = __popc(f[2]), c3 = __popc(f[3]);
+  const int c = c0 + c1 + c2 + c3;
   int inc = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1649,22 +1654,38 @@ __global__ void __launch_bounds__(256) gen_tile_scan_kernel(
   }
   if (lid == 31) wsum[wid] = inc;
   __syncthreads();
-  int before = inc - c;
-  for (int w = 0; w < wid; ++w) before += wsum[w];
-  const int64_t j = j0 + tid;
-  const bool valid = j < lane_num;
-  const int64_t y = y0 + before;
-  const int64_t x = j * sigma - y;
-  const int leader = lid & ~(omega - 1);
-  const int64_t tsx = __shfl_sync(kFull, x, leader);
-  const int64_t tsy = __shfl_sync(kFull, y, leader);
-  if (valid) lane_desc[j] = (flags << (2 * ob)) | (uint32_t(y - tsy) << ob) | uint32_t(x - tsx);
-  const unsigned ballot = __ballot_sync(kFull, valid && flags != 0u);
-  const unsigned gmask = omega >= 32 ? kFull : ((1u << omega) - 1u);
-  const bool any_down = ((ballot >> leader) & gmask) != 0u;
-  if (valid && lid == leader) {
-    tile_x[j / omega] = uint32_t(tsx);
-    tile_y[j / omega] = uint32_t(tsy) | (any_down ? 0u : kLongRowMask);
+  int base = inc - c;
+  for (int w = 0; w < wid; ++w) base += wsum[w];
+  pre[4 * tid] = base;
+  pre[4 * tid + 1] = base + c0;
+  pre[4 * tid + 2] = base + c0 + c1;
+  pre[4 * tid + 3] = base + c0 + c1 + c2;
+  if (tid == 255) pre[kK1Lanes] = base + c;
+  __syncthreads();
+  uint32_t d[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int l = 4 * tid + k;
+    const int ld = l & ~(omega - 1);  // the tile's first lane
+    const int64_t j = j0 + l;
+    const int64_t y = y0 + pre[l];
+    const int64_t x = j * sigma - y;
+    const int64_t tsy = y0 + pre[ld];
+    const int64_t tsx = (j0 + ld) * sigma - tsy;
+    d[k] = (f[k] << (2 * ob)) | (uint32_t(y - tsy) << ob) | uint32_t(x - tsx);
+    if (l == ld && j < lane_num) {
+      const bool any_down = pre[imin64(ld + omega, kK1Lanes)] > pre[ld];
+      tile_x[j / omega] = uint32_t(tsx);
+      tile_y[j / omega] = uint32_t(tsy) | (any_down ? 0u : kLongRowMask);
+    }
+  }
+  const int64_t j = j0 + 4 * tid;
+  if (j + 3 < lane_num) {
+    *reinterpret_cast<uint4*>(lane_desc + j) = make_uint4(d[0], d[1], d[2], d[3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (j + k < lane_num) lane_desc[j + k] = d[k];
   }
 }
 
@@ -2259,11 +2280,12 @@ void launch_generate_tile(mbx_context* ctx, const uint32_t* ro, int64_t n_rows, 
   if (lanes > 0) {
     const int64_t blocks = (lanes + 255) / 256;
     if (small) {
+      const int64_t cblocks = (lanes + kK1Lanes - 1) / kK1Lanes;
       int64_t* bnd = nullptr;
-      MBX_CUDA(cudaMallocAsync(&bnd, size_t(blocks + 1) * 8 + 64, ctx->stream));
-      gen_tile_bounds_kernel<<<static_cast<unsigned>((blocks + 256) / 256), 256, 0,
-                               ctx->stream>>>(ro, n_rows, nnz, c.sigma, blocks, bnd);
-      gen_tile_scan_kernel<<<static_cast<unsigned>(blocks), 256, 0, ctx->stream>>>(
+      MBX_CUDA(cudaMallocAsync(&bnd, size_t(cblocks + 1) * 8 + 64, ctx->stream));
+      gen_tile_bounds_kernel<<<static_cast<unsigned>((cblocks + 256) / 256), 256, 0,
+                               ctx->stream>>>(ro, n_rows, nnz, c.sigma, cblocks, bnd);
+      gen_tile_scan_kernel<<<static_cast<unsigned>(cblocks), 256, 0, ctx->stream>>>(
           ro, n_rows, nnz, c.omega, c.sigma, c.offset_bits, lanes, bnd, t->tile_x, t->tile_y,
           t->lane_desc);
       ++ctx->launches;

@@ -1,7 +1,8 @@
 """Preprocessing split (TILE, x hub cache, slot copy) against one SpMV, repeated
 so first-use costs (memory pool growth, module loading) show separately:
 python scripts/prof/preproc.py [case ...], cases s24, s24r (degree-relabelled),
-s24f64, s24rf64, s20, c5, c5f64."""
+s24f64, s24rf64, s20, c3 (power-law f64), c5, c5f64.  LAYOUT=0 runs K2 on
+the staged CSR order (no slot copy)."""
 import os
 import sys
 import time
@@ -17,10 +18,14 @@ ctx = mb.Context(0)
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 ctx.set_stream(s.cuda_stream)
+if os.environ.get("LAYOUT"):
+    ctx.set_layout(int(os.environ["LAYOUT"]))
 
 
 def make(case):
     dt = np.float64 if "f64" in case else np.float32
+    if case.startswith("c3"):
+        return mb.DeviceMatrix.powerlaw(ctx, 22, seed=3, dtype=np.float64), np.float64
     if case.startswith("c5"):
         return mb.DeviceMatrix.stencil27(ctx, 400, dt), dt
     scale = int(case[1:3])

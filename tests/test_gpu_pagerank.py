@@ -292,8 +292,9 @@ def test_plan_recaptures_after_matrix_buffers_change(ctx):
     assert np.array_equal(a.pi.view(np.uint32), b.pi.view(np.uint32))
     # the plan object: run, rebuild the hub cache + slots, run again
     plan = mb.PageRankPlan(P, be.tile_, c, cfg)
-    xd = torch.empty(n, dtype=torch.float32, device="cuda")
+    xd = torch.zeros(n, dtype=torch.float32, device="cuda")
     yd = torch.empty(n, dtype=torch.float32, device="cuda")
+    ro0, cols0, vals0 = P.download()
     plan.run()
     r1, h1 = plan.result(want_history=True)
     P.build_xcache()
@@ -303,6 +304,11 @@ def test_plan_recaptures_after_matrix_buffers_change(ctx):
     plan.run()
     r2, h2 = plan.result(want_history=True)
     assert np.array_equal(h1, h2) and r1.l1_residual == r2.l1_residual
+    # the re-captured plan's workspace grew with the hub table (it used to
+    # write the gathered hub values past its end, into whatever followed)
+    ro1, cols1, vals1 = P.download()
+    assert np.array_equal(cols0, cols1) and np.array_equal(vals0.view(np.uint32),
+                                                           vals1.view(np.uint32))
     y2b = mb.spmv_merbit(P, t2, c2, x, mb.DualBuffer(n, np.float32))
     assert np.array_equal(y2.view(np.uint32), y2b.view(np.uint32))
     plan.close()
