@@ -253,6 +253,9 @@ MBX_API int mbx_matrix_build_xcache(mbx_context* ctx, mbx_matrix* m,
                                     int max_hubs, double* seconds);
 MBX_API int mbx_matrix_xcache_info(const mbx_matrix* m, int* hubs,
                                    double* coverage);
+/* The hub columns (xcache_info's count of them) into host_out, in slot
+ * order: ascending column ids. */
+MBX_API int mbx_matrix_hub_columns(const mbx_matrix* m, int32_t* host_out);
 /* Compact form: once the K2 slot copy for TILE t exists (an SpMV or a
  * PageRank plan with t built it), free the CSR values and columns -- the slot
  * copy holds every (value, column) -- keeping a private copy of t's arrays.

@@ -659,6 +659,17 @@ MBX_API int mbx_matrix_xcache_ptrs(const mbx_matrix* m, const int32_t** cols_hub
   });
 }
 
+MBX_API int mbx_matrix_hub_columns(const mbx_matrix* m, int32_t* host_out) {
+  return guarded([&] {
+    if (m->hub_avail <= 0 || !host_out) return;
+    mbx_context* ctx = m->ctx;
+    Device dg(ctx->device);
+    MBX_CUDA(cudaMemcpyAsync(host_out, m->hub_cols, size_t(m->hub_avail) * 4,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    MBX_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 MBX_API int mbx_matrix_compact(mbx_matrix* m, const mbx_tile* t) {
   return guarded([&] {
     mbx_context* ctx = m->ctx;

@@ -98,15 +98,19 @@ namespace {
 constexpr int64_t kSampleRuns = int64_t(1) << 17;  // 32 nonzeros each (4 M samples)
 
 __global__ void count_sample_kernel(const int32_t* __restrict__ cols, int64_t nnz,
-                                    int64_t stride_runs, uint32_t* __restrict__ cnt) {
+                                    int64_t stride_runs, uint32_t* __restrict__ cnt,
+                                    uint32_t* __restrict__ cmax) {
   const int lid = threadIdx.x & 31;
   const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t runs = (nnz + 31) / 32;
+  uint32_t mx = 0;  // the largest count this thread produced
   for (int64_t r = w * stride_runs; r < runs; r += nw * stride_runs) {
     const int64_t k = r * 32 + lid;
-    if (k < nnz) atomicAdd(cnt + __ldg(cols + k), 1u);
+    if (k < nnz) mx = max(mx, atomicAdd(cnt + __ldg(cols + k), 1u) + 1u);
   }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lid == 0 && mx) atomicMax(cmax, mx);
 }
 
 // candidates: columns whose sampled count exceeds `t`
@@ -123,6 +127,144 @@ __global__ void gather_counts_kernel(const uint32_t* __restrict__ cnt,
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < k;
        i += int64_t(gridDim.x) * blockDim.x)
     out[i] = cnt[ids[i]];
+}
+
+// Histogram of the sampled counts (bins 1..kHistBins-1, the last one
+// holding every count >= kHistBins-1, whose true sum and maximum are kept
+// aside): what the selection below needs to pick the hub SET without sorting.
+constexpr int kHistBins = 8192;
+
+struct HubPick {
+  unsigned long long covered;  // sampled references of the chosen hubs
+  unsigned long long capsum;   // sum of the counts in the last bin
+  uint32_t capmax;             // largest count in the last bin (0: empty)
+  uint32_t cmax;               // largest sampled count (count_sample_kernel)
+  int32_t h;                   // hubs chosen
+  uint32_t tau;                // every count > tau is a hub ...
+  int32_t need;                // ... and the first `need` columns with count == tau
+  int32_t ties;                // columns with count == tau
+  int32_t fallback;            // ties inside the last bin: rank by sorting instead
+  int32_t pad;
+};
+
+__global__ void __launch_bounds__(512) count_hist_kernel(const uint32_t* __restrict__ cnt,
+                                                         int64_t n, uint32_t* __restrict__ hist,
+                                                         HubPick* pick, int64_t S,
+                                                         int64_t min_refs) {
+  if (int64_t(pick->cmax) * S <= min_refs) return;  // no table (counted by the sample)
+  __shared__ uint32_t h[kHistBins];
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t c = __ldcs(cnt + i);
+    if (c == 0) continue;
+    if (c >= kHistBins - 1) {
+      atomicAdd(&pick->capsum, (unsigned long long)c);
+      atomicMax(&pick->capmax, c);
+    }
+    atomicAdd(&h[c < kHistBins - 1 ? c : kHistBins - 1], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
+    if (h[i]) atomicAdd(hist + i, h[i]);
+}
+
+// One block: the hub set = the hmax columns of largest count above t (ties
+// in ascending column order), i.e. exactly what sorting by (count desc,
+// column asc) and taking the first min(hmax, #above t) picks.  pick must be
+// zeroed before count_hist_kernel.
+__global__ void __launch_bounds__(1024) hub_pick_kernel(const uint32_t* __restrict__ hist,
+                                                        uint32_t t, int64_t hmax,
+                                                        HubPick* pick, int64_t S,
+                                                        int64_t min_refs) {
+  if (int64_t(pick->cmax) * S <= min_refs) return;
+  constexpr int kPer = kHistBins / 1024;
+  using Scan = cub::BlockScan<unsigned long long, 1024>;
+  __shared__ typename Scan::TempStorage ts;
+  __shared__ uint32_t top, s_tau;
+  __shared__ unsigned long long tot;
+  __shared__ int s_h;
+  const int tid = threadIdx.x;
+  const int r = 1023 - tid;  // bins [kPer*r, kPer*r + kPer): thread 0 holds the top
+  if (tid == 0) {
+    top = 0;
+    s_h = 0;
+    s_tau = 0;
+  }
+  __syncthreads();
+  unsigned long long own = 0;
+  uint32_t hv[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int b = kPer * r + k;
+    hv[k] = hist[b];
+    if (hv[k]) atomicMax(&top, uint32_t(b));
+    if (b > int64_t(t)) own += hv[k];
+  }
+  unsigned long long above = 0;  // selectable columns in the bins above this thread's
+  Scan(ts).ExclusiveSum(own, above);
+  if (tid == 1023) tot = above + own;
+  __syncthreads();
+  if (tid == 0) pick->fallback = t >= uint32_t(kHistBins - 1) ? 1 : 0;
+  const unsigned long long want = tot < (unsigned long long)(hmax > 0 ? hmax : 0)
+                                      ? tot
+                                      : (unsigned long long)(hmax > 0 ? hmax : 0);
+  if (want > 0 && above < want && above + own >= want) {
+    // this thread's bins hold the crossing
+    unsigned long long cum = above;
+    for (int k = kPer - 1; k >= 0; --k) {
+      const int b = kPer * r + k;
+      if (b <= int64_t(t) || hv[k] == 0) continue;
+      if (cum + hv[k] >= want) {
+        s_tau = uint32_t(b);
+        s_h = int(want);
+        pick->need = int32_t(want - cum);
+        pick->ties = int32_t(hv[k]);
+        if (b == kHistBins - 1 && want - cum < hv[k]) pick->fallback = 1;
+        break;
+      }
+      cum += hv[k];
+    }
+  }
+  __syncthreads();
+  if (s_h == 0) return;  // block-uniform
+  // sampled references the hubs cover: the bins above tau + need * tau
+  const uint32_t tau = s_tau;
+  unsigned long long cov = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int b = kPer * r + k;
+    if (uint32_t(b) > tau)
+      cov += b == kHistBins - 1 ? pick->capsum : (unsigned long long)b * hv[k];
+  }
+  unsigned long long cs = 0;
+  Scan(ts).ExclusiveSum(cov, cs);
+  if (tid == 1023) {
+    pick->covered = cs + cov + (unsigned long long)pick->need * tau;
+    pick->h = s_h;
+    pick->tau = tau;
+  }
+}
+
+__global__ void flag_pick_kernel(const uint32_t* __restrict__ cnt, int64_t n, uint32_t tau,
+                                 int all_ties, uint8_t* __restrict__ flag) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t c = cnt[i];
+    flag[i] = c > tau || (all_ties && c == tau);
+  }
+}
+
+struct CountIs {
+  const uint32_t* cnt;
+  uint32_t v;
+  __device__ bool operator()(int32_t i) const { return cnt[i] == v; }
+};
+
+__global__ void set_flags_kernel(const int32_t* __restrict__ ids, int k, uint8_t* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) flag[ids[i]] = 1;
 }
 
 }  // namespace
@@ -169,26 +311,37 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   uint32_t* cnt = nullptr;
   MBX_CUDA(cudaMallocAsync(&cnt, n * 4 + 64, s));
   MBX_CUDA(cudaMemsetAsync(cnt, 0, n * 4, s));
-  count_sample_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(m->cols, m->nnz, S, cnt);
+  uint32_t* hist = nullptr;
+  HubPick* dpick = nullptr;
+  MBX_CUDA(cudaMallocAsync(&hist, kHistBins * 4 + sizeof(HubPick) + 64, s));
+  dpick = reinterpret_cast<HubPick*>(hist + kHistBins);
+  MBX_CUDA(cudaMemsetAsync(hist, 0, kHistBins * 4 + sizeof(HubPick), s));
+  count_sample_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(m->cols, m->nnz, S, cnt,
+                                                                  &dpick->cmax);
   ++ctx->launches;
-  // no column can reach even the shared-line threshold (a stencil: at most
-  // 27 references per column): no table, nothing more to do
-  uint32_t* dmax = nullptr;
-  size_t tb = 0;
-  MBX_CUDA(cub::DeviceReduce::Max(nullptr, tb, cnt, dmax, n, s));
-  void* temp = nullptr;
-  MBX_CUDA(cudaMallocAsync(&temp, tb + 64, s));
-  MBX_CUDA(cudaMallocAsync(&dmax, 64, s));
-  MBX_CUDA(cub::DeviceReduce::Max(temp, tb, cnt, dmax, n, s));
-  uint32_t cmax = 0;
-  MBX_CUDA(cudaMemcpyAsync(&cmax, dmax, 4, cudaMemcpyDeviceToHost, s));
+  // one pass over the counts: their histogram, then the hub set's
+  // threshold (hub_pick_kernel) -- one host synchronisation for the lot
+  const int64_t cap_lines = m->nnz / (ctas * 50);
+  const uint32_t t = uint32_t(min_refs_shared / S);
+  const int64_t hmax = std::min<int64_t>(slots, cap_lines << (m->precision == MBX_F32 ? 5 : 4));
+  count_hist_kernel<<<unsigned(ctx->sm_count) * 2, 512, 0, s>>>(cnt, n, hist, dpick, S,
+                                                                int64_t(min_refs));
+  hub_pick_kernel<<<1, 1024, 0, s>>>(hist, t, hmax, dpick, S, int64_t(min_refs));
+  ctx->launches += 2;
+  MBX_CUDA(cudaGetLastError());
+  HubPick pick{};
+  MBX_CUDA(cudaMemcpyAsync(&pick, dpick, sizeof(HubPick), cudaMemcpyDeviceToHost, s));
   MBX_CUDA(cudaStreamSynchronize(s));
-  cudaFreeAsync(temp, s);
-  cudaFreeAsync(dmax, s);
+  cudaFreeAsync(hist, s);
+  const uint32_t cmax = pick.cmax;
+  size_t tb = 0;
+  void* temp = nullptr;
   auto done = [&] {
     cudaFreeAsync(cnt, s);
     MBX_CUDA(cudaStreamSynchronize(s));
   };
+  // no column can reach even the shared-line threshold (a stencil: at most
+  // 27 references per column): no table, nothing more to do
   if (int64_t(cmax) * S <= int64_t(min_refs)) return done();
   m->hub_prefix = 0;
   if (m->vmap) {
@@ -203,7 +356,6 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
     MBX_CUDA(cudaStreamSynchronize(s));
     if (cand > 0) hc[cand - 1] = raw[cand - 1];
     for (int i = cand - 2; i >= 0; --i) hc[i] = std::max(raw[i], hc[i + 1]);
-    const int64_t cap_lines = m->nnz / (ctas * 50);
     const int line_shift = m->precision == MBX_F32 ? 5 : 4;
     int h = 0;
     int64_t covered = 0;
@@ -223,9 +375,49 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
     }
     return done();
   }
-  // candidates: every column whose (scaled) sampled count passes the lower
-  // threshold, ranked by count descending (stable: ties in column order)
-  const uint32_t t = uint32_t(min_refs_shared / S);
+  if (!pick.fallback) {
+    // the hub set straight from the threshold: every column counted above
+    // tau, plus the first `need` (in column order) counted exactly tau --
+    // selected in ascending column order, which is the slot order
+    const int h = pick.h;
+    if (h > 0) {
+      const unsigned grid = unsigned(ctx->sm_count) * 8;
+      uint8_t* flag = nullptr;
+      int64_t* dk = nullptr;
+      MBX_CUDA(cudaMallocAsync(&flag, n + 64, s));
+      MBX_CUDA(cudaMallocAsync(&dk, 64, s));
+      const bool all_ties = pick.need == pick.ties;
+      flag_pick_kernel<<<grid, 256, 0, s>>>(cnt, n, pick.tau, all_ties ? 1 : 0, flag);
+      ++ctx->launches;
+      cub::CountingInputIterator<int32_t> it(0);
+      if (!all_ties) {
+        int32_t* ties = nullptr;
+        MBX_CUDA(cudaMallocAsync(&ties, size_t(pick.ties) * 4 + 64, s));
+        tb = 0;
+        MBX_CUDA(cub::DeviceSelect::If(nullptr, tb, it, ties, dk, n, CountIs{cnt, pick.tau}, s));
+        MBX_CUDA(cudaMallocAsync(&temp, tb + 64, s));
+        MBX_CUDA(cub::DeviceSelect::If(temp, tb, it, ties, dk, n, CountIs{cnt, pick.tau}, s));
+        cudaFreeAsync(temp, s);
+        set_flags_kernel<<<(pick.need + 255) / 256, 256, 0, s>>>(ties, pick.need, flag);
+        ++ctx->launches;
+        cudaFreeAsync(ties, s);
+      }
+      MBX_CUDA(cudaMallocAsync(&m->hub_cols, size_t(h) * 4 + 64, s));
+      tb = 0;
+      MBX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flag, m->hub_cols, dk, n, s));
+      MBX_CUDA(cudaMallocAsync(&temp, tb + 64, s));
+      MBX_CUDA(cub::DeviceSelect::Flagged(temp, tb, it, flag, m->hub_cols, dk, n, s));
+      cudaFreeAsync(temp, s);
+      cudaFreeAsync(flag, s);
+      cudaFreeAsync(dk, s);
+      m->hub_avail = h;
+      m->hub_coverage = std::min(1.0, double(pick.covered) * double(S) / double(m->nnz));
+    }
+    return done();
+  }
+  // (ties among counts past the histogram's last bin) candidates: every
+  // column whose (scaled) sampled count passes the lower threshold, ranked
+  // by count descending (stable: ties in column order)
   uint8_t* flag = nullptr;
   int32_t *cid = nullptr, *cid_sorted = nullptr;
   uint32_t *ccnt = nullptr, *ccnt_sorted = nullptr;
@@ -274,7 +466,6 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   // the shared-memory budget with every column referenced more than
   // min_refs_shared times, under the same 2 %-of-a-CTA's-gathers line cap
   // as a relabelled prefix.
-  const int64_t cap_lines = m->nnz / (ctas * 50);
   const int line_shift = m->precision == MBX_F32 ? 5 : 4;  // entries per 128-byte line
   int h = 0;
   int64_t covered = 0;

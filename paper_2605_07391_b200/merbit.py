@@ -362,6 +362,13 @@ class DeviceMatrix:
         _check(_lib.lib().mbx_matrix_xcache_info(self.h, C.byref(hubs), C.byref(cov)))
         return hubs.value, cov.value
 
+    def hub_columns(self) -> np.ndarray:
+        """The x hub cache's columns in slot order (ascending ids)."""
+        h = self.xcache_info()[0]
+        out = np.zeros(max(h, 1), np.int32)
+        _check(_lib.lib().mbx_matrix_hub_columns(self.h, out.ctypes.data))
+        return out[:h]
+
     def build_transition(self) -> "DeviceMatrix":
         """build_transition (solvers.hpp:36-74) on the device: P = A^T D^-1 of
         this adjacency pattern, in this matrix's precision."""

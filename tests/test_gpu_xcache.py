@@ -1,0 +1,58 @@
+"""The x hub cache's column selection (xcache.cu): the hub set is the top-h
+columns by reference count, ties in ascending column order, stored in
+ascending column order (a column's slot is its rank).  Below kSampleRuns
+runs of 32 nonzeros the sample stride is 1, so the counts the device ranks
+are the exact column counts and the set can be checked on the host."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2605_07391_b200 as mb
+
+pytestmark = pytest.mark.gpu
+
+
+def top_by_count(cols, n, h):
+    cnt = np.bincount(cols, minlength=n)
+    order = np.lexsort((np.arange(n), -cnt))  # count desc, column asc
+    return np.sort(order[:h]), cnt
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("scale", [14, 16])
+def test_hub_set_is_top_h_by_count(ctx, dtype, scale):
+    A = mb.DeviceMatrix.rmat(ctx, scale, 16, seed=2, transition=True, dtype=dtype)
+    A.build_xcache()
+    hubs = A.hub_columns()
+    h = hubs.size
+    assert h > 0
+    assert np.all(np.diff(hubs) > 0)  # ascending, unique
+    _, cols, _ = A.download(want_values=False)
+    want, cnt = top_by_count(cols, A.n_cols, h)
+    assert np.array_equal(hubs, want)
+    # and the SpMV through the table is bitwise the one without it
+    c = mb.SimtConfig.make(32, 14 if dtype == np.float32 else 7, 128)
+    t = mb.generate_tile_for(A, c)
+    x = O.hash_uniform(5, A.n_cols, -1.0, 1.0, dtype)
+    y1 = mb.spmv_merbit(A, t, c, x, mb.DualBuffer(A.n_rows, dtype)).copy()
+    A.build_xcache(0)
+    y0 = mb.spmv_merbit(A, t, c, x, mb.DualBuffer(A.n_rows, dtype))
+    assert np.array_equal(y0.view(np.uint8), y1.view(np.uint8))
+
+
+def test_capped_counts_rank_exactly(ctx):
+    """Counts past the selection histogram's last bin (>= 8191): the device
+    falls back to sorting them, still the exact top-h.  Column c is
+    referenced 8200 + c times (c < 300); a 100-hub cap picks 200..299."""
+    counts = 8200 + np.arange(300)
+    n_rows = int(counts.max())
+    rows = [np.nonzero(counts > r)[0].astype(np.int32) for r in range(n_rows)]
+    ro = np.zeros(n_rows + 1, np.int64)
+    ro[1:] = np.cumsum([len(r) for r in rows])
+    cols = np.concatenate(rows)
+    vals = np.ones(cols.size, np.float32)
+    A = mb.DeviceMatrix.from_csr(ctx, O.Csr(n_rows, 300, ro, cols, vals))
+    A.build_xcache(100)
+    assert np.array_equal(A.hub_columns(), np.arange(200, 300))
+    A.build_xcache(300)
+    assert np.array_equal(A.hub_columns(), np.arange(300))
