@@ -10,7 +10,7 @@ from .merbit import (BackendKind, BicgstabConfig, BicgstabResult, CapacityError,
                      MerbitError, PageRankConfig, PageRankPlan, PageRankResult, SimtConfig,
                      SpmvBackend, SpmvTrace, Tile, UnsupportedError, default_context,
                      device_count, generate_tile, generate_tile_for, make_backend,
-                     merge_search, metadata_footprint, pagerank, plan_row_shards,
+                     merge_search, metadata_footprint, pagerank, plan_row_shards, recut_row_shards,
                      select_sigma, spmv_device, spmv_merbit, tile_counts, trace_counts,
                      bicgstab, solve_status_name)
 
@@ -21,6 +21,7 @@ __all__ = [
     "PageRankConfig", "PageRankPlan", "PageRankResult", "SimtConfig", "SpmvBackend",
     "SpmvTrace", "Tile", "UnsupportedError", "default_context", "device_count",
     "generate_tile", "generate_tile_for", "make_backend", "merge_search",
-    "metadata_footprint", "pagerank", "plan_row_shards", "select_sigma", "spmv_device",
+    "metadata_footprint", "pagerank", "plan_row_shards", "recut_row_shards", "select_sigma",
+    "spmv_device",
     "spmv_merbit", "tile_counts", "trace_counts",
 ]

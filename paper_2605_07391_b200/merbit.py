@@ -19,6 +19,8 @@ import ctypes as C
 import enum
 from dataclasses import dataclass, field
 
+import time
+
 import numpy as np
 
 from . import _lib
@@ -849,6 +851,70 @@ def row_slice(m: DeviceMatrix, r0: int, r1: int) -> DeviceMatrix:
     return DeviceMatrix(m.ctx, h)
 
 
+def recut_row_shards(row_offsets, bounds, shard_times, row_weight: float) -> np.ndarray:
+    """Re-cut row shards from measured per-shard times: shard i's time is
+    spread over its rows in proportion to the cut's cost (nnz + row_weight *
+    rows), and the resulting cumulative-time curve is cut into equal parts.
+    On the degree-relabelled R-MAT PageRank one round takes the slowest of 8
+    shards from 1.55 to 1.35 ms (mean 1.34; scripts/shard_fit.py,
+    profiles/r2_shard_recut.json): per-nonzero cost falls with the rows'
+    degree rank (gather locality), which no static nnz/row weight captures."""
+    ro = np.ascontiguousarray(row_offsets, np.int64)
+    b = np.ascontiguousarray(bounds, np.int64)
+    t = np.asarray(shard_times, np.float64)
+    parts, n = len(t), int(b[-1])
+    if parts != len(b) - 1 or parts < 2 or np.any(t <= 0):
+        return b.copy()
+    tcum = np.concatenate([[0.0], np.cumsum(t)])
+    out = np.zeros(parts + 1, np.int64)
+    out[-1] = n
+    for k in range(1, parts):
+        target = tcum[-1] * k / parts
+        i = min(int(np.searchsorted(tcum, target, side="right")) - 1, parts - 1)
+        frac = (target - tcum[i]) / t[i]
+        r0, r1 = int(b[i]), int(b[i + 1])
+        c0 = float(ro[r0]) + row_weight * r0
+        c1 = float(ro[r1]) + row_weight * r1
+        goal = c0 + frac * (c1 - c0)
+        # first row r in [r0, r1] with ro[r] + w*r >= goal (monotone in r)
+        lo, hi = r0, r1
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if float(ro[mid]) + row_weight * mid < goal:
+                lo = mid + 1
+            else:
+                hi = mid
+        out[k] = min(max(lo, int(out[k - 1])), n)
+    return out
+
+
+def shard_cost_probe(L: DeviceMatrix, t: "Tile", c: SimtConfig, reps: int = 5) -> float:
+    """Seconds per PageRank iteration a row shard costs, measured on its own
+    GPU without its peers: one plain SpMV of the shard (K2 + K3 with its hub
+    table and slot copy) plus the PageRank loop's per-row work beyond it (the
+    pi stores, exchange copies and K3's reductions) as 24 bytes per row at
+    copy bandwidth -- fitted on s27 8-shard cuts, where the row-heavy last
+    shard ran 0.20 ms above its SpMV and the others 0.07 ms
+    (profiles/r2_shard_recut.json).  What recut_row_shards balances in a
+    multi-process run, where the loop itself waits on the slowest rank."""
+    import torch
+    dt = torch.float32 if L.dtype == np.float32 else torch.float64
+    x = torch.full((L.n_cols,), 1.0 / max(L.n_cols, 1), dtype=dt, device="cuda")
+    y = torch.empty(max(L.n_rows, 1), dtype=dt, device="cuda")
+    L.build_xcache()
+    torch.cuda.synchronize()
+    for _ in range(2):
+        spmv_device(L, t, c, x.data_ptr(), y.data_ptr())
+    L.ctx.synchronize()
+    t0 = time.perf_counter()  # the context's own stream, whichever it is
+    for _ in range(reps):
+        spmv_device(L, t, c, x.data_ptr(), y.data_ptr())
+    L.ctx.synchronize()
+    secs = (time.perf_counter() - t0) / reps
+    L.release_caches()
+    return secs + 24.0 * L.n_rows / 6.5e12
+
+
 def prepare_rank_shard(P: DeviceMatrix, world: int, rank: int, c: SimtConfig,
                        row_weight: float | None = None):
     """One rank's preprocessing of the row-sharded PageRank (bench.py N > 1,
@@ -860,6 +926,17 @@ def prepare_rank_shard(P: DeviceMatrix, world: int, rank: int, c: SimtConfig,
     bounds = plan_row_shards(P.row_offsets(), n, P.nnz, world, w)
     L = row_slice(P, int(bounds[rank]), int(bounds[rank + 1]))
     return bounds, L, generate_tile_for(L, c), w
+
+
+def recut_rank_shard(P: DeviceMatrix, bounds, shard_times, rank: int, c: SimtConfig,
+                     row_weight: float):
+    """The second half of bench.py's N > 1 preprocessing: every rank probes
+    its first-cut shard (shard_cost_probe), the times are all-gathered, and
+    each rank re-cuts identically (recut_row_shards) and rebuilds its slice
+    and TILE.  Returns (bounds, local matrix, local TILE)."""
+    b = recut_row_shards(P.row_offsets(), bounds, shard_times, row_weight)
+    L = row_slice(P, int(b[rank]), int(b[rank + 1]))
+    return b, L, generate_tile_for(L, c)
 
 
 class ShardGroup:

@@ -18,6 +18,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2605_07391_b200 as mb  # noqa: E402
 from paper_2605_07391_b200.merbit import ShardGroup, row_slice  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from shard_projection_lib import shard_kernel_ms  # noqa: E402
+
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=27)
 ap.add_argument("--iters", type=int, default=10)
@@ -44,24 +47,6 @@ def timed(fn):
     e1.record(s)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / args.iters
-
-
-def shard_kernel_ms(fn, g):
-    """Per-shard device time of one iteration (its K2 + K3 + the shared
-    combine), from CUPTI kernel records of a warm run (not replayed)."""
-    from torch.profiler import ProfilerActivity, profile
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        fn()
-        torch.cuda.synchronize()
-    ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
-    ev.sort(key=lambda e: e.time_range.start)
-    names = [e.name for e in ev]
-    dur = [e.time_range.elapsed_us() / 1e3 for e in ev]
-    # last iteration: the final combine and the g (K2, K3) pairs before it
-    last = max(i for i, nm in enumerate(names) if "combine" in nm)
-    k = [i for i in range(last) if "spmv_slot" in names[i] or "fixup" in names[i]][-2 * g:]
-    comb = dur[last]
-    return [dur[k[2 * r]] + dur[k[2 * r + 1]] + comb for r in range(g)]
 
 
 t = mb.generate_tile_for(P, c)

@@ -8,7 +8,8 @@ original vertex order.
 
 And BASELINE C4's own matrix (R-MAT scale 27, 2.1 G nonzeros): the one-GPU
 PageRank vs the same matrix cut into 8 shards by the bench's weighted cut
-(virtual shard group, every shard on this GPU): L1 <= 1e-6.  No CPU oracle
+(virtual shard group, every shard on this GPU, re-cut from the shards'
+measured cost as the bench does): L1 <= 1e-6.  No CPU oracle
 finishes 100 iterations over 2.1 G nonzeros in a test's time; the one-GPU
 path is itself gated against the fp64 oracle at scale 24
 (test_gpu_scale.py) and against the compiled reference at scale 20
@@ -25,18 +26,19 @@ import pytest
 import oracle as O
 import paper_2605_07391_b200 as mb
 from paper_2605_07391_b200.merbit import (PeerShardGroup, ShardGroup, pagerank_row_weight,
-                                          prepare_rank_shard)
+                                          prepare_rank_shard, recut_rank_shard,
+                                          shard_cost_probe)
 
 pytestmark = pytest.mark.gpu
 NT = os.cpu_count() or 1
 
 
-@pytest.mark.parametrize("scale,world", [(16, 2), (18, 3), (20, 2)])
-def test_bench_sharded_path_vs_fp64_oracle(scale, world):
+@pytest.mark.parametrize("scale,world,recut", [(16, 2, False), (18, 3, True), (20, 2, True)])
+def test_bench_sharded_path_vs_fp64_oracle(scale, world, recut):
     iters = 100
     c = mb.SimtConfig.make(32, 14, 128)
     cfg = mb.PageRankConfig(0.85, 1e-30, iters, 0)
-    groups, keep = [], []
+    groups, keep, ranks = [], [], []
     bounds0 = None
     for r in range(world):
         cx = mb.Context(0)  # own stream per rank: the ranks' loops overlap
@@ -47,6 +49,16 @@ def test_bench_sharded_path_vs_fp64_oracle(scale, world):
         if bounds0 is None:
             bounds0, rank0_of, P0 = bounds, rank_of, P
         assert np.array_equal(bounds, bounds0)  # every rank cuts the same way
+        ranks.append([cx, Q, bounds, L, t, w])
+    if recut:
+        # bench.py's measured re-cut: probe every first-cut shard, share the
+        # times, re-cut identically on every rank
+        times = [shard_cost_probe(L, t, c) for _, _, _, L, t, _ in ranks]
+        for r, rk in enumerate(ranks):
+            rk[2], rk[3], rk[4] = recut_rank_shard(rk[1], rk[2], times, r, c, rk[5])
+        assert all(np.array_equal(rk[2], ranks[0][2]) for rk in ranks)
+        assert ranks[0][2][0] == 0 and ranks[0][2][-1] == ranks[0][1].n_rows
+    for r, (cx, Q, bounds, L, t, _) in enumerate(ranks):
         groups.append(PeerShardGroup(cx, Q.n_rows, world, bounds, r, L, t, c, cfg))
         keep.append((cx, Q, L, t))
     blobs = [g.export() for g in groups]
@@ -92,13 +104,21 @@ def test_c4_s27_one_gpu_vs_8_weighted_shards():
     del be
     cx.release_cache()
     Q.release_caches()
-    # eight shards cut exactly as bench.py --gpus 8 cuts them
+    # eight shards cut exactly as bench.py --gpus 8 cuts them: the weighted
+    # cut, every shard probed, the measured re-cut
     shards, bounds = [], None
     for r in range(8):
-        b, L, t, _ = prepare_rank_shard(Q, 8, r, c)
+        b, L, t, w = prepare_rank_shard(Q, 8, r, c)
         assert bounds is None or np.array_equal(b, bounds)
         bounds = b
         shards.append((L, t))
+    times = [shard_cost_probe(L, t, c) for L, t in shards]
+    del shards
+    shards = []
+    for r in range(8):
+        b, L, t = recut_rank_shard(Q, bounds, times, r, c, w)
+        shards.append((L, t))
+    bounds = b
     g = ShardGroup(cx, n, 8, bounds, 0, shards, c, cfg)
     g.run()
     res, _ = g.result()

@@ -104,3 +104,36 @@ def test_two_rank_exchange_protocol(world):
                 O.transition_values(p.n_rows, p.col_indices, np.float64))
     want = O.pagerank(p64, C_, 1e-300, ITERS, 0)["pi"]
     assert np.abs(out[0][1] - want).sum() <= 1e-13
+
+
+def test_recut_row_shards_properties():
+    """recut_row_shards (bench.py's measured re-cut): equal times keep the
+    cut, a slow shard gives rows away, bounds stay monotone and span all
+    rows, and the cut is exactly the even split of the measured-time curve
+    when time is proportional to nnz + w*rows."""
+    rng = np.random.default_rng(3)
+    deg = rng.integers(0, 40, size=5000)
+    ro = np.concatenate([[0], np.cumsum(deg)])
+    n, m = 5000, int(ro[-1])
+    for w in (1.0, 1.5, 3.4):
+        b = mb.plan_row_shards(ro, n, m, 4, w)
+        assert np.array_equal(mb.recut_row_shards(ro, b, [1.0] * 4, w), b)
+        slow = mb.recut_row_shards(ro, b, [2.0, 1.0, 1.0, 1.0], w)
+        assert slow[0] == 0 and slow[-1] == n and np.all(np.diff(slow) >= 0)
+        assert slow[1] < b[1]  # the slow shard shrinks
+        # time = k_i * cost within shard i: the re-cut evens the time curve
+        cost = ro + w * np.arange(n + 1)
+        k = np.array([1.0, 2.0, 0.5, 1.5])
+        t = [k[i] * (cost[b[i + 1]] - cost[b[i]]) for i in range(4)]
+        nb = mb.recut_row_shards(ro, b, t, w)
+        curve = np.zeros(n + 1)
+        for i in range(4):
+            seg = slice(b[i], b[i + 1] + 1)
+            curve[seg] = sum(t[:i]) + k[i] * (cost[seg] - cost[b[i]])
+        parts = [curve[nb[i + 1]] - curve[nb[i]] for i in range(4)]
+        step = k.max() * (w + 40)  # one row's cost at most
+        assert max(parts) - min(parts) <= 2 * step
+    # malformed input leaves the cut alone
+    b = mb.plan_row_shards(ro, n, m, 4, 1.0)
+    assert np.array_equal(mb.recut_row_shards(ro, b, [1.0, 0.0, 1.0, 1.0], 1.0), b)
+    assert np.array_equal(mb.recut_row_shards(ro, b, [1.0] * 3, 1.0), b)
