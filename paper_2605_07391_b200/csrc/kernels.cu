@@ -837,19 +837,32 @@ struct SlotParams {
 };
 
 // gather x for the steps in `mask` (bit i: slot i is a live element)
+#ifndef MBX_GATHER
+#define MBX_GATHER 0
+#endif
 template <typename T, int SIGMA, bool HUB>
 __device__ __forceinline__ void gather_slots(const T* __restrict__ x, const T* hub,
                                              const int (&col)[SIGMA], uint32_t mask,
                                              T (&xv)[SIGMA]) {
 #pragma unroll
   for (int i = 0; i < SIGMA; ++i) {
-    xv[i] = T(0);
-    if ((mask >> i) & 1u) {
-      const int c = col[i];
-      if (HUB && c < 0)
-        xv[i] = hub[c & 0x7FFFFFFF];
-      else
-        xv[i] = __ldg(x + c);
+    const int c = col[i];
+    if (MBX_GATHER == 1) {
+      // every slot, no branches: a dead slot (column 0) reads x[0] (an L1
+      // hit) and its product is masked by the walk; a hub reference is a
+      // generic load from shared memory
+      const T* p = (HUB && c < 0) ? hub + (c & 0x7FFFFFFF) : x + c;
+      xv[i] = *p;
+    } else if (MBX_GATHER == 2) {
+      xv[i] = (HUB && c < 0) ? hub[c & 0x7FFFFFFF] : __ldg(x + c);
+    } else {
+      xv[i] = T(0);
+      if ((mask >> i) & 1u) {
+        if (HUB && c < 0)
+          xv[i] = hub[c & 0x7FFFFFFF];
+        else
+          xv[i] = __ldg(x + c);
+      }
     }
   }
 }
@@ -1013,13 +1026,20 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
       else
         load_slot_cols<SIGMA, G>(cb, lid, col, pol);
     };
-    if (PF && lid == 0 && ci + 1 < nc) {
-      // one bulk L2 prefetch per stream for the next tile: its column and
-      // value slots then arrive at L2 latency instead of DRAM latency
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cb + TS),
+    if (PF && lid == 0 && cnext >= 0) {
+      // one bulk L2 prefetch per stream for the next tile this warp walks
+      // (the next one of this range, or the first of its next range, with
+      // that range's tile entries and descriptors): its slots then arrive at
+      // L2 latency instead of DRAM latency
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.scols + cnext * TS),
                    "r"(unsigned(TS * 4)));
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vb + TS),
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.svals + cnext * TS),
                    "r"(unsigned(TS * sizeof(T))));
+      if (ci + 1 == nc) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p.lane_desc + cnext * 32));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p.tile_x + cnext));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p.tile_y + cnext));
+      }
     }
     if (ty0 & kLongRowMask) {
       // marked tile: one row; lane-strided subtotals + halving tree
