@@ -1652,12 +1652,15 @@ __global__ void __launch_bounds__(256) gen_tile_scan_kernel(
   const int64_t r1 = imin64(bnd[blockIdx.x + 1], n - 1);  // last row that can end inside
   reinterpret_cast<uint4*>(fl)[tid] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
+  const float inv_sigma = 1.0f / float(sigma);
 #pragma unroll 4
   for (int64_t r = y0 + tid; r <= r1; r += 256) {
     const int64_t p = int64_t(__ldg(ro + r + 1)) + r - d0;  // e_r - d0 >= 0
     if (p < span) {
-      const int q = int(p);  // < kK1Lanes * sigma
-      const int l = q / sigma;
+      const int q = int(p);  // < kK1Lanes * sigma <= 2^15: q / sigma from the
+      int l = __float2int_rz(float(q) * inv_sigma);  // float reciprocal, corrected
+      l += (l + 1) * sigma <= q ? 1 : 0;
+      l -= l * sigma > q ? 1 : 0;
       atomicOr(&fl[l], 1u << (q - l * sigma));
     }
   }
@@ -1687,14 +1690,17 @@ __global__ void __launch_bounds__(256) gen_tile_scan_kernel(
   for (int k = 0; k < 4; ++k) {
     const int l = 4 * tid + k;
     const int ld = l & ~(omega - 1);  // the tile's first lane
+    const int pl = pre[l], pld = pre[ld];
+    // offsets from the tile's start point, in 32 bits: rows and nonzeros
+    // consumed by the lanes before this one in its tile
+    const int dy = pl - pld;
+    const int dx = (l - ld) * sigma - dy;
+    d[k] = (f[k] << (2 * ob)) | (uint32_t(dy) << ob) | uint32_t(dx);
     const int64_t j = j0 + l;
-    const int64_t y = y0 + pre[l];
-    const int64_t x = j * sigma - y;
-    const int64_t tsy = y0 + pre[ld];
-    const int64_t tsx = (j0 + ld) * sigma - tsy;
-    d[k] = (f[k] << (2 * ob)) | (uint32_t(y - tsy) << ob) | uint32_t(x - tsx);
     if (l == ld && j < lane_num) {
-      const bool any_down = pre[imin64(ld + omega, kK1Lanes)] > pre[ld];
+      const int64_t tsy = y0 + pld;
+      const int64_t tsx = j * sigma - tsy;
+      const bool any_down = pre[imin64(ld + omega, kK1Lanes)] > pld;
       tile_x[j / omega] = uint32_t(tsx);
       tile_y[j / omega] = uint32_t(tsy) | (any_down ? 0u : kLongRowMask);
     }
