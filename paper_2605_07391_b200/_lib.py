@@ -196,7 +196,12 @@ def lib():
         except ImportError:
             pass
         L = C.CDLL(LIB_PATH)
+        # an A/B build of an older revision (MBX_LIB_PATH) may lack newer
+        # entry points: bind what it has; the in-tree library must have all
+        ab_build = bool(os.environ.get("MBX_LIB_PATH"))
         for name, (args, res) in SIGNATURES.items():
+            if ab_build and not hasattr(L, name):
+                continue
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = res

@@ -73,7 +73,7 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   if (m->hub_cols && m->hub_avail > 0 && g.omega == 32 && ctx->tuning.max_hubs != 0 &&
       (ctx->tuning.max_hubs < 0 || ctx->tuning.max_hubs >= m->hub_avail)) {
     const int slots = max_hub_slots(ctx, g.warps_per_cta, ctx->tuning.ctas_per_sm, g.sigma,
-                                    m->precision);
+                                    m->precision, m->n_cols);
     if (slots >= m->hub_avail) g.hub_count = m->hub_avail;
   }
   // lane-major slot copy for this TILE (built once, outside any capture)

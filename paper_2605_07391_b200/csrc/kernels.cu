@@ -2092,16 +2092,28 @@ size_t spmv_smem_bytes(const Geometry& g, int precision) {
 
 int default_sigma(int precision) { return precision == MBX_F32 ? 14 : 7; }
 
+// Shared memory K2 takes per SM by default: what it does not take stays L1
+// (256 KB unified per SM).  Measured on degree-relabelled R-MAT PageRank
+// fp32 (scripts/prof/pr_iter.py, SMEM=): up to x = 128 MB (s25) the hubs
+// win -- 160 KB: s24 790 vs 830 us at 128 KB, s25 1693 vs 1745 us; at
+// 256 MB (s26) 128 KB and 96 KB tie (3.82 ms, 160 KB 4.02 ms); at 512 MB
+// (s27) 96 KB is best (9.05 vs 9.21 ms at 128 KB, 10.0 ms at 160 KB).
+int default_smem_budget(int precision, int64_t n_cols) {
+  const int64_t xbytes = n_cols * int64_t(value_size(precision));
+  if (xbytes > (int64_t(384) << 20)) return 96 * 1024;
+  if (xbytes > (int64_t(192) << 20)) return 128 * 1024;
+  return precision == MBX_F32 ? 160 * 1024 : 128 * 1024;
+}
+
 int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, int sigma,
-                  int precision) {
+                  int precision, int64_t n_cols) {
   int per_sm = 0, optin = 0;
   MBX_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
                                   ctx->device));
   MBX_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const int64_t reserve = 1024;  // per-CTA system reservation
   const int budget = ctx->tuning.smem_per_sm > 0 ? ctx->tuning.smem_per_sm
-                     : precision == MBX_F32       ? 160 * 1024
-                                                  : 128 * 1024;
+                                                  : default_smem_budget(precision, n_cols);
   if (budget < per_sm) per_sm = budget;
   int64_t per_cta = per_sm / ctas_per_sm - reserve;
   if (per_cta > optin) per_cta = optin;

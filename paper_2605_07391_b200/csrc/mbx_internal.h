@@ -229,8 +229,12 @@ void* host_scratch(mbx_context* ctx, size_t bytes);
 Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
                        int block_size);
 size_t spmv_smem_bytes(const Geometry& g, int precision);
+// hub slots the K2 shared-memory budget leaves for a matrix with n_cols
+// columns (the budget shrinks as x outgrows L2: the L1 it leaves matters more)
 int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, int sigma,
-                  int precision);
+                  int precision, int64_t n_cols);
+// K2's default shared memory per SM (Tuning::smem_per_sm = -1)
+int default_smem_budget(int precision, int64_t n_cols);
 void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs);
 // slot_of[c] = hub slot of column c or -1 (n_cols int32; the caller frees)
 // hub lookup words (hub_cols ascending): .x = hub bits of columns 32w..32w+31,

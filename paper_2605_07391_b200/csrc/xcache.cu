@@ -286,7 +286,7 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   ++m->gen;      // and the graphs captured over the old buffers
   const Tuning& tu = ctx->tuning;
   int slots = max_hub_slots(ctx, tu.warps_per_cta, tu.ctas_per_sm,
-                            m->precision == MBX_F32 ? 14 : 7, m->precision);
+                            m->precision == MBX_F32 ? 14 : 7, m->precision, m->n_cols);
   if (max_hubs >= 0) slots = std::min(slots, max_hubs);
   if (slots <= 0 || m->nnz == 0 || m->n_cols == 0) return;
   const int64_t n = m->n_cols;
