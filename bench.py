@@ -440,8 +440,9 @@ def main():
                     help="skip the extras (N = 1: SpMV f32/f64, C1, C3, C5, C4 on one GPU; "
                          "N > 1: the one-GPU anchor, the NCCL exchange, C2 sharded)")
     ap.add_argument("--spmv-reps", type=int, default=30)
-    ap.add_argument("--no-recut", action="store_true",
-                    help="N > 1: keep the weighted cut (no measured re-cut of the row shards)")
+    ap.add_argument("--recut", action="store_true",
+                    help="N > 1: re-cut the row shards from a per-rank cost probe "
+                         "(off by default: the weighted cut measured better at s27)")
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
                     help="N > 1: fused = the commit stores into the peers' buffers (P2P, "
                          "one device barrier per iteration); nccl = one ncclAllGather")
@@ -524,12 +525,12 @@ def main():
         return ShardGroup(ctx, n_global, world, bounds, rank, [(Lm, tile)], cfg, prc, ids[0])
 
     def cut_rank_shard(M):
-        """bench's row cut of M for this rank: the weighted cut, then (unless
-        --no-recut) the measured re-cut -- every rank probes its first-cut
-        shard on its own GPU (one plain SpMV + the loop's per-row work), the
-        times are shared, and every rank re-cuts the same way."""
+        """bench's row cut of M for this rank: the weighted cut, then (with
+        --recut) the measured re-cut -- every rank probes its first-cut shard
+        on its own GPU (one plain SpMV + the loop's per-row work), the times
+        are shared, and every rank re-cuts the same way."""
         b, L, t, w = prepare_rank_shard(M, world, rank, cfg)
-        if args.no_recut:
+        if not args.recut:
             return b, L, t, None
         probe = shard_cost_probe(L, t, cfg)
         times = [None] * world
@@ -838,7 +839,7 @@ def main():
                                   "degree" else "natural") + "), preprocessing amortised"
                                + (f", {world} row shards (weighted cut, row weight "
                                   f"{mb.merbit.pagerank_row_weight(n)}"
-                                  + ("" if args.no_recut else ", re-cut from measured shard cost")
+                                  + (", re-cut from measured shard cost" if args.recut else "")
                                   + "), exchange: "
                                   + ("fused P2P stores in the commit" if args.exchange == "fused"
                                      else "ncclAllGather") if world > 1 else ""),

@@ -161,10 +161,11 @@ PAGERANK_ROW_WEIGHT = 3.4
 def pagerank_row_weight(n_vertices: int, value_bytes: int = 4) -> float:
     """Row weight for plan_row_shards.  Once pi no longer sits in L2 (s27:
     512 MB) each gathered nonzero costs more relative to a row's commit; with
-    round 2's store-only commit the measured best cut there is ~1.5 (slowest
-    of 8 shards 1.519 ms vs 1.574 at 2.5 and 1.587 at 3.0,
-    profiles/r2_shard_projection.json); at s24 (64 MB of pi) 3.4."""
-    return PAGERANK_ROW_WEIGHT if n_vertices * value_bytes <= (96 << 20) else 1.5
+    round 2's store-only commit and the K2 shared-memory budget that shrinks
+    with x, the measured best cut at s27 is 2.5 (slowest of 8 shards 1.186 ms
+    vs 1.245 at 2.0, 1.215 at 3.0, 1.452 at 1.5; profiles/r2_shard_recut.json);
+    at s24 (64 MB of pi) 3.4."""
+    return PAGERANK_ROW_WEIGHT if n_vertices * value_bytes <= (96 << 20) else 2.5
 
 
 def plan_row_shards(row_offsets, n_rows: int, nnz: int, parts: int,
@@ -855,10 +856,11 @@ def recut_row_shards(row_offsets, bounds, shard_times, row_weight: float) -> np.
     """Re-cut row shards from measured per-shard times: shard i's time is
     spread over its rows in proportion to the cut's cost (nnz + row_weight *
     rows), and the resulting cumulative-time curve is cut into equal parts.
-    On the degree-relabelled R-MAT PageRank one round takes the slowest of 8
-    shards from 1.55 to 1.35 ms (mean 1.34; scripts/shard_fit.py,
-    profiles/r2_shard_recut.json): per-nonzero cost falls with the rows'
-    degree rank (gather locality), which no static nnz/row weight captures."""
+    With the shards' own measured times one round took the slowest of 8 s27
+    shards from 1.53 to 1.35 ms (mean 1.34) under a fixed 160 KB hub budget;
+    bench.py --recut feeds it shard_cost_probe times instead, which track the
+    group's cost less well since the budget depends on x
+    (profiles/r2_shard_recut.json)."""
     ro = np.ascontiguousarray(row_offsets, np.int64)
     b = np.ascontiguousarray(bounds, np.int64)
     t = np.asarray(shard_times, np.float64)
