@@ -244,8 +244,11 @@ MBX_API int mbx_matrix_destroy(mbx_matrix* m);
 /* x hub cache (no reference counterpart; an sm_100a-specific preprocessing
  * step next to generate_tile): ranks columns by reference count and stages
  * the most referenced x entries in shared memory during SpMV.  Results are
- * bitwise identical with and without it.  max_hubs < 0: as many as the
- * shared-memory budget of the context tuning allows; 0: remove the cache. */
+ * bitwise identical with and without it.  max_hubs < 0: automatic -- no
+ * table for a matrix with fewer than 4096 nonzeros per resident K2 warp
+ * (there the SpMV is latency-bound and a table does not pay), else as many
+ * hubs as the shared-memory budget of the context tuning allows; > 0: at
+ * most that many, whatever the size; 0: remove the cache. */
 /* Slot copy currently cached on the matrix: slots (0 if none) and the
  * seconds its one-time build took (part of preprocessing). */
 MBX_API int mbx_matrix_slot_info(const mbx_matrix* m, int64_t* slots, double* seconds);

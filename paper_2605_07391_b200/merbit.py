@@ -213,7 +213,8 @@ class Context:
 
     def set_tuning(self, warps_per_cta: int = 32, ctas_per_sm: int = 1, max_hubs: int = -1,
                    smem_per_sm: int | None = None, prefetch: int | None = None):
-        """K2 launch shape (persistent grid), x hub-cache cap (-1 auto, 0 off),
+        """K2 launch shape (persistent grid), x hub-cache cap (-1 automatic, 0 off,
+        > 0 a cap that also forces a table on small matrices),
         shared-memory budget per SM and the next tile's staging (0 none,
         1 L2 prefetch, 2 TMA bulk copy into shared memory, -1 auto)."""
         _check(_lib.lib().mbx_context_set_tuning(self.h, warps_per_cta, ctas_per_sm, max_hubs))
@@ -355,7 +356,10 @@ class DeviceMatrix:
 
     def build_xcache(self, max_hubs: int = -1) -> float:
         """Rank columns by reference count and stage the hottest x entries in
-        shared memory during SpMV (results bitwise unchanged).  Returns seconds."""
+        shared memory during SpMV (results bitwise unchanged).  max_hubs < 0:
+        automatic (no table below 4096 nonzeros per resident K2 warp, where
+        it does not pay); > 0: at most that many whatever the size; 0: none.
+        Returns seconds."""
         secs = C.c_double()
         _check(_lib.lib().mbx_matrix_build_xcache(self.ctx.h, self.h, max_hubs, C.byref(secs)))
         return secs.value

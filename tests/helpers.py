@@ -4,6 +4,10 @@ import hashlib
 import numpy as np
 
 CONFIGS = [(32, 14, 128), (32, 7, 128), (4, 4, 16)]
+# build_xcache(FORCE_HUBS): a hub table whatever the matrix size (the
+# automatic mode skips matrices too small for it to pay, i.e. every small
+# test matrix; the hub code paths are tested with it forced)
+FORCE_HUBS = 1 << 30
 
 
 def h(*arrays):

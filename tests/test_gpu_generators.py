@@ -5,6 +5,7 @@ import pytest
 
 import oracle as O
 import paper_2605_07391_b200 as mb
+from helpers import FORCE_HUBS
 
 pytestmark = pytest.mark.gpu
 
@@ -68,7 +69,7 @@ def test_powerlaw_c3_structure_and_spmv(ctx, dtype):
     sigma = 7 if dtype == np.float64 else 14
     c = mb.SimtConfig.make(32, sigma, 128)
     t = mb.generate_tile_for(m, c)
-    m.build_xcache()
+    m.build_xcache(FORCE_HUBS)
     tr = mb.trace_counts(t)
     assert tr.fast_tiles > 0 and tr.skipped_tiles >= 0
     x = O.hash_uniform(5, n, -1.0, 1.0, dtype)

@@ -5,6 +5,7 @@ import pytest
 
 import oracle as O
 import paper_2605_07391_b200 as mb
+from helpers import FORCE_HUBS
 
 pytestmark = pytest.mark.gpu
 
@@ -297,7 +298,8 @@ def test_plan_recaptures_after_matrix_buffers_change(ctx):
     ro0, cols0, vals0 = P.download()
     plan.run()
     r1, h1 = plan.result(want_history=True)
-    P.build_xcache()
+    P.build_xcache(FORCE_HUBS)
+    assert P.xcache_info()[0] > 0
     torch.cuda.synchronize()
     mb.spmv_device(P, t2, c2, xd.data_ptr(), yd.data_ptr())
     ctx.synchronize()

@@ -21,6 +21,7 @@ import torch
 
 import oracle as O
 import paper_2605_07391_b200 as mb
+from helpers import FORCE_HUBS
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 NT = os.cpu_count() or 1
@@ -62,7 +63,7 @@ def test_s20_pagerank_vs_reference_pagerank_double(cx):
     Q, _ = P.relabel_by_degree(want_rank=False)
     be = type("B", (), {})()
     be.matrix, be.tile_, be.c = Q, mb.generate_tile_for(Q, c), c
-    Q.build_xcache()
+    Q.build_xcache(FORCE_HUBS)  # the bench's hub path (automatic mode skips s20)
     r = mb.pagerank(None, mb.PageRankConfig(0.85, 1e-30, 100, 0), backend=be)
     p64 = O.Csr(n, n, ro, cols, O.transition_values(n, cols, np.float64))
     want = ref.pagerank_csr(p64, 0.85, 1e-300, 100, 0)

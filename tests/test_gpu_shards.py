@@ -8,6 +8,7 @@ import pytest
 
 import oracle as O
 import paper_2605_07391_b200 as mb
+from helpers import FORCE_HUBS
 from paper_2605_07391_b200.merbit import ShardGroup, row_slice
 
 pytestmark = pytest.mark.gpu
@@ -27,9 +28,21 @@ def sharded_pagerank(ctx, P, parts, iters, c, row_weight=1.0):
     return grp.gather_pi(), res, hist, b
 
 
+@pytest.mark.parametrize("hubs", [False, True])
 @pytest.mark.parametrize("row_weight", [1.0, mb.merbit.PAGERANK_ROW_WEIGHT])
 @pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
-def test_sharded_matches_fp64_oracle_and_single_gpu(ctx, parts, row_weight):
+def test_sharded_matches_fp64_oracle_and_single_gpu(ctx, parts, row_weight, hubs):
+    """hubs: every shard view builds a (forced) x hub table over its remapped
+    columns, as the large shards of the bench do automatically."""
+    if hubs:
+        ctx.set_tuning(32, 1, FORCE_HUBS)
+    try:
+        _sharded_vs_oracle(ctx, parts, row_weight, hubs)
+    finally:
+        ctx.set_tuning(32, 1, -1)
+
+
+def _sharded_vs_oracle(ctx, parts, row_weight, hubs):
     P = mb.DeviceMatrix.rmat(ctx, 14, 16, seed=7, transition=True, dtype=np.float32)
     ro, cols, _ = P.download(want_values=False)
     c = mb.SimtConfig.make(32, 14, 128)
@@ -42,6 +55,8 @@ def test_sharded_matches_fp64_oracle_and_single_gpu(ctx, parts, row_weight):
     assert abs(res.mass - 1.0) <= 1e-5
     # same answer as the single-GPU fused loop, to fp32 rounding
     t = mb.generate_tile_for(P, c)
+    if hubs:
+        P.build_xcache(FORCE_HUBS)
     be = type("B", (), {})()
     be.matrix, be.tile_, be.c = P, t, c
     single = mb.pagerank(None, mb.PageRankConfig(0.85, 1e-30, 60, 0), backend=be)

@@ -8,7 +8,7 @@ import pytest
 
 import oracle as O
 import paper_2605_07391_b200 as mb
-from helpers import CONFIGS, first_violation, h, tolerance_bound
+from helpers import CONFIGS, FORCE_HUBS, first_violation, h, tolerance_bound
 
 pytestmark = pytest.mark.gpu
 
@@ -244,8 +244,8 @@ def test_slot_and_staged_layouts_agree(ctx):
 
 
 @pytest.mark.parametrize("tuning", [(32, 1, 0, 147456, 1), (16, 2, 0, 147456, 0),
-                                    (8, 4, 0, 147456, 1), (32, 1, -1, 131072, 1),
-                                    (16, 2, -1, 147456, 0)])
+                                    (8, 4, 0, 147456, 1), (32, 1, FORCE_HUBS, 131072, 1),
+                                    (16, 2, FORCE_HUBS, 147456, 0)])
 @pytest.mark.parametrize("layout", [1, 0])
 def test_launch_shapes_and_hub_cache_are_bitwise_invariant(tuning, layout):
     """Every K2 launch shape, the L2 prefetch and the shared-memory x hub cache
@@ -281,7 +281,7 @@ def test_compact_matrix_round_trip(ctx, dtype, relabel):
     ro, cols, vals = A.download()
     c = mb.SimtConfig.make(32, 14 if dtype == np.float32 else 7, 128)
     t = mb.generate_tile_for(A, c)
-    A.build_xcache()
+    A.build_xcache(FORCE_HUBS)
     x = O.hash_uniform(9, A.n_cols, -1.0, 1.0, dtype)
     y1 = mb.spmv_merbit(A, t, c, x, mb.DualBuffer(A.n_rows, dtype)).copy()
     if A.slot_info()[0] == 0:  # staged K2 layout: no slot copy to compact onto

@@ -8,6 +8,7 @@ import pytest
 
 import oracle as O
 import paper_2605_07391_b200 as mb
+from helpers import FORCE_HUBS
 
 pytestmark = pytest.mark.gpu
 
@@ -22,7 +23,7 @@ def top_by_count(cols, n, h):
 @pytest.mark.parametrize("scale", [14, 16])
 def test_hub_set_is_top_h_by_count(ctx, dtype, scale):
     A = mb.DeviceMatrix.rmat(ctx, scale, 16, seed=2, transition=True, dtype=dtype)
-    A.build_xcache()
+    A.build_xcache(FORCE_HUBS)
     hubs = A.hub_columns()
     h = hubs.size
     assert h > 0
@@ -56,3 +57,17 @@ def test_capped_counts_rank_exactly(ctx):
     assert np.array_equal(A.hub_columns(), np.arange(200, 300))
     A.build_xcache(300)
     assert np.array_equal(A.hub_columns(), np.arange(300))
+
+
+def test_automatic_mode_skips_small_matrices(ctx):
+    """build_xcache() (automatic): no table below 4096 nonzeros per resident
+    K2 warp (148 x 32 warps: ~19.4 M nonzeros), where K2 is latency-bound;
+    a table above it."""
+    A = mb.DeviceMatrix.rmat(ctx, 16, 16, seed=2, transition=True, dtype=np.float32)
+    A.build_xcache()
+    assert A.xcache_info()[0] == 0
+    A.build_xcache(FORCE_HUBS)
+    assert A.xcache_info()[0] > 0
+    B = mb.DeviceMatrix.rmat(ctx, 21, 16, seed=2, transition=True, dtype=np.float32)
+    B.build_xcache()
+    assert B.xcache_info()[0] > 0
