@@ -965,11 +965,29 @@ struct StageBytes {
   static constexpr size_t value = size_t(32 * SIGMA) * 4 + 128 + 16;
 };
 
+#ifndef MBX_META_PF
+#define MBX_META_PF 1
+#endif
+// a range's tile entries (lane i <= nc holds entry c0 + i), loaded one range
+// ahead so the walk of a range starts without a memory round trip
+__device__ __forceinline__ void load_range_meta(const uint32_t* tile_x, const uint32_t* tile_y,
+                                                const Geometry& g, int64_t range, int lid,
+                                                uint64_t pol, uint32_t& mtx, uint32_t& mty) {
+  mtx = mty = 0;
+  if (range < 0) return;
+  const int64_t c0 = range * g.chunks_per_range;
+  const int nc = static_cast<int>(imin64(c0 + g.chunks_per_range, g.num_chunks) - c0);
+  if (lid <= nc) {
+    mtx = ld_stream_u32(tile_x + c0 + lid, pol);
+    mty = ld_stream_u32(tile_y + c0 + lid, pol);
+  }
+}
+
 template <typename T, int SIGMA, bool PR, bool HUB, int MODE>
 __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub, T* rowbuf,
                                            int64_t range, int lid, uint64_t pol, T base,
                                            unsigned char* stg, uint32_t& phase,
-                                           int64_t next_range) {
+                                           int64_t next_range, uint32_t& pmx, uint32_t& pmy) {
   constexpr bool PF = MODE == 1;
   constexpr bool TMA = MODE == 2;
   int32_t* colbuf = reinterpret_cast<int32_t*>(stg);
@@ -985,7 +1003,11 @@ __device__ __forceinline__ void slot_range(const SlotParams<T>& p, const T* hub,
   const uint32_t omask = (1u << ob) - 1u;
 
   uint32_t mtx = 0, mty = 0;
-  if (lid <= nc) {
+  if (MBX_META_PF) {
+    mtx = pmx;
+    mty = pmy;
+    load_range_meta(p.tile_x, p.tile_y, g, next_range, lid, pol, pmx, pmy);
+  } else if (lid <= nc) {
     mtx = ld_stream_u32(p.tile_x + c0 + lid, pol);
     mty = ld_stream_u32(p.tile_y + c0 + lid, pol);
   }
@@ -1209,9 +1231,13 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
                   reinterpret_cast<uint32_t*>(stg + size_t(32 * SIGMA) * 4), p.scols, p.lane_desc,
                   first * g.chunks_per_range, 32 * SIGMA, pol);
   }
+  uint32_t pmx = 0, pmy = 0;
+  if (MBX_META_PF)
+    load_range_meta(p.tile_x, p.tile_y, g, first < g.num_ranges ? first : -1, lid, pol, pmx, pmy);
   for (int64_t range = first; range < g.num_ranges; range += wstride)
     slot_range<T, SIGMA, PR, HUB, MODE>(p, hub, rowbuf, range, lid, pol, base, stg, phase,
-                                        range + wstride < g.num_ranges ? range + wstride : -1);
+                                        range + wstride < g.num_ranges ? range + wstride : -1,
+                                        pmx, pmy);
   if (PR && p.pr.npeer) __threadfence_system();  // NVLink stores performed (fused exchange)
 }
 
