@@ -1523,11 +1523,13 @@ __global__ void __launch_bounds__(256, PR ? kK3BlocksPerSM : 1)
       constexpr uint32_t gmask = kR >= 32 ? ~0u : ((1u << kR) - 1u);
       const bool dall = pr.dang_from >= 0 && r0 >= pr.dang_from;
       const bool dnone = pr.dang_from >= 0 && r0 + kR <= pr.dang_from;
-      if ((mw & gmask) == 0 && !pr.yardstick && (dall || dnone)) {
-        // the common group: no carry row, all or none dangling, constant
-        // yardstick -- partial sums in T over the group, one fp64 add each;
-        // ERR from the group's extremes (|pi - s| peaks at one of them, and
-        // rounding is monotone: the same value as the per-row maximum)
+      if (!pr.yardstick && (dall || dnone)) {
+        // the common group: all or none dangling, constant yardstick --
+        // partial sums in T over the group's rows that are not carry rows
+        // (the fold took those), one fp64 add each; ERR from the group's
+        // extremes (|pi - s| peaks at one of them, and rounding is
+        // monotone: the same value as the per-row maximum)
+        const uint32_t live = ~mw & gmask;
         T rs = T(0), ms = T(0), ds = T(0), hi = -INFINITY, lo = INFINITY;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1535,18 +1537,20 @@ __global__ void __launch_bounds__(256, PR ? kK3BlocksPerSM : 1)
           const T* pb = reinterpret_cast<const T*>(&b[u]);
 #pragma unroll
           for (int v = 0; v < kV; ++v) {
-            rs += fabs(pa[v] - pb[v]);
-            ms += fabs(pa[v]);
-            ds += pa[v];
-            hi = fmax(hi, pa[v]);
-            lo = fmin(lo, pa[v]);
+            const bool in = (live >> (u * kV + v)) & 1u;
+            rs += in ? fabs(pa[v] - pb[v]) : T(0);
+            ms += in ? fabs(pa[v]) : T(0);
+            ds += in ? pa[v] : T(0);
+            hi = in ? fmax(hi, pa[v]) : hi;
+            lo = in ? fmin(lo, pa[v]) : lo;
           }
         }
         acc.resid += static_cast<double>(rs);
         acc.mass += static_cast<double>(ms);
         if (dall) acc.dang += static_cast<double>(ds);
-        acc.err = fmax(acc.err, fmax(fabs(static_cast<double>(hi) - pr.yard_const),
-                                     fabs(static_cast<double>(lo) - pr.yard_const)));
+        if (live)
+          acc.err = fmax(acc.err, fmax(fabs(static_cast<double>(hi) - pr.yard_const),
+                                       fabs(static_cast<double>(lo) - pr.yard_const)));
         continue;
       }
 #pragma unroll

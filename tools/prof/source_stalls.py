@@ -1,6 +1,7 @@
 """Warp-stall samples of an ncu report per CUDA source line (needs
 --import-source on and -lineinfo): ncu -i REP --page source --csv
---print-source cuda,sass, aggregated over each line's SASS."""
+--print-source cuda,sass, aggregated over each line's SASS.
+python tools/prof/source_stalls.py REP [top] [kernel-regex]"""
 import csv
 import io
 import subprocess
@@ -10,8 +11,10 @@ import sys
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
-                          "cuda,sass"], capture_output=True, text=True, check=True).stdout
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if len(sys.argv) > 3:
+        cmd += ["-k", "regex:" + sys.argv[3]]
+    out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     # rows: ["Line No","Source","Address","Source", metrics...]; a line row
     # carries the line number, its SASS rows follow with an empty line no.
