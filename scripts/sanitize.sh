@@ -33,3 +33,12 @@ MBX_GRAPH_MODE=unrolled timeout 1500 $CS --tool synccheck python -m pytest -q -x
   -k "walkthrough or fuzz or edge or long_row or many_rows or ring or cycle or dangling or short_rows or empty or odd or dense or device_driven or degree_relabel or stencil or laplacian or singular or trivial or corpus" \
   > gpurun_out/sanitize_tests_synccheck.log 2>&1
 echo "tests synccheck rc=$? :: $(grep -E 'passed|failed|ERROR SUMMARY' gpurun_out/sanitize_tests_synccheck.log | tail -2 | tr '\n' ' ')"
+# the preprocessing kernels of late round 2 (K1 bounds + scan, hub sampling /
+# histogram / pick / selection, word map, slot copy with both hub encodings):
+# the exact-top-h and capped-count hub tests and the compact round trips
+for tool in memcheck racecheck initcheck; do
+  timeout 1500 $CS --tool $tool python -m pytest -q -x -m gpu -p no:cacheprovider \
+    tests/test_gpu_xcache.py tests/test_gpu_spmv.py -k "top_h or capped or compact" \
+    > gpurun_out/sanitize_preproc_$tool.log 2>&1
+  echo "preprocessing $tool rc=$? :: $(grep -E 'passed|failed|ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/sanitize_preproc_$tool.log | tail -2 | tr '\n' ' ')"
+done
