@@ -256,6 +256,11 @@ MBX_API int mbx_matrix_build_xcache(mbx_context* ctx, mbx_matrix* m,
                                     int max_hubs, double* seconds);
 MBX_API int mbx_matrix_xcache_info(const mbx_matrix* m, int* hubs,
                                    double* coverage);
+/* Gather locality measured by the last mbx_matrix_build_xcache sample: the
+ * mean number of distinct 32-byte sectors of x that 32 consecutive nonzeros
+ * touch (-1 when the build did not sample: automatic mode on a small matrix,
+ * or never built).  Below 16 the fp32 K2 prefetches each next tile into L2. */
+MBX_API int mbx_matrix_gather_profile(const mbx_matrix* m, double* sectors_per_32);
 /* The hub columns (xcache_info's count of them) into host_out, in slot
  * order: ascending column ids. */
 MBX_API int mbx_matrix_hub_columns(const mbx_matrix* m, int32_t* host_out);

@@ -124,6 +124,7 @@ SIGNATURES = {
     "mbx_matrix_xcache_info": ([VP, C.POINTER(C.c_int), C.POINTER(C.c_double)], C.c_int),
     "mbx_matrix_xcache_ptrs": ([VP, C.POINTER(VP), C.POINTER(VP)], C.c_int),
     "mbx_matrix_hub_columns": ([VP, VP], C.c_int),
+    "mbx_matrix_gather_profile": ([VP, C.POINTER(C.c_double)], C.c_int),
     "mbx_matrix_upload": ([VP, C.c_int, C.c_int64, C.c_int64, VP, VP, VP, C.POINTER(VP)], C.c_int),
     "mbx_matrix_upload_i32": ([VP, C.c_int, C.c_int64, C.c_int64, VP, VP, VP, C.POINTER(VP)],
                               C.c_int),

@@ -68,7 +68,7 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   const int64_t fit = std::max<int64_t>(1, g.num_chunks / (8 * warps));
   g.chunks_per_range = int(std::max<int64_t>(1, std::min<int64_t>({31, block_size / 32, fit})));
   g.num_ranges = (g.num_chunks + g.chunks_per_range - 1) / g.chunks_per_range;
-  g.prefetch = resolve_prefetch(ctx->tuning.prefetch, m->precision);
+  g.prefetch = resolve_prefetch(ctx->tuning.prefetch, m->precision, m->gather_sectors);
   g.hub_count = 0;
   if (m->hub_cols && m->hub_avail > 0 && g.omega == 32 && ctx->tuning.max_hubs != 0 &&
       (ctx->tuning.max_hubs < 0 || ctx->tuning.max_hubs >= m->hub_avail)) {
@@ -656,6 +656,12 @@ MBX_API int mbx_matrix_xcache_ptrs(const mbx_matrix* m, const int32_t** cols_hub
   return guarded([&] {
     if (cols_hub) *cols_hub = m->cols_hub;
     if (hub_cols) *hub_cols = m->hub_cols;
+  });
+}
+
+MBX_API int mbx_matrix_gather_profile(const mbx_matrix* m, double* sectors_per_32) {
+  return guarded([&] {
+    if (sectors_per_32) *sectors_per_32 = m->gather_sectors;
   });
 }
 

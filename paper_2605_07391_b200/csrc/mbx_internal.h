@@ -170,6 +170,9 @@ struct mbx_matrix_s {
   int hub_avail = 0;
   int hub_prefix = 0;         // 1: hub_cols is 0..hub_avail-1 (degree-relabelled)
   double hub_coverage = 0.0;  // fraction of nonzeros that reference a hub
+  // distinct 32-byte x sectors per 32 consecutive nonzeros, from the hub
+  // selection's sample (-1: not measured); picks K2's next-tile staging
+  double gather_sectors = -1.0;
   uint64_t version = 0;       // bumped whenever cols_hub is rebuilt
   // bumped whenever a device buffer a captured PageRank plan may reference
   // (slot copy, cols_hub, hub_cols) is freed or rebuilt: plans compare it
@@ -261,7 +264,7 @@ void ensure_csr(mbx_context* ctx, const mbx_matrix* m);
 void free_compact_tile(mbx_context* ctx, const mbx_matrix* m);
 int default_sigma(int precision);
 // Tuning::prefetch with -1 (auto) resolved for a precision
-int resolve_prefetch(int tuning, int precision);
+int resolve_prefetch(int tuning, int precision, double gather_sectors = -1.0);
 
 // ---- kernels (kernels.cu) ----
 void launch_generate_tile(mbx_context* ctx, const uint32_t* ro, int64_t n_rows,

@@ -97,20 +97,39 @@ namespace {
 // x entry, so results do not depend on which columns are chosen.
 constexpr int64_t kSampleRuns = int64_t(1) << 17;  // 32 nonzeros each (4 M samples)
 
+// Also the gather locality of the sample: how many distinct 32-byte sectors
+// of x a run of 32 consecutive nonzeros touches (a stencil ~10, a random
+// or power-law matrix ~30), which picks K2's next-tile staging.
 __global__ void count_sample_kernel(const int32_t* __restrict__ cols, int64_t nnz,
-                                    int64_t stride_runs, uint32_t* __restrict__ cnt,
-                                    uint32_t* __restrict__ cmax) {
+                                    int64_t stride_runs, int sector_shift,
+                                    uint32_t* __restrict__ cnt, uint32_t* __restrict__ cmax,
+                                    unsigned long long* __restrict__ sectors,
+                                    unsigned long long* __restrict__ full_runs) {
   const int lid = threadIdx.x & 31;
   const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t runs = (nnz + 31) / 32;
   uint32_t mx = 0;  // the largest count this thread produced
+  unsigned long long sec = 0, nr = 0;
   for (int64_t r = w * stride_runs; r < runs; r += nw * stride_runs) {
     const int64_t k = r * 32 + lid;
-    if (k < nnz) mx = max(mx, atomicAdd(cnt + __ldg(cols + k), 1u) + 1u);
+    const int32_t c = k < nnz ? __ldg(cols + k) : -1;
+    if (k < nnz) mx = max(mx, atomicAdd(cnt + c, 1u) + 1u);
+    if (r * 32 + 32 <= nnz) {  // warp-uniform: a full run
+      const unsigned same = __match_any_sync(0xffffffffu, c >> sector_shift);
+      const unsigned leaders = __ballot_sync(0xffffffffu, lid == __ffs(same) - 1);
+      sec += __popc(leaders);
+      ++nr;
+    }
   }
   mx = __reduce_max_sync(0xffffffffu, mx);
-  if (lid == 0 && mx) atomicMax(cmax, mx);
+  if (lid == 0) {
+    if (mx) atomicMax(cmax, mx);
+    if (nr) {
+      atomicAdd(sectors, sec);
+      atomicAdd(full_runs, nr);
+    }
+  }
 }
 
 // candidates: columns whose sampled count exceeds `t`
@@ -135,6 +154,8 @@ __global__ void gather_counts_kernel(const uint32_t* __restrict__ cnt,
 constexpr int kHistBins = 8192;
 
 struct HubPick {
+  unsigned long long sectors;    // distinct x sectors over the sampled full runs ...
+  unsigned long long full_runs;  // ... and the number of those runs
   unsigned long long covered;  // sampled references of the chosen hubs
   unsigned long long capsum;   // sum of the counts in the last bin
   uint32_t capmax;             // largest count in the last bin (0: empty)
@@ -282,6 +303,7 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   m->hub_avail = 0;
   m->hub_prefix = 0;
   m->hub_coverage = 0.0;
+  m->gather_sectors = -1.0;
   ++m->version;  // invalidates slot copies built over the old encoding
   ++m->gen;      // and the graphs captured over the old buffers
   const Tuning& tu = ctx->tuning;
@@ -326,8 +348,9 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   MBX_CUDA(cudaMallocAsync(&hist, kHistBins * 4 + sizeof(HubPick) + 64, s));
   dpick = reinterpret_cast<HubPick*>(hist + kHistBins);
   MBX_CUDA(cudaMemsetAsync(hist, 0, kHistBins * 4 + sizeof(HubPick), s));
-  count_sample_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(m->cols, m->nnz, S, cnt,
-                                                                  &dpick->cmax);
+  count_sample_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(
+      m->cols, m->nnz, S, m->precision == MBX_F32 ? 3 : 2, cnt, &dpick->cmax, &dpick->sectors,
+      &dpick->full_runs);
   ++ctx->launches;
   // one pass over the counts: their histogram, then the hub set's
   // threshold (hub_pick_kernel) -- one host synchronisation for the lot
@@ -343,6 +366,7 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   MBX_CUDA(cudaMemcpyAsync(&pick, dpick, sizeof(HubPick), cudaMemcpyDeviceToHost, s));
   MBX_CUDA(cudaStreamSynchronize(s));
   cudaFreeAsync(hist, s);
+  m->gather_sectors = pick.full_runs ? double(pick.sectors) / double(pick.full_runs) : -1.0;
   const uint32_t cmax = pick.cmax;
   size_t tb = 0;
   void* temp = nullptr;

@@ -369,6 +369,13 @@ class DeviceMatrix:
         _check(_lib.lib().mbx_matrix_xcache_info(self.h, C.byref(hubs), C.byref(cov)))
         return hubs.value, cov.value
 
+    def gather_sectors(self) -> float:
+        """Distinct 32-byte x sectors per 32 consecutive nonzeros, from the
+        last build_xcache's sample (-1: not sampled)."""
+        v = C.c_double()
+        _check(_lib.lib().mbx_matrix_gather_profile(self.h, C.byref(v)))
+        return v.value
+
     def hub_columns(self) -> np.ndarray:
         """The x hub cache's columns in slot order (ascending ids)."""
         h = self.xcache_info()[0]

@@ -2,7 +2,7 @@
 so first-use costs (memory pool growth, module loading) show separately:
 python scripts/prof/preproc.py [case ...], cases s24, s24r (degree-relabelled),
 s24f64, s24rf64, s20, c3 (power-law f64), c5, c5f64.  LAYOUT=0 runs K2 on
-the staged CSR order (no slot copy)."""
+the staged CSR order (no slot copy); MODE= sets K2's next-tile staging."""
 import os
 import sys
 import time
@@ -20,6 +20,8 @@ torch.cuda.set_stream(s)
 ctx.set_stream(s.cuda_stream)
 if os.environ.get("LAYOUT"):
     ctx.set_layout(int(os.environ["LAYOUT"]))
+if os.environ.get("MODE"):  # K2 next-tile staging: 0 none, 1 L2 prefetch, 2 TMA
+    ctx.set_tuning(32, 1, -1, prefetch=int(os.environ["MODE"]))
 
 
 def make(case):
@@ -62,7 +64,8 @@ for case in cases:
     torch.cuda.synchronize()
     sp = e0.elapsed_time(e1) / 20
     best = [min(r[i] for r in rows) for i in range(4)]
-    print(f"{case}: nnz {A.nnz} hubs {A.xcache_info()[0]} spmv {sp:.3f} ms | "
+    print(f"{case}: nnz {A.nnz} hubs {A.xcache_info()[0]} sectors/32 {A.gather_sectors():.1f} "
+          f"spmv {sp:.3f} ms | "
           + " | ".join(f"rep{i} tile {r[0]:.3f} xc {r[1]:.3f} slots {r[2]:.3f} first {r[3]:.3f}"
                        for i, r in enumerate(rows))
           + f" || best pre {sum(best[:3]):.3f} ms = {sum(best[:3]) / sp:.2f}x spmv; "

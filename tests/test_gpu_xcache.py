@@ -71,3 +71,27 @@ def test_automatic_mode_skips_small_matrices(ctx):
     B = mb.DeviceMatrix.rmat(ctx, 21, 16, seed=2, transition=True, dtype=np.float32)
     B.build_xcache()
     assert B.xcache_info()[0] > 0
+
+
+def test_gather_profile_picks_the_staging(ctx):
+    """The hub sample also measures gather locality (distinct 32-byte x
+    sectors per 32 consecutive nonzeros): a 27-point stencil ~11, R-MAT ~31.
+    Below 16 the fp32 K2 prefetches each next tile into L2 -- results are
+    bitwise those of the unprefetched kernel."""
+    S = mb.DeviceMatrix.stencil27(ctx, 64, np.float32)
+    S.build_xcache(FORCE_HUBS)
+    assert S.xcache_info()[0] == 0  # no column can be a hub (27 references)
+    assert 0.0 < S.gather_sectors() < 16.0
+    R = mb.DeviceMatrix.rmat(ctx, 16, 16, seed=2, transition=True, dtype=np.float32)
+    R.build_xcache(FORCE_HUBS)
+    assert R.gather_sectors() > 24.0
+    c = mb.SimtConfig.make(32, 14, 128)
+    t = mb.generate_tile_for(S, c)
+    x = O.hash_uniform(7, S.n_cols, -1.0, 1.0, np.float32)
+    y_auto = mb.spmv_merbit(S, t, c, x, mb.DualBuffer(S.n_rows, np.float32)).copy()
+    ctx.set_tuning(32, 1, -1, prefetch=0)
+    try:
+        y0 = mb.spmv_merbit(S, t, c, x, mb.DualBuffer(S.n_rows, np.float32))
+    finally:
+        ctx.set_tuning(32, 1, -1, prefetch=-1)
+    assert np.array_equal(y0.view(np.uint32), y_auto.view(np.uint32))
