@@ -95,3 +95,31 @@ def test_gather_profile_picks_the_staging(ctx):
     finally:
         ctx.set_tuning(32, 1, -1, prefetch=-1)
     assert np.array_equal(y0.view(np.uint32), y_auto.view(np.uint32))
+
+
+def test_hub_budget_shrinks_as_x_outgrows_l2():
+    """K2's shared-memory budget per SM depends on x's size (160 KB up to
+    192 MB of fp32 x, 128 KB to 384 MB, 96 KB beyond): the same 40,000
+    columns referenced 1024 times each (a table needs > 4 x 148 references)
+    fill 38,652 hub slots when x has 1 M entries, 30,460 at 64 M entries
+    (256 MB) and 22,268 at 120 M (480 MB) -- with the default K2 layout (the
+    slot copy; the staged layout's larger per-warp buffers leave fewer)."""
+    ctx = mb.Context(0)
+    hot, refs = 40000, 1024
+    n_rows = hot * refs // 32
+    # row r: hot columns (7919 r + 1249 i) mod 40000, i < 32 -- distinct in a
+    # row, each column exactly `refs` times, and no aliasing with the
+    # selection's every-S-th-run sample
+    r = np.arange(n_rows, dtype=np.int64)[:, None]
+    i = np.arange(32, dtype=np.int64)[None, :]
+    cols = (((7919 * r + 1249 * i) % hot) * 25).astype(np.int32)
+    cols.sort(axis=1)
+    ro = np.arange(n_rows + 1, dtype=np.int64) * 32
+    got = []
+    for n_cols in (1 << 20, 64 << 20, 120 << 20):
+        A = mb.DeviceMatrix.from_csr(ctx, O.Csr(n_rows, n_cols, ro, cols.reshape(-1),
+                                                np.ones(cols.size, np.float32)))
+        A.build_xcache(FORCE_HUBS)
+        got.append(A.xcache_info()[0])
+        del A
+    assert got == [38652, 30460, 22268], got
