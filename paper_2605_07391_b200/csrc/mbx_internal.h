@@ -239,7 +239,6 @@ int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, in
 // K2's default shared memory per SM (Tuning::smem_per_sm = -1)
 int default_smem_budget(int precision, int64_t n_cols);
 void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs);
-// slot_of[c] = hub slot of column c or -1 (n_cols int32; the caller frees)
 // hub lookup words (hub_cols ascending): .x = hub bits of columns 32w..32w+31,
 // .y = slot of the first of them
 uint2* hub_word_map(mbx_context* ctx, const mbx_matrix* m);
