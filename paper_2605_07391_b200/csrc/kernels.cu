@@ -1244,9 +1244,14 @@ __global__ void __launch_bounds__(1024) spmv_slot_kernel(SlotParams<T> p) {
 // hub encoding of a column: prefix > 0 -- the hubs are columns 0..prefix-1
 // (degree-relabelled), slot c; else the hub word map (nullptr: no hubs)
 __device__ __forceinline__ int32_t hub_encode(const uint2* __restrict__ map, int prefix,
-                                              int32_t c) {
+                                              int32_t c, const uint32_t* bloom = nullptr) {
   if (prefix > 0) return c < prefix ? int32_t(0x80000000u | uint32_t(c)) : c;
-  return map ? hub_word_encode(map, c) : c;
+  if (!map) return c;
+  if (bloom) {  // shared-memory Bloom filter: most non-hubs never touch the map
+    const uint32_t b = hub_bloom_bit(c);
+    if (!((bloom[b >> 5] >> (b & 31)) & 1u)) return c;
+  }
+  return hub_word_encode(map, c);
 }
 
 // slot copy CTAs resident per SM: 4 caps the fp32 kernel at 64 registers
@@ -1265,12 +1270,20 @@ __global__ void __launch_bounds__(256, MBX_SLOT_MINB) build_slots_kernel(
     const T* __restrict__ vals, const int32_t* __restrict__ cols, const uint2* __restrict__ map,
     int prefix, const uint32_t* __restrict__ tile_x, const uint32_t* __restrict__ tile_y,
     const uint32_t* __restrict__ lane_desc, int64_t lane_num, int64_t num_chunks, int64_t total,
-    int ob, T* __restrict__ svals, int32_t* __restrict__ scols) {
+    int ob, T* __restrict__ svals, int32_t* __restrict__ scols,
+    const uint32_t* __restrict__ gbloom) {
   constexpr int G = 8 / int(sizeof(T));
   constexpr int E = 32 * SIGMA;
   static_assert(SIGMA % G == 0, "slot groups");
   __shared__ T sv[8][E];
   __shared__ int32_t sc[8][E];
+  extern __shared__ uint32_t sbloom[];  // natural-order hubs: the Bloom filter
+  const uint32_t* bl = nullptr;
+  if (gbloom) {
+    for (int i = threadIdx.x; i < kHubBloomWords; i += blockDim.x) sbloom[i] = gbloom[i];
+    __syncthreads();
+    bl = sbloom;
+  }
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const uint32_t omask = (1u << ob) - 1u;
   const int64_t nw = int64_t(gridDim.x) * (blockDim.x >> 5);
@@ -1291,7 +1304,7 @@ __global__ void __launch_bounds__(256, MBX_SLOT_MINB) build_slots_kernel(
         const int k = i * 32 + l;
         if (k < n) {
           sv[w][k] = lv[i];
-          sc[w][k] = hub_encode(map, prefix, lc[i]);
+          sc[w][k] = hub_encode(map, prefix, lc[i], bl);
         }
       }
     }
@@ -2240,14 +2253,19 @@ bool ensure_slots(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t, cons
   uint2* map = hub && !prefix ? hub_word_map(ctx, m) : nullptr;
   const unsigned grid = grid_for((g.num_chunks + 7) / 8, 1, int64_t(ctx->sm_count) * 8);
   const int64_t total = g.nnz + g.n_rows;
+  const uint32_t* bloom =
+      map ? reinterpret_cast<const uint32_t*>(map + hub_map_words(m->n_cols)) : nullptr;
+  const size_t dyn = map ? size_t(kHubBloomWords) * 4 : 0;
   if (m->precision == MBX_F32)
-    build_slots_kernel<float, 14><<<grid, 256, 0, ctx->stream>>>(
+    build_slots_kernel<float, 14><<<grid, 256, dyn, ctx->stream>>>(
         static_cast<const float*>(m->vals), m->cols, map, prefix, t->tile_x, t->tile_y,
-        t->lane_desc, g.lane_num, g.num_chunks, total, g.ob, static_cast<float*>(sc.vals), sc.cols);
+        t->lane_desc, g.lane_num, g.num_chunks, total, g.ob, static_cast<float*>(sc.vals), sc.cols,
+        bloom);
   else
-    build_slots_kernel<double, 7><<<grid, 256, 0, ctx->stream>>>(
+    build_slots_kernel<double, 7><<<grid, 256, dyn, ctx->stream>>>(
         static_cast<const double*>(m->vals), m->cols, map, prefix, t->tile_x, t->tile_y,
-        t->lane_desc, g.lane_num, g.num_chunks, total, g.ob, static_cast<double*>(sc.vals), sc.cols);
+        t->lane_desc, g.lane_num, g.num_chunks, total, g.ob, static_cast<double*>(sc.vals), sc.cols,
+        bloom);
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
   MBX_CUDA(cudaEventRecord(e1, ctx->stream));

@@ -241,8 +241,16 @@ int default_smem_budget(int precision, int64_t n_cols);
 void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs);
 // hub lookup words (hub_cols ascending): .x = hub bits of columns 32w..32w+31,
 // .y = slot of the first of them
+// The map is followed by a 2^17-bit Bloom filter of the hub columns
+// (kHubBloomWords u32, hub_bloom_bit): most non-hub columns are rejected from
+// shared memory without touching the map.
 uint2* hub_word_map(mbx_context* ctx, const mbx_matrix* m);
+constexpr int kHubBloomWords = 4096;
+inline size_t hub_map_words(int64_t n_cols) { return size_t(n_cols / 32 + 1); }
 #ifdef __CUDACC__
+__device__ __forceinline__ uint32_t hub_bloom_bit(int32_t c) {
+  return (uint32_t(c) * 0x9E3779B1u) >> 15;  // 17 bits
+}
 // column c -> (INT32_MIN | slot) for a hub, c otherwise
 __device__ __forceinline__ int32_t hub_word_encode(const uint2* __restrict__ map, int32_t c) {
   const uint2 e = __ldg(map + (c >> 5));

@@ -62,13 +62,16 @@ __global__ void fill_kernel(int32_t* v, int64_t n, int32_t val) {
 
 // word map of the (ascending) hub list: map[w].x = the hubs among columns
 // 32w..32w+31 as bits, map[w].y = slot of the first of them
-__global__ void hub_word_kernel(const int32_t* __restrict__ hub_cols, int h, uint2* map) {
+__global__ void hub_word_kernel(const int32_t* __restrict__ hub_cols, int h, uint2* map,
+                                uint32_t* bloom) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= h) return;
   const int32_t c = hub_cols[i];
   const int32_t w = c >> 5;
   atomicOr(&map[w].x, 1u << (c & 31));
   if (i == 0 || (hub_cols[i - 1] >> 5) != w) map[w].y = uint32_t(i);
+  const uint32_t b = hub_bloom_bit(c);
+  atomicOr(bloom + (b >> 5), 1u << (b & 31));
 }
 
 __global__ void encode_kernel(const int32_t* __restrict__ cols, int64_t nnz,
@@ -536,10 +539,12 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
 uint2* hub_word_map(mbx_context* ctx, const mbx_matrix* m) {
   cudaStream_t s = ctx->stream;
   uint2* map = nullptr;
-  const size_t words = size_t(m->n_cols / 32 + 1);
-  MBX_CUDA(cudaMallocAsync(&map, words * 8 + 64, s));
-  MBX_CUDA(cudaMemsetAsync(map, 0, words * 8, s));
-  hub_word_kernel<<<(m->hub_avail + 255) / 256, 256, 0, s>>>(m->hub_cols, m->hub_avail, map);
+  const size_t words = hub_map_words(m->n_cols);
+  const size_t bytes = words * 8 + size_t(kHubBloomWords) * 4;
+  MBX_CUDA(cudaMallocAsync(&map, bytes + 64, s));
+  MBX_CUDA(cudaMemsetAsync(map, 0, bytes, s));
+  hub_word_kernel<<<(m->hub_avail + 255) / 256, 256, 0, s>>>(
+      m->hub_cols, m->hub_avail, map, reinterpret_cast<uint32_t*>(map + words));
   ++ctx->launches;
   MBX_CUDA(cudaGetLastError());
   return map;
