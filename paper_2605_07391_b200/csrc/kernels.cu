@@ -840,6 +840,9 @@ struct SlotParams {
 #ifndef MBX_GATHER
 #define MBX_GATHER 0
 #endif
+#ifndef MBX_GATHER_NOHUB
+#define MBX_GATHER_NOHUB 1
+#endif
 template <typename T, int SIGMA, bool HUB>
 __device__ __forceinline__ void gather_slots(const T* __restrict__ x, const T* hub,
                                              const int (&col)[SIGMA], uint32_t mask,
@@ -847,7 +850,12 @@ __device__ __forceinline__ void gather_slots(const T* __restrict__ x, const T* h
 #pragma unroll
   for (int i = 0; i < SIGMA; ++i) {
     const int c = col[i];
-    if (MBX_GATHER == 1) {
+    if (!HUB && MBX_GATHER_NOHUB) {
+      // no hub table (small, stencil-like or uniform matrices): every slot
+      // gathers, branch-free -- a dead slot holds column 0 (an L1 hit) and
+      // its product is masked by the walk
+      xv[i] = __ldg(x + c);
+    } else if (MBX_GATHER == 1) {
       // every slot, no branches: a dead slot (column 0) reads x[0] (an L1
       // hit) and its product is masked by the walk; a hub reference is a
       // generic load from shared memory
