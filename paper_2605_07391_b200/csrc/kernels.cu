@@ -2131,16 +2131,17 @@ void launch_spmv_t(mbx_context* ctx, const mbx_matrix* m, const mbx_tile* t,
 
 }  // namespace
 
-// K2's next-tile staging when the tuning leaves it to the library: fp64 TMA
-// staging (mode 2: s24 fp64 SpMV -9 %); fp32 none, except for matrices whose
-// gathers are local (few distinct x sectors per 32 nonzeros: a stencil),
-// where K2 streams at HBM speed and the L2 prefetch of the next tile keeps
-// the stream fed (C5 fp32 2.74 -> 2.56 ms); on gather-bound matrices the
-// prefetch's extra requests cost (R-MAT s24 +10 %, C3 fp64 +5 %).
+// K2's next-tile staging when the tuning leaves it to the library.  Matrices
+// whose gathers are local (few distinct x sectors per 32 nonzeros: a
+// stencil) stream at HBM speed, and the L2 prefetch of the next tile keeps
+// the stream fed (C5 fp32 2.50 -> 2.35 ms, fp64 4.23 -> 4.16 ms against
+// modes 0 / 2); on gather-bound matrices its extra requests cost (R-MAT s24
+// fp32 +10 %, C3 fp64 +7 %), and there fp64 takes the TMA staging (mode 2:
+// s24 fp64 SpMV -9 %) and fp32 none.
 int resolve_prefetch(int tuning, int precision, double gather_sectors) {
   if (tuning >= 0) return tuning;
-  if (precision == MBX_F64) return 2;
-  return gather_sectors > 0.0 && gather_sectors < 16.0 ? 1 : 0;
+  if (gather_sectors > 0.0 && gather_sectors < 16.0) return 1;
+  return precision == MBX_F64 ? 2 : 0;
 }
 
 size_t stage_bytes(int sigma) { return size_t(32 * sigma) * 4 + 128 + 16; }
