@@ -397,6 +397,21 @@ def spmv_numbers(mb, ctx, stream, scale, dtype, reps, peak, make=None, label=Non
            "preprocess_first_ms": sum(pre[0]) * 1e3,
            "preprocess_first_over_spmv": sum(pre[0]) / ts,
            "xcache_hubs": A.xcache_info()[0], "xcache_coverage": A.xcache_info()[1]}
+    # the same K2/K3 over the staged CSR order (layout 0: no slot copy): the
+    # preprocessing / steady-state trade the slot copy makes, and after how
+    # many SpMVs the copy has paid for itself
+    try:
+        ctx.set_layout(0)
+        mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr())
+        ts0 = time_device(stream, lambda: mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr()),
+                          max(3, reps // 2))
+        out["staged_layout"] = {
+            "ms": ts0 * 1e3, "frac": b / ts0 / 1e9 / peak,
+            "preprocess_ms": (tile_s + xc_s) * 1e3,
+            "preprocess_over_spmv": (tile_s + xc_s) / ts0,
+            "slot_copy_pays_after_spmvs": (slot_s / (ts0 - ts)) if ts0 > ts else None}
+    finally:
+        ctx.set_layout(1)
     out.update(comparator_numbers(A, c, x, y, stream, ts, max(3, reps // 3)))
     if reference is not None:
         # the reference's CPU path on this box (a bounded sample when the full

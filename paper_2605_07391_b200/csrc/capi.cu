@@ -61,6 +61,15 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   g.warps_per_cta = ctx->tuning.warps_per_cta;
   g.grid = ctx->sm_count * ctx->tuning.ctas_per_sm;
   g.sms = ctx->sm_count;
+  if (ctx->tuning.shape_auto && m->precision == MBX_F32 && !(m->hub_cols && m->hub_avail > 0) &&
+      m->nnz < small_matrix_nnz(ctx)) {
+    // a small fp32 matrix without a hub table is latency-bound (a warp walks
+    // ~8 tiles): two CTAs of 16 warps per SM retire their tails
+    // independently (scripts/prof/c1_shape.py, R-MAT s20: 58.9 -> 56.8 us;
+    // fp64 s20 75.0 -> 78.7 us, so fp64 keeps one CTA of 32)
+    g.warps_per_cta = 16;
+    g.grid = ctx->sm_count * 2;
+  }
   // b/32 tiles per warp range (the reference's block of b/omega tiles), but
   // at least ~8 ranges per resident warp so small matrices do not leave the
   // persistent grid with a long tail
@@ -598,11 +607,14 @@ MBX_API int mbx_context_set_tuning_ex(mbx_context* ctx, int smem_per_sm, int pre
 MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta, int ctas_per_sm,
                                    int max_hubs) {
   return guarded([&] {
-    require(warps_per_cta >= 1 && warps_per_cta <= 32 && ctas_per_sm >= 1 && ctas_per_sm <= 32,
-            MBX_CONFIG_ERROR, "warps_per_cta in [1,32], ctas_per_sm in [1,32]");
-    ctx->tuning.warps_per_cta = warps_per_cta;
-    ctx->tuning.ctas_per_sm = ctas_per_sm;
+    const bool automatic = warps_per_cta == 0 && ctas_per_sm == 0;
+    require(automatic || (warps_per_cta >= 1 && warps_per_cta <= 32 && ctas_per_sm >= 1 &&
+                          ctas_per_sm <= 32),
+            MBX_CONFIG_ERROR, "warps_per_cta in [1,32], ctas_per_sm in [1,32] (or both 0)");
+    ctx->tuning.warps_per_cta = automatic ? 32 : warps_per_cta;
+    ctx->tuning.ctas_per_sm = automatic ? 1 : ctas_per_sm;
     ctx->tuning.max_hubs = max_hubs;
+    ctx->tuning.shape_auto = automatic;
     ++ctx->tuning_epoch;
     drop_pr_cache(ctx);
   });

@@ -53,6 +53,9 @@ struct Geometry {
 struct Tuning {
   int warps_per_cta = 32;
   int ctas_per_sm = 1;
+  // launch shape left to the library (no mbx_context_set_tuning call): small
+  // fp32 matrices without a hub table take 16 warps x 2 CTAs per SM
+  bool shape_auto = true;
   int max_hubs = -1;  // -1: fill the shared-memory budget; 0: disable
   // Shared memory K2 may take per SM.  The rest stays L1, which also stages
   // every in-flight miss: a hub table that squeezes L1 below ~80 KB starves
@@ -236,6 +239,15 @@ size_t spmv_smem_bytes(const Geometry& g, int precision);
 // columns (the budget shrinks as x outgrows L2: the L1 it leaves matters more)
 int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, int sigma,
                   int precision, int64_t n_cols);
+// Below this many nonzeros (4096 per resident K2 warp of the tuned launch
+// shape) K2 is latency-bound -- a warp walks a handful of tiles: the
+// automatic x hub table is skipped (it changes nothing there, R-MAT fp32 SpMV
+// with / without, scripts/prof/small_hub_probe.py: s19 34.8 / 31.6 us, s20
+// 59.9 / 60.0 us, s21 103 / 114 us, s22 193 / 230 us) and fp32 takes the
+// small-matrix launch shape (make_geometry).
+inline int64_t small_matrix_nnz(const mbx_context* ctx) {
+  return int64_t(4096) * ctx->sm_count * ctx->tuning.ctas_per_sm * ctx->tuning.warps_per_cta;
+}
 // K2's default shared memory per SM (Tuning::smem_per_sm = -1)
 int default_smem_budget(int precision, int64_t n_cols);
 void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs);

@@ -315,15 +315,8 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   if (max_hubs >= 0) slots = std::min(slots, max_hubs);
   if (slots <= 0 || m->nnz == 0 || m->n_cols == 0) return;
   // Automatic mode: a table only pays once K2 is bound by its gather
-  // requests.  With few nonzeros per resident warp K2 is latency-bound (a
-  // warp walks a handful of tiles) and the table changes nothing or costs:
-  // R-MAT fp32 SpMV with / without, scripts/prof/small_hub_probe.py: s19
-  // (1.7 K nonzeros per warp) 34.8 / 31.6 us, s20 (3.4 K) 59.9 / 60.0 us,
-  // s21 (6.8 K) 103 / 114 us, s22 193 / 230 us.
-  constexpr int64_t kMinNnzPerWarp = 4096;
-  if (max_hubs < 0 &&
-      m->nnz < kMinNnzPerWarp * int64_t(ctx->sm_count) * tu.ctas_per_sm * tu.warps_per_cta)
-    return;
+  // requests, not on a latency-bound small matrix (small_matrix_nnz).
+  if (max_hubs < 0 && m->nnz < small_matrix_nnz(ctx)) return;
   const int64_t n = m->n_cols;
   const int64_t runs = (m->nnz + 31) / 32;
   // A hub pays off only if it is referenced several times more often than

@@ -180,7 +180,7 @@ def test_pagerank_plan_cache(ctx):
     assert d.iterations == e.iterations and np.array_equal(d.pi, e.pi)
     ctx.set_tuning(32, 1, 0)  # no hub table: plan rebuilt, result unchanged
     f = mb.pagerank(None, cfg, backend=be)
-    ctx.set_tuning(32, 1, -1)
+    ctx.set_tuning()
     assert np.array_equal(a.pi.view(np.uint32), f.pi.view(np.uint32))
     # a new matrix (possibly at the freed address) gets its own plan
     del be, P

@@ -39,7 +39,7 @@ def test_sharded_matches_fp64_oracle_and_single_gpu(ctx, parts, row_weight, hubs
     try:
         _sharded_vs_oracle(ctx, parts, row_weight, hubs)
     finally:
-        ctx.set_tuning(32, 1, -1)
+        ctx.set_tuning()
 
 
 def _sharded_vs_oracle(ctx, parts, row_weight, hubs):

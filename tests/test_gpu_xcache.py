@@ -93,7 +93,7 @@ def test_gather_profile_picks_the_staging(ctx):
     try:
         y0 = mb.spmv_merbit(S, t, c, x, mb.DualBuffer(S.n_rows, np.float32))
     finally:
-        ctx.set_tuning(32, 1, -1, prefetch=-1)
+        ctx.set_tuning(prefetch=-1)
     assert np.array_equal(y0.view(np.uint32), y_auto.view(np.uint32))
 
 
