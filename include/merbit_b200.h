@@ -181,7 +181,7 @@ MBX_API int mbx_context_synchronize(mbx_context* ctx);
 /* Kernel launch shape of K2 (omega == 32): warps per CTA, resident CTAs per
  * SM (persistent grid), hub-cache cap (-1 auto, 0 off).  Both shape
  * arguments 0 (the default): automatic -- 32 warps x 1 CTA, except 16 x 2
- * for a small fp32 matrix without a hub table. */
+ * for a small matrix without a hub table. */
 MBX_API int mbx_context_set_tuning(mbx_context* ctx, int warps_per_cta,
                                    int ctas_per_sm, int max_hubs);
 /* Shared-memory budget per SM for K2 (bytes; the rest is L1) and how K2

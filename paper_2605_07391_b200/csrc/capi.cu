@@ -61,12 +61,12 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   g.warps_per_cta = ctx->tuning.warps_per_cta;
   g.grid = ctx->sm_count * ctx->tuning.ctas_per_sm;
   g.sms = ctx->sm_count;
-  if (ctx->tuning.shape_auto && m->precision == MBX_F32 && !(m->hub_cols && m->hub_avail > 0) &&
-      m->nnz < small_matrix_nnz(ctx)) {
-    // a small fp32 matrix without a hub table is latency-bound (a warp walks
-    // ~8 tiles): two CTAs of 16 warps per SM retire their tails
-    // independently (scripts/prof/c1_shape.py, R-MAT s20: 58.9 -> 56.8 us;
-    // fp64 s20 75.0 -> 78.7 us, so fp64 keeps one CTA of 32)
+  const bool small = ctx->tuning.shape_auto && !(m->hub_cols && m->hub_avail > 0) &&
+                     m->nnz < small_matrix_nnz(ctx);
+  if (small) {
+    // a small matrix without a hub table is latency-bound (a warp walks ~8
+    // tiles): two CTAs of 16 warps per SM retire their tails independently
+    // (scripts/prof/c1_shape.py, R-MAT s20 fp32: 58.4 -> 56.9 us)
     g.warps_per_cta = 16;
     g.grid = ctx->sm_count * 2;
   }
@@ -78,6 +78,10 @@ Geometry make_geometry(const mbx_context* ctx, const mbx_matrix* m, const mbx_ti
   g.chunks_per_range = int(std::max<int64_t>(1, std::min<int64_t>({31, block_size / 32, fit})));
   g.num_ranges = (g.num_chunks + g.chunks_per_range - 1) / g.chunks_per_range;
   g.prefetch = resolve_prefetch(ctx->tuning.prefetch, m->precision, m->gather_sectors);
+  // ... and without the fp64 TMA staging, whose round trip per tile only
+  // pays on a request-bound matrix (R-MAT s20 fp64: 74.7 us with it, 72.4 us
+  // at 16 x 2 without)
+  if (small && ctx->tuning.prefetch < 0 && g.prefetch == 2) g.prefetch = 0;
   g.hub_count = 0;
   if (m->hub_cols && m->hub_avail > 0 && g.omega == 32 && ctx->tuning.max_hubs != 0 &&
       (ctx->tuning.max_hubs < 0 || ctx->tuning.max_hubs >= m->hub_avail)) {

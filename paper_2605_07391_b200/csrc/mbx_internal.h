@@ -54,7 +54,7 @@ struct Tuning {
   int warps_per_cta = 32;
   int ctas_per_sm = 1;
   // launch shape left to the library (no mbx_context_set_tuning call): small
-  // fp32 matrices without a hub table take 16 warps x 2 CTAs per SM
+  // matrices without a hub table take 16 warps x 2 CTAs per SM
   bool shape_auto = true;
   int max_hubs = -1;  // -1: fill the shared-memory budget; 0: disable
   // Shared memory K2 may take per SM.  The rest stays L1, which also stages
@@ -243,7 +243,7 @@ int max_hub_slots(const mbx_context* ctx, int warps_per_cta, int ctas_per_sm, in
 // shape) K2 is latency-bound -- a warp walks a handful of tiles: the
 // automatic x hub table is skipped (it changes nothing there, R-MAT fp32 SpMV
 // with / without, scripts/prof/small_hub_probe.py: s19 34.8 / 31.6 us, s20
-// 59.9 / 60.0 us, s21 103 / 114 us, s22 193 / 230 us) and fp32 takes the
+// 59.9 / 60.0 us, s21 103 / 114 us, s22 193 / 230 us) and K2 takes the
 // small-matrix launch shape (make_geometry).
 inline int64_t small_matrix_nnz(const mbx_context* ctx) {
   return int64_t(4096) * ctx->sm_count * ctx->tuning.ctas_per_sm * ctx->tuning.warps_per_cta;

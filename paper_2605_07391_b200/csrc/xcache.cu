@@ -366,10 +366,9 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   const uint32_t cmax = pick.cmax;
   size_t tb = 0;
   void* temp = nullptr;
-  auto done = [&] {
-    cudaFreeAsync(cnt, s);
-    MBX_CUDA(cudaStreamSynchronize(s));
-  };
+  // (stream-ordered: the selection's kernels, the slot copy and K2 follow
+  // on the same stream, so nothing waits for them on the host)
+  auto done = [&] { cudaFreeAsync(cnt, s); };
   // no column can reach even the shared-line threshold (a stencil: at most
   // 27 references per column): no table, nothing more to do
   if (int64_t(cmax) * S <= int64_t(min_refs)) return done();

@@ -214,7 +214,7 @@ class Context:
     def set_tuning(self, warps_per_cta: int = 0, ctas_per_sm: int = 0, max_hubs: int = -1,
                    smem_per_sm: int | None = None, prefetch: int | None = None):
         """K2 launch shape (persistent grid; 0, 0: automatic -- 32 x 1, or 16 x 2
-        for a small fp32 matrix without a hub table), x hub-cache cap (-1 automatic, 0 off,
+        for a small matrix without a hub table), x hub-cache cap (-1 automatic, 0 off,
         > 0 a cap that also forces a table on small matrices),
         shared-memory budget per SM and the next tile's staging (0 none,
         1 L2 prefetch, 2 TMA bulk copy into shared memory, -1 auto)."""

@@ -23,7 +23,7 @@ c = mb.SimtConfig.make(32, 14 if dt == np.float32 else 7, 128)
 t = mb.generate_tile_for(A, c)
 for rep in range(2):
     for (w, cps) in [(0, 0), (32, 1), (16, 2), (8, 4)]:
-        ctx.set_tuning(w, cps, -1)
+        ctx.set_tuning(w, cps, -1, prefetch=int(os.environ.get("MODE", -1)))
         A.build_xcache()
         for _ in range(3):
             mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr())
@@ -33,5 +33,5 @@ for rep in range(2):
             mb.spmv_device(A, t, c, x.data_ptr(), y.data_ptr())
         e1.record(s)
         torch.cuda.synchronize()
-        print(f"s{scale} {w}x{cps} hubs {A.xcache_info()[0]}: "
+        print(f"s{scale} mode {os.environ.get('MODE', '-')} {w}x{cps} hubs {A.xcache_info()[0]}: "
               f"{e0.elapsed_time(e1) / 200 * 1e3:.1f} us", flush=True)
