@@ -271,24 +271,91 @@ __global__ void __launch_bounds__(1024) hub_pick_kernel(const uint32_t* __restri
   }
 }
 
-__global__ void flag_pick_kernel(const uint32_t* __restrict__ cnt, int64_t n, uint32_t tau,
-                                 int all_ties, uint8_t* __restrict__ flag) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const uint32_t c = cnt[i];
-    flag[i] = c > tau || (all_ties && c == tau);
-  }
-}
-
-struct CountIs {
+// The hub set in one selection pass: every column counted above tau, plus the
+// columns counted exactly tau below `cut` -- the column after the need-th tie
+// in column order (tie_cut_kernel), n when every tie is in.
+struct PickPred {
   const uint32_t* cnt;
-  uint32_t v;
-  __device__ bool operator()(int32_t i) const { return cnt[i] == v; }
+  uint32_t tau;
+  const int64_t* cut;
+  __device__ bool operator()(int32_t i) const {
+    const uint32_t c = cnt[i];
+    return c > tau || (c == tau && int64_t(i) < *cut);
+  }
 };
 
-__global__ void set_flags_kernel(const int32_t* __restrict__ ids, int k, uint8_t* flag) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < k) flag[ids[i]] = 1;
+// ties (count == tau) per chunk of kTieChunk columns, one block per chunk
+constexpr int kTieChunk = 8192;
+__global__ void __launch_bounds__(256) tie_count_kernel(const uint32_t* __restrict__ cnt,
+                                                        int64_t n, uint32_t tau,
+                                                        uint32_t* __restrict__ chunk_ties) {
+  using Reduce = cub::BlockReduce<uint32_t, 256>;
+  __shared__ typename Reduce::TempStorage tr;
+  const int64_t base = int64_t(blockIdx.x) * kTieChunk;
+  uint32_t k = 0;
+  for (int i = threadIdx.x * 4; i < kTieChunk && base + i < n; i += 256 * 4) {
+    if (base + i + 4 <= n) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(cnt + base + i));
+      k += (v.x == tau) + (v.y == tau) + (v.z == tau) + (v.w == tau);
+    } else {
+      for (int j = 0; j < 4 && base + i + j < n; ++j) k += cnt[base + i + j] == tau;
+    }
+  }
+  const uint32_t t = Reduce(tr).Sum(k);
+  if (threadIdx.x == 0) chunk_ties[blockIdx.x] = t;
+}
+
+// One block: the chunk in which the running tie count reaches `need`, then
+// the position of the need-th tie inside it; *cut = that column + 1.
+__global__ void __launch_bounds__(1024) tie_cut_kernel(const uint32_t* __restrict__ cnt,
+                                                       int64_t n, uint32_t tau,
+                                                       const uint32_t* __restrict__ chunk_ties,
+                                                       int64_t nchunks, int64_t need,
+                                                       int64_t* __restrict__ cut) {
+  using Scan = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename Scan::TempStorage ts;
+  __shared__ int64_t s_chunk, s_before, carry;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_chunk = -1;
+    s_before = 0;
+    carry = 0;
+  }
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < nchunks; b0 += 1024) {  // block-uniform trip count
+    const int64_t b = b0 + tid;
+    const int64_t v = b < nchunks ? int64_t(chunk_ties[b]) : 0;
+    int64_t ex = 0;
+    Scan(ts).ExclusiveSum(v, ex);
+    const int64_t c0 = carry;
+    if (v > 0 && c0 + ex < need && c0 + ex + v >= need) {
+      s_chunk = b;
+      s_before = c0 + ex;
+    }
+    __syncthreads();
+    if (tid == 1023) carry = c0 + ex + v;
+    __syncthreads();
+    if (s_chunk >= 0) break;
+  }
+  if (s_chunk < 0) {  // (need == every tie: not called)
+    if (tid == 0) *cut = n;
+    return;
+  }
+  // inside the chunk: 8 consecutive columns per thread, in column order
+  const int64_t base = s_chunk * kTieChunk + int64_t(tid) * 8;
+  int64_t k = 0;
+  for (int j = 0; j < 8; ++j) k += (base + j < n && cnt[base + j] == tau) ? 1 : 0;
+  int64_t ex = 0;
+  Scan(ts).ExclusiveSum(k, ex);
+  const int64_t want = need - s_before;  // the want-th tie of the chunk (1-based)
+  if (ex < want && ex + k >= want) {
+    int64_t seen = ex;
+    for (int j = 0; j < 8; ++j)
+      if (base + j < n && cnt[base + j] == tau && ++seen == want) {
+        *cut = base + j + 1;
+        break;
+      }
+  }
 }
 
 }  // namespace
@@ -410,34 +477,29 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
     // selected in ascending column order, which is the slot order
     const int h = pick.h;
     if (h > 0) {
-      const unsigned grid = unsigned(ctx->sm_count) * 8;
-      uint8_t* flag = nullptr;
-      int64_t* dk = nullptr;
-      MBX_CUDA(cudaMallocAsync(&flag, n + 64, s));
+      int64_t* dk = nullptr;  // [0] selected count, [1] the tie cut
       MBX_CUDA(cudaMallocAsync(&dk, 64, s));
-      const bool all_ties = pick.need == pick.ties;
-      flag_pick_kernel<<<grid, 256, 0, s>>>(cnt, n, pick.tau, all_ties ? 1 : 0, flag);
-      ++ctx->launches;
-      cub::CountingInputIterator<int32_t> it(0);
-      if (!all_ties) {
-        int32_t* ties = nullptr;
-        MBX_CUDA(cudaMallocAsync(&ties, size_t(pick.ties) * 4 + 64, s));
-        tb = 0;
-        MBX_CUDA(cub::DeviceSelect::If(nullptr, tb, it, ties, dk, n, CountIs{cnt, pick.tau}, s));
-        MBX_CUDA(cudaMallocAsync(&temp, tb + 64, s));
-        MBX_CUDA(cub::DeviceSelect::If(temp, tb, it, ties, dk, n, CountIs{cnt, pick.tau}, s));
-        cudaFreeAsync(temp, s);
-        set_flags_kernel<<<(pick.need + 255) / 256, 256, 0, s>>>(ties, pick.need, flag);
-        ++ctx->launches;
-        cudaFreeAsync(ties, s);
+      int64_t* cut = dk + 1;
+      if (pick.need == pick.ties) {
+        MBX_CUDA(cudaMemcpyAsync(cut, &n, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      } else {
+        const int64_t nchunks = (n + kTieChunk - 1) / kTieChunk;
+        uint32_t* chunk_ties = nullptr;
+        MBX_CUDA(cudaMallocAsync(&chunk_ties, size_t(nchunks) * 4 + 64, s));
+        tie_count_kernel<<<unsigned(nchunks), 256, 0, s>>>(cnt, n, pick.tau, chunk_ties);
+        tie_cut_kernel<<<1, 1024, 0, s>>>(cnt, n, pick.tau, chunk_ties, nchunks,
+                                          int64_t(pick.need), cut);
+        ctx->launches += 2;
+        cudaFreeAsync(chunk_ties, s);
       }
       MBX_CUDA(cudaMallocAsync(&m->hub_cols, size_t(h) * 4 + 64, s));
+      cub::CountingInputIterator<int32_t> it(0);
+      const PickPred pred{cnt, pick.tau, cut};
       tb = 0;
-      MBX_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flag, m->hub_cols, dk, n, s));
+      MBX_CUDA(cub::DeviceSelect::If(nullptr, tb, it, m->hub_cols, dk, n, pred, s));
       MBX_CUDA(cudaMallocAsync(&temp, tb + 64, s));
-      MBX_CUDA(cub::DeviceSelect::Flagged(temp, tb, it, flag, m->hub_cols, dk, n, s));
+      MBX_CUDA(cub::DeviceSelect::If(temp, tb, it, m->hub_cols, dk, n, pred, s));
       cudaFreeAsync(temp, s);
-      cudaFreeAsync(flag, s);
       cudaFreeAsync(dk, s);
       m->hub_avail = h;
       m->hub_coverage = std::min(1.0, double(pick.covered) * double(S) / double(m->nnz));
