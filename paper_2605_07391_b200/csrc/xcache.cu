@@ -103,11 +103,20 @@ constexpr int64_t kSampleRuns = int64_t(1) << 17;  // 32 nonzeros each (4 M samp
 // Also the gather locality of the sample: how many distinct 32-byte sectors
 // of x a run of 32 consecutive nonzeros touches (a stencil ~10, a random
 // or power-law matrix ~30), which picks K2's next-tile staging.
-__global__ void count_sample_kernel(const int32_t* __restrict__ cols, int64_t nnz,
-                                    int64_t stride_runs, int sector_shift,
-                                    uint32_t* __restrict__ cnt, uint32_t* __restrict__ cmax,
-                                    unsigned long long* __restrict__ sectors,
-                                    unsigned long long* __restrict__ full_runs) {
+// The first kSamplePriv columns are counted in shared memory per block and
+// flushed once (only the entries the block touched): R-MAT's hottest column
+// ids are the lowest ones -- column 0 alone takes 0.76^scale of the
+// references, serialised at one L2 atomic unit -- and a degree-relabelled
+// graph keeps all its hubs there.
+constexpr int kSamplePriv = 4096;
+
+__global__ void __launch_bounds__(1024) count_sample_kernel(
+    const int32_t* __restrict__ cols, int64_t nnz, int64_t stride_runs, int sector_shift,
+    uint32_t* __restrict__ cnt, uint32_t* __restrict__ cmax,
+    unsigned long long* __restrict__ sectors, unsigned long long* __restrict__ full_runs) {
+  __shared__ uint32_t priv[kSamplePriv];
+  for (int i = threadIdx.x; i < kSamplePriv; i += blockDim.x) priv[i] = 0;
+  __syncthreads();
   const int lid = threadIdx.x & 31;
   const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -117,7 +126,10 @@ __global__ void count_sample_kernel(const int32_t* __restrict__ cols, int64_t nn
   for (int64_t r = w * stride_runs; r < runs; r += nw * stride_runs) {
     const int64_t k = r * 32 + lid;
     const int32_t c = k < nnz ? __ldg(cols + k) : -1;
-    if (k < nnz) mx = max(mx, atomicAdd(cnt + c, 1u) + 1u);
+    if (c >= kSamplePriv)
+      mx = max(mx, atomicAdd(cnt + c, 1u) + 1u);
+    else if (c >= 0)
+      atomicAdd(priv + c, 1u);
     if (r * 32 + 32 <= nnz) {  // warp-uniform: a full run
       const unsigned same = __match_any_sync(0xffffffffu, c >> sector_shift);
       const unsigned leaders = __ballot_sync(0xffffffffu, lid == __ffs(same) - 1);
@@ -125,6 +137,10 @@ __global__ void count_sample_kernel(const int32_t* __restrict__ cols, int64_t nn
       ++nr;
     }
   }
+  __syncthreads();
+  // flush: the last block to add to a column sees its full count
+  for (int i = threadIdx.x; i < kSamplePriv; i += blockDim.x)
+    if (priv[i]) mx = max(mx, atomicAdd(cnt + i, priv[i]) + priv[i]);
   mx = __reduce_max_sync(0xffffffffu, mx);
   if (lid == 0) {
     if (mx) atomicMax(cmax, mx);
@@ -179,15 +195,44 @@ __global__ void __launch_bounds__(512) count_hist_kernel(const uint32_t* __restr
   __shared__ uint32_t h[kHistBins];
   for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const uint32_t c = __ldcs(cnt + i);
-    if (c == 0) continue;
+  // counts 1..kLow-1 (most sampled columns: every thread of a block would
+  // hit the same few bins) are tallied in registers and added once per warp
+  constexpr int kLow = 4;
+  uint32_t low[kLow] = {};
+  auto tally = [&](uint32_t c) {
+    if (c < kLow) {
+#pragma unroll
+      for (int b = 1; b < kLow; ++b) low[b] += c == uint32_t(b) ? 1u : 0u;
+      return;
+    }
     if (c >= kHistBins - 1) {
       atomicAdd(&pick->capsum, (unsigned long long)c);
       atomicMax(&pick->capmax, c);
     }
     atomicAdd(&h[c < kHistBins - 1 ? c : kHistBins - 1], 1u);
+  };
+  // 16-byte loads, two per step in flight (cnt is 256-byte aligned)
+  const int64_t n4 = n / 4;
+  const int64_t tstride = int64_t(gridDim.x) * blockDim.x;
+  const uint4* c4 = reinterpret_cast<const uint4*>(cnt);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += 2 * tstride) {
+    const uint4 a = __ldcs(c4 + i);
+    const uint4 b = i + tstride < n4 ? __ldcs(c4 + i + tstride) : make_uint4(0, 0, 0, 0);
+    tally(a.x);
+    tally(a.y);
+    tally(a.z);
+    tally(a.w);
+    tally(b.x);
+    tally(b.y);
+    tally(b.z);
+    tally(b.w);
+  }
+  for (int64_t i = n4 * 4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += tstride)
+    tally(cnt[i]);
+#pragma unroll
+  for (int b = 1; b < kLow; ++b) {
+    const uint32_t t = __reduce_add_sync(0xffffffffu, low[b]);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(&h[b], t);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
@@ -271,78 +316,89 @@ __global__ void __launch_bounds__(1024) hub_pick_kernel(const uint32_t* __restri
   }
 }
 
-// The hub set in one selection pass: every column counted above tau, plus the
-// columns counted exactly tau below `cut` -- the column after the need-th tie
-// in column order (tie_cut_kernel), n when every tie is in.
-struct PickPred {
-  const uint32_t* cnt;
-  uint32_t tau;
-  const int64_t* cut;
-  __device__ bool operator()(int32_t i) const {
-    const uint32_t c = cnt[i];
-    return c > tau || (c == tau && int64_t(i) < *cut);
-  }
-};
+// The hub set, ascending: every column counted above tau, plus the columns
+// counted exactly tau up to the need-th such column in column order.  Three
+// passes over chunks of kPickChunk columns, no global sort or select:
+// pick_count (per chunk: columns above tau, ties), pick_scan (one block: the
+// chunk holding the need-th tie, the exact cut inside it, every chunk's
+// output offset), pick_write (per chunk: a block scan places its hubs).
+constexpr int kPickChunk = 8192;
+constexpr int kPickThreads = 256;
+constexpr int kPickPer = kPickChunk / kPickThreads;  // consecutive columns per thread
 
-// ties (count == tau) per chunk of kTieChunk columns, one block per chunk
-constexpr int kTieChunk = 8192;
-__global__ void __launch_bounds__(256) tie_count_kernel(const uint32_t* __restrict__ cnt,
-                                                        int64_t n, uint32_t tau,
-                                                        uint32_t* __restrict__ chunk_ties) {
-  using Reduce = cub::BlockReduce<uint32_t, 256>;
+__global__ void __launch_bounds__(kPickThreads) pick_count_kernel(
+    const uint32_t* __restrict__ cnt, int64_t n, uint32_t tau, uint32_t* __restrict__ above,
+    uint32_t* __restrict__ ties) {
+  using Reduce = cub::BlockReduce<uint32_t, kPickThreads>;
   __shared__ typename Reduce::TempStorage tr;
-  const int64_t base = int64_t(blockIdx.x) * kTieChunk;
-  uint32_t k = 0;
-  for (int i = threadIdx.x * 4; i < kTieChunk && base + i < n; i += 256 * 4) {
-    if (base + i + 4 <= n) {
-      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(cnt + base + i));
-      k += (v.x == tau) + (v.y == tau) + (v.z == tau) + (v.w == tau);
+  const int64_t base = int64_t(blockIdx.x) * kPickChunk;
+  uint32_t ka = 0, kt = 0;
+  for (int i = threadIdx.x * 4; i < kPickChunk && base + i < n; i += kPickThreads * 4) {
+    if (base + i + 4 <= n) {  // 16-byte loads (cnt is 256-byte aligned)
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(cnt + base + i));
+      ka += (v.x > tau) + (v.y > tau) + (v.z > tau) + (v.w > tau);
+      kt += (v.x == tau) + (v.y == tau) + (v.z == tau) + (v.w == tau);
     } else {
-      for (int j = 0; j < 4 && base + i + j < n; ++j) k += cnt[base + i + j] == tau;
+      for (int j = 0; j < 4 && base + i + j < n; ++j) {
+        ka += cnt[base + i + j] > tau;
+        kt += cnt[base + i + j] == tau;
+      }
     }
   }
-  const uint32_t t = Reduce(tr).Sum(k);
-  if (threadIdx.x == 0) chunk_ties[blockIdx.x] = t;
+  const uint32_t ta = Reduce(tr).Sum(ka);
+  __syncthreads();
+  const uint32_t tt = Reduce(tr).Sum(kt);
+  if (threadIdx.x == 0) {
+    above[blockIdx.x] = ta;
+    ties[blockIdx.x] = tt;
+  }
 }
 
-// One block: the chunk in which the running tie count reaches `need`, then
-// the position of the need-th tie inside it; *cut = that column + 1.
-__global__ void __launch_bounds__(1024) tie_cut_kernel(const uint32_t* __restrict__ cnt,
-                                                       int64_t n, uint32_t tau,
-                                                       const uint32_t* __restrict__ chunk_ties,
-                                                       int64_t nchunks, int64_t need,
-                                                       int64_t* __restrict__ cut) {
+__global__ void __launch_bounds__(1024) pick_scan_kernel(
+    const uint32_t* __restrict__ cnt, int64_t n, uint32_t tau,
+    const uint32_t* __restrict__ above, const uint32_t* __restrict__ ties, int64_t nchunks,
+    int64_t need, int64_t* __restrict__ chunk_off, int64_t* __restrict__ cut) {
   using Scan = cub::BlockScan<int64_t, 1024>;
   __shared__ typename Scan::TempStorage ts;
-  __shared__ int64_t s_chunk, s_before, carry;
+  __shared__ int64_t s_chunk, s_before, carry_t, carry_o;
   const int tid = threadIdx.x;
   if (tid == 0) {
     s_chunk = -1;
     s_before = 0;
-    carry = 0;
+    carry_t = 0;
+    carry_o = 0;
   }
   __syncthreads();
   for (int64_t b0 = 0; b0 < nchunks; b0 += 1024) {  // block-uniform trip count
     const int64_t b = b0 + tid;
-    const int64_t v = b < nchunks ? int64_t(chunk_ties[b]) : 0;
+    const int64_t vt = b < nchunks ? int64_t(ties[b]) : 0;
     int64_t ex = 0;
-    Scan(ts).ExclusiveSum(v, ex);
-    const int64_t c0 = carry;
-    if (v > 0 && c0 + ex < need && c0 + ex + v >= need) {
+    Scan(ts).ExclusiveSum(vt, ex);
+    const int64_t t0 = carry_t + ex;  // ties in the chunks before b
+    if (vt > 0 && t0 < need && t0 + vt >= need) {
       s_chunk = b;
-      s_before = c0 + ex;
+      s_before = t0;
+    }
+    // ties this chunk admits, then the output offsets
+    const int64_t adm = vt == 0 ? 0 : (t0 >= need ? 0 : (t0 + vt <= need ? vt : need - t0));
+    const int64_t sel = (b < nchunks ? int64_t(above[b]) : 0) + adm;
+    __syncthreads();
+    int64_t off = 0;
+    Scan(ts).ExclusiveSum(sel, off);
+    if (b < nchunks) chunk_off[b] = carry_o + off;
+    __syncthreads();
+    if (tid == 1023) {
+      carry_t += ex + vt;
+      carry_o += off + sel;
     }
     __syncthreads();
-    if (tid == 1023) carry = c0 + ex + v;
-    __syncthreads();
-    if (s_chunk >= 0) break;
   }
-  if (s_chunk < 0) {  // (need == every tie: not called)
-    if (tid == 0) *cut = n;
+  if (s_chunk < 0) {  // no tie admitted
+    if (tid == 0) *cut = 0;
     return;
   }
-  // inside the chunk: 8 consecutive columns per thread, in column order
-  const int64_t base = s_chunk * kTieChunk + int64_t(tid) * 8;
+  // inside the crossing chunk: 8 consecutive columns per thread
+  const int64_t base = s_chunk * kPickChunk + int64_t(tid) * 8;
   int64_t k = 0;
   for (int j = 0; j < 8; ++j) k += (base + j < n && cnt[base + j] == tau) ? 1 : 0;
   int64_t ex = 0;
@@ -356,6 +412,39 @@ __global__ void __launch_bounds__(1024) tie_cut_kernel(const uint32_t* __restric
         break;
       }
   }
+}
+
+__global__ void __launch_bounds__(kPickThreads) pick_write_kernel(
+    const uint32_t* __restrict__ cnt, int64_t n, uint32_t tau, const int64_t* __restrict__ cut,
+    const int64_t* __restrict__ chunk_off, int32_t* __restrict__ out) {
+  using Scan = cub::BlockScan<uint32_t, kPickThreads>;
+  __shared__ typename Scan::TempStorage ts;
+  const int64_t base = int64_t(blockIdx.x) * kPickChunk + int64_t(threadIdx.x) * kPickPer;
+  const int64_t cu = *cut;
+  uint32_t c[kPickPer];
+#pragma unroll
+  for (int j = 0; j < kPickPer; j += 4) {
+    if (base + j + 4 <= n) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(cnt + base + j));
+      c[j] = v.x;
+      c[j + 1] = v.y;
+      c[j + 2] = v.z;
+      c[j + 3] = v.w;
+    } else {
+      for (int q = 0; q < 4; ++q) c[j + q] = base + j + q < n ? cnt[base + j + q] : 0u;
+    }
+  }
+  uint32_t mine = 0;
+#pragma unroll
+  for (int j = 0; j < kPickPer; ++j)
+    mine += (c[j] > tau || (c[j] == tau && base + j < cu)) ? 1u : 0u;
+  uint32_t ex = 0;
+  Scan(ts).ExclusiveSum(mine, ex);
+  if (!mine) return;
+  int64_t o = chunk_off[blockIdx.x] + ex;
+#pragma unroll
+  for (int j = 0; j < kPickPer; ++j)
+    if (c[j] > tau || (c[j] == tau && base + j < cu)) out[o++] = int32_t(base + j);
 }
 
 }  // namespace
@@ -411,7 +500,7 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   MBX_CUDA(cudaMallocAsync(&hist, kHistBins * 4 + sizeof(HubPick) + 64, s));
   dpick = reinterpret_cast<HubPick*>(hist + kHistBins);
   MBX_CUDA(cudaMemsetAsync(hist, 0, kHistBins * 4 + sizeof(HubPick), s));
-  count_sample_kernel<<<unsigned(ctx->sm_count) * 8, 256, 0, s>>>(
+  count_sample_kernel<<<unsigned(ctx->sm_count) * 2, 1024, 0, s>>>(
       m->cols, m->nnz, S, m->precision == MBX_F32 ? 3 : 2, cnt, &dpick->cmax, &dpick->sectors,
       &dpick->full_runs);
   ++ctx->launches;
@@ -477,30 +566,22 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
     // selected in ascending column order, which is the slot order
     const int h = pick.h;
     if (h > 0) {
-      int64_t* dk = nullptr;  // [0] selected count, [1] the tie cut
-      MBX_CUDA(cudaMallocAsync(&dk, 64, s));
-      int64_t* cut = dk + 1;
-      if (pick.need == pick.ties) {
-        MBX_CUDA(cudaMemcpyAsync(cut, &n, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-      } else {
-        const int64_t nchunks = (n + kTieChunk - 1) / kTieChunk;
-        uint32_t* chunk_ties = nullptr;
-        MBX_CUDA(cudaMallocAsync(&chunk_ties, size_t(nchunks) * 4 + 64, s));
-        tie_count_kernel<<<unsigned(nchunks), 256, 0, s>>>(cnt, n, pick.tau, chunk_ties);
-        tie_cut_kernel<<<1, 1024, 0, s>>>(cnt, n, pick.tau, chunk_ties, nchunks,
-                                          int64_t(pick.need), cut);
-        ctx->launches += 2;
-        cudaFreeAsync(chunk_ties, s);
-      }
+      const int64_t nchunks = (n + kPickChunk - 1) / kPickChunk;
+      uint32_t* chunk_cnt = nullptr;  // above | ties
+      int64_t* chunk_off = nullptr;   // nchunks offsets, then the tie cut
+      MBX_CUDA(cudaMallocAsync(&chunk_cnt, size_t(nchunks) * 8 + 64, s));
+      MBX_CUDA(cudaMallocAsync(&chunk_off, size_t(nchunks + 1) * 8 + 64, s));
+      int64_t* cut = chunk_off + nchunks;
+      pick_count_kernel<<<unsigned(nchunks), kPickThreads, 0, s>>>(cnt, n, pick.tau, chunk_cnt,
+                                                                   chunk_cnt + nchunks);
+      pick_scan_kernel<<<1, 1024, 0, s>>>(cnt, n, pick.tau, chunk_cnt, chunk_cnt + nchunks,
+                                          nchunks, int64_t(pick.need), chunk_off, cut);
       MBX_CUDA(cudaMallocAsync(&m->hub_cols, size_t(h) * 4 + 64, s));
-      cub::CountingInputIterator<int32_t> it(0);
-      const PickPred pred{cnt, pick.tau, cut};
-      tb = 0;
-      MBX_CUDA(cub::DeviceSelect::If(nullptr, tb, it, m->hub_cols, dk, n, pred, s));
-      MBX_CUDA(cudaMallocAsync(&temp, tb + 64, s));
-      MBX_CUDA(cub::DeviceSelect::If(temp, tb, it, m->hub_cols, dk, n, pred, s));
-      cudaFreeAsync(temp, s);
-      cudaFreeAsync(dk, s);
+      pick_write_kernel<<<unsigned(nchunks), kPickThreads, 0, s>>>(cnt, n, pick.tau, cut,
+                                                                   chunk_off, m->hub_cols);
+      ctx->launches += 3;
+      cudaFreeAsync(chunk_cnt, s);
+      cudaFreeAsync(chunk_off, s);
       m->hub_avail = h;
       m->hub_coverage = std::min(1.0, double(pick.covered) * double(S) / double(m->nnz));
     }

@@ -347,3 +347,26 @@ def test_trace_deposits_conserve_every_product(ctx, cfg):
     want, mag = O.spmv_csr_f64(a, x, want_abs=True)
     assert (np.abs(totals - want) <= 1e-12 * np.where(mag > 0, mag, 1)).all()
     assert (np.abs(y - want) <= 1e-12 * np.where(mag > 0, mag, 1)).all()
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_automatic_launch_shape(dtype):
+    """set_tuning(0, 0): the automatic K2 launch shape (16 x 2 and no TMA
+    staging for a small matrix without a hub table) -- bitwise the result of
+    an explicit 32 x 1 launch; a half-automatic shape is a config error."""
+    ctx = mb.Context(0)
+    m = mb.DeviceMatrix.rmat(ctx, 15, 16, seed=6, dtype=dtype)
+    c = mb.SimtConfig.make(32, 14 if dtype == np.float32 else 7, 128)
+    t = mb.generate_tile_for(m, c)
+    x = O.hash_uniform(3, m.n_cols, -1.0, 1.0, dtype)
+    ys = []
+    for shape in ((0, 0), (32, 1), (0, 0)):
+        ctx.set_tuning(*shape, -1)
+        m.build_xcache()
+        assert m.xcache_info()[0] == 0  # small: no automatic hub table
+        ys.append(mb.spmv_merbit(m, t, c, x, mb.DualBuffer(m.n_rows, dtype)).copy())
+    u = np.uint32 if dtype == np.float32 else np.uint64
+    assert np.array_equal(ys[0].view(u), ys[1].view(u))
+    assert np.array_equal(ys[0].view(u), ys[2].view(u))
+    with pytest.raises(mb.ConfigError):
+        ctx.set_tuning(0, 1, -1)
