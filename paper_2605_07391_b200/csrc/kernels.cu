@@ -1671,7 +1671,7 @@ __global__ void gen_tile_kernel(const uint32_t* __restrict__ ro, int64_t n, int6
   }
 }
 
-// K1 for omega dividing 32 (the default 32): one CTA per 1024 lanes, no
+// K1 for omega dividing 32 (the default 32): one CTA per kK1Lanes lanes, no
 // per-lane search.  The merge path moves down exactly at diagonal
 // e_r = ro[r+1] + r (the step after row r's last nonzero), so a lane's step
 // flags are the row ends that fall in its sigma diagonals, and its start
@@ -1682,7 +1682,17 @@ __global__ void gen_tile_kernel(const uint32_t* __restrict__ ro, int64_t n, int6
 // (shared-memory atomicOr), and a block scan of the flag popcounts gives
 // every lane's (x, y).  The per-lane binary search of gen_tile_kernel cost
 // ~log2(n) dependent loads per lane.  Output byte-identical.
-constexpr int kK1Lanes = 1024;  // lanes per CTA (4 per thread)
+#ifndef MBX_K1_THREADS
+#define MBX_K1_THREADS 128
+#endif
+#ifndef MBX_K1_PER
+#define MBX_K1_PER 4
+#endif
+constexpr int kK1Threads = MBX_K1_THREADS;
+constexpr int kK1Per = MBX_K1_PER;             // lanes per thread (a multiple of 4)
+// (CTA shape measured, scripts/prof/k1_ab.sh: 128 x 4 lanes 1-2 % ahead of 256 x 4,
+// 512 x 4 +6 %, 128 x 8 +13-30 %)
+constexpr int kK1Lanes = kK1Threads * kK1Per;  // lanes per CTA
 
 __global__ void gen_tile_bounds_kernel(const uint32_t* __restrict__ ro, int64_t n, int64_t m,
                                        int sigma, int64_t blocks, int64_t* __restrict__ bnd) {
@@ -1693,13 +1703,13 @@ __global__ void gen_tile_bounds_kernel(const uint32_t* __restrict__ ro, int64_t 
   bnd[b] = y;
 }
 
-__global__ void __launch_bounds__(256) gen_tile_scan_kernel(
+__global__ void __launch_bounds__(kK1Threads) gen_tile_scan_kernel(
     const uint32_t* __restrict__ ro, int64_t n, int64_t m, int omega, int sigma, int ob,
     int64_t lane_num, const int64_t* __restrict__ bnd, uint32_t* __restrict__ tile_x,
     uint32_t* __restrict__ tile_y, uint32_t* __restrict__ lane_desc) {
-  __shared__ uint32_t fl[kK1Lanes];
+  __shared__ __align__(16) uint32_t fl[kK1Lanes];
   __shared__ int pre[kK1Lanes + 1];  // row ends before each lane (CTA-relative)
-  __shared__ int wsum[8];
+  __shared__ int wsum[kK1Threads / 32];
   const int tid = threadIdx.x, lid = tid & 31, wid = tid >> 5;
   const int64_t j0 = int64_t(blockIdx.x) * kK1Lanes;
   const int64_t d0 = j0 * sigma;
@@ -1707,14 +1717,16 @@ __global__ void __launch_bounds__(256) gen_tile_scan_kernel(
   const int64_t span = imin64(int64_t(kK1Lanes) * sigma, total - d0);  // this CTA's diagonals
   const int64_t y0 = bnd[blockIdx.x];
   const int64_t r1 = imin64(bnd[blockIdx.x + 1], n - 1);  // last row that can end inside
-  reinterpret_cast<uint4*>(fl)[tid] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+  for (int v = 0; v < kK1Per / 4; ++v)
+    reinterpret_cast<uint4*>(fl)[tid * (kK1Per / 4) + v] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
   const float inv_sigma = 1.0f / float(sigma);
-#pragma unroll 4
-  for (int64_t r = y0 + tid; r <= r1; r += 256) {
+#pragma unroll 8
+  for (int64_t r = y0 + tid; r <= r1; r += kK1Threads) {
     const int64_t p = int64_t(__ldg(ro + r + 1)) + r - d0;  // e_r - d0 >= 0
     if (p < span) {
-      const int q = int(p);  // < kK1Lanes * sigma <= 2^15: q / sigma from the
+      const int q = int(p);  // < kK1Lanes * sigma <= 2^16: q / sigma from the
       int l = __float2int_rz(float(q) * inv_sigma);  // float reciprocal, corrected
       l += (l + 1) * sigma <= q ? 1 : 0;
       l -= l * sigma > q ? 1 : 0;
@@ -1722,10 +1734,22 @@ __global__ void __launch_bounds__(256) gen_tile_scan_kernel(
     }
   }
   __syncthreads();
-  const uint4 f4 = reinterpret_cast<const uint4*>(fl)[tid];
-  const uint32_t f[4] = {f4.x, f4.y, f4.z, f4.w};
-  const int c0 = __popc(f[0]), c1 = __popc(f[1]), c2 = __popc(f[2]), c3 = __popc(f[3]);
-  const int c = c0 + c1 + c2 + c3;
+  uint32_t f[kK1Per];
+  int cl[kK1Per];
+  int c = 0;
+#pragma unroll
+  for (int v = 0; v < kK1Per / 4; ++v) {
+    const uint4 f4 = reinterpret_cast<const uint4*>(fl)[tid * (kK1Per / 4) + v];
+    f[4 * v] = f4.x;
+    f[4 * v + 1] = f4.y;
+    f[4 * v + 2] = f4.z;
+    f[4 * v + 3] = f4.w;
+  }
+#pragma unroll
+  for (int k = 0; k < kK1Per; ++k) {
+    cl[k] = __popc(f[k]);
+    c += cl[k];
+  }
   int inc = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1736,16 +1760,17 @@ __global__ void __launch_bounds__(256) gen_tile_scan_kernel(
   __syncthreads();
   int base = inc - c;
   for (int w = 0; w < wid; ++w) base += wsum[w];
-  pre[4 * tid] = base;
-  pre[4 * tid + 1] = base + c0;
-  pre[4 * tid + 2] = base + c0 + c1;
-  pre[4 * tid + 3] = base + c0 + c1 + c2;
-  if (tid == 255) pre[kK1Lanes] = base + c;
-  __syncthreads();
-  uint32_t d[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int l = 4 * tid + k;
+  for (int k = 0; k < kK1Per; ++k) {
+    pre[kK1Per * tid + k] = base;
+    base += cl[k];
+  }
+  if (tid == kK1Threads - 1) pre[kK1Lanes] = base;
+  __syncthreads();
+  uint32_t d[kK1Per];
+#pragma unroll
+  for (int k = 0; k < kK1Per; ++k) {
+    const int l = kK1Per * tid + k;
     const int ld = l & ~(omega - 1);  // the tile's first lane
     const int pl = pre[l], pld = pre[ld];
     // offsets from the tile's start point, in 32 bits: rows and nonzeros
@@ -1762,12 +1787,15 @@ __global__ void __launch_bounds__(256) gen_tile_scan_kernel(
       tile_y[j / omega] = uint32_t(tsy) | (any_down ? 0u : kLongRowMask);
     }
   }
-  const int64_t j = j0 + 4 * tid;
-  if (j + 3 < lane_num) {
-    *reinterpret_cast<uint4*>(lane_desc + j) = make_uint4(d[0], d[1], d[2], d[3]);
+  const int64_t j = j0 + kK1Per * tid;
+  if (j + kK1Per - 1 < lane_num) {
+#pragma unroll
+    for (int v = 0; v < kK1Per / 4; ++v)
+      reinterpret_cast<uint4*>(lane_desc + j)[v] =
+          make_uint4(d[4 * v], d[4 * v + 1], d[4 * v + 2], d[4 * v + 3]);
   } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < kK1Per; ++k)
       if (j + k < lane_num) lane_desc[j + k] = d[k];
   }
 }
@@ -2394,7 +2422,7 @@ void launch_generate_tile(mbx_context* ctx, const uint32_t* ro, int64_t n_rows, 
       MBX_CUDA(cudaMallocAsync(&bnd, size_t(cblocks + 1) * 8 + 64, ctx->stream));
       gen_tile_bounds_kernel<<<static_cast<unsigned>((cblocks + 256) / 256), 256, 0,
                                ctx->stream>>>(ro, n_rows, nnz, c.sigma, cblocks, bnd);
-      gen_tile_scan_kernel<<<static_cast<unsigned>(cblocks), 256, 0, ctx->stream>>>(
+      gen_tile_scan_kernel<<<static_cast<unsigned>(cblocks), kK1Threads, 0, ctx->stream>>>(
           ro, n_rows, nnz, c.omega, c.sigma, c.offset_bits, lanes, bnd, t->tile_x, t->tile_y,
           t->lane_desc);
       ++ctx->launches;

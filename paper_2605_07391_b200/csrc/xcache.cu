@@ -103,6 +103,29 @@ constexpr int64_t kSampleRuns = int64_t(1) << 17;  // 32 nonzeros each (4 M samp
 // Also the gather locality of the sample: how many distinct 32-byte sectors
 // of x a run of 32 consecutive nonzeros touches (a stencil ~10, a random
 // or power-law matrix ~30), which picks K2's next-tile staging.
+// Distinct 32-byte x sectors in runs of 32 consecutive nonzeros (every
+// stride-th run) -- the pilot that tells a local matrix (a stencil) from a
+// request-bound one before any counting.
+__global__ void sector_sample_kernel(const int32_t* __restrict__ cols, int64_t nnz,
+                                     int64_t stride_runs, int sector_shift,
+                                     unsigned long long* __restrict__ out) {
+  const int lid = threadIdx.x & 31;
+  const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t full = nnz / 32;
+  unsigned long long sec = 0, nr = 0;
+  for (int64_t r = w * stride_runs; r < full; r += nw * stride_runs) {
+    const int32_t c = __ldg(cols + r * 32 + lid);
+    const unsigned same = __match_any_sync(0xffffffffu, c >> sector_shift);
+    sec += __popc(__ballot_sync(0xffffffffu, lid == __ffs(same) - 1));
+    ++nr;
+  }
+  if (lid == 0 && nr) {
+    atomicAdd(out, sec);
+    atomicAdd(out + 1, nr);
+  }
+}
+
 // The first kSamplePriv columns are counted in shared memory per block and
 // flushed once (only the entries the block touched): R-MAT's hottest column
 // ids are the lowest ones -- column 0 alone takes 0.76^scale of the
@@ -113,7 +136,10 @@ constexpr int kSamplePriv = 4096;
 __global__ void __launch_bounds__(1024) count_sample_kernel(
     const int32_t* __restrict__ cols, int64_t nnz, int64_t stride_runs, int sector_shift,
     uint32_t* __restrict__ cnt, uint32_t* __restrict__ cmax,
-    unsigned long long* __restrict__ sectors, unsigned long long* __restrict__ full_runs) {
+    unsigned long long* __restrict__ sectors, unsigned long long* __restrict__ full_runs,
+    const unsigned long long* __restrict__ pilot, int local_sectors) {
+  // a local matrix (pilot: sectors, runs) gets no table: nothing to count
+  if (pilot && pilot[1] && pilot[0] < (unsigned long long)local_sectors * pilot[1]) return;
   __shared__ uint32_t priv[kSamplePriv];
   for (int i = threadIdx.x; i < kSamplePriv; i += blockDim.x) priv[i] = 0;
   __syncthreads();
@@ -185,7 +211,14 @@ struct HubPick {
   int32_t ties;                // columns with count == tau
   int32_t fallback;            // ties inside the last bin: rank by sorting instead
   int32_t pad;
+  unsigned long long psectors;  // pilot sample (automatic mode): distinct sectors ...
+  unsigned long long pruns;     // ... over this many full runs
 };
+
+// Gathers this local (fewer distinct x sectors per run than this) coalesce
+// and hit L1: no hub table is built for them (automatic mode), and K2 takes
+// the L2 prefetch staging (resolve_prefetch).
+constexpr int kLocalSectors = 16;
 
 __global__ void __launch_bounds__(512) count_hist_kernel(const uint32_t* __restrict__ cnt,
                                                          int64_t n, uint32_t* __restrict__ hist,
@@ -500,9 +533,17 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   MBX_CUDA(cudaMallocAsync(&hist, kHistBins * 4 + sizeof(HubPick) + 64, s));
   dpick = reinterpret_cast<HubPick*>(hist + kHistBins);
   MBX_CUDA(cudaMemsetAsync(hist, 0, kHistBins * 4 + sizeof(HubPick), s));
+  const int sector_shift = m->precision == MBX_F32 ? 3 : 2;
+  const bool pilot = max_hubs < 0;  // automatic mode: local matrices get no table
+  if (pilot) {
+    constexpr int64_t kPilotRuns = int64_t(1) << 14;
+    sector_sample_kernel<<<unsigned(ctx->sm_count) * 2, 256, 0, s>>>(
+        m->cols, m->nnz, std::max<int64_t>(1, runs / kPilotRuns), sector_shift, &dpick->psectors);
+    ++ctx->launches;
+  }
   count_sample_kernel<<<unsigned(ctx->sm_count) * 2, 1024, 0, s>>>(
-      m->cols, m->nnz, S, m->precision == MBX_F32 ? 3 : 2, cnt, &dpick->cmax, &dpick->sectors,
-      &dpick->full_runs);
+      m->cols, m->nnz, S, sector_shift, cnt, &dpick->cmax, &dpick->sectors, &dpick->full_runs,
+      pilot ? &dpick->psectors : nullptr, kLocalSectors);
   ++ctx->launches;
   // one pass over the counts: their histogram, then the hub set's
   // threshold (hub_pick_kernel) -- one host synchronisation for the lot
@@ -525,6 +566,11 @@ void build_xcache(mbx_context* ctx, mbx_matrix* m, int max_hubs) {
   // (stream-ordered: the selection's kernels, the slot copy and K2 follow
   // on the same stream, so nothing waits for them on the host)
   auto done = [&] { cudaFreeAsync(cnt, s); };
+  if (pilot && pick.pruns && pick.psectors < (unsigned long long)kLocalSectors * pick.pruns) {
+    // local gathers (the sample and selection kernels returned at once)
+    m->gather_sectors = double(pick.psectors) / double(pick.pruns);
+    return done();
+  }
   // no column can reach even the shared-line threshold (a stencil: at most
   // 27 references per column): no table, nothing more to do
   if (int64_t(cmax) * S <= int64_t(min_refs)) return done();
