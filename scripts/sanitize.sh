@@ -38,7 +38,7 @@ echo "tests synccheck rc=$? :: $(grep -E 'passed|failed|ERROR SUMMARY' gpurun_ou
 # the exact-top-h and capped-count hub tests and the compact round trips
 for tool in memcheck racecheck initcheck; do
   timeout 1500 $CS --tool $tool python -m pytest -q -x -m gpu -p no:cacheprovider \
-    tests/test_gpu_xcache.py tests/test_gpu_spmv.py -k "top_h or capped or compact" \
+    tests/test_gpu_xcache.py tests/test_gpu_spmv.py -k "top_h or capped or compact or automatic or stencil or local" \
     > gpurun_out/sanitize_preproc_$tool.log 2>&1
   echo "preprocessing $tool rc=$? :: $(grep -E 'passed|failed|ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/sanitize_preproc_$tool.log | tail -2 | tr '\n' ' ')"
 done

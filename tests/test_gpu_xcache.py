@@ -97,6 +97,28 @@ def test_gather_profile_picks_the_staging(ctx):
     assert np.array_equal(y0.view(np.uint32), y_auto.view(np.uint32))
 
 
+def test_automatic_mode_skips_local_matrices(ctx):
+    """build_xcache() (automatic) on a matrix big enough for a table: a
+    device pilot of distinct x sectors per run finds the stencil's gathers
+    local (< 16) and no column is counted -- no table, the locality kept for
+    K2's staging; R-MAT (~31 sectors) goes on to the counted selection.
+    SpMV results are bitwise those of a forced table."""
+    S = mb.DeviceMatrix.stencil27(ctx, 100, np.float32)  # 27 M nonzeros
+    S.build_xcache()
+    assert S.xcache_info()[0] == 0
+    assert 0.0 < S.gather_sectors() < 16.0
+    c = mb.SimtConfig.make(32, 14, 128)
+    t = mb.generate_tile_for(S, c)
+    x = O.hash_uniform(5, S.n_cols, -1.0, 1.0, np.float32)
+    y_auto = mb.spmv_merbit(S, t, c, x, mb.DualBuffer(S.n_rows, np.float32)).copy()
+    S.build_xcache(FORCE_HUBS)
+    y_forced = mb.spmv_merbit(S, t, c, x, mb.DualBuffer(S.n_rows, np.float32))
+    assert np.array_equal(y_auto.view(np.uint32), y_forced.view(np.uint32))
+    R = mb.DeviceMatrix.rmat(ctx, 21, 16, seed=2, transition=True, dtype=np.float32)
+    R.build_xcache()
+    assert R.xcache_info()[0] > 0 and R.gather_sectors() > 24.0
+
+
 def test_hub_budget_shrinks_as_x_outgrows_l2():
     """K2's shared-memory budget per SM depends on x's size (160 KB up to
     192 MB of fp32 x, 128 KB to 384 MB, 96 KB beyond): the same 40,000
