@@ -1708,7 +1708,7 @@ __global__ void __launch_bounds__(kK1Threads) gen_tile_scan_kernel(
     int64_t lane_num, const int64_t* __restrict__ bnd, uint32_t* __restrict__ tile_x,
     uint32_t* __restrict__ tile_y, uint32_t* __restrict__ lane_desc) {
   __shared__ __align__(16) uint32_t fl[kK1Lanes];
-  __shared__ int pre[kK1Lanes + 1];  // row ends before each lane (CTA-relative)
+  __shared__ __align__(16) int pre[kK1Lanes + 4];  // row ends before each lane (CTA-relative)
   __shared__ int wsum[kK1Threads / 32];
   const int tid = threadIdx.x, lid = tid & 31, wid = tid >> 5;
   const int64_t j0 = int64_t(blockIdx.x) * kK1Lanes;
@@ -1760,11 +1760,18 @@ __global__ void __launch_bounds__(kK1Threads) gen_tile_scan_kernel(
   __syncthreads();
   int base = inc - c;
   for (int w = 0; w < wid; ++w) base += wsum[w];
+  // this thread's lanes' prefixes stay in registers; the block sees them
+  // through 16-byte stores (conflict-free, unlike kK1Per-strided words)
+  int pv[kK1Per];
 #pragma unroll
   for (int k = 0; k < kK1Per; ++k) {
-    pre[kK1Per * tid + k] = base;
+    pv[k] = base;
     base += cl[k];
   }
+#pragma unroll
+  for (int v = 0; v < kK1Per / 4; ++v)
+    reinterpret_cast<int4*>(pre)[tid * (kK1Per / 4) + v] =
+        make_int4(pv[4 * v], pv[4 * v + 1], pv[4 * v + 2], pv[4 * v + 3]);
   if (tid == kK1Threads - 1) pre[kK1Lanes] = base;
   __syncthreads();
   uint32_t d[kK1Per];
@@ -1772,7 +1779,7 @@ __global__ void __launch_bounds__(kK1Threads) gen_tile_scan_kernel(
   for (int k = 0; k < kK1Per; ++k) {
     const int l = kK1Per * tid + k;
     const int ld = l & ~(omega - 1);  // the tile's first lane
-    const int pl = pre[l], pld = pre[ld];
+    const int pl = pv[k], pld = pre[ld];
     // offsets from the tile's start point, in 32 bits: rows and nonzeros
     // consumed by the lanes before this one in its tile
     const int dy = pl - pld;

@@ -1,5 +1,6 @@
-# K1 CTA shape A/B (exp/k1_<threads>_<lanes per thread>)
+# K1 A/B: working tree vs HEAD (exp/head)
 cd $GRAFT_REPO_ROOT
-for i in 1 2; do for v in k1_256_4 k1_128_4 k1_512_4 k1_128_8; do
-  TAG=$v MBX_LIB_PATH=exp/$v/libmerbit_b200.so python scripts/prof/k1_time.py 2>&1 | grep tile
-done; done
+for i in 1 2; do
+  TAG=tree python scripts/prof/k1_time.py 2>&1 | grep tile
+  TAG=head MBX_LIB_PATH=exp/head/libmerbit_b200.so python scripts/prof/k1_time.py 2>&1 | grep tile
+done
