@@ -22,7 +22,7 @@ y = torch.empty(A.n_rows, device="cuda", dtype=tdt)
 c = mb.SimtConfig.make(32, 14 if dt == np.float32 else 7, 128)
 t = mb.generate_tile_for(A, c)
 for rep in range(2):
-    for (w, cps) in [(0, 0), (32, 1), (16, 2), (8, 4)]:
+    for (w, cps) in [tuple(int(v) for v in s.split("x")) for s in os.environ.get("SHAPES", "0x0,32x1,16x2,8x4").split(",")]:
         ctx.set_tuning(w, cps, -1, prefetch=int(os.environ.get("MODE", -1)))
         A.build_xcache()
         for _ in range(3):
